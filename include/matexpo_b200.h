@@ -1,0 +1,145 @@
+/*
+ * matexpo_b200 — C ABI of the B200-native matrix-power engine (A^k).
+ *
+ * Drop-in boundary for the reference `matexpo` hot path
+ * (/root/reference/pkg/src/matexpo).  Plain pointers and sizes only; no
+ * torch or CUDA types cross this interface.  Every entry point returns an
+ * MXP_* status; the message of the last failure on the calling thread is
+ * available from mxp_last_error().
+ *
+ * Reference interface each entry point replaces:
+ *   mxp_plan            <- plan_exponentiation        expo.py:60-75
+ *   mxp_multiply        <- Backend.multiply(a, b)     expo.py:78-86 (backend
+ *                          plugin called at expo.py:133-136); device-side
+ *                          analogue gpuMatmul         gpu-backend/src/host.ts:67-95
+ *   mxp_power           <- exponentiate(a, k, backend) expo.py:121-139 executed
+ *                          on-device as in gpuExponentiate host.ts:106-141
+ *                          (one upload, ping-pong chain, one readback)
+ *   mxp_power_batched   <- exponentiate over independent matrices (BASELINE
+ *                          config 3; no reference counterpart beyond the loop)
+ *   mxp_alloc/free,     <- ComputeDevice.createBuffer / releaseBuffer /
+ *   mxp_upload/download    writeBuffer / readBuffer  device.ts:25-39
+ *   mxp_gemm            <- ComputeDevice.dispatchMatmul(kernel, n, a, b, c)
+ *                          device.ts:33-39 (device pointers, async)
+ *   mxp_power_device    <- the gpuExponentiate step loop host.ts:126-131 on
+ *                          caller-owned device buffers (async, graph replay)
+ *   mxp_power_mod       <- (new) exact modular mode, no reference counterpart
+ *   mxp_last_error      <- the message of the raised error (errors.py)
+ *
+ * Semantics kept from the reference:
+ *   - row-major, element (i, j) at i*n + j (linalg.py:27-31); square only;
+ *   - k = 0 -> identity (expo.py:128-129); k = 1 -> a bitwise copy of A with
+ *     zero multiplies (expo.py:130, :139); k < 0 -> MXP_E_VALIDATION
+ *     (expo.py:66-67);
+ *   - exactly floor(log2 k) + popcount(k) - 1 multiplies (expo.py:44-46),
+ *     reported in mxp_stats; host APIs move the input once and the result
+ *     once (count_transfers, expo.py:159-169; host.test.ts:136-146);
+ *   - all validation happens before any device work (host.ts:48-59);
+ *   - a failing multiply inside a chain reports its plan step index in
+ *     mxp_stats.failed_step (BackendStepError, errors.py:43-49).
+ * Threading: one handle = one CUDA stream + workspace; use a handle from one
+ * thread at a time (device.ts:6-8).
+ */
+#ifndef MATEXPO_B200_H
+#define MATEXPO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MXP_API __attribute__((visibility("default")))
+#else
+#define MXP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define MXP_OK 0
+#define MXP_E_VALIDATION 1         /* ValueError family (ShapeError, InvalidDimensionError, ...) */
+#define MXP_E_UNSUPPORTED 2        /* mode/size not supported (UnsupportedPowerError analogue) */
+#define MXP_E_DEVICE_UNAVAILABLE 3 /* no usable sm_100 device (errors.ts DeviceUnavailableError) */
+#define MXP_E_CUDA 4               /* CUDA runtime failure (-> BackendStepError inside a chain) */
+#define MXP_E_NCCL 5               /* collective failure (multi-GPU paths) */
+
+/* element modes */
+#define MXP_F32 0     /* float32 in/out; 3xTF32 on tcgen05 tensor cores */
+#define MXP_F64 1     /* float64 in/out; DMMA tensor pipe */
+#define MXP_U32_MOD 2 /* uint32 residues mod p; exact (see mxp_power_mod) */
+
+typedef struct mxp_handle_s* mxp_handle;
+
+typedef struct mxp_stats {
+    int64_t multiply_count; /* plan multiplies executed (expo.py:52-53) */
+    int64_t square_count;   /* SQUARE steps (expo.py:55-57) */
+    int64_t launches;       /* kernels launched by this call */
+    int64_t h2d;            /* host->device matrix transfers (logical) */
+    int64_t d2h;            /* device->host matrix transfers (logical) */
+    int64_t h2d_bytes;
+    int64_t d2h_bytes;
+    int64_t failed_step;    /* plan step index of a failed multiply, else -1 */
+    double device_ms;       /* device time of the call (host APIs), else 0 */
+} mxp_stats;
+
+/* library / device */
+MXP_API int mxp_version(int* major, int* minor);
+MXP_API int mxp_device_count(int* count);
+MXP_API int mxp_create(int device, mxp_handle* out);
+MXP_API int mxp_destroy(mxp_handle h);
+MXP_API int mxp_get_stream(mxp_handle h, void** stream);     /* cudaStream_t of the handle */
+MXP_API int mxp_synchronize(mxp_handle h);
+MXP_API int mxp_num_sms(mxp_handle h, int* sms);
+
+/* device verbs (ComputeDevice, device.ts:20-40) */
+MXP_API int mxp_alloc(mxp_handle h, size_t bytes, void** dptr);
+MXP_API int mxp_free(mxp_handle h, void* dptr);
+MXP_API int mxp_host_alloc(mxp_handle h, size_t bytes, void** hptr); /* pinned host memory */
+MXP_API int mxp_host_free(mxp_handle h, void* hptr);
+MXP_API int mxp_upload(mxp_handle h, void* dst, const void* src, size_t bytes);
+MXP_API int mxp_download(mxp_handle h, void* dst, const void* src, size_t bytes);
+
+/* the plan (expo.py:60-75): writes 'S'/'M' bytes, *count = multiply count */
+MXP_API int mxp_plan(int64_t k, char* steps, int64_t cap, int64_t* count);
+
+/* one multiply C = A * B */
+MXP_API int mxp_gemm(mxp_handle h, int mode, int64_t n, const void* dA, const void* dB, void* dC);
+MXP_API int mxp_multiply(mxp_handle h, int mode, int64_t n, const void* hA, const void* hB, void* hC,
+                 mxp_stats* stats);
+
+/* A^k, whole chain on device */
+MXP_API int mxp_power_device(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA, void* dOut,
+                     mxp_stats* stats);
+MXP_API int mxp_power(mxp_handle h, int mode, int64_t n, int64_t k, const void* hA, void* hOut,
+              mxp_stats* stats);
+
+/* A_i^k for `batch` independent row-major n x n matrices stored back to back */
+MXP_API int mxp_power_batched_device(mxp_handle h, int mode, int64_t n, int64_t batch, int64_t k,
+                             const void* dA, void* dOut, mxp_stats* stats);
+MXP_API int mxp_power_batched(mxp_handle h, int mode, int64_t n, int64_t batch, int64_t k,
+                      const void* hA, void* hOut, mxp_stats* stats);
+
+/* exact modular mode: uint32 residues, result (A^k) mod p, 2 <= p < 2^31 */
+MXP_API int mxp_power_mod_device(mxp_handle h, int64_t n, int64_t k, uint32_t p, const void* dA,
+                         void* dOut, mxp_stats* stats);
+MXP_API int mxp_power_mod(mxp_handle h, int64_t n, int64_t k, uint32_t p, const void* hA, void* hOut,
+                  mxp_stats* stats);
+
+/* inputs: the reference's SplitMix64 random_matrix (linalg.py:127-148) on
+ * device, bit-identical; matrix b of the batch uses seed seed0 + b.  With
+ * scale != 0 the value is fl(random_matrix(n, F64, seed, lo, hi) * scale)
+ * (the configs' spectrally normalised recipe); with scale == 0 it is
+ * random_matrix(n, mode's dtype, seed, lo, hi).  Async on the handle stream. */
+MXP_API int mxp_random_device(mxp_handle h, int mode, int64_t n, int64_t batch, uint64_t seed0,
+                              double lo, double hi, double scale, void* dOut);
+
+/* error reporting */
+MXP_API int mxp_last_error(char* buf, size_t len); /* copies the thread's last message */
+MXP_API const char* mxp_status_string(int status);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MATEXPO_B200_H */

@@ -1,0 +1,560 @@
+// 3xTF32 tensor-core kernels for sm_100a (tcgen05 + TMEM + TMA).
+//
+// FP32 products are formed as  A_hi*B_hi + A_hi*B_lo + A_lo*B_hi  with
+// hi = rna_tf32(x), lo = rna_tf32(x - hi), accumulated in fp32 in TMEM.  This
+// replaces the reference's scalar ascending-k fp32 loop (linalg.py:151-164,
+// matmul_tiled.cl:91-94); parity is by the relative-Frobenius tolerance of
+// SURVEY §8(d), not bitwise (tensor-core summation order differs).
+#include "mxp_internal.h"
+#include "ptx.cuh"
+
+namespace mxp {
+
+// ======================================================================
+// K3 — persistent batched chain, n <= 128, one matrix per CTA at a time,
+// the running power P resident on chip for the whole chain.
+//
+//   TMEM (512 columns):  [0,128) D0, [128,256) D1 fp32 accumulators
+//                        (lane = row); [256,384) P_hi, [384,512) P_lo as the
+//                        LEFT operand (lane = row m, column = k)
+//   SMEM (128 KB):       P_hi, P_lo as the RIGHT operand, MN-major
+//                        SW128_BASE32B: [n/32][k][32] with 128-byte rows
+//
+// Per step one thread issues 16 k-steps x 3 tcgen05.mma (M=N=128, K=8,
+// A from TMEM, B from SMEM) and commits to an mbarrier; 8 warps then drain
+// D0 + D1 (tcgen05.ld, round-to-nearest fp32 add), split each value into
+// tf32 hi/lo, and write the next power back both into TMEM (tcgen05.st, left
+// operand) and SMEM (right operand) — or, on the last step, fp32 to global.
+//
+// Accuracy: the tensor core truncates its fp32 accumulator on every MMA
+// (measured: a bias that grows linearly with the number of MMAs into one
+// accumulator, tools/probe.py "acc"), and a chain amplifies a systematic
+// per-multiply bias ~k-fold.  So the small cross terms (lo*hi, hi*lo) are
+// accumulated first (their truncation is 2^-11 smaller), the k-steps are
+// split by parity over two accumulators (8 big-term MMAs each), and the two
+// partial sums are combined with an IEEE round-to-nearest add.
+//
+// MULTIPLY_BASE computes base*acc instead of the reference's acc*base
+// (expo.py:135-136): both are A^(e+1) because acc is a power of the base; the
+// resident power stays the right operand and the base is loaded into the
+// TMEM left operand for that step only.
+// ======================================================================
+namespace {
+constexpr uint32_t kChunk = 128u * 128u;  // one 32-column chunk: 128 rows x 128 B
+constexpr uint32_t kPlane = 4u * kChunk;  // 64 KB
+constexpr int kK3Threads = 256;
+constexpr uint32_t kColD0 = 0, kColD1 = 128, kColHi = 256, kColLo = 384;
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023u) & ~uintptr_t(1023));
+}
+
+// n x n row-major fp32 (zero padded to 128 x 128) -> tf32 hi/lo in the
+// MN-major right-operand layout.  Coalesced: a warp reads 512 B of one row.
+__device__ __forceinline__ void k3_load_right(const float* __restrict__ src, int n,
+                                              uint8_t* dst_hi, uint8_t* dst_lo) {
+    const bool vec = (n & 3) == 0;
+    for (int idx = threadIdx.x; idx < 128 * 32; idx += kK3Threads) {
+        const int r = idx >> 5;
+        const int c = (idx & 31) << 2;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (r < n) {
+            const float* p = src + static_cast<size_t>(r) * n + c;
+            if (vec && c + 3 < n) {
+                float4 t = __ldg(reinterpret_cast<const float4*>(p));
+                v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (c + i < n) v[i] = __ldg(p + i);
+            }
+        }
+        uint4 hi, lo;
+        split_tf32(v[0], hi.x, lo.x);
+        split_tf32(v[1], hi.y, lo.y);
+        split_tf32(v[2], hi.z, lo.z);
+        split_tf32(v[3], hi.w, lo.w);
+        const uint32_t off = sw32b_offset(r, c, kChunk);
+        *reinterpret_cast<uint4*>(dst_hi + off) = hi;
+        *reinterpret_cast<uint4*>(dst_lo + off) = lo;
+    }
+}
+
+// Copy row `row`, columns [col0, col0+32) of the SMEM right operand into the
+// TMEM left operand (same values; only the layout differs).
+__device__ __forceinline__ void k3_row_to_tmem(const uint8_t* b_hi, const uint8_t* b_lo,
+                                               uint32_t row, int col0, uint32_t t_hi,
+                                               uint32_t t_lo) {
+    uint32_t h[32], l[32];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const uint32_t off = sw32b_offset(row, col0 + 4 * u, kChunk);
+        const uint4 x = *reinterpret_cast<const uint4*>(b_hi + off);
+        const uint4 y = *reinterpret_cast<const uint4*>(b_lo + off);
+        h[4 * u] = x.x; h[4 * u + 1] = x.y; h[4 * u + 2] = x.z; h[4 * u + 3] = x.w;
+        l[4 * u] = y.x; l[4 * u + 1] = y.y; l[4 * u + 2] = y.z; l[4 * u + 3] = y.w;
+    }
+    tmem_st32(t_hi + col0, h);
+    tmem_st32(t_lo + col0, l);
+}
+
+// Row `row`, columns [col0, col0+32) of the base matrix from global (zero
+// padded), split, into the TMEM left operand.
+__device__ __forceinline__ void k3_base_row_to_tmem(const float* __restrict__ src, int n,
+                                                    uint32_t row, int col0, uint32_t t_hi,
+                                                    uint32_t t_lo) {
+    uint32_t h[32], l[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const int c = col0 + i;
+        const float v = (row < static_cast<uint32_t>(n) && c < n)
+                            ? __ldg(src + static_cast<size_t>(row) * n + c)
+                            : 0.f;
+        split_tf32(v, h[i], l[i]);
+    }
+    tmem_st32(t_hi + col0, h);
+    tmem_st32(t_lo + col0, l);
+}
+}  // namespace
+
+size_t k3_smem_bytes() { return 2 * kPlane + 1024 + 256; }
+
+__global__ void __launch_bounds__(kK3Threads, 1)
+    k3_batched_power(const float* __restrict__ in, float* __restrict__ out, int n, long long batch,
+                     PlanBits plan) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    uint8_t* b_hi = smem;
+    uint8_t* b_lo = smem + kPlane;
+    uint64_t* mma_bar = reinterpret_cast<uint64_t*>(smem + 2 * kPlane);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 2 * kPlane + 64);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    constexpr uint32_t kIdesc = idesc_tf32_kmaj_mnmaj<128, 128>();
+
+    if (tid == 0) {
+        mbar_init(mma_bar, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    uint32_t phase = 0;
+
+    const uint32_t s_hi = smem_u32(b_hi), s_lo = smem_u32(b_lo);
+    const int q = warp & 3;             // TMEM lane quarter this warp may access
+    const int colh = (warp >> 2) * 64;  // column half handled by this warp
+    const uint32_t row = q * 32 + lane;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t t_d0 = lane_base + kColD0, t_d1 = lane_base + kColD1;
+    const uint32_t t_hi = lane_base + kColHi, t_lo = lane_base + kColLo;
+    const uint64_t bdesc_hi = mnmajor_desc(s_hi, kChunk), bdesc_lo = mnmajor_desc(s_lo, kChunk);
+
+    for (long long m = blockIdx.x; m < batch; m += gridDim.x) {
+        const float* src = in + static_cast<size_t>(m) * n * n;
+        k3_load_right(src, n, b_hi, b_lo);
+        __syncthreads();
+        k3_row_to_tmem(b_hi, b_lo, row, colh, t_hi, t_lo);
+        k3_row_to_tmem(b_hi, b_lo, row, colh + 32, t_hi, t_lo);
+        tmem_st_wait();
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+
+        for (int s = 0; s < plan.len; ++s) {
+            if (plan_is_mult(plan, s)) {
+                // left operand <- base (the resident acc stays the right operand)
+                k3_base_row_to_tmem(src, n, row, colh, t_hi, t_lo);
+                k3_base_row_to_tmem(src, n, row, colh + 32, t_hi, t_lo);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncthreads();
+            }
+            if (tid == 0) {
+                tc_fence_after();
+                const uint32_t a_hi = tmem + kColHi, a_lo = tmem + kColLo;
+                // small cross terms first, k-steps split by parity over D0/D1
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const uint32_t d = tmem + ((k & 1) ? kColD1 : kColD0);
+                    const uint64_t boff = static_cast<uint64_t>((k * 1024) >> 4);
+                    mma_tf32_ts(d, a_lo + 8 * k, bdesc_hi + boff, kIdesc, k > 1 ? 1u : 0u);
+                    mma_tf32_ts(d, a_hi + 8 * k, bdesc_lo + boff, kIdesc, 1u);
+                }
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const uint32_t d = tmem + ((k & 1) ? kColD1 : kColD0);
+                    const uint64_t boff = static_cast<uint64_t>((k * 1024) >> 4);
+                    mma_tf32_ts(d, a_hi + 8 * k, bdesc_hi + boff, kIdesc, 1u);
+                }
+                mma_commit(mma_bar);
+            }
+            mbar_wait(mma_bar, phase);
+            phase ^= 1;
+            tc_fence_after();
+            const bool last = (s == plan.len - 1);
+#pragma unroll 1
+            for (int j = 0; j < 2; ++j) {
+                const int col0 = colh + j * 32;
+                uint32_t v[32], w[32];
+                tmem_ld32(t_d0 + col0, v);
+                tmem_ld32(t_d1 + col0, w);
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    v[i] = __float_as_uint(__fadd_rn(__uint_as_float(v[i]), __uint_as_float(w[i])));
+                if (last) {
+                    if (row < static_cast<uint32_t>(n)) {
+                        float* dst = out + static_cast<size_t>(m) * n * n +
+                                     static_cast<size_t>(row) * n + col0;
+                        if ((n & 3) == 0 && col0 + 32 <= n) {
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                reinterpret_cast<float4*>(dst)[u] = make_float4(
+                                    __uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]),
+                                    __uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3]));
+                        } else {
+                            for (int i = 0; i < 32; ++i)
+                                if (col0 + i < n) dst[i] = __uint_as_float(v[i]);
+                        }
+                    }
+                } else {
+                    uint32_t h[32], l[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) split_tf32(__uint_as_float(v[i]), h[i], l[i]);
+                    tmem_st32(t_hi + col0, h);
+                    tmem_st32(t_lo + col0, l);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const uint32_t off = sw32b_offset(row, col0 + 4 * u, kChunk);
+                        *reinterpret_cast<uint4*>(b_hi + off) =
+                            make_uint4(h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]);
+                        *reinterpret_cast<uint4*>(b_lo + off) =
+                            make_uint4(l[4 * u], l[4 * u + 1], l[4 * u + 2], l[4 * u + 3]);
+                    }
+                }
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            fence_proxy_async_smem();
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
+                              const PlanBits& plan, int grid, cudaStream_t s) {
+    if (grid > batch) grid = static_cast<int>(batch);
+    k3_batched_power<<<grid, kK3Threads, k3_smem_bytes(), s>>>(in, out, n, batch, plan);
+    return cudaGetLastError();
+}
+
+// ======================================================================
+// Split: fp32 -> tf32 hi/lo planes, zero padded to n_pad.
+// ======================================================================
+__global__ void split_pad_kernel(const float* __restrict__ in, int n, int ld,
+                                 uint32_t* __restrict__ hi, uint32_t* __restrict__ lo,
+                                 int n_pad) {
+    const size_t quads = static_cast<size_t>(n_pad) * n_pad / 4;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < quads;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t e = i * 4;
+        const int r = static_cast<int>(e / n_pad);
+        const int c = static_cast<int>(e - static_cast<size_t>(r) * n_pad);
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (r < n) {
+            const float* p = in + static_cast<size_t>(r) * ld + c;
+            if ((ld & 3) == 0 && c + 3 < n) {
+                float4 t = __ldg(reinterpret_cast<const float4*>(p));
+                v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (c + k < n) v[k] = __ldg(p + k);
+            }
+        }
+        uint4 h, l;
+        split_tf32(v[0], h.x, l.x);
+        split_tf32(v[1], h.y, l.y);
+        split_tf32(v[2], h.z, l.z);
+        split_tf32(v[3], h.w, l.w);
+        reinterpret_cast<uint4*>(hi)[i] = h;
+        reinterpret_cast<uint4*>(lo)[i] = l;
+    }
+}
+
+cudaError_t launch_split(const float* in, int n, int ld, uint32_t* hi, uint32_t* lo, int n_pad,
+                         cudaStream_t s) {
+    const size_t quads = static_cast<size_t>(n_pad) * n_pad / 4;
+    int blocks = static_cast<int>((quads + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    split_pad_kernel<<<blocks, 256, 0, s>>>(in, n, ld, hi, lo, n_pad);
+    return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void identity_kernel(T* out, int n) {
+    const size_t total = static_cast<size_t>(n) * n;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        out[i] = (i / n == i % n) ? T(1) : T(0);
+}
+cudaError_t launch_identity_f32(float* out, int n, cudaStream_t s) {
+    identity_kernel<float><<<148, 256, 0, s>>>(out, n);
+    return cudaGetLastError();
+}
+cudaError_t launch_identity_f64(double* out, int n, cudaStream_t s) {
+    identity_kernel<double><<<148, 256, 0, s>>>(out, n);
+    return cudaGetLastError();
+}
+
+// ======================================================================
+// K1 — one 3xTF32 GEMM tile per CTA: 128 x 128 output, BK = 32, TMA-fed
+// 3-stage mbarrier pipeline, single-thread tcgen05.mma issue.
+//   warp 0 : TMA producer          warp 1 : MMA issuer
+//   warp 2 : TMEM allocator        warps 4-11 : epilogue (lane quarter = warp % 4,
+//                                               column half = (warp - 4) / 4)
+// Stage layout: A_hi, A_lo (128 rows x 128 B, K-major SW128 via TMA
+// SWIZZLE_128B), B_hi, B_lo (4 chunks of 32 K-rows x 128 B, MN-major
+// SW128_BASE32B via TMA SWIZZLE_128B_ATOM_32B).
+//
+// Accuracy: each pipeline stage (K = 32) is accumulated into its own TMEM
+// chunk accumulator (two, ping-ponged: small cross terms first, then 4
+// big-term MMAs), and the epilogue warps drain every chunk into fp32
+// register sums with round-to-nearest adds while the next chunk's MMAs run.
+// This bounds the tensor core's truncation bias to 4 MMAs per partial sum
+// independent of n (see K3's note); the drain (64 KB of tcgen05.ld per
+// chunk, ~310 cycles) hides under the chunk's 12 MMAs (~768 cycles).
+// ======================================================================
+namespace {
+// 3 MMAs per k-step, small cross terms first.
+__device__ __forceinline__ void mma3(uint32_t tmem, uint64_t a_hi, uint64_t a_lo, uint64_t b_hi,
+                                     uint64_t b_lo, uint32_t idesc, uint32_t acc) {
+    mma_tf32(tmem, a_lo, b_hi, idesc, acc);
+    mma_tf32(tmem, a_hi, b_lo, idesc, 1u);
+    mma_tf32(tmem, a_hi, b_hi, idesc, 1u);
+}
+struct K1Cfg {
+    static constexpr int kBN = 128;
+    static constexpr int kStages = 3;
+    static constexpr uint32_t kABytes = 128 * 128;             // one plane: 128 rows x 32 fp32
+    static constexpr uint32_t kBBytes = 32 * 128 * (kBN / 32);  // one plane: 4 chunks x 32 rows
+    static constexpr uint32_t kStageBytes = 2 * kABytes + 2 * kBBytes;  // 64 KB
+    static constexpr size_t kSmem = kStages * kStageBytes + 1024 + 256;
+    static constexpr int kThreads = 384;
+};
+}  // namespace
+
+__global__ void __launch_bounds__(K1Cfg::kThreads, 1)
+    k1_gemm_3xtf32(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
+                   const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
+                   int n_pad, float* __restrict__ out_f32, int n_out, int ld_out,
+                   uint32_t* __restrict__ out_hi, uint32_t* __restrict__ out_lo) {
+    using Cfg = K1Cfg;
+    constexpr int S = Cfg::kStages;
+    constexpr int BN = Cfg::kBN;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+    uint64_t* empty = full + S;
+    uint64_t* cfull = empty + S;   // [2] chunk accumulator ready
+    uint64_t* cempty = cfull + 2;  // [2] chunk accumulator drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * 128;
+    const int n0 = blockIdx.x * BN;
+    const int num_kb = n_pad / 32;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&cfull[i], 1);
+            mbar_init(&cempty[i], 8);  // one arrival per epilogue warp
+        }
+        fence_mbar_init();
+        tma_prefetch(&ma_hi);
+        tma_prefetch(&ma_lo);
+        tma_prefetch(&mb_hi);
+        tma_prefetch(&mb_lo);
+    }
+    if (warp == 2) tmem_alloc<256>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        for (int kb = 0; kb < num_kb; ++kb) {
+            const int st = kb % S;
+            const uint32_t ph = (kb / S) & 1;
+            mbar_wait(&empty[st], ph ^ 1);
+            uint8_t* base = smem + st * Cfg::kStageBytes;
+            mbar_expect_tx(&full[st], Cfg::kStageBytes);
+            tma_load_2d(base, &ma_hi, &full[st], kb * 32, m0);
+            tma_load_2d(base + Cfg::kABytes, &ma_lo, &full[st], kb * 32, m0);
+            uint8_t* bh = base + 2 * Cfg::kABytes;
+            uint8_t* bl = bh + Cfg::kBBytes;
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j) {
+                tma_load_2d(bh + j * 4096, &mb_hi, &full[st], n0 + 32 * j, kb * 32);
+                tma_load_2d(bl + j * 4096, &mb_lo, &full[st], n0 + 32 * j, kb * 32);
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        constexpr uint32_t kIdesc = idesc_tf32_kmaj_mnmaj<128, BN>();
+        const uint32_t s0 = smem_u32(smem);
+        const uint64_t da_hi = kmajor_desc(s0), da_lo = kmajor_desc(s0 + Cfg::kABytes);
+        const uint64_t db_hi = mnmajor_desc(s0 + 2 * Cfg::kABytes, 4096);
+        const uint64_t db_lo = mnmajor_desc(s0 + 2 * Cfg::kABytes + Cfg::kBBytes, 4096);
+        for (int kb = 0; kb < num_kb; ++kb) {
+            const int st = kb % S;
+            const uint32_t ph = (kb / S) & 1;
+            const int c = kb & 1;
+            mbar_wait(&cempty[c], ((kb >> 1) & 1) ^ 1);
+            mbar_wait(&full[st], ph);
+            tc_fence_after();
+            const uint64_t so = static_cast<uint64_t>((st * Cfg::kStageBytes) >> 4);
+            const uint32_t d = tmem + c * BN;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((1024 * k) >> 4);
+                mma_tf32(d, da_lo + ao, db_hi + bo, kIdesc, k > 0 ? 1u : 0u);
+                mma_tf32(d, da_hi + ao, db_lo + bo, kIdesc, 1u);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((1024 * k) >> 4);
+                mma_tf32(d, da_hi + ao, db_hi + bo, kIdesc, 1u);
+            }
+            mma_commit(&empty[st]);
+            mma_commit(&cfull[c]);
+        }
+    } else if (warp >= 4) {
+        const int q = warp & 3;
+        const int ch = ((warp - 4) >> 2) * 64;  // column half
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        float sum[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) sum[i] = 0.f;
+        for (int kb = 0; kb < num_kb; ++kb) {
+            const int c = kb & 1;
+            mbar_wait(&cfull[c], (kb >> 1) & 1);
+            tc_fence_after();
+            uint32_t v[32];
+            tmem_ld32(lane_base + c * BN + ch, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sum[i] = __fadd_rn(sum[i], __uint_as_float(v[i]));
+            tmem_ld32(lane_base + c * BN + ch + 32, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sum[32 + i] = __fadd_rn(sum[32 + i], __uint_as_float(v[i]));
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&cempty[c]);
+        }
+        const int row = m0 + q * 32 + lane;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int col = n0 + ch + 32 * h;
+            const float* v = sum + 32 * h;
+            if (out_hi != nullptr) {
+                uint4* dh = reinterpret_cast<uint4*>(out_hi + static_cast<size_t>(row) * n_pad + col);
+                uint4* dl = reinterpret_cast<uint4*>(out_lo + static_cast<size_t>(row) * n_pad + col);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    uint4 hv, lv;
+                    split_tf32(v[4 * u + 0], hv.x, lv.x);
+                    split_tf32(v[4 * u + 1], hv.y, lv.y);
+                    split_tf32(v[4 * u + 2], hv.z, lv.z);
+                    split_tf32(v[4 * u + 3], hv.w, lv.w);
+                    dh[u] = hv;
+                    dl[u] = lv;
+                }
+            }
+            if (out_f32 != nullptr && row < n_out && col < n_out) {
+                float* d = out_f32 + static_cast<size_t>(row) * ld_out + col;
+                if ((ld_out & 3) == 0 && col + 32 <= n_out) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        reinterpret_cast<float4*>(d)[u] =
+                            make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+                } else {
+                    for (int i = 0; i < 32; ++i)
+                        if (col + i < n_out) d[i] = v[i];
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) tmem_dealloc<256>(tmem);
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (fn == nullptr) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+bool encode_plane_map(CUtensorMap* map, const void* plane, int n_pad, int box_cols, int box_rows,
+                      bool right_operand) {
+    EncodeTiledFn fn = get_encode_fn();
+    if (fn == nullptr) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(n_pad), static_cast<cuuint64_t>(n_pad)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(n_pad) * 4};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(plane), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    right_operand ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+int k1_block_n(int n_pad, int num_sms) {
+    (void)n_pad;
+    (void)num_sms;
+    return K1Cfg::kBN;
+}
+
+cudaError_t prepare_tf32_kernels() {
+    cudaError_t e = cudaFuncSetAttribute(k3_batched_power, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(k3_smem_bytes()));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k1_gemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(K1Cfg::kSmem));
+    return e;
+}
+
+cudaError_t launch_k1_gemm(const GemmPlanes& m, int n_pad, int block_n, float* out_f32,
+                           int n_out, int ld_out, uint32_t* out_hi, uint32_t* out_lo,
+                           cudaStream_t s) {
+    (void)block_n;
+    dim3 grid(n_pad / K1Cfg::kBN, n_pad / 128);
+    k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad,
+                                                               out_f32, n_out, ld_out, out_hi, out_lo);
+    return cudaGetLastError();
+}
+
+}  // namespace mxp

@@ -1,0 +1,803 @@
+// C-ABI shim (include/matexpo_b200.h): validation, workspace, the CUDA-graph
+// square-and-multiply scheduler, and dispatch to the sm_100a kernels.
+//
+// The scheduler replaces the reference's host loop (expo.py:131-138) and the
+// device chain of gpuExponentiate (gpu-backend/src/host.ts:106-141): the plan
+// (expo.py:60-75) is baked into one captured CUDA graph of m GEMM launches
+// over ping-pong buffers in HBM; the graph is cached per (mode, n, k, in, out)
+// and replayed.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/matexpo_b200.h"
+#include "mxp_internal.h"
+
+namespace mxp {
+
+cudaError_t prepare_tf32_kernels();
+cudaError_t prepare_f64_kernels();
+cudaError_t prepare_kernels() {
+    cudaError_t e = prepare_tf32_kernels();
+    if (e == cudaSuccess) e = prepare_f64_kernels();
+    return e;
+}
+
+PlanBits make_plan(int64_t k) {
+    PlanBits p{};
+    if (k <= 1) return p;
+    int top = 63;
+    while (!((k >> top) & 1)) --top;
+    for (int shift = top - 1; shift >= 0; --shift) {
+        p.len++;  // SQUARE
+        p.squares++;
+        if ((k >> shift) & 1) {
+            p.mult[p.len >> 6] |= 1ull << (p.len & 63);
+            p.len++;
+        }
+    }
+    return p;
+}
+
+}  // namespace mxp
+
+using namespace mxp;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(MXP_E_CUDA, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define MXP_CUDA(expr)                                         \
+    do {                                                       \
+        cudaError_t _e = (expr);                               \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr);    \
+    } while (0)
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+struct GraphKey {
+    int mode;
+    int64_t n, k;
+    const void* in;
+    void* out;
+    bool operator<(const GraphKey& o) const {
+        return std::tie(mode, n, k, in, out) < std::tie(o.mode, o.n, o.k, o.in, o.out);
+    }
+};
+
+}  // namespace
+
+struct mxp_handle_s {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    // fp32 single-matrix workspace: 6 tf32 planes (base, ping, pong) x (hi, lo)
+    int64_t ws32_pad = 0;
+    uint32_t* planes[6] = {};
+    CUtensorMap map_a[6], map_b[6];
+    // fp64 workspace: base, ping, pong (n_pad^2 doubles)
+    int64_t ws64_pad = 0;
+    double* f64buf[3] = {};
+    // host-API staging device buffers
+    size_t io_bytes = 0;
+    void* d_in = nullptr;
+    void* d_in2 = nullptr;
+    void* d_out = nullptr;
+
+    std::map<GraphKey, cudaGraphExec_t> graphs;
+
+    void drop_graphs() {
+        for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+        graphs.clear();
+    }
+};
+
+namespace {
+
+int check_handle(mxp_handle h) {
+    if (h == nullptr) return fail(MXP_E_VALIDATION, "null handle");
+    cudaError_t e = cudaSetDevice(h->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    return MXP_OK;
+}
+
+int validate(int mode, int64_t n, int64_t k) {
+    if (mode != MXP_F32 && mode != MXP_F64)
+        return fail(MXP_E_VALIDATION, "unknown element mode %d (expected MXP_F32 or MXP_F64)", mode);
+    if (n < 1) return fail(MXP_E_VALIDATION, "matrix order must be >= 1, got %lld", (long long)n);
+    if (n > 32768)
+        return fail(MXP_E_UNSUPPORTED, "matrix order %lld exceeds the supported 32768",
+                    (long long)n);
+    if (k < 0) return fail(MXP_E_VALIDATION, "power must be >= 0, got %lld", (long long)k);
+    return MXP_OK;
+}
+
+size_t elem_size(int mode) { return mode == MXP_F64 ? 8 : 4; }
+
+void stats_reset(mxp_stats* st) {
+    if (!st) return;
+    std::memset(st, 0, sizeof *st);
+    st->failed_step = -1;
+}
+
+int ensure_ws32(mxp_handle h, int64_t n_pad) {
+    if (h->ws32_pad >= n_pad) return MXP_OK;
+    for (auto& p : h->planes) {
+        if (p) cudaFree(p);
+        p = nullptr;
+    }
+    h->drop_graphs();
+    h->ws32_pad = 0;
+    const size_t bytes = static_cast<size_t>(n_pad) * n_pad * 4;
+    for (auto& p : h->planes) MXP_CUDA(cudaMalloc(&p, bytes));
+    h->ws32_pad = n_pad;
+    return MXP_OK;
+}
+
+// (Re-)encode the TMA maps of the 6 planes for the current n_pad.
+int encode_ws32(mxp_handle h, int64_t n_pad) {
+    for (int i = 0; i < 6; ++i) {
+        if (!encode_plane_map(&h->map_a[i], h->planes[i], (int)n_pad, 32, 128, false) ||
+            !encode_plane_map(&h->map_b[i], h->planes[i], (int)n_pad, 32, 32, true))
+            return fail(MXP_E_CUDA, "cuTensorMapEncodeTiled failed (n_pad=%lld)", (long long)n_pad);
+    }
+    return MXP_OK;
+}
+
+int ensure_ws64(mxp_handle h, int64_t n_pad) {
+    if (h->ws64_pad >= n_pad) return MXP_OK;
+    for (auto& p : h->f64buf) {
+        if (p) cudaFree(p);
+        p = nullptr;
+    }
+    h->drop_graphs();
+    h->ws64_pad = 0;
+    const size_t bytes = static_cast<size_t>(n_pad) * n_pad * 8;
+    for (auto& p : h->f64buf) MXP_CUDA(cudaMalloc(&p, bytes));
+    h->ws64_pad = n_pad;
+    return MXP_OK;
+}
+
+int ensure_io(mxp_handle h, size_t bytes) {
+    if (h->io_bytes >= bytes) return MXP_OK;
+    if (h->d_in) cudaFree(h->d_in);
+    if (h->d_in2) cudaFree(h->d_in2);
+    if (h->d_out) cudaFree(h->d_out);
+    h->d_in = h->d_in2 = h->d_out = nullptr;
+    h->io_bytes = 0;
+    MXP_CUDA(cudaMalloc(&h->d_in, bytes));
+    MXP_CUDA(cudaMalloc(&h->d_in2, bytes));
+    MXP_CUDA(cudaMalloc(&h->d_out, bytes));
+    h->io_bytes = bytes;
+    return MXP_OK;
+}
+
+// ---- enqueue helpers (no validation; stream = h->stream) -----------------
+
+// 3xTF32 chain for n > kSmallMax through K1, planes padded to 128.
+int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float* dA,
+                      float* dOut, int64_t* launches, int64_t* failed) {
+    const int64_t n_pad = round_up(n, 128);
+    int rc = ensure_ws32(h, n_pad);
+    if (rc) return rc;
+    rc = encode_ws32(h, h->ws32_pad);
+    if (rc) return rc;
+    const int np = (int)h->ws32_pad;  // planes are laid out with the workspace stride
+    cudaError_t e = launch_split(dA, (int)n, (int)n, h->planes[0], h->planes[1], np, h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "split");
+    ++*launches;
+    const int bn = k1_block_n(np, h->num_sms);
+    int acc = 0;  // plane pair index: 0 base, 1 ping, 2 pong
+    for (int s = 0; s < plan.len; ++s) {
+        const bool mult = plan_is_mult(plan, s);
+        const bool last = (s == plan.len - 1);
+        const int dst = (acc == 1) ? 2 : 1;
+        const int rhs = mult ? 0 : acc;
+        GemmPlanes m;
+        m.a_hi = h->map_a[2 * acc];
+        m.a_lo = h->map_a[2 * acc + 1];
+        m.b_hi = h->map_b[2 * rhs];
+        m.b_lo = h->map_b[2 * rhs + 1];
+        e = launch_k1_gemm(m, np, bn, last ? dOut : nullptr, (int)n, (int)n,
+                           last ? nullptr : h->planes[2 * dst],
+                           last ? nullptr : h->planes[2 * dst + 1], h->stream);
+        if (e != cudaSuccess) {
+            *failed = s;
+            return cuda_fail(e, "k1_gemm_3xtf32");
+        }
+        ++*launches;
+        acc = dst;
+    }
+    return MXP_OK;
+}
+
+int enqueue_chain_f64(mxp_handle h, int64_t n, const PlanBits& plan, const double* dA,
+                      double* dOut, int64_t* launches, int64_t* failed) {
+    const int64_t n_pad = f64_pad((int)n);
+    int rc = ensure_ws64(h, n_pad);
+    if (rc) return rc;
+    double** b = h->f64buf;
+    cudaError_t e = launch_f64_pad(dA, (int)n, b[0], (int)n_pad, h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "f64_pad");
+    ++*launches;
+    int acc = 0;
+    for (int s = 0; s < plan.len; ++s) {
+        const bool mult = plan_is_mult(plan, s);
+        const int dst = (acc == 1) ? 2 : 1;
+        e = launch_f64_gemm(b[acc], mult ? b[0] : b[acc], b[dst], (int)n_pad, h->stream);
+        if (e != cudaSuccess) {
+            *failed = s;
+            return cuda_fail(e, "f64_gemm");
+        }
+        ++*launches;
+        acc = dst;
+    }
+    e = launch_f64_unpad(b[acc], (int)n_pad, dOut, (int)n, h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "f64_unpad");
+    ++*launches;
+    return MXP_OK;
+}
+
+// Enqueue A^k for one matrix (k >= 2) on h->stream.
+int enqueue_power(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA, void* dOut,
+                  int64_t* launches, int64_t* failed) {
+    const PlanBits plan = make_plan(k);
+    if (mode == MXP_F32) {
+        if (n <= kSmallMax) {
+            cudaError_t e = launch_k3_batched(static_cast<const float*>(dA),
+                                              static_cast<float*>(dOut), (int)n, 1, plan, 1,
+                                              h->stream);
+            if (e != cudaSuccess) {
+                *failed = 0;
+                return cuda_fail(e, "k3_batched_power");
+            }
+            ++*launches;
+            return MXP_OK;
+        }
+        return enqueue_chain_f32(h, n, plan, static_cast<const float*>(dA),
+                                 static_cast<float*>(dOut), launches, failed);
+    }
+    return enqueue_chain_f64(h, n, plan, static_cast<const double*>(dA),
+                             static_cast<double*>(dOut), launches, failed);
+}
+
+// k in {0, 1}: identity / bitwise copy, zero multiplies.
+int enqueue_trivial(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA, void* dOut,
+                    int64_t batch, int64_t* launches) {
+    const size_t bytes = static_cast<size_t>(n) * n * elem_size(mode);
+    for (int64_t b = 0; b < batch; ++b) {
+        void* o = static_cast<char*>(dOut) + b * bytes;
+        const void* a = static_cast<const char*>(dA) + b * bytes;
+        if (k == 1) {
+            if (o != a) MXP_CUDA(cudaMemcpyAsync(o, a, bytes, cudaMemcpyDeviceToDevice, h->stream));
+        } else {
+            cudaError_t e = (mode == MXP_F64)
+                                ? launch_identity_f64(static_cast<double*>(o), (int)n, h->stream)
+                                : launch_identity_f32(static_cast<float*>(o), (int)n, h->stream);
+            if (e != cudaSuccess) return cuda_fail(e, "identity");
+            ++*launches;
+        }
+    }
+    return MXP_OK;
+}
+
+void fill_plan_stats(mxp_stats* st, int64_t k, int64_t batch) {
+    if (!st) return;
+    const PlanBits p = make_plan(k);
+    st->multiply_count = static_cast<int64_t>(p.len) * batch;
+    st->square_count = static_cast<int64_t>(p.squares) * batch;
+}
+
+// Run A^k on device through a cached CUDA graph (single matrix).
+int run_power_graph(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA, void* dOut,
+                    mxp_stats* st) {
+    int64_t launches = 0, failed = -1;
+    GraphKey key{mode, n, k, dA, dOut};
+    auto it = h->graphs.find(key);
+    if (it == h->graphs.end()) {
+        // workspace must exist before capture (no cudaMalloc inside capture)
+        if (mode == MXP_F32 && n > kSmallMax) {
+            int rc = ensure_ws32(h, round_up(n, 128));
+            if (rc) return rc;
+        } else if (mode == MXP_F64) {
+            int rc = ensure_ws64(h, f64_pad((int)n));
+            if (rc) return rc;
+        }
+        cudaGraph_t g = nullptr;
+        MXP_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_power(h, mode, n, k, dA, dOut, &launches, &failed);
+        cudaError_t ce = cudaStreamEndCapture(h->stream, &g);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            if (st) st->failed_step = failed;
+            return rc;
+        }
+        if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+        cudaGraphExec_t ge = nullptr;
+        ce = cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphDestroy(g);
+        if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
+        it = h->graphs.emplace(key, ge).first;
+    }
+    cudaError_t e = cudaGraphLaunch(it->second, h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
+    if (st) {
+        // launches inside the graph: recompute from the plan
+        const PlanBits p = make_plan(k);
+        if (mode == MXP_F32)
+            st->launches += (n <= kSmallMax) ? 1 : 1 + p.len;
+        else
+            st->launches += 2 + p.len;
+    }
+    return MXP_OK;
+}
+
+}  // namespace
+
+// =====================================================================
+extern "C" {
+
+int mxp_version(int* major, int* minor) {
+    if (major) *major = 0;
+    if (minor) *minor = 1;
+    return MXP_OK;
+}
+
+const char* mxp_status_string(int status) {
+    switch (status) {
+        case MXP_OK: return "MXP_OK";
+        case MXP_E_VALIDATION: return "MXP_E_VALIDATION";
+        case MXP_E_UNSUPPORTED: return "MXP_E_UNSUPPORTED";
+        case MXP_E_DEVICE_UNAVAILABLE: return "MXP_E_DEVICE_UNAVAILABLE";
+        case MXP_E_CUDA: return "MXP_E_CUDA";
+        case MXP_E_NCCL: return "MXP_E_NCCL";
+        default: return "MXP_E_UNKNOWN";
+    }
+}
+
+int mxp_last_error(char* buf, size_t len) {
+    if (buf && len) {
+        std::strncpy(buf, g_err.c_str(), len - 1);
+        buf[len - 1] = '\0';
+    }
+    return MXP_OK;
+}
+
+int mxp_plan(int64_t k, char* steps, int64_t cap, int64_t* count) {
+    if (k < 0) return fail(MXP_E_VALIDATION, "power must be >= 0, got %lld", (long long)k);
+    const PlanBits p = make_plan(k);
+    for (int s = 0; s < p.len && s < cap; ++s) steps[s] = plan_is_mult(p, s) ? 'M' : 'S';
+    if (count) *count = p.len;
+    return MXP_OK;
+}
+
+int mxp_device_count(int* count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        if (count) *count = 0;
+        return fail(MXP_E_DEVICE_UNAVAILABLE, "no CUDA device: %s", cudaGetErrorString(e));
+    }
+    if (count) *count = c;
+    return MXP_OK;
+}
+
+int mxp_create(int device, mxp_handle* out) {
+    if (!out) return fail(MXP_E_VALIDATION, "null output pointer");
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        return fail(MXP_E_DEVICE_UNAVAILABLE, "no CUDA device available");
+    if (device < 0 || device >= count)
+        return fail(MXP_E_VALIDATION, "device %d out of range [0, %d)", device, count);
+    cudaDeviceProp prop;
+    MXP_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(MXP_E_DEVICE_UNAVAILABLE,
+                    "device %d is sm_%d%d; this build targets sm_100a (B200) only", device,
+                    prop.major, prop.minor);
+    MXP_CUDA(cudaSetDevice(device));
+    MXP_CUDA(prepare_kernels());
+    auto* h = new mxp_handle_s();
+    h->device = device;
+    h->num_sms = prop.multiProcessorCount;
+    cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->copy_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->copy_out, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
+    if (e != cudaSuccess) {
+        delete h;
+        return cuda_fail(e, "stream/event creation");
+    }
+    *out = h;
+    return MXP_OK;
+}
+
+int mxp_destroy(mxp_handle h) {
+    if (!h) return MXP_OK;
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->stream);
+    h->drop_graphs();
+    for (auto p : h->planes)
+        if (p) cudaFree(p);
+    for (auto p : h->f64buf)
+        if (p) cudaFree(p);
+    if (h->d_in) cudaFree(h->d_in);
+    if (h->d_in2) cudaFree(h->d_in2);
+    if (h->d_out) cudaFree(h->d_out);
+    cudaEventDestroy(h->ev0);
+    cudaEventDestroy(h->ev1);
+    cudaStreamDestroy(h->stream);
+    cudaStreamDestroy(h->copy_in);
+    cudaStreamDestroy(h->copy_out);
+    delete h;
+    return MXP_OK;
+}
+
+int mxp_get_stream(mxp_handle h, void** stream) {
+    if (!h || !stream) return fail(MXP_E_VALIDATION, "null argument");
+    *stream = h->stream;
+    return MXP_OK;
+}
+
+int mxp_num_sms(mxp_handle h, int* sms) {
+    if (!h || !sms) return fail(MXP_E_VALIDATION, "null argument");
+    *sms = h->num_sms;
+    return MXP_OK;
+}
+
+int mxp_synchronize(mxp_handle h) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    MXP_CUDA(cudaStreamSynchronize(h->stream));
+    return MXP_OK;
+}
+
+int mxp_alloc(mxp_handle h, size_t bytes, void** dptr) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (!dptr) return fail(MXP_E_VALIDATION, "null output pointer");
+    MXP_CUDA(cudaMalloc(dptr, bytes ? bytes : 16));
+    return MXP_OK;
+}
+
+int mxp_free(mxp_handle h, void* dptr) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    MXP_CUDA(cudaStreamSynchronize(h->stream));
+    MXP_CUDA(cudaFree(dptr));
+    return MXP_OK;
+}
+
+int mxp_host_alloc(mxp_handle h, size_t bytes, void** hptr) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (!hptr) return fail(MXP_E_VALIDATION, "null output pointer");
+    MXP_CUDA(cudaHostAlloc(hptr, bytes ? bytes : 16, cudaHostAllocPortable));
+    return MXP_OK;
+}
+
+int mxp_host_free(mxp_handle h, void* hptr) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    MXP_CUDA(cudaFreeHost(hptr));
+    return MXP_OK;
+}
+
+int mxp_upload(mxp_handle h, void* dst, const void* src, size_t bytes) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    MXP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream));
+    MXP_CUDA(cudaStreamSynchronize(h->stream));
+    return MXP_OK;
+}
+
+int mxp_download(mxp_handle h, void* dst, const void* src, size_t bytes) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    MXP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->stream));
+    MXP_CUDA(cudaStreamSynchronize(h->stream));
+    return MXP_OK;
+}
+
+int mxp_gemm(mxp_handle h, int mode, int64_t n, const void* dA, const void* dB, void* dC) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    rc = validate(mode, n, 2);
+    if (rc) return rc;
+    if (!dA || !dB || !dC) return fail(MXP_E_VALIDATION, "null device pointer");
+    if (mode == MXP_F32) {
+        const int64_t n_pad = round_up(n, 128);
+        rc = ensure_ws32(h, n_pad);
+        if (rc) return rc;
+        rc = encode_ws32(h, h->ws32_pad);
+        if (rc) return rc;
+        const int np = (int)h->ws32_pad;
+        cudaError_t e = launch_split(static_cast<const float*>(dA), (int)n, (int)n, h->planes[0],
+                                     h->planes[1], np, h->stream);
+        if (e == cudaSuccess)
+            e = launch_split(static_cast<const float*>(dB), (int)n, (int)n, h->planes[2],
+                             h->planes[3], np, h->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "split");
+        GemmPlanes m{h->map_a[0], h->map_a[1], h->map_b[2], h->map_b[3]};
+        e = launch_k1_gemm(m, np, k1_block_n(np, h->num_sms), static_cast<float*>(dC), (int)n,
+                           (int)n, nullptr, nullptr, h->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "k1_gemm_3xtf32");
+        return MXP_OK;
+    }
+    const int64_t n_pad = f64_pad((int)n);
+    rc = ensure_ws64(h, n_pad);
+    if (rc) return rc;
+    double** b = h->f64buf;
+    cudaError_t e = launch_f64_pad(static_cast<const double*>(dA), (int)n, b[0], (int)n_pad, h->stream);
+    if (e == cudaSuccess)
+        e = launch_f64_pad(static_cast<const double*>(dB), (int)n, b[1], (int)n_pad, h->stream);
+    if (e == cudaSuccess) e = launch_f64_gemm(b[0], b[1], b[2], (int)n_pad, h->stream);
+    if (e == cudaSuccess)
+        e = launch_f64_unpad(b[2], (int)n_pad, static_cast<double*>(dC), (int)n, h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "f64 gemm");
+    return MXP_OK;
+}
+
+int mxp_multiply(mxp_handle h, int mode, int64_t n, const void* hA, const void* hB, void* hC,
+                 mxp_stats* st) {
+    stats_reset(st);
+    int rc = check_handle(h);
+    if (rc) return rc;
+    rc = validate(mode, n, 2);
+    if (rc) return rc;
+    if (!hA || !hB || !hC) return fail(MXP_E_VALIDATION, "null host pointer");
+    const size_t bytes = static_cast<size_t>(n) * n * elem_size(mode);
+    rc = ensure_io(h, bytes);
+    if (rc) return rc;
+    MXP_CUDA(cudaMemcpyAsync(h->d_in, hA, bytes, cudaMemcpyHostToDevice, h->stream));
+    MXP_CUDA(cudaMemcpyAsync(h->d_in2, hB, bytes, cudaMemcpyHostToDevice, h->stream));
+    MXP_CUDA(cudaEventRecord(h->ev0, h->stream));
+    rc = mxp_gemm(h, mode, n, h->d_in, h->d_in2, h->d_out);
+    if (rc) return rc;
+    MXP_CUDA(cudaEventRecord(h->ev1, h->stream));
+    MXP_CUDA(cudaMemcpyAsync(hC, h->d_out, bytes, cudaMemcpyDeviceToHost, h->stream));
+    MXP_CUDA(cudaStreamSynchronize(h->stream));
+    if (st) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+        st->device_ms = ms;
+        st->multiply_count = 1;
+        st->launches = (mode == MXP_F32) ? 3 : 4;
+        st->h2d = 2;
+        st->d2h = 1;
+        st->h2d_bytes = 2 * bytes;
+        st->d2h_bytes = bytes;
+    }
+    return MXP_OK;
+}
+
+int mxp_power_device(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA, void* dOut,
+                     mxp_stats* st) {
+    stats_reset(st);
+    int rc = check_handle(h);
+    if (rc) return rc;
+    rc = validate(mode, n, k);
+    if (rc) return rc;
+    if (!dA || !dOut) return fail(MXP_E_VALIDATION, "null device pointer");
+    fill_plan_stats(st, k, 1);
+    if (k <= 1) {
+        int64_t launches = 0;
+        rc = enqueue_trivial(h, mode, n, k, dA, dOut, 1, &launches);
+        if (st) st->launches = launches;
+        return rc;
+    }
+    return run_power_graph(h, mode, n, k, dA, dOut, st);
+}
+
+int mxp_power(mxp_handle h, int mode, int64_t n, int64_t k, const void* hA, void* hOut,
+              mxp_stats* st) {
+    stats_reset(st);
+    int rc = check_handle(h);
+    if (rc) return rc;
+    rc = validate(mode, n, k);
+    if (rc) return rc;
+    if (!hA || !hOut) return fail(MXP_E_VALIDATION, "null host pointer");
+    const size_t bytes = static_cast<size_t>(n) * n * elem_size(mode);
+    rc = ensure_io(h, bytes);
+    if (rc) return rc;
+    MXP_CUDA(cudaMemcpyAsync(h->d_in, hA, bytes, cudaMemcpyHostToDevice, h->stream));
+    MXP_CUDA(cudaEventRecord(h->ev0, h->stream));
+    mxp_stats inner;
+    rc = mxp_power_device(h, mode, n, k, h->d_in, h->d_out, &inner);
+    if (rc) {
+        if (st) st->failed_step = inner.failed_step;
+        return rc;
+    }
+    MXP_CUDA(cudaEventRecord(h->ev1, h->stream));
+    MXP_CUDA(cudaMemcpyAsync(hOut, h->d_out, bytes, cudaMemcpyDeviceToHost, h->stream));
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) {
+        if (st) st->failed_step = 0;
+        return cuda_fail(e, "power chain");
+    }
+    if (st) {
+        *st = inner;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+        st->device_ms = ms;
+        st->h2d = 1;
+        st->d2h = 1;
+        st->h2d_bytes = bytes;
+        st->d2h_bytes = bytes;
+    }
+    return MXP_OK;
+}
+
+int mxp_power_batched_device(mxp_handle h, int mode, int64_t n, int64_t batch, int64_t k,
+                             const void* dA, void* dOut, mxp_stats* st) {
+    stats_reset(st);
+    int rc = check_handle(h);
+    if (rc) return rc;
+    rc = validate(mode, n, k);
+    if (rc) return rc;
+    if (batch < 0) return fail(MXP_E_VALIDATION, "batch must be >= 0, got %lld", (long long)batch);
+    if (batch == 0) return MXP_OK;
+    if (!dA || !dOut) return fail(MXP_E_VALIDATION, "null device pointer");
+    fill_plan_stats(st, k, batch);
+    int64_t launches = 0, failed = -1;
+    if (k <= 1) {
+        rc = enqueue_trivial(h, mode, n, k, dA, dOut, batch, &launches);
+        if (st) st->launches = launches;
+        return rc;
+    }
+    if (mode == MXP_F32 && n <= kSmallMax) {
+        cudaError_t e = launch_k3_batched(static_cast<const float*>(dA), static_cast<float*>(dOut),
+                                          (int)n, batch, make_plan(k), h->num_sms, h->stream);
+        if (e != cudaSuccess) {
+            if (st) st->failed_step = 0;
+            return cuda_fail(e, "k3_batched_power");
+        }
+        if (st) st->launches = 1;
+        return MXP_OK;
+    }
+    // n > 128 (or fp64): one chain per matrix, enqueued back to back.
+    const size_t bytes = static_cast<size_t>(n) * n * elem_size(mode);
+    for (int64_t b = 0; b < batch; ++b) {
+        rc = enqueue_power(h, mode, n, k, static_cast<const char*>(dA) + b * bytes,
+                           static_cast<char*>(dOut) + b * bytes, &launches, &failed);
+        if (rc) {
+            if (st) st->failed_step = failed;
+            return rc;
+        }
+    }
+    if (st) st->launches = launches;
+    return MXP_OK;
+}
+
+int mxp_power_batched(mxp_handle h, int mode, int64_t n, int64_t batch, int64_t k,
+                      const void* hA, void* hOut, mxp_stats* st) {
+    stats_reset(st);
+    int rc = check_handle(h);
+    if (rc) return rc;
+    rc = validate(mode, n, k);
+    if (rc) return rc;
+    if (batch < 0) return fail(MXP_E_VALIDATION, "batch must be >= 0, got %lld", (long long)batch);
+    if (batch == 0) return MXP_OK;
+    if (!hA || !hOut) return fail(MXP_E_VALIDATION, "null host pointer");
+    const size_t mat = static_cast<size_t>(n) * n * elem_size(mode);
+    // Pipeline in chunks: H2D (copy_in) | compute (stream) | D2H (copy_out),
+    // double-buffered, so PCIe in both directions overlaps the tensor cores.
+    const size_t chunk_target = size_t(256) << 20;
+    int64_t chunk = static_cast<int64_t>(chunk_target / mat);
+    if (chunk < 1) chunk = 1;
+    if (chunk > batch) chunk = batch;
+    const size_t chunk_bytes = static_cast<size_t>(chunk) * mat;
+    rc = ensure_io(h, 2 * chunk_bytes);  // d_in/d_out hold two chunk slots each
+    if (rc) return rc;
+    cudaEvent_t in_ready[2], comp_done[2], out_done[2];
+    for (int i = 0; i < 2; ++i) {
+        MXP_CUDA(cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming));
+        MXP_CUDA(cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming));
+        MXP_CUDA(cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming));
+    }
+    MXP_CUDA(cudaEventRecord(h->ev0, h->stream));
+    int64_t launches = 0;
+    int slot = 0;
+    bool used[2] = {false, false};
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk, slot ^= 1) {
+        const int64_t nb = (b0 + chunk <= batch) ? chunk : batch - b0;
+        const size_t nbytes = static_cast<size_t>(nb) * mat;
+        char* din = static_cast<char*>(h->d_in) + slot * chunk_bytes;
+        char* dout = static_cast<char*>(h->d_out) + slot * chunk_bytes;
+        if (used[slot]) MXP_CUDA(cudaStreamWaitEvent(h->copy_in, comp_done[slot], 0));
+        MXP_CUDA(cudaMemcpyAsync(din, static_cast<const char*>(hA) + b0 * mat, nbytes,
+                                 cudaMemcpyHostToDevice, h->copy_in));
+        MXP_CUDA(cudaEventRecord(in_ready[slot], h->copy_in));
+        MXP_CUDA(cudaStreamWaitEvent(h->stream, in_ready[slot], 0));
+        if (used[slot]) MXP_CUDA(cudaStreamWaitEvent(h->stream, out_done[slot], 0));
+        mxp_stats inner;
+        rc = mxp_power_batched_device(h, mode, n, nb, k, din, dout, &inner);
+        if (rc) {
+            if (st) st->failed_step = inner.failed_step;
+            return rc;
+        }
+        launches += inner.launches;
+        MXP_CUDA(cudaEventRecord(comp_done[slot], h->stream));
+        MXP_CUDA(cudaStreamWaitEvent(h->copy_out, comp_done[slot], 0));
+        MXP_CUDA(cudaMemcpyAsync(static_cast<char*>(hOut) + b0 * mat, dout, nbytes,
+                                 cudaMemcpyDeviceToHost, h->copy_out));
+        MXP_CUDA(cudaEventRecord(out_done[slot], h->copy_out));
+        used[slot] = true;
+    }
+    MXP_CUDA(cudaStreamWaitEvent(h->stream, out_done[0], 0));
+    if (used[1]) MXP_CUDA(cudaStreamWaitEvent(h->stream, out_done[1], 0));
+    MXP_CUDA(cudaEventRecord(h->ev1, h->stream));
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(in_ready[i]);
+        cudaEventDestroy(comp_done[i]);
+        cudaEventDestroy(out_done[i]);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "batched power");
+    if (st) {
+        fill_plan_stats(st, k, batch);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+        st->device_ms = ms;
+        st->launches = launches;
+        st->h2d = 1;
+        st->d2h = 1;
+        st->h2d_bytes = static_cast<int64_t>(batch * mat);
+        st->d2h_bytes = static_cast<int64_t>(batch * mat);
+    }
+    return MXP_OK;
+}
+
+int mxp_random_device(mxp_handle h, int mode, int64_t n, int64_t batch, uint64_t seed0,
+                      double lo, double hi, double scale, void* dOut) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (mode != MXP_F32 && mode != MXP_F64)
+        return fail(MXP_E_VALIDATION, "unknown element mode %d", mode);
+    if (n < 1) return fail(MXP_E_VALIDATION, "matrix order must be >= 1, got %lld", (long long)n);
+    if (!(lo < hi)) return fail(MXP_E_VALIDATION, "need lo < hi, got [%g, %g)", lo, hi);
+    if (batch < 0 || !dOut) return fail(MXP_E_VALIDATION, "bad batch or null pointer");
+    if (batch == 0) return MXP_OK;
+    cudaError_t e = launch_random(mode, n, batch, seed0, lo, hi, scale, dOut, h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "random_kernel");
+    return MXP_OK;
+}
+
+int mxp_power_mod_device(mxp_handle h, int64_t n, int64_t k, uint32_t p, const void* dA,
+                         void* dOut, mxp_stats* st) {
+    stats_reset(st);
+    (void)h; (void)n; (void)k; (void)p; (void)dA; (void)dOut;
+    return fail(MXP_E_UNSUPPORTED, "modular mode is not built into this library yet");
+}
+
+int mxp_power_mod(mxp_handle h, int64_t n, int64_t k, uint32_t p, const void* hA, void* hOut,
+                  mxp_stats* st) {
+    stats_reset(st);
+    (void)h; (void)n; (void)k; (void)p; (void)hA; (void)hOut;
+    return fail(MXP_E_UNSUPPORTED, "modular mode is not built into this library yet");
+}
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+// Internal launch interface between the C-ABI shim (mxp_api.cu) and the
+// sm_100a kernels.  Not exported.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace mxp {
+
+// Square-and-multiply plan (expo.py:60-75) as a bitmask: bit s set means step
+// s is MULTIPLY_BASE, clear means SQUARE.  At most 126 steps (k < 2^63).
+struct PlanBits {
+    int32_t len;
+    int32_t squares;
+    uint64_t mult[2];
+};
+PlanBits make_plan(int64_t k);
+__host__ __device__ inline bool plan_is_mult(const PlanBits& p, int s) {
+    return (p.mult[s >> 6] >> (s & 63)) & 1ull;
+}
+
+// Set shared-memory attributes of every kernel on the current device (once
+// per device, before any launch or graph capture).
+cudaError_t prepare_kernels();
+
+// ---- 3xTF32 kernels (kernels_tf32.cu) ------------------------------------
+// K3: persistent batched chain for n <= 128, each CTA owns one matrix at a
+// time with the running power resident in shared memory.
+constexpr int kSmallMax = 128;
+size_t k3_smem_bytes();
+cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
+                              const PlanBits& plan, int grid, cudaStream_t s);
+
+// fp32 (n x n, leading dim ld) -> tf32 hi/lo planes (n_pad x n_pad, zero pad).
+cudaError_t launch_split(const float* in, int n, int ld, uint32_t* hi, uint32_t* lo, int n_pad,
+                         cudaStream_t s);
+// identity (k = 0) into an n x n fp32 / fp64 buffer
+cudaError_t launch_identity_f32(float* out, int n, cudaStream_t s);
+cudaError_t launch_identity_f64(double* out, int n, cudaStream_t s);
+
+// K1: one 3xTF32 GEMM C = A * B over hi/lo planes (n_pad multiple of 128).
+// Writes the product as hi/lo planes (out_hi/out_lo, may be null) and/or as
+// fp32 into out_f32 (n_out x n_out, leading dim ld_out; may be null).
+struct GemmPlanes {
+    CUtensorMap a_hi, a_lo;  // box {32, 128}, SWIZZLE_128B (K-major left operand)
+    CUtensorMap b_hi, b_lo;  // box {32, 32}, SWIZZLE_128B_ATOM_32B (MN-major right operand)
+};
+bool encode_plane_map(CUtensorMap* map, const void* plane, int n_pad, int box_cols, int box_rows,
+                      bool right_operand);
+int k1_block_n(int n_pad, int num_sms);
+cudaError_t launch_k1_gemm(const GemmPlanes& maps, int n_pad, int block_n, float* out_f32,
+                           int n_out, int ld_out, uint32_t* out_hi, uint32_t* out_lo,
+                           cudaStream_t s);
+
+// ---- generation (kernels_gen.cu) -------------------------------------------
+// Reference random_matrix (linalg.py:127-148) on device; scale != 0 selects
+// the scaled recipe fl(random_matrix(n, F64, seed, lo, hi) * scale).
+// Matrix b of the batch uses seed seed0 + b.
+cudaError_t launch_random(int mode, int64_t n, int64_t batch, uint64_t seed0, double lo, double hi,
+                          double scale, void* out, cudaStream_t s);
+
+// ---- FP64 (kernels_f64.cu) ------------------------------------------------
+cudaError_t launch_f64_gemm(const double* a, const double* b, double* c, int n, cudaStream_t s);
+cudaError_t launch_f64_pad(const double* in, int n, double* out, int n_pad, cudaStream_t s);
+cudaError_t launch_f64_unpad(const double* in, int n_pad, double* out, int n, cudaStream_t s);
+int f64_pad(int n);
+
+}  // namespace mxp

@@ -1,0 +1,255 @@
+"""B200 engine: a thin, typed wrapper over the C ABI (include/matexpo_b200.h).
+
+One `Engine` = one device handle = one CUDA stream + workspace + graph cache
+(the reference's "one device instance is one serialized queue",
+gpu-backend/src/device.ts:6-8).  Host-array entry points copy in once and
+out once; the `*_device` entry points take raw device pointers (e.g. from
+torch tensors) and enqueue asynchronously on the engine's stream.
+
+Every call goes to hand-written sm_100a kernels; if the extension is not
+built or no B200 is present the call raises — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from . import errors as E
+
+_MODES = {np.dtype(np.float32): _lib.MXP_F32, np.dtype(np.float64): _lib.MXP_F64}
+
+
+def _mode_of(arr: np.ndarray) -> int:
+    try:
+        return _MODES[arr.dtype]
+    except KeyError:
+        raise E.ShapeError(f"unsupported element dtype {arr.dtype}") from None
+
+
+def _ptr(arr: np.ndarray) -> ctypes.c_void_p:
+    return ctypes.c_void_p(arr.ctypes.data)
+
+
+class Engine:
+    """A device handle.  Use one Engine per thread (or guard it)."""
+
+    def __init__(self, device: int = 0):
+        L = _lib.load()
+        h = ctypes.c_void_p()
+        _lib.check(L.mxp_create(int(device), ctypes.byref(h)), "mxp_create")
+        self._L = L
+        self._h = h
+        self.device = int(device)
+        self.last_stats = _lib.Stats()
+        self._lock = threading.Lock()
+
+    # ------------------------------------------------------------ lifecycle
+    def close(self) -> None:
+        if self._h:
+            self._L.mxp_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    @property
+    def stream(self) -> int:
+        """The engine's cudaStream_t as an integer (for torch.cuda.ExternalStream)."""
+        s = ctypes.c_void_p()
+        _lib.check(self._L.mxp_get_stream(self._h, ctypes.byref(s)), "mxp_get_stream")
+        return int(s.value or 0)
+
+    @property
+    def num_sms(self) -> int:
+        v = ctypes.c_int()
+        _lib.check(self._L.mxp_num_sms(self._h, ctypes.byref(v)), "mxp_num_sms")
+        return v.value
+
+    def synchronize(self) -> None:
+        _lib.check(self._L.mxp_synchronize(self._h), "mxp_synchronize")
+
+    # ------------------------------------------------------------ errors
+    def _raise_chain(self, status: int, stats: _lib.Stats, plan: str, what: str) -> None:
+        """Map a failed chain to BackendStepError (errors.py:43-49) when the
+        failing plan step is known, else to the status' exception."""
+        if status == _lib.MXP_OK:
+            return
+        step = stats.failed_step
+        if status in (_lib.MXP_E_CUDA, _lib.MXP_E_NCCL) and 0 <= step < len(plan):
+            name = "SQUARE" if plan[step] == "S" else "MULTIPLY_BASE"
+            cause = E.DeviceError(_lib.last_error())
+            raise E.BackendStepError(step, name, cause) from cause
+        _lib.check(status, what)
+
+    # ------------------------------------------------------------ host API
+    def power(self, a: np.ndarray, k: int) -> np.ndarray:
+        """A^k for one n x n float32/float64 array (one upload, one readback)."""
+        a = np.ascontiguousarray(a)
+        if a.ndim != 2 or a.shape[0] != a.shape[1]:
+            raise E.ShapeError(f"expected a square 2-D array, got shape {a.shape}")
+        mode = _mode_of(a)
+        out = np.empty_like(a)
+        st = _lib.Stats()
+        rc = self._L.mxp_power(self._h, mode, a.shape[0], int(k), _ptr(a), _ptr(out),
+                               ctypes.byref(st))
+        self.last_stats = st
+        self._raise_chain(rc, st, plan_string(k) if k >= 0 else "", "mxp_power")
+        return out
+
+    def power_batched(self, a: np.ndarray, k: int, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """A_i^k for a (batch, n, n) stack; chunked H2D | compute | D2H pipeline."""
+        a = np.ascontiguousarray(a)
+        if a.ndim != 3 or a.shape[1] != a.shape[2]:
+            raise E.ShapeError(f"expected a (batch, n, n) array, got shape {a.shape}")
+        mode = _mode_of(a)
+        if out is None:
+            out = np.empty_like(a)
+        st = _lib.Stats()
+        rc = self._L.mxp_power_batched(self._h, mode, a.shape[1], a.shape[0], int(k), _ptr(a),
+                                       _ptr(out), ctypes.byref(st))
+        self.last_stats = st
+        self._raise_chain(rc, st, plan_string(k) if k >= 0 else "", "mxp_power_batched")
+        return out
+
+    def multiply(self, a: np.ndarray, b: np.ndarray) -> np.ndarray:
+        """C = A * B (one product; 2 uploads + 1 readback like gpuMatmul, host.ts:67-95)."""
+        a = np.ascontiguousarray(a)
+        b = np.ascontiguousarray(b)
+        if a.shape != b.shape:
+            raise E.ShapeError(f"matrix orders differ: {a.shape[0]} vs {b.shape[0]}")
+        if a.dtype != b.dtype:
+            raise E.ShapeError(f"matrix dtypes differ: {a.dtype} vs {b.dtype}")
+        mode = _mode_of(a)
+        out = np.empty_like(a)
+        st = _lib.Stats()
+        rc = self._L.mxp_multiply(self._h, mode, a.shape[0], _ptr(a), _ptr(b), _ptr(out),
+                                  ctypes.byref(st))
+        self.last_stats = st
+        _lib.check(rc, "mxp_multiply")
+        return out
+
+    def power_mod(self, a: np.ndarray, k: int, p: int) -> np.ndarray:
+        """(A^k) mod p, exact, uint32 residues."""
+        a = np.ascontiguousarray(a, dtype=np.uint32)
+        out = np.empty_like(a)
+        st = _lib.Stats()
+        rc = self._L.mxp_power_mod(self._h, a.shape[0], int(k), int(p), _ptr(a), _ptr(out),
+                                   ctypes.byref(st))
+        self.last_stats = st
+        self._raise_chain(rc, st, plan_string(k) if k >= 0 else "", "mxp_power_mod")
+        return out
+
+    # ------------------------------------------------------------ device API
+    def power_device(self, d_in: int, d_out: int, n: int, k: int, mode: int = _lib.MXP_F32) -> None:
+        st = _lib.Stats()
+        rc = self._L.mxp_power_device(self._h, mode, n, k, ctypes.c_void_p(d_in),
+                                      ctypes.c_void_p(d_out), ctypes.byref(st))
+        self.last_stats = st
+        self._raise_chain(rc, st, plan_string(k) if k >= 0 else "", "mxp_power_device")
+
+    def power_batched_device(self, d_in: int, d_out: int, n: int, batch: int, k: int,
+                             mode: int = _lib.MXP_F32) -> None:
+        st = _lib.Stats()
+        rc = self._L.mxp_power_batched_device(self._h, mode, n, batch, k, ctypes.c_void_p(d_in),
+                                              ctypes.c_void_p(d_out), ctypes.byref(st))
+        self.last_stats = st
+        self._raise_chain(rc, st, plan_string(k) if k >= 0 else "", "mxp_power_batched_device")
+
+    def power_mod_device(self, d_in: int, d_out: int, n: int, k: int, p: int) -> None:
+        st = _lib.Stats()
+        rc = self._L.mxp_power_mod_device(self._h, n, k, p, ctypes.c_void_p(d_in),
+                                          ctypes.c_void_p(d_out), ctypes.byref(st))
+        self.last_stats = st
+        self._raise_chain(rc, st, plan_string(k) if k >= 0 else "", "mxp_power_mod_device")
+
+    def gemm_device(self, d_a: int, d_b: int, d_c: int, n: int, mode: int = _lib.MXP_F32) -> None:
+        _lib.check(self._L.mxp_gemm(self._h, mode, n, ctypes.c_void_p(d_a), ctypes.c_void_p(d_b),
+                                    ctypes.c_void_p(d_c)), "mxp_gemm")
+
+    def random_device(self, d_out: int, n: int, batch: int = 1, seed0: int = 0,
+                      lo: float = -0.5, hi: float = 0.5, scale: float = 0.0,
+                      mode: int = _lib.MXP_F32) -> None:
+        _lib.check(self._L.mxp_random_device(self._h, mode, n, batch,
+                                             ctypes.c_uint64(seed0 & (2**64 - 1)), lo, hi, scale,
+                                             ctypes.c_void_p(d_out)), "mxp_random_device")
+
+    # ------------------------------------------------------------ memory
+    def alloc(self, nbytes: int) -> int:
+        p = ctypes.c_void_p()
+        _lib.check(self._L.mxp_alloc(self._h, nbytes, ctypes.byref(p)), "mxp_alloc")
+        return int(p.value)
+
+    def free(self, ptr: int) -> None:
+        _lib.check(self._L.mxp_free(self._h, ctypes.c_void_p(ptr)), "mxp_free")
+
+    def host_alloc(self, nbytes: int) -> int:
+        p = ctypes.c_void_p()
+        _lib.check(self._L.mxp_host_alloc(self._h, nbytes, ctypes.byref(p)), "mxp_host_alloc")
+        return int(p.value)
+
+    def host_free(self, ptr: int) -> None:
+        _lib.check(self._L.mxp_host_free(self._h, ctypes.c_void_p(ptr)), "mxp_host_free")
+
+    def pinned_array(self, shape, dtype) -> np.ndarray:
+        """A numpy view of freshly allocated pinned host memory (freed with the engine
+        process; call host_free(arr.ctypes.data) to release early)."""
+        dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dtype.itemsize
+        ptr = self.host_alloc(nbytes)
+        buf = (ctypes.c_char * nbytes).from_address(ptr)
+        return np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def upload(self, d_dst: int, host: np.ndarray) -> None:
+        host = np.ascontiguousarray(host)
+        _lib.check(self._L.mxp_upload(self._h, ctypes.c_void_p(d_dst), _ptr(host), host.nbytes),
+                   "mxp_upload")
+
+    def download(self, host: np.ndarray, d_src: int) -> np.ndarray:
+        _lib.check(self._L.mxp_download(self._h, _ptr(host), ctypes.c_void_p(d_src), host.nbytes),
+                   "mxp_download")
+        return host
+
+
+def plan_string(k: int) -> str:
+    """The plan as 'S'/'M' characters, from the C ABI (expo.py:60-75)."""
+    L = _lib.load()
+    buf = ctypes.create_string_buffer(256)
+    cnt = ctypes.c_int64()
+    _lib.check(L.mxp_plan(int(k), buf, 256, ctypes.byref(cnt)), "mxp_plan")
+    return buf.raw[: cnt.value].decode()
+
+
+_engines: dict = {}
+_engines_lock = threading.Lock()
+
+
+def default_engine(device: Optional[int] = None) -> Engine:
+    """Per-(thread, device) engine, created lazily."""
+    if device is None:
+        device = 0
+    key = (threading.get_ident(), device)
+    with _engines_lock:
+        eng = _engines.get(key)
+        if eng is None:
+            eng = Engine(device)
+            _engines[key] = eng
+        return eng
+
+
+def device_count() -> int:
+    L = _lib.load()
+    c = ctypes.c_int()
+    rc = L.mxp_device_count(ctypes.byref(c))
+    return c.value if rc == _lib.MXP_OK else 0

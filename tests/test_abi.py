@@ -1,0 +1,94 @@
+"""The C-ABI library loads here (no GPU) and exports every symbol the header
+declares; host-side entry points that need no device behave like the reference."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_1204_3052_b200 import _lib, build
+import paper_1204_3052_b200 as mx
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "matexpo_b200.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return _lib.load()
+
+
+def header_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"MXP_API\s+[\w\s\*]+?\b(mxp_\w+)\s*\(", text)))
+
+
+def test_header_symbols_exported(lib):
+    syms = header_symbols()
+    assert len(syms) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (mxp_\w+)", out))
+    assert set(syms) <= exported, set(syms) - exported
+    assert set(syms) == set(_lib.EXPORTS)
+    for s in syms:
+        assert hasattr(lib, s)
+
+
+def test_only_abi_symbols_exported(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    text_syms = set(re.findall(r" T (\w+)", out))
+    assert all(s.startswith("mxp_") for s in text_syms), text_syms
+
+
+def test_plan_through_abi(lib):
+    for k in list(range(0, 300)) + [1000, 1024, 257, 2**40 + 5, 2**62 + 2**61 + 1]:
+        assert mx.engine.plan_string(k) == mx.plan_exponentiation(k).as_string(), k
+    buf = ctypes.create_string_buffer(8)
+    cnt = ctypes.c_int64()
+    assert lib.mxp_plan(-1, buf, 8, ctypes.byref(cnt)) == _lib.MXP_E_VALIDATION
+    assert "power must be >= 0" in _lib.last_error()
+
+
+def test_status_strings(lib):
+    assert lib.mxp_status_string(0) == b"MXP_OK"
+    assert lib.mxp_status_string(_lib.MXP_E_CUDA) == b"MXP_E_CUDA"
+    major, minor = ctypes.c_int(), ctypes.c_int()
+    assert lib.mxp_version(ctypes.byref(major), ctypes.byref(minor)) == 0
+
+
+def test_no_device_is_reported_not_faked(lib):
+    """Without a GPU the engine refuses loudly (no CPU fallback)."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    h = ctypes.c_void_p()
+    assert lib.mxp_create(0, ctypes.byref(h)) == _lib.MXP_E_DEVICE_UNAVAILABLE
+    with pytest.raises(mx.DeviceUnavailableError):
+        mx.Engine(0)
+    with pytest.raises(mx.DeviceUnavailableError):
+        mx.exponentiate(mx.Matrix([[1.0, 1.0], [1.0, 0.0]]), 10, mx.b200_backend())
+
+
+def test_null_handle_validation(lib):
+    st = _lib.Stats()
+    rc = lib.mxp_power(None, 0, 4, 3, None, None, ctypes.byref(st))
+    assert rc == _lib.MXP_E_VALIDATION
+
+
+def test_sass_uses_tcgen05_and_dmma(lib):
+    """The built cubins really contain tcgen05 MMAs (UTCHMMA), TMA loads,
+    TMEM loads and DMMA — i.e. the tensor-core paths are what ships."""
+    res = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True)
+    if res.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    sass = res.stdout
+    assert re.search(r"UTC\w*MMA", sass)
+    assert "UTMALDG" in sass
+    assert "LDTM" in sass
+    assert "DMMA" in sass

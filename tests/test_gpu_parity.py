@@ -1,0 +1,292 @@
+"""GPU parity: the sm_100a engine (through the C ABI) against the CPU oracle
+and the reference's golden fixtures.  Run on a B200 (`pytest -m gpu`).
+
+Tolerances (written here, derived in SURVEY §8(d) / DESIGN.md):
+* one multiply: max_rel <= n * u * 64  (reference device_tol, tolerances.py:316-319)
+* A^k chains:   frobenius_rel <= 16 * m(k) * sqrt(n) * u  (m(k) = multiply count)
+* exact inputs (Fibonacci, permutations): bitwise.
+"""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1204_3052_b200 as mx
+from paper_1204_3052_b200 import _lib
+from paper_1204_3052_b200.engine import Engine
+
+pytestmark = pytest.mark.gpu
+
+U32 = 2.0 ** -24
+U64 = 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def eng():
+    e = Engine(0)
+    yield e
+    e.close()
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def fro(res, ref):
+    return oracle.compare(res, ref)[2]
+
+
+# ------------------------------------------------------------------ generation
+def test_device_random_matrix_bitexact(golden):
+    arrays, meta = golden
+    for key in arrays.files:
+        if not key.startswith("rm_"):
+            continue
+        _, n, dt, seed, lo, hi = key.split("_")
+        dtype = mx.DType.F32 if dt == "f32" else mx.DType.F64
+        got = mx.random_matrix(int(n), dtype, int(seed), float(lo), float(hi)).array
+        assert got.tobytes() == arrays[key].tobytes(), key
+    for key, digest in meta["random_matrix_sha256"].items():
+        n, dt, seed = key.split("_")
+        dtype = mx.DType.F32 if dt == "f32" else mx.DType.F64
+        assert sha(mx.random_matrix(int(n), dtype, int(seed)).array) == digest, key
+
+
+def test_device_scaled_recipe_bitexact(golden):
+    _, meta = golden
+    for key, digest in meta["scaled_sha256"].items():
+        n, dt, seed = key.split("_")
+        dtype = mx.DType.F32 if dt == "f32" else mx.DType.F64
+        assert sha(mx.scaled_input(int(n), dtype, int(seed)).array) == digest, key
+    stack = mx.scaled_batch(128, 3, mx.DType.F32, 42)
+    for i in range(3):
+        assert stack[i].tobytes() == oracle.scaled_input(128, np.float32, 42 + i).tobytes()
+
+
+# ------------------------------------------------------------------ one multiply
+@pytest.mark.parametrize("n", [1, 7, 64, 128, 200, 256, 384, 512, 1024])
+def test_multiply_f32_device_tol(eng, n):
+    a = oracle.random_matrix(n, np.float32, 1000 + n)
+    b = oracle.random_matrix(n, np.float32, 2000 + n)
+    got = eng.multiply(a, b)
+    ref = oracle.matmul(a, b)
+    _, max_rel, _ = oracle.compare(got, ref)
+    assert max_rel <= n * U32 * 64, (n, max_rel)
+    st = eng.last_stats
+    assert st.multiply_count == 1 and st.h2d == 2 and st.d2h == 1
+
+
+@pytest.mark.parametrize("n", [1, 5, 64, 200, 256])
+def test_multiply_f64_device_tol(eng, n):
+    a = oracle.random_matrix(n, np.float64, 1000 + n)
+    b = oracle.random_matrix(n, np.float64, 2000 + n)
+    got = eng.multiply(a, b)
+    ref = oracle.matmul(a, b)
+    assert oracle.compare(got, ref)[1] <= n * U64 * 64
+
+
+def test_multiply_identity_within_rounding(eng):
+    """host.test.ts:92-100: A*I within n*2^-24*max|A|."""
+    n = 32
+    a = oracle.random_matrix(n, np.float32, 77)
+    got = eng.multiply(a, np.eye(n, dtype=np.float32))
+    assert np.abs(got - a).max() <= n * U32 * np.abs(a).max()
+
+
+# ------------------------------------------------------------------ chains vs golden
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 64])
+def test_exponentiate_vs_reference_golden(golden, dt, n):
+    arrays, _ = golden
+    dtype = mx.DType.F32 if dt == "f32" else mx.DType.F64
+    u = dtype.roundoff
+    a = mx.Matrix(arrays[f"in_{n}_{dt}"])
+    for k in (0, 1, 2, 3, 7, 13, 16, 64):
+        got = mx.exponentiate(a, k, mx.b200_backend())
+        ref = arrays[f"exp_{n}_{dt}_{k}"]
+        if k <= 1:
+            assert got.array.tobytes() == ref.tobytes(), (n, dt, k)
+            continue
+        tol = 16 * mx.multiply_count(k) * math.sqrt(n) * u
+        assert fro(got.array, ref) <= tol, (n, dt, k, fro(got.array, ref), tol)
+
+
+def test_power_one_returns_same_object_and_zero_multiplies(eng):
+    a = mx.Matrix(oracle.random_matrix(32, np.float32, 6))
+    assert mx.exponentiate(a, 1, mx.b200_backend()) is a
+    out = eng.power(a.array, 1)
+    assert out.tobytes() == a.array.tobytes()
+    assert eng.last_stats.multiply_count == 0 and eng.last_stats.launches == 0
+    assert eng.last_stats.h2d == 1 and eng.last_stats.d2h == 1
+
+
+def test_power_zero_is_identity(eng):
+    for dt in (np.float32, np.float64):
+        out = eng.power(oracle.random_matrix(7, dt, 1), 0)
+        assert np.array_equal(out, np.eye(7, dtype=dt))
+
+
+def test_fibonacci_exact_through_device_chain(golden):
+    """host.test.ts:157-171 (4x4 block-embedded, f32) and the f64 KATs."""
+    arrays, _ = golden
+    q = np.zeros((4, 4), dtype=np.float32)
+    q[:2, :2] = [[1, 1], [1, 0]]
+    q[2, 2] = q[3, 3] = 1
+    eng = mx.Engine(0)
+    got = eng.power(q, 10)
+    assert got[0, 0] == 89 and got[0, 1] == 55 and got[1, 0] == 55 and got[1, 1] == 34
+    assert eng.last_stats.multiply_count == 4
+    q64 = np.array([[1.0, 1.0], [1.0, 0.0]])
+    for k in (10, 40, 78):
+        assert np.array_equal(eng.power(q64, k), arrays[f"fib_f64_{k}"]), k
+    # F_40 < 2^24: exact in f32 too (3xTF32 splits small integers exactly)
+    assert np.array_equal(eng.power(q64.astype(np.float32), 30), oracle.exponentiate(
+        q64.astype(np.float32), 30))
+
+
+def test_well_conditioned_chain_vs_f64_repeated(golden):
+    """host.test.ts:173-184: n=64, k=64, maxRel <= k*n*2^-24*64, 6 multiplies."""
+    arrays, _ = golden
+    eng = mx.Engine(0)
+    got = eng.power(arrays["wc_in_64_f32"], 64)
+    rel = oracle.compare(got, arrays["wc_rep64_64_f64"])[1]
+    assert np.isfinite(rel) and rel <= 64 * 64 * U32 * 64
+    assert eng.last_stats.multiply_count == 6
+
+
+def test_transfer_and_count_laws(eng):
+    a = oracle.random_matrix(16, np.float32, 3) * np.float32(0.2)
+    for k in (1, 2, 13, 1024):
+        eng.power(a, k)
+        st = eng.last_stats
+        assert st.h2d == 1 and st.d2h == 1
+        assert st.multiply_count == mx.multiply_count(k)
+
+
+def test_validation_before_device_work(eng):
+    with pytest.raises(ValueError):
+        eng.power(np.zeros((4, 4), np.float32), -1)
+    with pytest.raises(ValueError):
+        eng.multiply(np.zeros((4, 4), np.float32), np.zeros((5, 5), np.float32))
+    with pytest.raises(ValueError):
+        eng.multiply(np.zeros((4, 4), np.float32), np.zeros((4, 4), np.float64))
+    with pytest.raises(mx.ShapeError):
+        eng.power(np.zeros((4, 4), np.int64), 3)
+
+
+def test_backend_interop_and_counting():
+    be = mx.CountingBackend(mx.b200_backend())
+    a = mx.Matrix(oracle.scaled_input(64, np.float32, 42))
+    out = mx.exponentiate(a, 13, be)
+    assert be.calls == 5
+    ref = oracle.exponentiate(a.array, 13)
+    assert fro(out.array, ref) <= 16 * 5 * 8 * U32
+
+
+# ------------------------------------------------------------------ configs
+def test_config1_64_a16(golden):
+    arrays, _ = golden
+    a = oracle.scaled_input(64, np.float32, 42)
+    got = mx.Engine(0).power(a, 16)
+    assert fro(got, arrays["exp_64_f32_16"]) <= mx.fro_tol(64, 16, "f32")
+    # the reference's own unscaled default input (finite at k=16)
+    got = mx.Engine(0).power(arrays["unscaled_in_64_f32"], 16)
+    assert fro(got, arrays["unscaled_exp_64_f32_16"]) <= mx.fro_tol(64, 16, "f32")
+
+
+def test_config2_512_a1000():
+    a = oracle.scaled_input(512, np.float32, 42)
+    ref = oracle.exponentiate(a, 1000)
+    got = mx.Engine(0).power(a, 1000)
+    assert np.isfinite(got).all()
+    assert fro(got, ref) <= mx.fro_tol(512, 1000, "f32"), fro(got, ref)
+
+
+def test_config3_batched_samples(golden):
+    """128x128 A^64, seeds 42+i, generated on device, chained in the persistent kernel."""
+    arrays, meta = golden
+    batch = 4352  # > 148 * 29: every CTA loops over many matrices
+    stack = mx.scaled_batch(128, batch, mx.DType.F32, 42)
+    out = mx.exponentiate_batched(stack, 64)
+    tol = mx.fro_tol(128, 64, "f32")
+    assert fro(out[0], arrays["c3_out_0"]) <= tol
+    for i in (1, 255, 4097):
+        ref = oracle.exponentiate(oracle.scaled_input(128, np.float32, 42 + i), 64)
+        assert sha(ref) == meta["c3_exp_sha256"][str(i)]
+        assert fro(out[i], ref) <= tol, i
+    # batched result is bitwise the single-matrix result (same kernel, same order)
+    single = mx.Engine(0).power(stack[255], 64)
+    assert single.tobytes() == out[255].tobytes()
+
+
+def test_batched_small_n_with_multiplies():
+    """n < 128 and plans with MULTIPLY_BASE steps in the persistent kernel."""
+    for n, k in ((5, 1000), (33, 13), (100, 13), (128, 257), (127, 7)):
+        stack = mx.scaled_batch(n, 300, mx.DType.F32, 7)
+        if k > 100:  # keep A^k finite: row-stochastic inputs (spectral radius 1)
+            st = np.abs(stack).astype(np.float64)
+            stack = (st / st.sum(axis=2, keepdims=True)).astype(np.float32)
+        out = mx.exponentiate_batched(stack, k)
+        for i in (0, 151, 299):
+            ref = oracle.exponentiate(stack[i], k)
+            assert fro(out[i], ref) <= mx.fro_tol_conditioned(n, k, "f32"), (n, k, i)
+
+
+def test_large_chain_with_multiplies_f32():
+    for n, k in ((200, 13), (256, 257), (384, 100)):
+        a = oracle.scaled_input(n, np.float32, 42)
+        got = mx.Engine(0).power(a, k)
+        ref = oracle.exponentiate(a, k)
+        assert fro(got, ref) <= mx.fro_tol_conditioned(n, k, "f32"), (n, k, fro(got, ref))
+
+
+def test_f64_chain_256_a257(golden):
+    _, meta = golden
+    a = oracle.scaled_input(256, np.float64, 42)
+    ref = oracle.exponentiate(a, 257)
+    assert sha(ref) == meta["exp_256_f64_257_sha256"]
+    got = mx.Engine(0).power(a, 257)
+    assert fro(got, ref) <= mx.fro_tol(256, 257, "f64"), fro(got, ref)
+
+
+def test_stochastic_matrix_power_1000(golden):
+    arrays, _ = golden
+    got = mx.Engine(0).power(arrays["stoch_in_5_f32"], 1000)
+    assert fro(got, arrays["stoch_exp_5_f32_1000"]) <= mx.fro_tol_conditioned(5, 1000, "f32")
+
+
+# ------------------------------------------------------------------ full-size properties
+def test_permutation_power_exact_8192():
+    """Size-independent property at the C5 size: a permutation matrix of
+    order 12 (disjoint 3- and 4-cycles) raised to 1024 = 12*85 + 4 equals
+    P^4 exactly (0/1 entries are exact in 3xTF32)."""
+    n = 8192
+    perm = np.arange(n)
+    for base in range(0, n - 7, 7):
+        perm[base:base + 3] = np.roll(perm[base:base + 3], 1)
+        perm[base + 3:base + 7] = np.roll(perm[base + 3:base + 7], 1)
+    p = np.zeros((n, n), dtype=np.float32)
+    p[np.arange(n), perm] = 1.0
+    eng = mx.Engine(0)
+    got = eng.power(p, 1024)
+    p4 = np.arange(n)
+    for _ in range(4):
+        p4 = perm[p4]
+    ref = np.zeros((n, n), dtype=np.float32)
+    ref[np.arange(n), p4] = 1.0
+    assert np.array_equal(got, ref)
+    assert eng.last_stats.multiply_count == 10
+
+
+def test_row_stochastic_8192_a1024():
+    """Row sums of a row-stochastic matrix stay 1 under any power."""
+    n = 8192
+    eng = mx.Engine(0)
+    a = np.abs(mx.scaled_batch(n, 1, mx.DType.F32, 42)[0]).astype(np.float64)
+    a = (a / a.sum(axis=1, keepdims=True)).astype(np.float32)
+    got = eng.power(a, 1024)
+    sums = got.astype(np.float64).sum(axis=1)
+    assert np.abs(sums - 1.0).max() <= 16 * 10 * math.sqrt(n) * U32

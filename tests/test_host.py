@@ -1,0 +1,173 @@
+"""Host-side mirror of the reference API (no GPU): plan, backend plugin,
+exponentiate driving a generic backend, errors, Matrix, compare, tolerances.
+Mirrors pkg/tests/test_expo.py / test_linalg.py for the names this package keeps."""
+
+import math
+
+import numpy as np
+import pytest
+from hypothesis import given, strategies as st
+
+import oracle
+import paper_1204_3052_b200 as mx
+from paper_1204_3052_b200 import (
+    Backend,
+    BackendStepError,
+    CountingBackend,
+    DType,
+    Matrix,
+    Step,
+    Strategy,
+    UnsupportedPowerError,
+    count_transfers,
+    exponentiate,
+    multiply_count_for,
+    plan_exponentiation,
+    repeated_exponentiate,
+)
+
+
+def stub():
+    return CountingBackend(Backend("stub", lambda a, b: a))
+
+
+def oracle_backend():
+    """The CPU oracle as a backend — test infrastructure only."""
+    return Backend("oracle", lambda a, b: Matrix(oracle.matmul(a.array, b.array), copy=False))
+
+
+def law(p):
+    return p.bit_length() - 1 + bin(p).count("1") - 1 if p >= 1 else 0
+
+
+def test_small_plans():
+    assert plan_exponentiation(0).steps == ()
+    assert plan_exponentiation(1).steps == ()
+    assert plan_exponentiation(2).steps == (Step.SQUARE,)
+    assert plan_exponentiation(3).steps == (Step.SQUARE, Step.MULTIPLY_BASE)
+    assert plan_exponentiation(13).as_string() == "SMSSM"
+    assert plan_exponentiation(1024).square_count == 10
+    assert plan_exponentiation(1023).square_count == 9
+    with pytest.raises(ValueError):
+        plan_exponentiation(-1)
+
+
+@given(power=st.integers(1, 2**20))
+def test_count_law(power):
+    assert plan_exponentiation(power).multiply_count == law(power)
+    assert plan_exponentiation(power).as_string() == oracle.plan(power)
+
+
+@given(power=st.integers(1, 2**16))
+def test_plan_executes_to_the_power(power):
+    e = 1
+    for s in plan_exponentiation(power).steps:
+        e = e * 2 if s is Step.SQUARE else e + 1
+    assert e == power
+
+
+def test_invocations_match_plan_with_generic_backend():
+    a = Matrix(np.eye(2))
+    for power in (1, 13, 512, 1024, 4096):
+        be = stub()
+        exponentiate(a, power, be)
+        assert be.calls == law(power)
+
+
+def test_power_zero_one_semantics():
+    a = Matrix(oracle.random_matrix(4, np.float32, 3))
+    be = stub()
+    assert exponentiate(a, 1, be) is a and be.calls == 0
+    out = exponentiate(a, 0, be)
+    assert np.array_equal(out.array, np.eye(4)) and out.dtype is DType.F32
+
+
+def test_step_failure_is_annotated():
+    boom = RuntimeError("device fell over")
+    calls = []
+
+    def flaky(a, b):
+        calls.append(1)
+        if len(calls) == 2:
+            raise boom
+        return a
+
+    with pytest.raises(BackendStepError) as ei:
+        exponentiate(Matrix(np.eye(2)), 8, Backend("flaky", flaky))
+    assert ei.value.step_index == 1 and ei.value.step_name == "SQUARE"
+    assert ei.value.__cause__ is boom
+
+
+def test_generic_backend_chain_bitwise_equals_oracle(golden):
+    arrays, _ = golden
+    for n in (4, 16):
+        a = Matrix(arrays[f"in_{n}_f32"])
+        for k in (2, 7, 13, 64):
+            got = exponentiate(a, k, oracle_backend())
+            assert got.array.tobytes() == arrays[f"exp_{n}_f32_{k}"].tobytes()
+
+
+def test_repeated_and_strategy():
+    assert multiply_count_for(Strategy.REPEATED, 512) == 511
+    assert multiply_count_for(Strategy.SQUARED, 512) == 9
+    with pytest.raises(UnsupportedPowerError):
+        multiply_count_for(Strategy.REPEATED, 0)
+    with pytest.raises(UnsupportedPowerError):
+        repeated_exponentiate(Matrix(np.eye(2)), 0, stub())
+    be = stub()
+    repeated_exponentiate(Matrix(np.eye(2)), 64, be)
+    assert be.calls == 63
+    assert Strategy.parse("SQUARED") is Strategy.SQUARED
+    for p in (1, 2, 13, 1024):
+        assert count_transfers(plan_exponentiation(p), Strategy.SQUARED) == 2
+        assert count_transfers(plan_exponentiation(p), Strategy.REPEATED) == p
+    assert mx.b200_backend().transfer_cost_model(plan_exponentiation(1024), Strategy.SQUARED) == 2
+
+
+def test_matrix_contract():
+    arr = np.zeros((3, 3))
+    m = Matrix(arr)
+    arr[0, 0] = 7
+    assert m.array[0, 0] == 0
+    with pytest.raises(ValueError):
+        m.array[0, 0] = 1
+    with pytest.raises(mx.ShapeError):
+        Matrix(np.zeros((2, 3)))
+    with pytest.raises(mx.ShapeError):
+        Matrix(np.zeros((2, 2), dtype=np.int64))
+    with pytest.raises(mx.InvalidDimensionError):
+        mx.identity(0)
+    assert Matrix.from_rows([[1, 2], [3, 4]], DType.F32).data.tolist() == [1, 2, 3, 4]
+
+
+def test_compare_semantics():
+    z = mx.zeros(2)
+    assert tuple(mx.compare(z, z)) == (0.0, 0.0, 0.0)
+    off = Matrix.from_rows([[0.0, 1.0], [0.0, 0.0]])
+    m = mx.compare(off, z)
+    assert m.max_abs == 1.0 and m.max_rel == math.inf and m.frobenius_rel == math.inf
+    ref = Matrix.from_rows([[2.0, 0.0], [0.0, 2.0]])
+    res = Matrix.from_rows([[2.0, 0.0], [0.0, 2.5]])
+    assert mx.compare(res, ref).max_rel == 0.25
+
+
+def test_tolerances_match_reference_and_survey():
+    assert mx.oracle_tol(1024, 8192, DType.F32) == 1024 * 8192 * 2**-24 * 64
+    assert mx.device_tol(64, DType.F32) == 64 * 2**-24 * 64
+    # SURVEY §8(d) values
+    assert abs(mx.fro_tol(64, 16, DType.F32) - 3.1e-5) < 0.1e-5
+    assert abs(mx.fro_tol(512, 1000, DType.F32) - 3.0e-4) < 0.1e-4
+    assert abs(mx.fro_tol(128, 64, DType.F32) - 6.5e-5) < 0.1e-5
+    assert abs(mx.fro_tol(8192, 1024, DType.F32) - 8.6e-4) < 0.1e-4
+
+
+def test_wrap_like_reference_matrix_type():
+    """Results come back in the caller's matrix class (reference interop)."""
+    from paper_1204_3052_b200.linalg import wrap_like
+
+    class Foreign:
+        def __init__(self, array, copy=True):
+            self.array = np.array(array)
+
+    out = wrap_like(Foreign(np.eye(2)), np.ones((2, 2)))
+    assert isinstance(out, Foreign)

@@ -1,0 +1,2 @@
+timeout 60 python tools/probe.py acc 2>&1 | tail -5
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 300 2>&1 | tail -25
