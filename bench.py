@@ -1,0 +1,443 @@
+#!/usr/bin/env python
+"""Benchmark: effective TFLOP/s (2 n^3 * multiplies / s) and matrices/s for A^k.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference ...      # the reference CPU path (oracle port)
+
+Workload (BASELINE.json configs; the metric is quoted "at 1/2/4/8 B200",
+which is config 3's batch-sharded form):  c3 = 65536 x 128x128 FP32 A^64
+(3xTF32), inputs fl(random_matrix(128, F64, 42+i) * sqrt(12/128)) generated on
+device.  Each rank runs its own 65536-matrix batch (weak scaling, no
+collective on the data path).  A "step" is one pass of the chain over the
+batch: ONE launch of the persistent sm_100a kernel.  Inputs (4.3 GB) exceed
+the 126 MB L2, so no flush is needed between steps.
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = ("effective TFLOP/s (2N^3·mults/s) and matrices/s for A^k at 1/2/4/8 B200 "
+          "vs CPU ref")
+
+WORKLOADS = {
+    "c3": dict(name="batched 65536 x 128x128 FP32 (3xTF32) A^64", n=128, batch=65536, k=64,
+               dtype="f32"),
+    "c2": dict(name="512x512 FP32 (3xTF32) A^1000", n=512, batch=1, k=1000, dtype="f32"),
+    "c5": dict(name="8192x8192 FP32 (3xTF32) A^1024 (1 GPU)", n=8192, batch=1, k=1024,
+               dtype="f32"),
+    "c4": dict(name="4096x4096 FP64 (DMMA) A^257", n=4096, batch=1, k=257, dtype="f64"),
+    "c1": dict(name="64x64 FP32 (3xTF32) A^16", n=64, batch=1, k=16, dtype="f32"),
+}
+
+
+def mults(k: int) -> int:
+    return k.bit_length() - 1 + bin(k).count("1") - 1 if k >= 1 else 0
+
+
+def flops(w: dict) -> float:
+    return 2.0 * w["n"] ** 3 * mults(w["k"]) * w["batch"]
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event reasons during a region."""
+
+    BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+            0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+            0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period: float = 0.005):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - clocks are reported as unavailable
+            self._nv = None
+        self.period = period
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+            except Exception:  # noqa: BLE001
+                try:
+                    self.reasons |= int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h))
+                except Exception:  # noqa: BLE001
+                    pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        reasons = [name for bit, name in self.BITS.items() if self.reasons & bit]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- peaks
+def measured_peaks() -> dict:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def tf32_peak_tflops(device) -> float:
+    """cuBLAS TF32 GEMM 8192^3, best of 10 (the denominator for 3xTF32; the
+    driver's MEASURED_PEAKS.json carries bf16 only).  Library GEMM used only
+    as a peak reference, never on the measured path."""
+    import torch
+
+    torch.backends.cuda.matmul.allow_tf32 = True
+    n = 8192
+    a = torch.randn(n, n, device=device)
+    b = torch.randn(n, n, device=device)
+    for _ in range(3):
+        a @ b
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(10):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        a @ b
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    del a, b
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return 2.0 * n ** 3 / (best / 1e3) / 1e12
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            data = json.load(fh)
+        return data.get(kernel, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU
+def cpu_sample(w: dict, budget_s: float = 12.0) -> dict:
+    """Time the oracle port (CPU restatement of the reference's naive chain,
+    bit-identical to it) on a bounded sample of the workload, all threads."""
+    import numpy as np
+
+    import oracle
+
+    threads = oracle.max_threads()
+    n, k = w["n"], w["k"]
+    dt = np.float32 if w["dtype"] == "f32" else np.float64
+    m = mults(k)
+    if w["batch"] > 1:
+        # whole chains of independent matrices, one per thread at a time
+        count = threads
+        stack = oracle.scaled_batch(n, count, dt, 42)
+        t0 = time.perf_counter()
+        oracle.exponentiate_batched(stack, k, threads)
+        dt_s = time.perf_counter() - t0
+        count = max(threads, int(count * min(budget_s / max(dt_s, 1e-3), 64)))
+        count = min(count, 4096)
+        stack = oracle.scaled_batch(n, count, dt, 42)
+        t0 = time.perf_counter()
+        oracle.exponentiate_batched(stack, k, threads)
+        dt_s = time.perf_counter() - t0
+        fl = 2.0 * n ** 3 * m * count
+        sample = f"{count} full A^{k} chains of {n}x{n} (seeds 42..{41 + count}) on {threads} threads"
+        per_unit_s = dt_s / count
+        full_s = per_unit_s * w["batch"]
+    elif n <= 1024:
+        a = oracle.scaled_input(n, dt, 42)
+        t0 = time.perf_counter()
+        oracle.exponentiate(a, k, threads)
+        dt_s = time.perf_counter() - t0
+        fl = 2.0 * n ** 3 * m
+        sample = f"one full A^{k} chain of {n}x{n} on {threads} threads"
+        full_s = dt_s
+    else:
+        # rows of one multiply, extrapolated to m multiplies (labelled)
+        a = oracle.scaled_input(n, dt, 42)
+        rows = 16
+        t0 = time.perf_counter()
+        oracle.matmul_rows(a, a, 0, rows, threads)
+        dt_s = time.perf_counter() - t0
+        rows = max(16, min(n, int(rows * budget_s / max(dt_s, 1e-3))))
+        t0 = time.perf_counter()
+        oracle.matmul_rows(a, a, 0, rows, threads)
+        dt_s = time.perf_counter() - t0
+        fl = 2.0 * n * n * rows
+        sample = (f"{rows} rows of one {n}x{n} multiply on {threads} threads, extrapolated "
+                  f"x{n / rows:.0f} rows x{m} multiplies")
+        full_s = dt_s * (n / rows) * m
+    return {"value": fl / dt_s / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+            "sample": sample, "sample_seconds": dt_s, "est_full_workload_seconds": full_s,
+            "matrices_per_s": w["batch"] / full_s if w["batch"] > 1 else 1.0 / full_s}
+
+
+# ----------------------------------------------------------------------------- GPU
+def run_device(eng, w: dict, steps: int, warmup: int, seed0: int, dist=None, sample=True):
+    """Device-resident inputs, CUDA-event timing on the engine's stream."""
+    import torch
+
+    from paper_1204_3052_b200 import _lib
+
+    n, B, k = w["n"], w["batch"], w["k"]
+    mode = _lib.MXP_F32 if w["dtype"] == "f32" else _lib.MXP_F64
+    es = 4 if w["dtype"] == "f32" else 8
+    nbytes = n * n * B * es
+    d_in = eng.alloc(nbytes)
+    d_out = eng.alloc(nbytes)
+    eng.random_device(d_in, n, B, seed0, -0.5, 0.5, math.sqrt(12.0 / n), mode)
+
+    def step():
+        if B > 1:
+            eng.power_batched_device(d_in, d_out, n, B, k, mode)
+        else:
+            eng.power_device(d_in, d_out, n, k, mode)
+
+    for _ in range(warmup):
+        step()
+    eng.synchronize()
+    launches = eng.last_stats.launches
+    stream = torch.cuda.ExternalStream(eng.stream)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(torch.cuda.current_device()) if sample else None
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    if sampler:
+        sampler.__enter__()
+    start.record(stream)
+    for _ in range(steps):
+        step()
+    end.record(stream)
+    end.synchronize()
+    if sampler:
+        sampler.__exit__()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = start.elapsed_time(end) / steps
+    eng.free(d_in)
+    eng.free(d_out)
+    return ms, launches, (sampler.summary() if sampler else None)
+
+
+def run_e2e(eng, w: dict, steps: int = 3) -> dict:
+    """Same metric through the public host API: pinned host input -> H2D ->
+    chain -> D2H into pinned host output, every step."""
+    import numpy as np
+
+    from paper_1204_3052_b200 import _lib
+
+    n, B, k = w["n"], w["batch"], w["k"]
+    dt = np.float32 if w["dtype"] == "f32" else np.float64
+    mode = _lib.MXP_F32 if w["dtype"] == "f32" else _lib.MXP_F64
+    shape = (B, n, n) if B > 1 else (n, n)
+    host_in = eng.pinned_array(shape, dt)
+    host_out = eng.pinned_array(shape, dt)
+    d = eng.alloc(host_in.nbytes)
+    eng.random_device(d, n, B, 42, -0.5, 0.5, math.sqrt(12.0 / n), mode)
+    eng.download(host_in, d)
+    eng.free(d)
+
+    def call():
+        if B > 1:
+            eng.power_batched(host_in, k, out=host_out)
+        else:
+            host_out[...] = eng.power(host_in, k)
+
+    call()  # warm (allocations, graph capture)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    st = eng.last_stats
+    med = statistics.median(times)
+    res = {"value": flops(w) / med / 1e12, "unit": "TFLOP/s",
+           "h2d_bytes_per_step": int(st.h2d_bytes), "d2h_bytes_per_step": int(st.d2h_bytes),
+           "ms_per_step": med * 1e3, "matrices_per_s": B / med,
+           "timing": f"host wall clock around the synchronous public call, median of {steps}"}
+    eng.host_free(host_in.ctypes.data)
+    eng.host_free(host_out.ctypes.data)
+    return res
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-extras", action="store_true", help="skip the secondary configs")
+    ap.add_argument("--quick", action="store_true",
+                    help="device timing only (no e2e / CPU baseline / peak GEMM): for ncu runs")
+    args = ap.parse_args()
+    w = WORKLOADS[args.workload]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": w["name"], "n": w["n"], "batch_per_gpu": w["batch"], "k": w["k"],
+              "multiplies_per_matrix": mults(w["k"]), "global_batch": w["batch"] * world,
+              "input": "fl(random_matrix(n, F64, 42+i) * sqrt(12/n)) generated on device",
+              "l2": "inputs larger than L2 (no flush needed)" if w["batch"] > 1 else
+                    "single matrix chain, L2-resident by design (graph replay)",
+              "parallelism": f"batch-sharded x{world} (no collective)" if world > 1 else "1 GPU"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        samples = []
+        for i in range(args.warmup + args.steps):
+            r = cpu_sample(w, budget_s=2.0)
+            if i >= args.warmup:
+                samples.append(r)
+        val = statistics.median(s["value"] for s in samples)
+        cpu = dict(samples[-1])
+        cpu["value"] = val
+        print(json.dumps({"metric": METRIC, "value": val, "unit": "TFLOP/s", "impl": "reference",
+                          "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": statistics.median(s["sample_seconds"] for s in samples) * 1e3,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                          "dtype": w["dtype"], "data": "synthetic (SURVEY §8(d) recipe)",
+                          "config": config, "cpu_baseline": cpu,
+                          "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = tdist
+    else:
+        torch.cuda.set_device(local)
+
+    import paper_1204_3052_b200 as mx
+
+    eng = mx.Engine(local)
+    ms, launches, clocks = run_device(eng, w, args.steps, args.warmup,
+                                      seed0=42 + rank * w["batch"], dist=dist)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    fl = flops(w)
+    value = world * fl / (ms / 1e3) / 1e12
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks = measured_peaks()
+    tf32 = None
+    if not args.quick:
+        try:
+            tf32 = tf32_peak_tflops(torch.device("cuda", local))
+        except Exception:  # noqa: BLE001
+            tf32 = None
+    if tf32:
+        peak, src = tf32 / 3.0, f"cuBLAS TF32 8192^3 measured in this run ({tf32:.0f} TFLOP/s) / 3"
+    elif peaks.get("bf16_tflops"):
+        peak, src = peaks["bf16_tflops"] / 6.0, "MEASURED_PEAKS bf16 burst / 2 (tf32) / 3"
+    else:
+        peak, src = 1590.0 / 6.0, "fallback 1.59 PF bf16 / 6"
+    kernel_ms = ms / max(launches, 1) if w["batch"] > 1 else ms
+    achieved = fl / (kernel_ms / 1e3) / 1e12 if w["batch"] > 1 else value
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": ncu_traffic("k3_batched_power"),
+                "kernel": "k3_batched_power" if w["batch"] > 1 else "k1_gemm_3xtf32 chain",
+                "peak_source": src, "algorithmic_flops_per_launch": fl / max(launches, 1),
+                "bf16_measured_peak": peaks.get("bf16_tflops")}
+    out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f32 (3xTF32 tcgen05)" if w["dtype"] == "f32" else "f64 (DMMA)",
+           "data": "synthetic (SURVEY §8(d) recipe, device SplitMix64)", "config": config,
+           "matrices_per_s": world * w["batch"] / (ms / 1e3),
+           "roofline": roofline, "clocks": clocks,
+           "gpu_launches": args.steps * launches}
+    if args.quick:
+        print(json.dumps(out))
+        return
+    try:
+        out["e2e"] = run_e2e(eng, w)
+    except Exception as exc:  # noqa: BLE001
+        out["e2e"] = {"value": None, "error": str(exc)}
+    if world == 1:
+        try:
+            out["cpu_baseline"] = cpu_sample(w)
+        except Exception as exc:  # noqa: BLE001
+            out["cpu_baseline"] = {"value": None, "error": str(exc)}
+        if not args.no_extras:
+            extras = {}
+            for key in ("c1", "c2", "c4", "c5"):
+                if key == args.workload:
+                    continue
+                wx = WORKLOADS[key]
+                try:
+                    xms, xl, _ = run_device(eng, wx, 3 if wx["n"] >= 4096 else 20, 2, 42,
+                                            sample=False)
+                    extras[key] = {"workload": wx["name"], "ms": xms, "launches": xl,
+                                   "TFLOP/s": flops(wx) / (xms / 1e3) / 1e12}
+                except Exception as exc:  # noqa: BLE001
+                    extras[key] = {"error": str(exc)}
+            out["other_configs"] = extras
+    print(json.dumps(out))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -5,6 +5,8 @@
 // replaces the reference's scalar ascending-k fp32 loop (linalg.py:151-164,
 // matmul_tiled.cl:91-94); parity is by the relative-Frobenius tolerance of
 // SURVEY §8(d), not bitwise (tensor-core summation order differs).
+#include <cstring>
+
 #include "mxp_internal.h"
 #include "ptx.cuh"
 
@@ -49,61 +51,56 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023u) & ~uintptr_t(1023));
 }
 
-// n x n row-major fp32 (zero padded to 128 x 128) -> tf32 hi/lo in the
-// MN-major right-operand layout.  Coalesced: a warp reads 512 B of one row.
-__device__ __forceinline__ void k3_load_right(const float* __restrict__ src, int n,
-                                              uint8_t* dst_hi, uint8_t* dst_lo) {
-    const bool vec = (n & 3) == 0;
-    for (int idx = threadIdx.x; idx < 128 * 32; idx += kK3Threads) {
-        const int r = idx >> 5;
-        const int c = (idx & 31) << 2;
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (r < n) {
-            const float* p = src + static_cast<size_t>(r) * n + c;
-            if (vec && c + 3 < n) {
-                float4 t = __ldg(reinterpret_cast<const float4*>(p));
-                v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-            } else {
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (c + i < n) v[i] = __ldg(p + i);
-            }
-        }
-        uint4 hi, lo;
-        split_tf32(v[0], hi.x, lo.x);
-        split_tf32(v[1], hi.y, lo.y);
-        split_tf32(v[2], hi.z, lo.z);
-        split_tf32(v[3], hi.w, lo.w);
-        const uint32_t off = sw32b_offset(r, c, kChunk);
-        *reinterpret_cast<uint4*>(dst_hi + off) = hi;
-        *reinterpret_cast<uint4*>(dst_lo + off) = lo;
-    }
-}
-
-// Copy row `row`, columns [col0, col0+32) of the SMEM right operand into the
-// TMEM left operand (same values; only the layout differs).
-__device__ __forceinline__ void k3_row_to_tmem(const uint8_t* b_hi, const uint8_t* b_lo,
-                                               uint32_t row, int col0, uint32_t t_hi,
-                                               uint32_t t_lo) {
-    uint32_t h[32], l[32];
+// Write 32 split values (row `row`, columns [col0, col0+32)) into the SMEM
+// right operand (MN-major SW128_BASE32B).  The 16-byte unit order is flipped
+// for rows with (row >> 2) odd so the 8 rows of a quarter-warp hit 8 distinct
+// 16-byte bank groups (no conflicts).
+__device__ __forceinline__ void k3_put_right(uint32_t s_hi, uint32_t s_lo, uint32_t row, int col0,
+                                             const uint32_t (&h)[32], const uint32_t (&l)[32]) {
+    const uint32_t flip = (row >> 2) & 1u;
+    const uint32_t base = (col0 >> 5) * kChunk + row * 128u;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-        const uint32_t off = sw32b_offset(row, col0 + 4 * u, kChunk);
-        const uint4 x = *reinterpret_cast<const uint4*>(b_hi + off);
-        const uint4 y = *reinterpret_cast<const uint4*>(b_lo + off);
-        h[4 * u] = x.x; h[4 * u + 1] = x.y; h[4 * u + 2] = x.z; h[4 * u + 3] = x.w;
-        l[4 * u] = y.x; l[4 * u + 1] = y.y; l[4 * u + 2] = y.z; l[4 * u + 3] = y.w;
+        const int ua = u, ub = u ^ 1;
+        const uint32_t unit = static_cast<uint32_t>(u) ^ flip;
+        const uint32_t off = base + ((((unit >> 1) ^ (row & 3u)) << 1 | (unit & 1u)) << 4);
+        uint32_t h0 = flip ? h[4 * ub] : h[4 * ua], h1 = flip ? h[4 * ub + 1] : h[4 * ua + 1];
+        uint32_t h2 = flip ? h[4 * ub + 2] : h[4 * ua + 2], h3 = flip ? h[4 * ub + 3] : h[4 * ua + 3];
+        uint32_t l0 = flip ? l[4 * ub] : l[4 * ua], l1 = flip ? l[4 * ub + 1] : l[4 * ua + 1];
+        uint32_t l2 = flip ? l[4 * ub + 2] : l[4 * ua + 2], l3 = flip ? l[4 * ub + 3] : l[4 * ua + 3];
+        sts128(s_hi + off, h0, h1, h2, h3);
+        sts128(s_lo + off, l0, l1, l2, l3);
     }
-    tmem_st32(t_hi + col0, h);
-    tmem_st32(t_lo + col0, l);
 }
 
-// Row `row`, columns [col0, col0+32) of the base matrix from global (zero
-// padded), split, into the TMEM left operand.
-__device__ __forceinline__ void k3_base_row_to_tmem(const float* __restrict__ src, int n,
-                                                    uint32_t row, int col0, uint32_t t_hi,
-                                                    uint32_t t_lo) {
-    uint32_t h[32], l[32];
+// ... and the same values into the TMEM left operand as well.
+__device__ __forceinline__ void k3_put_row(uint32_t s_hi, uint32_t s_lo, uint32_t row, int col0,
+                                           const uint32_t (&h)[32], const uint32_t (&l)[32],
+                                           uint32_t t_hi, uint32_t t_lo) {
+    tmem_st32(t_hi + col0, h);
+    tmem_st32(t_lo + col0, l);
+    k3_put_right(s_hi, s_lo, row, col0, h, l);
+}
+
+// Row `row`, columns [col0, col0+32) of the staged input (TMA SWIZZLE_128B
+// layout: chunk c = 128 rows x 128 B, 16-byte unit u of row r at u ^ (r%8)).
+__device__ __forceinline__ void k3_stage_row(uint32_t s_stage, uint32_t row, int col0,
+                                             uint32_t (&h)[32], uint32_t (&l)[32]) {
+    const uint32_t base = s_stage + (col0 >> 5) * kChunk + row * 128u;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const uint4 x = lds128(base + ((static_cast<uint32_t>(u) ^ (row & 7u)) << 4));
+        split_tf32(__uint_as_float(x.x), h[4 * u], l[4 * u]);
+        split_tf32(__uint_as_float(x.y), h[4 * u + 1], l[4 * u + 1]);
+        split_tf32(__uint_as_float(x.z), h[4 * u + 2], l[4 * u + 2]);
+        split_tf32(__uint_as_float(x.w), h[4 * u + 3], l[4 * u + 3]);
+    }
+}
+
+// Fallback for n % 4 != 0 (no TMA map) and for MULTIPLY_BASE steps: row from
+// global, zero padded.
+__device__ __forceinline__ void k3_global_row(const float* __restrict__ src, int n, uint32_t row,
+                                              int col0, uint32_t (&h)[32], uint32_t (&l)[32]) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
         const int c = col0 + i;
@@ -112,22 +109,23 @@ __device__ __forceinline__ void k3_base_row_to_tmem(const float* __restrict__ sr
                             : 0.f;
         split_tf32(v, h[i], l[i]);
     }
-    tmem_st32(t_hi + col0, h);
-    tmem_st32(t_lo + col0, l);
 }
 }  // namespace
 
-size_t k3_smem_bytes() { return 2 * kPlane + 1024 + 256; }
+size_t k3_smem_bytes() { return 3 * kPlane + 1024 + 256; }
 
+// use_tma: the input tensor map is valid (n % 4 == 0); matrices are then
+// prefetched one ahead into a 64 KB staging buffer while the current chain
+// runs.  Otherwise every row is read from global at the start of its chain.
 __global__ void __launch_bounds__(kK3Threads, 1)
-    k3_batched_power(const float* __restrict__ in, float* __restrict__ out, int n, long long batch,
+    k3_batched_power(const __grid_constant__ CUtensorMap in_map, int use_tma,
+                     const float* __restrict__ in, float* __restrict__ out, int n, long long batch,
                      PlanBits plan) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
-    uint8_t* b_hi = smem;
-    uint8_t* b_lo = smem + kPlane;
-    uint64_t* mma_bar = reinterpret_cast<uint64_t*>(smem + 2 * kPlane);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 2 * kPlane + 64);
+    uint64_t* mma_bar = reinterpret_cast<uint64_t*>(smem + 3 * kPlane);
+    uint64_t* load_bar = mma_bar + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 3 * kPlane + 64);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -136,16 +134,18 @@ __global__ void __launch_bounds__(kK3Threads, 1)
 
     if (tid == 0) {
         mbar_init(mma_bar, 1);
+        mbar_init(load_bar, 1);
         fence_mbar_init();
+        if (use_tma) tma_prefetch(&in_map);
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    uint32_t phase = 0;
+    uint32_t mma_phase = 0, load_phase = 0;
 
-    const uint32_t s_hi = smem_u32(b_hi), s_lo = smem_u32(b_lo);
+    const uint32_t s_hi = smem_u32(smem), s_lo = s_hi + kPlane, s_stage = s_hi + 2 * kPlane;
     const int q = warp & 3;             // TMEM lane quarter this warp may access
     const int colh = (warp >> 2) * 64;  // column half handled by this warp
     const uint32_t row = q * 32 + lane;
@@ -154,22 +154,48 @@ __global__ void __launch_bounds__(kK3Threads, 1)
     const uint32_t t_hi = lane_base + kColHi, t_lo = lane_base + kColLo;
     const uint64_t bdesc_hi = mnmajor_desc(s_hi, kChunk), bdesc_lo = mnmajor_desc(s_lo, kChunk);
 
+    auto issue_load = [&](long long mm) {  // one thread
+        mbar_expect_tx(load_bar, 4 * kChunk);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            tma_load_3d(smem + 2 * kPlane + c * kChunk, &in_map, load_bar, 32 * c, 0,
+                        static_cast<int32_t>(mm));
+    };
+    if (use_tma && tid == 0 && blockIdx.x < batch) issue_load(blockIdx.x);
+
     for (long long m = blockIdx.x; m < batch; m += gridDim.x) {
         const float* src = in + static_cast<size_t>(m) * n * n;
-        k3_load_right(src, n, b_hi, b_lo);
-        __syncthreads();
-        k3_row_to_tmem(b_hi, b_lo, row, colh, t_hi, t_lo);
-        k3_row_to_tmem(b_hi, b_lo, row, colh + 32, t_hi, t_lo);
+        // ---- input -> right operand (SMEM) + left operand (TMEM)
+        if (use_tma) {
+            mbar_wait(load_bar, load_phase);
+            load_phase ^= 1;
+        }
+#pragma unroll 1
+        for (int j = 0; j < 2; ++j) {
+            uint32_t h[32], l[32];
+            if (use_tma)
+                k3_stage_row(s_stage, row, colh + 32 * j, h, l);
+            else
+                k3_global_row(src, n, row, colh + 32 * j, h, l);
+            k3_put_row(s_hi, s_lo, row, colh + 32 * j, h, l, t_hi, t_lo);
+        }
         tmem_st_wait();
         fence_proxy_async_smem();
         tc_fence_before();
         __syncthreads();
+        // staging is free again: prefetch the next matrix under this chain
+        if (use_tma && tid == 0 && m + gridDim.x < batch) issue_load(m + gridDim.x);
 
         for (int s = 0; s < plan.len; ++s) {
             if (plan_is_mult(plan, s)) {
                 // left operand <- base (the resident acc stays the right operand)
-                k3_base_row_to_tmem(src, n, row, colh, t_hi, t_lo);
-                k3_base_row_to_tmem(src, n, row, colh + 32, t_hi, t_lo);
+#pragma unroll 1
+                for (int j = 0; j < 2; ++j) {
+                    uint32_t h[32], l[32];
+                    k3_global_row(src, n, row, colh + 32 * j, h, l);
+                    tmem_st32(t_hi + colh + 32 * j, h);
+                    tmem_st32(t_lo + colh + 32 * j, l);
+                }
                 tmem_st_wait();
                 tc_fence_before();
                 __syncthreads();
@@ -193,8 +219,8 @@ __global__ void __launch_bounds__(kK3Threads, 1)
                 }
                 mma_commit(mma_bar);
             }
-            mbar_wait(mma_bar, phase);
-            phase ^= 1;
+            mbar_wait(mma_bar, mma_phase);
+            mma_phase ^= 1;
             tc_fence_after();
             const bool last = (s == plan.len - 1);
 #pragma unroll 1
@@ -225,16 +251,7 @@ __global__ void __launch_bounds__(kK3Threads, 1)
                     uint32_t h[32], l[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) split_tf32(__uint_as_float(v[i]), h[i], l[i]);
-                    tmem_st32(t_hi + col0, h);
-                    tmem_st32(t_lo + col0, l);
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const uint32_t off = sw32b_offset(row, col0 + 4 * u, kChunk);
-                        *reinterpret_cast<uint4*>(b_hi + off) =
-                            make_uint4(h[4 * u], h[4 * u + 1], h[4 * u + 2], h[4 * u + 3]);
-                        *reinterpret_cast<uint4*>(b_lo + off) =
-                            make_uint4(l[4 * u], l[4 * u + 1], l[4 * u + 2], l[4 * u + 3]);
-                    }
+                    k3_put_row(s_hi, s_lo, row, col0, h, l, t_hi, t_lo);
                 }
             }
             tmem_st_wait();
@@ -250,7 +267,13 @@ __global__ void __launch_bounds__(kK3Threads, 1)
 cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
                               const PlanBits& plan, int grid, cudaStream_t s) {
     if (grid > batch) grid = static_cast<int>(batch);
-    k3_batched_power<<<grid, kK3Threads, k3_smem_bytes(), s>>>(in, out, n, batch, plan);
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof map);
+    int use_tma = 0;
+    if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0)
+        use_tma = encode_batch_map(&map, in, n, batch) ? 1 : 0;
+    k3_batched_power<<<grid, kK3Threads, k3_smem_bytes(), s>>>(map, use_tma, in, out, n, batch,
+                                                               plan);
     return cudaGetLastError();
 }
 
@@ -368,8 +391,17 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int m0 = blockIdx.y * 128;
-    const int n0 = blockIdx.x * BN;
+    // Grouped raster: consecutive CTAs sweep a column of kGroupM row tiles
+    // before moving right, so the CTAs resident at once share A row slabs
+    // and B column slabs in L2 instead of each wave streaming all of B.
+    constexpr int kGroupM = 16;
+    const int num_m = n_pad / 128, num_n = n_pad / BN;
+    const int pid = blockIdx.x;
+    const int per_group = kGroupM * num_n;
+    const int first_m = (pid / per_group) * kGroupM;
+    const int gm = min(num_m - first_m, kGroupM);
+    const int m0 = (first_m + (pid % per_group) % gm) * 128;
+    const int n0 = ((pid % per_group) / gm) * BN;
     const int num_kb = n_pad / 32;
 
     if (threadIdx.x == 0) {
@@ -532,6 +564,22 @@ bool encode_plane_map(CUtensorMap* map, const void* plane, int n_pad, int box_co
     return r == CUDA_SUCCESS;
 }
 
+// 3-D map over a batch of row-major n x n fp32 matrices: box {32, 128, 1},
+// SWIZZLE_128B, rows/columns beyond n zero-filled by TMA.
+bool encode_batch_map(CUtensorMap* map, const void* base, int n, int64_t batch) {
+    EncodeTiledFn fn = get_encode_fn();
+    if (fn == nullptr) return false;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(n),
+                          static_cast<cuuint64_t>(batch)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(n) * 4, static_cast<cuuint64_t>(n) * n * 4};
+    cuuint32_t box[3] = {32, 128, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 int k1_block_n(int n_pad, int num_sms) {
     (void)n_pad;
     (void)num_sms;
@@ -551,7 +599,7 @@ cudaError_t launch_k1_gemm(const GemmPlanes& m, int n_pad, int block_n, float* o
                            int n_out, int ld_out, uint32_t* out_hi, uint32_t* out_lo,
                            cudaStream_t s) {
     (void)block_n;
-    dim3 grid(n_pad / K1Cfg::kBN, n_pad / 128);
+    dim3 grid((n_pad / K1Cfg::kBN) * (n_pad / 128));
     k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad,
                                                                out_f32, n_out, ld_out, out_hi, out_lo);
     return cudaGetLastError();

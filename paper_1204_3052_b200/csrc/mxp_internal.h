@@ -45,6 +45,7 @@ struct GemmPlanes {
     CUtensorMap a_hi, a_lo;  // box {32, 128}, SWIZZLE_128B (K-major left operand)
     CUtensorMap b_hi, b_lo;  // box {32, 32}, SWIZZLE_128B_ATOM_32B (MN-major right operand)
 };
+bool encode_batch_map(CUtensorMap* map, const void* base, int n, int64_t batch);
 bool encode_plane_map(CUtensorMap* map, const void* plane, int n_pad, int box_cols, int box_rows,
                       bool right_operand);
 int k1_block_n(int n_pad, int num_sms);

@@ -205,14 +205,33 @@ __host__ __device__ constexpr uint32_t idesc_tf32_kmaj_mnmaj() {
 // ---------------------------------------------------------------- 3xTF32 split
 // hi = rna_tf32(x), lo = rna_tf32(x - hi).  The tensor core reads only the
 // top 19 bits of each 32-bit operand, so both halves are pre-rounded.
+// rna (round to nearest, ties away from zero) on the bit pattern: add half an
+// ulp of the 10-bit mantissa (0x1000) and clear the 13 dropped bits.  Exact
+// for finite values (carry into the exponent is the correct rounding, and
+// overflow rounds to inf); inf stays inf.  Two integer ops instead of the
+// ~5-instruction cvt.rna.tf32.f32 lowering.
 __device__ __forceinline__ uint32_t cvt_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
+    return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
 }
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
     hi = cvt_tf32(x);
-    lo = cvt_tf32(x - __uint_as_float(hi));
+    lo = cvt_tf32(__fsub_rn(x, __uint_as_float(hi)));
+}
+
+// ---------------------------------------------------------------- shared memory
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                       uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+                 "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
 }
 
 // byte offset of element (r, c) inside a [c/32][r][32] fp32 tile whose column

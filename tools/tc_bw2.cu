@@ -18,6 +18,9 @@ __device__ __forceinline__ void issue16(uint32_t tmem, uint64_t adesc, uint64_t 
         if (MODE == 3) mma_tf32(tmem, a, b, id256, acc);
         if (MODE == 4) mma_tf32_ts(tmem + 128 * (k & 1), a_t + 8 * k, b, id128, k > 1 ? 1u : first);
         if (MODE == 5) mma_tf32(tmem + 256 * (k & 1), a, b, id256, k > 1 ? 1u : first);
+        if (MODE == 6) mma_tf32_ts(tmem + 64 * (k & 1), a_t + 8 * k, b, idesc_tf32_kmaj_mnmaj<128, 64>(), k > 1 ? 1u : first);
+        if (MODE == 7) mma_tf32_ts(tmem + 32 * (k & 1), a_t + 8 * k, b, idesc_tf32_kmaj_mnmaj<128, 32>(), k > 1 ? 1u : first);
+        if (MODE == 8) mma_tf32(tmem + 64 * (k & 1), a, b, idesc_tf32_kmaj_mnmaj<128, 64>(), k > 1 ? 1u : first);
     }
 }
 
@@ -73,5 +76,8 @@ int main() {
     run<3>("SS M128 N256 K8 (1 acc)");
     run<4>("TS M128 N128 K8 (2 accs)");
     run<5>("SS M128 N256 K8 (2 accs)");
+    run<6>("TS M128 N64 K8 (2 accs)");
+    run<7>("TS M128 N32 K8 (2 accs)");
+    run<8>("SS M128 N64 K8 (2 accs)");
     return 0;
 }
