@@ -44,25 +44,26 @@ namespace mxp {
 namespace {
 constexpr uint32_t kChunk = 128u * 128u;  // one 32-column chunk: 128 rows x 128 B
 constexpr uint32_t kPlane = 4u * kChunk;  // 64 KB
-constexpr int kK3Threads = 256;
+constexpr int kK3Threads = 512;  // 16 warps: 4 lane quarters x 4 column groups
 constexpr uint32_t kColD0 = 0, kColD1 = 128, kColHi = 256, kColLo = 384;
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023u) & ~uintptr_t(1023));
 }
 
-// Write 32 split values (row `row`, columns [col0, col0+32)) into the SMEM
-// right operand (MN-major SW128_BASE32B).  The 16-byte unit order is flipped
-// for rows with (row >> 2) odd so the 8 rows of a quarter-warp hit 8 distinct
-// 16-byte bank groups (no conflicts).
+// Write 16 split values (row `row`, columns [col0, col0+16), col0 % 16 == 0)
+// into the SMEM right operand (MN-major SW128_BASE32B).  The 16-byte unit
+// order is flipped for rows with (row >> 2) odd so the 8 rows of a
+// quarter-warp hit 8 distinct 16-byte bank groups (no conflicts).
 __device__ __forceinline__ void k3_put_right(uint32_t s_hi, uint32_t s_lo, uint32_t row, int col0,
-                                             const uint32_t (&h)[32], const uint32_t (&l)[32]) {
+                                             const uint32_t (&h)[16], const uint32_t (&l)[16]) {
     const uint32_t flip = (row >> 2) & 1u;
     const uint32_t base = (col0 >> 5) * kChunk + row * 128u;
+    const uint32_t u0 = (col0 & 31) >> 2;  // first 16-byte unit of this sub-chunk (0 or 4)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
         const int ua = u, ub = u ^ 1;
-        const uint32_t unit = static_cast<uint32_t>(u) ^ flip;
+        const uint32_t unit = u0 + (static_cast<uint32_t>(u) ^ flip);
         const uint32_t off = base + ((((unit >> 1) ^ (row & 3u)) << 1 | (unit & 1u)) << 4);
         uint32_t h0 = flip ? h[4 * ub] : h[4 * ua], h1 = flip ? h[4 * ub + 1] : h[4 * ua + 1];
         uint32_t h2 = flip ? h[4 * ub + 2] : h[4 * ua + 2], h3 = flip ? h[4 * ub + 3] : h[4 * ua + 3];
@@ -75,21 +76,22 @@ __device__ __forceinline__ void k3_put_right(uint32_t s_hi, uint32_t s_lo, uint3
 
 // ... and the same values into the TMEM left operand as well.
 __device__ __forceinline__ void k3_put_row(uint32_t s_hi, uint32_t s_lo, uint32_t row, int col0,
-                                           const uint32_t (&h)[32], const uint32_t (&l)[32],
+                                           const uint32_t (&h)[16], const uint32_t (&l)[16],
                                            uint32_t t_hi, uint32_t t_lo) {
-    tmem_st32(t_hi + col0, h);
-    tmem_st32(t_lo + col0, l);
+    tmem_st16(t_hi + col0, h);
+    tmem_st16(t_lo + col0, l);
     k3_put_right(s_hi, s_lo, row, col0, h, l);
 }
 
-// Row `row`, columns [col0, col0+32) of the staged input (TMA SWIZZLE_128B
+// Row `row`, columns [col0, col0+16) of the staged input (TMA SWIZZLE_128B
 // layout: chunk c = 128 rows x 128 B, 16-byte unit u of row r at u ^ (r%8)).
 __device__ __forceinline__ void k3_stage_row(uint32_t s_stage, uint32_t row, int col0,
-                                             uint32_t (&h)[32], uint32_t (&l)[32]) {
+                                             uint32_t (&h)[16], uint32_t (&l)[16]) {
     const uint32_t base = s_stage + (col0 >> 5) * kChunk + row * 128u;
+    const uint32_t u0 = (col0 & 31) >> 2;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        const uint4 x = lds128(base + ((static_cast<uint32_t>(u) ^ (row & 7u)) << 4));
+    for (int u = 0; u < 4; ++u) {
+        const uint4 x = lds128(base + (((u0 + u) ^ (row & 7u)) << 4));
         split_tf32(__uint_as_float(x.x), h[4 * u], l[4 * u]);
         split_tf32(__uint_as_float(x.y), h[4 * u + 1], l[4 * u + 1]);
         split_tf32(__uint_as_float(x.z), h[4 * u + 2], l[4 * u + 2]);
@@ -100,9 +102,9 @@ __device__ __forceinline__ void k3_stage_row(uint32_t s_stage, uint32_t row, int
 // Fallback for n % 4 != 0 (no TMA map) and for MULTIPLY_BASE steps: row from
 // global, zero padded.
 __device__ __forceinline__ void k3_global_row(const float* __restrict__ src, int n, uint32_t row,
-                                              int col0, uint32_t (&h)[32], uint32_t (&l)[32]) {
+                                              int col0, uint32_t (&h)[16], uint32_t (&l)[16]) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < 16; ++i) {
         const int c = col0 + i;
         const float v = (row < static_cast<uint32_t>(n) && c < n)
                             ? __ldg(src + static_cast<size_t>(row) * n + c)
@@ -120,8 +122,9 @@ size_t k3_smem_bytes() { return 3 * kPlane + 1024 + 256; }
 __global__ void __launch_bounds__(kK3Threads, 1)
     k3_batched_power(const __grid_constant__ CUtensorMap in_map, int use_tma,
                      const float* __restrict__ in, float* __restrict__ out, int n, long long batch,
-                     PlanBits plan) {
+                     PlanBits plan, long long* __restrict__ prof) {
     extern __shared__ uint8_t smem_raw[];
+    long long p_load = 0, p_mma = 0, p_epi = 0, p_t = 0;
     uint8_t* smem = align1024(smem_raw);
     uint64_t* mma_bar = reinterpret_cast<uint64_t*>(smem + 3 * kPlane);
     uint64_t* load_bar = mma_bar + 1;
@@ -147,7 +150,7 @@ __global__ void __launch_bounds__(kK3Threads, 1)
 
     const uint32_t s_hi = smem_u32(smem), s_lo = s_hi + kPlane, s_stage = s_hi + 2 * kPlane;
     const int q = warp & 3;             // TMEM lane quarter this warp may access
-    const int colh = (warp >> 2) * 64;  // column half handled by this warp
+    const int colg = (warp >> 2) * 32;  // 32-column group handled by this warp
     const uint32_t row = q * 32 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const uint32_t t_d0 = lane_base + kColD0, t_d1 = lane_base + kColD1;
@@ -165,6 +168,7 @@ __global__ void __launch_bounds__(kK3Threads, 1)
 
     for (long long m = blockIdx.x; m < batch; m += gridDim.x) {
         const float* src = in + static_cast<size_t>(m) * n * n;
+        if (prof) p_t = clock64();
         // ---- input -> right operand (SMEM) + left operand (TMEM)
         if (use_tma) {
             mbar_wait(load_bar, load_phase);
@@ -172,12 +176,12 @@ __global__ void __launch_bounds__(kK3Threads, 1)
         }
 #pragma unroll 1
         for (int j = 0; j < 2; ++j) {
-            uint32_t h[32], l[32];
+            uint32_t h[16], l[16];
             if (use_tma)
-                k3_stage_row(s_stage, row, colh + 32 * j, h, l);
+                k3_stage_row(s_stage, row, colg + 16 * j, h, l);
             else
-                k3_global_row(src, n, row, colh + 32 * j, h, l);
-            k3_put_row(s_hi, s_lo, row, colh + 32 * j, h, l, t_hi, t_lo);
+                k3_global_row(src, n, row, colg + 16 * j, h, l);
+            k3_put_row(s_hi, s_lo, row, colg + 16 * j, h, l, t_hi, t_lo);
         }
         tmem_st_wait();
         fence_proxy_async_smem();
@@ -185,16 +189,17 @@ __global__ void __launch_bounds__(kK3Threads, 1)
         __syncthreads();
         // staging is free again: prefetch the next matrix under this chain
         if (use_tma && tid == 0 && m + gridDim.x < batch) issue_load(m + gridDim.x);
+        if (prof) { long long t = clock64(); p_load += t - p_t; p_t = t; }
 
         for (int s = 0; s < plan.len; ++s) {
             if (plan_is_mult(plan, s)) {
                 // left operand <- base (the resident acc stays the right operand)
 #pragma unroll 1
                 for (int j = 0; j < 2; ++j) {
-                    uint32_t h[32], l[32];
-                    k3_global_row(src, n, row, colh + 32 * j, h, l);
-                    tmem_st32(t_hi + colh + 32 * j, h);
-                    tmem_st32(t_lo + colh + 32 * j, l);
+                    uint32_t h[16], l[16];
+                    k3_global_row(src, n, row, colg + 16 * j, h, l);
+                    tmem_st16(t_hi + colg + 16 * j, h);
+                    tmem_st16(t_lo + colg + 16 * j, l);
                 }
                 tmem_st_wait();
                 tc_fence_before();
@@ -221,36 +226,43 @@ __global__ void __launch_bounds__(kK3Threads, 1)
             }
             mbar_wait(mma_bar, mma_phase);
             mma_phase ^= 1;
+            if (prof) { long long t = clock64(); p_mma += t - p_t; p_t = t; }
             tc_fence_after();
             const bool last = (s == plan.len - 1);
-#pragma unroll 1
-            for (int j = 0; j < 2; ++j) {
-                const int col0 = colh + j * 32;
-                uint32_t v[32], w[32];
-                tmem_ld32(t_d0 + col0, v);
-                tmem_ld32(t_d1 + col0, w);
+            uint32_t v2[2][16];
+            {
+                uint32_t w0[16], w1[16];
+                tmem_ld16x4(t_d0 + colg, t_d1 + colg, t_d0 + colg + 16, t_d1 + colg + 16, v2[0], w0,
+                            v2[1], w1);
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    v[i] = __float_as_uint(__fadd_rn(__uint_as_float(v[i]), __uint_as_float(w[i])));
+                for (int i = 0; i < 16; ++i) {
+                    v2[0][i] = __float_as_uint(__fadd_rn(__uint_as_float(v2[0][i]), __uint_as_float(w0[i])));
+                    v2[1][i] = __float_as_uint(__fadd_rn(__uint_as_float(v2[1][i]), __uint_as_float(w1[i])));
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int col0 = colg + j * 16;
+                const uint32_t (&v)[16] = v2[j];
                 if (last) {
                     if (row < static_cast<uint32_t>(n)) {
                         float* dst = out + static_cast<size_t>(m) * n * n +
                                      static_cast<size_t>(row) * n + col0;
-                        if ((n & 3) == 0 && col0 + 32 <= n) {
+                        if ((n & 3) == 0 && col0 + 16 <= n) {
 #pragma unroll
-                            for (int u = 0; u < 8; ++u)
+                            for (int u = 0; u < 4; ++u)
                                 reinterpret_cast<float4*>(dst)[u] = make_float4(
                                     __uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]),
                                     __uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3]));
                         } else {
-                            for (int i = 0; i < 32; ++i)
+                            for (int i = 0; i < 16; ++i)
                                 if (col0 + i < n) dst[i] = __uint_as_float(v[i]);
                         }
                     }
                 } else {
-                    uint32_t h[32], l[32];
+                    uint32_t h[16], l[16];
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) split_tf32(__uint_as_float(v[i]), h[i], l[i]);
+                    for (int i = 0; i < 16; ++i) split_tf32(__uint_as_float(v[i]), h[i], l[i]);
                     k3_put_row(s_hi, s_lo, row, col0, h, l, t_hi, t_lo);
                 }
             }
@@ -258,11 +270,19 @@ __global__ void __launch_bounds__(kK3Threads, 1)
             tc_fence_before();
             fence_proxy_async_smem();
             __syncthreads();
+            if (prof) { long long t = clock64(); p_epi += t - p_t; p_t = t; }
         }
     }
     __syncthreads();
+    if (prof && blockIdx.x == 0 && tid == 0) {
+        prof[0] = p_load; prof[1] = p_mma; prof[2] = p_epi;
+    }
     if (warp == 1) tmem_dealloc<512>(tmem);
 }
+
+// Debug hook: when set (tools/), CTA 0 records per-phase cycle totals here.
+long long* g_k3_prof = nullptr;
+void k3_set_profile(long long* dev_buf) { g_k3_prof = dev_buf; }
 
 cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
                               const PlanBits& plan, int grid, cudaStream_t s) {
@@ -273,7 +293,7 @@ cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
     if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0)
         use_tma = encode_batch_map(&map, in, n, batch) ? 1 : 0;
     k3_batched_power<<<grid, kK3Threads, k3_smem_bytes(), s>>>(map, use_tma, in, out, n, batch,
-                                                               plan);
+                                                               plan, g_k3_prof);
     return cudaGetLastError();
 }
 

@@ -28,6 +28,7 @@ cudaError_t prepare_kernels();
 // time with the running power resident in shared memory.
 constexpr int kSmallMax = 128;
 size_t k3_smem_bytes();
+void k3_set_profile(long long* dev_buf);  // debug: per-phase cycle totals of CTA 0
 cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
                               const PlanBits& plan, int grid, cudaStream_t s);
 
