@@ -105,6 +105,12 @@ MXP_API int mxp_plan(int64_t k, char* steps, int64_t cap, int64_t* count);
 
 /* one multiply C = A * B */
 MXP_API int mxp_gemm(mxp_handle h, int mode, int64_t n, const void* dA, const void* dB, void* dC);
+/* a row block of one multiply: C[rows x n] = A[rows x n] * B[n x n] (row-major,
+ * leading dimension n).  The building block of the row-sharded multi-GPU chain:
+ * every element's arithmetic is the same as in mxp_gemm, so sharded results are
+ * bitwise equal to the single-GPU ones. */
+MXP_API int mxp_gemm_rows(mxp_handle h, int mode, int64_t n, int64_t rows, const void* dA,
+                          const void* dB, void* dC);
 MXP_API int mxp_multiply(mxp_handle h, int mode, int64_t n, const void* hA, const void* hB, void* hC,
                  mxp_stats* stats);
 

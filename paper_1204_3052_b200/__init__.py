@@ -69,4 +69,8 @@ def __getattr__(name):
         from .engine import Engine
 
         return Engine
+    if name in ("engine", "distributed", "build"):
+        import importlib
+
+        return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

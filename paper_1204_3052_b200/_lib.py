@@ -30,7 +30,7 @@ MXP_U32_MOD = 2
 # Every symbol the header declares (tests/test_abi.py checks the .so exports them).
 EXPORTS = (
     "mxp_version", "mxp_device_count", "mxp_create", "mxp_destroy", "mxp_get_stream",
-    "mxp_synchronize", "mxp_num_sms", "mxp_alloc", "mxp_free", "mxp_host_alloc",
+    "mxp_synchronize", "mxp_num_sms", "mxp_alloc", "mxp_free", "mxp_host_alloc", "mxp_gemm_rows",
     "mxp_host_free", "mxp_upload", "mxp_download", "mxp_plan", "mxp_gemm", "mxp_multiply",
     "mxp_power_device", "mxp_power", "mxp_power_batched_device", "mxp_power_batched",
     "mxp_power_mod_device", "mxp_power_mod", "mxp_random_device", "mxp_last_error",
@@ -92,6 +92,7 @@ def load() -> ctypes.CDLL:
             "mxp_download": [vp, vp, vp, sz],
             "mxp_plan": [i64, ctypes.c_char_p, i64, P(i64)],
             "mxp_gemm": [vp, c_int, i64, vp, vp, vp],
+            "mxp_gemm_rows": [vp, c_int, i64, i64, vp, vp, vp],
             "mxp_multiply": [vp, c_int, i64, vp, vp, vp, P(Stats)],
             "mxp_power_device": [vp, c_int, i64, i64, vp, vp, P(Stats)],
             "mxp_power": [vp, c_int, i64, i64, vp, vp, P(Stats)],

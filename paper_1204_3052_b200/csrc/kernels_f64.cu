@@ -135,24 +135,29 @@ cudaError_t prepare_f64_kernels() {
 }
 
 cudaError_t launch_f64_gemm(const double* a, const double* b, double* c, int n, cudaStream_t s) {
+    return launch_f64_gemm_rows(a, b, c, n, n, s);
+}
+
+cudaError_t launch_f64_gemm_rows(const double* a, const double* b, double* c, int n, int m,
+                                 cudaStream_t s) {
     constexpr int kSmem = kF64Smem;
-    dim3 grid(n / BN, n / BM);
+    dim3 grid(n / BN, m / BM);
     f64_gemm_kernel<<<grid, kThreads, kSmem, s>>>(a, b, c, n);
     return cudaGetLastError();
 }
 
-__global__ void f64_pad_kernel(const double* __restrict__ in, int n, double* __restrict__ out,
-                               int n_pad) {
-    const size_t total = static_cast<size_t>(n_pad) * n_pad;
+__global__ void f64_pad_kernel(const double* __restrict__ in, int n, int rows,
+                               double* __restrict__ out, int n_pad, int rows_pad) {
+    const size_t total = static_cast<size_t>(rows_pad) * n_pad;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int r = static_cast<int>(i / n_pad), c = static_cast<int>(i % n_pad);
-        out[i] = (r < n && c < n) ? in[static_cast<size_t>(r) * n + c] : 0.0;
+        out[i] = (r < rows && c < n) ? in[static_cast<size_t>(r) * n + c] : 0.0;
     }
 }
 __global__ void f64_unpad_kernel(const double* __restrict__ in, int n_pad, double* __restrict__ out,
-                                 int n) {
-    const size_t total = static_cast<size_t>(n) * n;
+                                 int n, int rows) {
+    const size_t total = static_cast<size_t>(rows) * n;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int r = static_cast<int>(i / n), c = static_cast<int>(i % n);
@@ -160,11 +165,19 @@ __global__ void f64_unpad_kernel(const double* __restrict__ in, int n_pad, doubl
     }
 }
 cudaError_t launch_f64_pad(const double* in, int n, double* out, int n_pad, cudaStream_t s) {
-    f64_pad_kernel<<<148 * 8, 256, 0, s>>>(in, n, out, n_pad);
-    return cudaGetLastError();
+    return launch_f64_pad_rows(in, n, n, out, n_pad, n_pad, s);
 }
 cudaError_t launch_f64_unpad(const double* in, int n_pad, double* out, int n, cudaStream_t s) {
-    f64_unpad_kernel<<<148 * 8, 256, 0, s>>>(in, n_pad, out, n);
+    return launch_f64_unpad_rows(in, n_pad, out, n, n, s);
+}
+cudaError_t launch_f64_pad_rows(const double* in, int n, int rows, double* out, int n_pad,
+                                int rows_pad, cudaStream_t s) {
+    f64_pad_kernel<<<148 * 8, 256, 0, s>>>(in, n, rows, out, n_pad, rows_pad);
+    return cudaGetLastError();
+}
+cudaError_t launch_f64_unpad_rows(const double* in, int n_pad, double* out, int n, int rows,
+                                  cudaStream_t s) {
+    f64_unpad_kernel<<<148 * 8, 256, 0, s>>>(in, n_pad, out, n, rows);
     return cudaGetLastError();
 }
 

@@ -302,15 +302,15 @@ cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
 // ======================================================================
 __global__ void split_pad_kernel(const float* __restrict__ in, int n, int ld,
                                  uint32_t* __restrict__ hi, uint32_t* __restrict__ lo,
-                                 int n_pad) {
-    const size_t quads = static_cast<size_t>(n_pad) * n_pad / 4;
+                                 int n_pad, int rows, int rows_pad) {
+    const size_t quads = static_cast<size_t>(rows_pad) * n_pad / 4;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < quads;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const size_t e = i * 4;
         const int r = static_cast<int>(e / n_pad);
         const int c = static_cast<int>(e - static_cast<size_t>(r) * n_pad);
         float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (r < n) {
+        if (r < rows) {
             const float* p = in + static_cast<size_t>(r) * ld + c;
             if ((ld & 3) == 0 && c + 3 < n) {
                 float4 t = __ldg(reinterpret_cast<const float4*>(p));
@@ -333,10 +333,15 @@ __global__ void split_pad_kernel(const float* __restrict__ in, int n, int ld,
 
 cudaError_t launch_split(const float* in, int n, int ld, uint32_t* hi, uint32_t* lo, int n_pad,
                          cudaStream_t s) {
-    const size_t quads = static_cast<size_t>(n_pad) * n_pad / 4;
+    return launch_split_rows(in, n, ld, n, hi, lo, n_pad, n_pad, s);
+}
+
+cudaError_t launch_split_rows(const float* in, int n, int ld, int rows, uint32_t* hi, uint32_t* lo,
+                              int n_pad, int rows_pad, cudaStream_t s) {
+    const size_t quads = static_cast<size_t>(rows_pad) * n_pad / 4;
     int blocks = static_cast<int>((quads + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    split_pad_kernel<<<blocks, 256, 0, s>>>(in, n, ld, hi, lo, n_pad);
+    split_pad_kernel<<<blocks, 256, 0, s>>>(in, n, ld, hi, lo, n_pad, rows, rows_pad);
     return cudaGetLastError();
 }
 
@@ -396,8 +401,8 @@ struct K1Cfg {
 __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
     k1_gemm_3xtf32(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                    const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
-                   int n_pad, float* __restrict__ out_f32, int n_out, int ld_out,
-                   uint32_t* __restrict__ out_hi, uint32_t* __restrict__ out_lo) {
+                   int n_pad, int m_pad, float* __restrict__ out_f32, int n_out, int m_out,
+                   int ld_out, uint32_t* __restrict__ out_hi, uint32_t* __restrict__ out_lo) {
     using Cfg = K1Cfg;
     constexpr int S = Cfg::kStages;
     constexpr int BN = Cfg::kBN;
@@ -415,7 +420,7 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
     // before moving right, so the CTAs resident at once share A row slabs
     // and B column slabs in L2 instead of each wave streaming all of B.
     constexpr int kGroupM = 16;
-    const int num_m = n_pad / 128, num_n = n_pad / BN;
+    const int num_m = m_pad / 128, num_n = n_pad / BN;
     const int pid = blockIdx.x;
     const int per_group = kGroupM * num_n;
     const int first_m = (pid / per_group) * kGroupM;
@@ -532,7 +537,7 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
                     dl[u] = lv;
                 }
             }
-            if (out_f32 != nullptr && row < n_out && col < n_out) {
+            if (out_f32 != nullptr && row < m_out && col < n_out) {
                 float* d = out_f32 + static_cast<size_t>(row) * ld_out + col;
                 if ((ld_out & 3) == 0 && col + 32 <= n_out) {
 #pragma unroll
@@ -570,10 +575,11 @@ static EncodeTiledFn get_encode_fn() {
 }
 
 bool encode_plane_map(CUtensorMap* map, const void* plane, int n_pad, int box_cols, int box_rows,
-                      bool right_operand) {
+                      bool right_operand, int rows) {
     EncodeTiledFn fn = get_encode_fn();
     if (fn == nullptr) return false;
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(n_pad), static_cast<cuuint64_t>(n_pad)};
+    if (rows <= 0) rows = n_pad;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(n_pad), static_cast<cuuint64_t>(rows)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(n_pad) * 4};
     cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
     cuuint32_t estr[2] = {1, 1};
@@ -618,10 +624,17 @@ cudaError_t prepare_tf32_kernels() {
 cudaError_t launch_k1_gemm(const GemmPlanes& m, int n_pad, int block_n, float* out_f32,
                            int n_out, int ld_out, uint32_t* out_hi, uint32_t* out_lo,
                            cudaStream_t s) {
+    return launch_k1_gemm_rows(m, n_pad, n_pad, block_n, out_f32, n_out, n_out, ld_out, out_hi,
+                               out_lo, s);
+}
+
+cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int block_n,
+                                float* out_f32, int n_out, int m_out, int ld_out, uint32_t* out_hi,
+                                uint32_t* out_lo, cudaStream_t s) {
     (void)block_n;
-    dim3 grid((n_pad / K1Cfg::kBN) * (n_pad / 128));
-    k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad,
-                                                               out_f32, n_out, ld_out, out_hi, out_lo);
+    dim3 grid((n_pad / K1Cfg::kBN) * (m_pad / 128));
+    k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(
+        m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo);
     return cudaGetLastError();
 }
 

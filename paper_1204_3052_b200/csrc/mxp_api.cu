@@ -99,6 +99,9 @@ struct mxp_handle_s {
     // fp64 workspace: base, ping, pong (n_pad^2 doubles)
     int64_t ws64_pad = 0;
     double* f64buf[3] = {};
+    // modular workspace: base limbs (3), acc limbs (3), T0..T2 (3), n_pad^2 doubles each
+    int64_t wsmod_pad = 0;
+    double* modbuf[9] = {};
     // host-API staging device buffers
     size_t io_bytes = 0;
     void* d_in = nullptr;
@@ -444,6 +447,8 @@ int mxp_destroy(mxp_handle h) {
         if (p) cudaFree(p);
     for (auto p : h->f64buf)
         if (p) cudaFree(p);
+    for (auto p : h->modbuf)
+        if (p) cudaFree(p);
     if (h->d_in) cudaFree(h->d_in);
     if (h->d_in2) cudaFree(h->d_in2);
     if (h->d_out) cudaFree(h->d_out);
@@ -558,6 +563,54 @@ int mxp_gemm(mxp_handle h, int mode, int64_t n, const void* dA, const void* dB, 
     if (e == cudaSuccess)
         e = launch_f64_unpad(b[2], (int)n_pad, static_cast<double*>(dC), (int)n, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "f64 gemm");
+    return MXP_OK;
+}
+
+int mxp_gemm_rows(mxp_handle h, int mode, int64_t n, int64_t rows, const void* dA, const void* dB,
+                  void* dC) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    rc = validate(mode, n, 2);
+    if (rc) return rc;
+    if (rows < 1 || rows > n)
+        return fail(MXP_E_VALIDATION, "row block must satisfy 1 <= rows <= n, got %lld", (long long)rows);
+    if (!dA || !dB || !dC) return fail(MXP_E_VALIDATION, "null device pointer");
+    const int64_t n_pad = round_up(n, 128), r_pad = round_up(rows, 128);
+    if (mode == MXP_F32) {
+        rc = ensure_ws32(h, n_pad);
+        if (rc) return rc;
+        const int np = (int)h->ws32_pad;
+        CUtensorMap a_hi, a_lo, b_hi, b_lo;
+        if (!encode_plane_map(&a_hi, h->planes[0], np, 32, 128, false, (int)r_pad) ||
+            !encode_plane_map(&a_lo, h->planes[1], np, 32, 128, false, (int)r_pad) ||
+            !encode_plane_map(&b_hi, h->planes[2], np, 32, 32, true) ||
+            !encode_plane_map(&b_lo, h->planes[3], np, 32, 32, true))
+            return fail(MXP_E_CUDA, "cuTensorMapEncodeTiled failed");
+        cudaError_t e = launch_split_rows(static_cast<const float*>(dA), (int)n, (int)n, (int)rows,
+                                          h->planes[0], h->planes[1], np, (int)r_pad, h->stream);
+        if (e == cudaSuccess)
+            e = launch_split(static_cast<const float*>(dB), (int)n, (int)n, h->planes[2],
+                             h->planes[3], np, h->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "split");
+        GemmPlanes m{a_hi, a_lo, b_hi, b_lo};
+        e = launch_k1_gemm_rows(m, np, (int)r_pad, k1_block_n(np, h->num_sms),
+                                static_cast<float*>(dC), (int)n, (int)rows, (int)n, nullptr, nullptr,
+                                h->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "k1_gemm_3xtf32");
+        return MXP_OK;
+    }
+    rc = ensure_ws64(h, n_pad);
+    if (rc) return rc;
+    double** b = h->f64buf;
+    cudaError_t e = launch_f64_pad_rows(static_cast<const double*>(dA), (int)n, (int)rows, b[0],
+                                        (int)n_pad, (int)r_pad, h->stream);
+    if (e == cudaSuccess)
+        e = launch_f64_pad(static_cast<const double*>(dB), (int)n, b[1], (int)n_pad, h->stream);
+    if (e == cudaSuccess) e = launch_f64_gemm_rows(b[0], b[1], b[2], (int)n_pad, (int)r_pad, h->stream);
+    if (e == cudaSuccess)
+        e = launch_f64_unpad_rows(b[2], (int)n_pad, static_cast<double*>(dC), (int)n, (int)rows,
+                                  h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "f64 gemm rows");
     return MXP_OK;
 }
 
@@ -789,15 +842,96 @@ int mxp_random_device(mxp_handle h, int mode, int64_t n, int64_t batch, uint64_t
 int mxp_power_mod_device(mxp_handle h, int64_t n, int64_t k, uint32_t p, const void* dA,
                          void* dOut, mxp_stats* st) {
     stats_reset(st);
-    (void)h; (void)n; (void)k; (void)p; (void)dA; (void)dOut;
-    return fail(MXP_E_UNSUPPORTED, "modular mode is not built into this library yet");
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (n < 1) return fail(MXP_E_VALIDATION, "matrix order must be >= 1, got %lld", (long long)n);
+    if (n > 32768)
+        return fail(MXP_E_UNSUPPORTED, "matrix order %lld exceeds the supported 32768", (long long)n);
+    if (k < 0) return fail(MXP_E_VALIDATION, "power must be >= 0, got %lld", (long long)k);
+    if (p < 2 || p >= (1u << 31))
+        return fail(MXP_E_VALIDATION, "modulus must satisfy 2 <= p < 2^31, got %u", p);
+    if (!dA || !dOut) return fail(MXP_E_VALIDATION, "null device pointer");
+    fill_plan_stats(st, k, 1);
+    const uint32_t* a = static_cast<const uint32_t*>(dA);
+    uint32_t* out = static_cast<uint32_t*>(dOut);
+    int64_t launches = 0;
+    if (k <= 1) {
+        cudaError_t e = launch_mod_trivial(out, a, (int)n, p, k == 1, h->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "mod_trivial");
+        if (st) st->launches = 1;
+        return MXP_OK;
+    }
+    const int64_t n_pad = f64_pad((int)n);
+    if (h->wsmod_pad < n_pad) {
+        for (auto& q : h->modbuf) {
+            if (q) cudaFree(q);
+            q = nullptr;
+        }
+        h->wsmod_pad = 0;
+        for (auto& q : h->modbuf)
+            MXP_CUDA(cudaMalloc(&q, static_cast<size_t>(n_pad) * n_pad * sizeof(double)));
+        h->wsmod_pad = n_pad;
+    }
+    const int np = (int)h->wsmod_pad;
+    double** B = h->modbuf;  // base: 0..2, acc: 3..5, T0,T1,T2: 6..8
+    cudaError_t e = launch_mod_split(a, (int)n, p, B[0], B[1], B[2], np, h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "mod_split");
+    ++launches;
+    const PlanBits plan = make_plan(k);
+    int acc = 0;  // limb set index: 0 = base planes, 3 = acc planes
+    for (int s = 0; s < plan.len; ++s) {
+        const int rhs = plan_is_mult(plan, s) ? 0 : acc;
+        const bool last = (s == plan.len - 1);
+        e = launch_f64_gemm(B[acc + 1], B[rhs + 1], B[7], np, h->stream);           // T1
+        if (e == cudaSuccess) e = launch_f64_gemm(B[acc], B[rhs], B[6], np, h->stream);  // T0
+        if (e == cudaSuccess) e = launch_f64_gemm(B[acc + 2], B[rhs + 2], B[8], np, h->stream);
+        if (e == cudaSuccess)
+            e = launch_mod_combine(B[6], B[7], B[8], p, np, B[3], B[4], B[5],
+                                   last ? out : nullptr, (int)n, h->stream);
+        if (e != cudaSuccess) {
+            if (st) st->failed_step = s;
+            return cuda_fail(e, "modular multiply");
+        }
+        launches += 4;
+        acc = 3;
+    }
+    if (st) st->launches = launches;
+    return MXP_OK;
 }
 
 int mxp_power_mod(mxp_handle h, int64_t n, int64_t k, uint32_t p, const void* hA, void* hOut,
                   mxp_stats* st) {
     stats_reset(st);
-    (void)h; (void)n; (void)k; (void)p; (void)hA; (void)hOut;
-    return fail(MXP_E_UNSUPPORTED, "modular mode is not built into this library yet");
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (n < 1) return fail(MXP_E_VALIDATION, "matrix order must be >= 1, got %lld", (long long)n);
+    if (!hA || !hOut) return fail(MXP_E_VALIDATION, "null host pointer");
+    const size_t bytes = static_cast<size_t>(n) * n * 4;
+    rc = ensure_io(h, bytes);
+    if (rc) return rc;
+    MXP_CUDA(cudaMemcpyAsync(h->d_in, hA, bytes, cudaMemcpyHostToDevice, h->stream));
+    MXP_CUDA(cudaEventRecord(h->ev0, h->stream));
+    mxp_stats inner;
+    rc = mxp_power_mod_device(h, n, k, p, h->d_in, h->d_out, &inner);
+    if (rc) {
+        if (st) st->failed_step = inner.failed_step;
+        return rc;
+    }
+    MXP_CUDA(cudaEventRecord(h->ev1, h->stream));
+    MXP_CUDA(cudaMemcpyAsync(hOut, h->d_out, bytes, cudaMemcpyDeviceToHost, h->stream));
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "modular power");
+    if (st) {
+        *st = inner;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+        st->device_ms = ms;
+        st->h2d = 1;
+        st->d2h = 1;
+        st->h2d_bytes = bytes;
+        st->d2h_bytes = bytes;
+    }
+    return MXP_OK;
 }
 
 }  // extern "C"

@@ -48,11 +48,17 @@ struct GemmPlanes {
 };
 bool encode_batch_map(CUtensorMap* map, const void* base, int n, int64_t batch);
 bool encode_plane_map(CUtensorMap* map, const void* plane, int n_pad, int box_cols, int box_rows,
-                      bool right_operand);
+                      bool right_operand, int rows = 0);
 int k1_block_n(int n_pad, int num_sms);
 cudaError_t launch_k1_gemm(const GemmPlanes& maps, int n_pad, int block_n, float* out_f32,
                            int n_out, int ld_out, uint32_t* out_hi, uint32_t* out_lo,
                            cudaStream_t s);
+// Row block: C[m_pad x n_pad] = A[m_pad x n_pad] * B[n_pad x n_pad].
+cudaError_t launch_k1_gemm_rows(const GemmPlanes& maps, int n_pad, int m_pad, int block_n,
+                                float* out_f32, int n_out, int m_out, int ld_out, uint32_t* out_hi,
+                                uint32_t* out_lo, cudaStream_t s);
+cudaError_t launch_split_rows(const float* in, int n, int ld, int rows, uint32_t* hi, uint32_t* lo,
+                              int n_pad, int rows_pad, cudaStream_t s);
 
 // ---- generation (kernels_gen.cu) -------------------------------------------
 // Reference random_matrix (linalg.py:127-148) on device; scale != 0 selects
@@ -63,8 +69,24 @@ cudaError_t launch_random(int mode, int64_t n, int64_t batch, uint64_t seed0, do
 
 // ---- FP64 (kernels_f64.cu) ------------------------------------------------
 cudaError_t launch_f64_gemm(const double* a, const double* b, double* c, int n, cudaStream_t s);
+// Row block: C[m x n] = A[m x n] * B[n x n] (m, n multiples of 128).
+cudaError_t launch_f64_gemm_rows(const double* a, const double* b, double* c, int n, int m,
+                                 cudaStream_t s);
+cudaError_t launch_f64_pad_rows(const double* in, int n, int rows, double* out, int n_pad,
+                                int rows_pad, cudaStream_t s);
+cudaError_t launch_f64_unpad_rows(const double* in, int n_pad, double* out, int n, int rows,
+                                  cudaStream_t s);
 cudaError_t launch_f64_pad(const double* in, int n, double* out, int n_pad, cudaStream_t s);
 cudaError_t launch_f64_unpad(const double* in, int n_pad, double* out, int n, cudaStream_t s);
 int f64_pad(int n);
+
+// ---- exact modular mode (kernels_mod.cu): 16-bit limbs, Karatsuba, DMMA ---
+cudaError_t launch_mod_split(const uint32_t* in, int n, uint32_t p, double* l0, double* l1,
+                             double* ls, int n_pad, cudaStream_t s);
+cudaError_t launch_mod_combine(const double* t0, const double* t1, const double* t2, uint32_t p,
+                               int n_pad, double* l0, double* l1, double* ls, uint32_t* out,
+                               int n, cudaStream_t s);
+cudaError_t launch_mod_trivial(uint32_t* out, const uint32_t* a, int n, uint32_t p, int copy,
+                               cudaStream_t s);
 
 }  // namespace mxp

@@ -1,0 +1,152 @@
+"""Multi-GPU execution: one process per GPU, torch.distributed for plumbing.
+
+Two strategies:
+
+* ``exponentiate_batched_sharded`` — independent matrices (config 3): rank r
+  takes the contiguous slice ``shard_range(batch, r, world)``; no collective
+  on the data path, results are bitwise the single-GPU ones.
+* ``exponentiate_row_sharded`` — one large matrix (config 5): rank g owns
+  rows R_g of the running power.  Each step computes its row block
+  ``P'[R_g, :] = P[R_g, :] @ RHS`` (RHS = P for SQUARE, the replicated base A
+  for MULTIPLY_BASE, accumulator on the left as in expo.py:133-136) and then
+  all-gathers the row blocks (NCCL over NVLink) so every rank holds the full
+  P' for the next squaring.  Every element keeps its full-K dot product on one
+  GPU, so the result is bitwise equal to the single-GPU chain.
+
+The per-step compute is injectable (``ops``) so the host-side sharding and
+collective logic is tested with the gloo backend on CPU (tests/
+test_distributed.py); on B200s the default ops call the C ABI
+(mxp_gemm_rows / mxp_power_batched_device) on the engine's CUDA stream,
+which is also the stream the NCCL all-gather is issued on.
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Optional
+
+from .expo import Step, plan_exponentiation
+
+
+def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous [start, end) slice of `total` units for `rank` (sizes differ by <= 1)."""
+    base, extra = divmod(total, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def padded_rows(n: int, world: int) -> int:
+    """Rows per rank when n is padded to a multiple of `world` (zero padding keeps
+    the top-left n x n block of every power exact)."""
+    return math.ceil(n / world)
+
+
+class EngineOps:
+    """Device ops over the C ABI, on the engine's stream (torch tensors in HBM)."""
+
+    def __init__(self, engine):
+        self.eng = engine
+
+    def stream(self):
+        import torch
+
+        return torch.cuda.ExternalStream(self.eng.stream)
+
+    def gemm_rows(self, a_rows, b, out):
+        from . import _lib
+
+        mode = _lib.MXP_F32 if str(b.dtype) == "torch.float32" else _lib.MXP_F64
+        self.eng.gemm_rows_device(a_rows.data_ptr(), b.data_ptr(), out.data_ptr(), b.shape[0],
+                                  a_rows.shape[0], mode)
+
+    def power_batched(self, a, k, out):
+        from . import _lib
+
+        mode = _lib.MXP_F32 if str(a.dtype) == "torch.float32" else _lib.MXP_F64
+        self.eng.power_batched_device(a.data_ptr(), out.data_ptr(), a.shape[1], a.shape[0], k, mode)
+
+
+def _all_gather_rows(full, local, group, dist):
+    """full[(r*rows):(r+1)*rows] <- local of rank r, on every rank."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(full, local.contiguous(), group=group)
+    else:  # gloo: list form
+        world = dist.get_world_size(group)
+        parts = list(full.chunk(world, dim=0))
+        dist.all_gather(parts, local.contiguous(), group=group)
+
+
+def exponentiate_row_sharded(a, power: int, group=None, ops=None):
+    """A^power for one n x n matrix with its rows sharded over the group.
+
+    `a` is the full base matrix (torch tensor, replicated on every rank, on
+    this rank's device).  Returns the full A^power on every rank.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    plan = plan_exponentiation(power)
+    n = a.shape[0]
+    if power == 0:
+        return torch.eye(n, dtype=a.dtype, device=a.device)
+    if power == 1:
+        return a.clone()
+    rows = padded_rows(n, world)
+    n_p = rows * world
+    if ops is None:
+        from .engine import default_engine
+
+        ops = EngineOps(default_engine(a.device.index or 0))
+    stream = ops.stream() if hasattr(ops, "stream") else None
+    ctx = torch.cuda.stream(stream) if stream is not None else _nullcontext()
+    with ctx:
+        base = torch.zeros((n_p, n_p), dtype=a.dtype, device=a.device)
+        base[:n, :n] = a  # zero padding never mixes into the top-left n x n block
+        full = base.clone()
+        local = torch.empty((rows, n_p), dtype=a.dtype, device=a.device)
+        r0 = rank * rows
+        for step in plan.steps:
+            rhs = full if step is Step.SQUARE else base
+            ops.gemm_rows(full[r0:r0 + rows], rhs, local)
+            nxt = torch.empty_like(full)
+            _all_gather_rows(nxt, local, group, dist)
+            full = nxt
+        return full[:n, :n].contiguous()
+
+
+def exponentiate_batched_sharded(a_local, power: int, ops=None):
+    """A_i^power for this rank's shard (independent matrices, no collective)."""
+    import torch
+
+    if ops is None:
+        from .engine import default_engine
+
+        ops = EngineOps(default_engine(a_local.device.index or 0))
+    out = torch.empty_like(a_local)
+    ops.power_batched(a_local, power, out)
+    return out
+
+
+def gather_batched(local, total: int, group=None):
+    """Concatenate every rank's shard (uneven shards allowed) on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    sizes = [shard_range(total, r, world)[1] - shard_range(total, r, world)[0] for r in range(world)]
+    width = max(sizes)
+    padded = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    padded[: local.shape[0]] = local
+    parts = [torch.empty_like(padded) for _ in range(world)]
+    dist.all_gather(parts, padded, group=group)
+    return torch.cat([p[:s] for p, s in zip(parts, sizes)], dim=0)
+
+
+class _nullcontext:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False

@@ -178,6 +178,13 @@ class Engine:
         _lib.check(self._L.mxp_gemm(self._h, mode, n, ctypes.c_void_p(d_a), ctypes.c_void_p(d_b),
                                     ctypes.c_void_p(d_c)), "mxp_gemm")
 
+    def gemm_rows_device(self, d_a: int, d_b: int, d_c: int, n: int, rows: int,
+                         mode: int = _lib.MXP_F32) -> None:
+        """C[rows x n] = A[rows x n] * B[n x n] on device (row block of one multiply)."""
+        _lib.check(self._L.mxp_gemm_rows(self._h, mode, n, rows, ctypes.c_void_p(d_a),
+                                         ctypes.c_void_p(d_b), ctypes.c_void_p(d_c)),
+                   "mxp_gemm_rows")
+
     def random_device(self, d_out: int, n: int, batch: int = 1, seed0: int = 0,
                       lo: float = -0.5, hi: float = 0.5, scale: float = 0.0,
                       mode: int = _lib.MXP_F32) -> None:

@@ -290,3 +290,82 @@ def test_row_stochastic_8192_a1024():
     got = eng.power(a, 1024)
     sums = got.astype(np.float64).sum(axis=1)
     assert np.abs(sums - 1.0).max() <= 16 * 10 * math.sqrt(n) * U32
+
+
+# ------------------------------------------------------------------ exact modular mode
+@pytest.mark.parametrize("n,k,p", [(2, 60, 10), (5, 6, 97), (64, 13, 2**31 - 1), (130, 257, 65521),
+                                   (200, 1000, 1000003), (1, 5, 7), (257, 2, 2**31 - 1)])
+def test_modular_bitexact_vs_oracle(eng, n, k, p):
+    rng = np.random.default_rng(n * 1000 + k)
+    a = rng.integers(0, 2**32 - 1, size=(n, n), dtype=np.uint64).astype(np.uint32)
+    got = eng.power_mod(a, k, p)
+    ref = oracle.exponentiate_mod(a, k, p)
+    assert np.array_equal(got, ref), (n, k, p)
+    assert eng.last_stats.multiply_count == mx.multiply_count(k)
+
+
+def test_modular_kats(eng):
+    q = np.array([[1, 1], [1, 0]], dtype=np.uint32)
+    assert np.array_equal(eng.power_mod(q, 60, 10), np.eye(2))      # Pisano period pi(10) = 60
+    assert np.array_equal(eng.power_mod(q, 16, 7), np.eye(2))       # pi(7) = 16
+    fib = [0, 1]
+    for _ in range(200):
+        fib.append(fib[-1] + fib[-2])
+    p = 2**31 - 1
+    got = eng.power_mod(q, 150, p)
+    assert int(got[0, 1]) == fib[150] % p and int(got[0, 0]) == fib[151] % p
+    n = 4096  # permutation of order 12 at a large size: P^12 == I exactly
+    perm = np.arange(n)
+    for base in range(0, n - 7, 7):
+        perm[base:base + 3] = np.roll(perm[base:base + 3], 1)
+        perm[base + 3:base + 7] = np.roll(perm[base + 3:base + 7], 1)
+    pm = np.zeros((n, n), dtype=np.uint32)
+    pm[np.arange(n), perm] = 1
+    assert np.array_equal(eng.power_mod(pm, 12, 1000003), np.eye(n, dtype=np.uint32))
+    assert np.array_equal(eng.power_mod(pm, 0, 5), np.eye(n, dtype=np.uint32))
+    with pytest.raises(ValueError):
+        eng.power_mod(q, 3, 1)
+
+
+# ------------------------------------------------------------------ multi-GPU building blocks
+@pytest.mark.parametrize("n,rows", [(256, 128), (300, 77), (8192, 1024)])
+def test_gemm_rows_bitwise_equals_full_multiply(n, rows):
+    """A row block of one multiply is bitwise the same rows of the full product
+    (the property that makes row-sharded chains equal to single-GPU ones)."""
+    import torch
+
+    eng = mx.Engine(0)
+    a = torch.from_numpy(oracle.random_matrix(n, np.float32, 3)).cuda()
+    b = torch.from_numpy(oracle.random_matrix(n, np.float32, 4)).cuda()
+    full = torch.empty_like(a)
+    part = torch.empty((rows, n), dtype=a.dtype, device=a.device)
+    r0 = n - rows
+    eng.gemm_device(a.data_ptr(), b.data_ptr(), full.data_ptr(), n)
+    eng.gemm_rows_device(a[r0:].contiguous().data_ptr(), b.data_ptr(), part.data_ptr(), n, rows)
+    eng.synchronize()
+    assert torch.equal(part, full[r0:])
+
+
+def test_row_sharded_chain_single_rank_nccl():
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1204_3052_b200 import distributed as D
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        a = torch.from_numpy(oracle.scaled_input(512, np.float32, 42)).cuda()
+        got = D.exponentiate_row_sharded(a, 1000)
+        torch.cuda.synchronize()
+        ref = mx.Engine(0).power(a.cpu().numpy(), 1000)
+        assert np.array_equal(got.cpu().numpy(), ref)  # bitwise: same kernels, same order
+        batch = torch.from_numpy(mx.scaled_batch(64, 10, mx.DType.F32, 1)).cuda()
+        out = D.exponentiate_batched_sharded(batch, 64)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), mx.exponentiate_batched(batch.cpu().numpy(), 64))
+    finally:
+        dist.destroy_process_group()
