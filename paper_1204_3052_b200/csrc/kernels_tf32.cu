@@ -74,6 +74,23 @@ __device__ __forceinline__ void k3_put_right(uint32_t s_hi, uint32_t s_lo, uint3
     }
 }
 
+// One plane only (16 values of row `row`, columns [col0, col0+16)).
+__device__ __forceinline__ void k3_put_half(uint32_t s_plane, uint32_t row, int col0,
+                                            const uint32_t (&h)[16]) {
+    const uint32_t flip = (row >> 2) & 1u;
+    const uint32_t base = (col0 >> 5) * kChunk + row * 128u;
+    const uint32_t u0 = (col0 & 31) >> 2;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int ua = u, ub = u ^ 1;
+        const uint32_t unit = u0 + (static_cast<uint32_t>(u) ^ flip);
+        const uint32_t off = base + ((((unit >> 1) ^ (row & 3u)) << 1 | (unit & 1u)) << 4);
+        uint32_t h0 = flip ? h[4 * ub] : h[4 * ua], h1 = flip ? h[4 * ub + 1] : h[4 * ua + 1];
+        uint32_t h2 = flip ? h[4 * ub + 2] : h[4 * ua + 2], h3 = flip ? h[4 * ub + 3] : h[4 * ua + 3];
+        sts128(s_plane + off, h0, h1, h2, h3);
+    }
+}
+
 // ... and the same values into the TMEM left operand as well.
 __device__ __forceinline__ void k3_put_row(uint32_t s_hi, uint32_t s_lo, uint32_t row, int col0,
                                            const uint32_t (&h)[16], const uint32_t (&l)[16],
@@ -116,18 +133,28 @@ __device__ __forceinline__ void k3_global_row(const float* __restrict__ src, int
 
 size_t k3_smem_bytes() { return 3 * kPlane + 1024 + 256; }
 
-// use_tma: the input tensor map is valid (n % 4 == 0); matrices are then
-// prefetched one ahead into a 64 KB staging buffer while the current chain
-// runs.  Otherwise every row is read from global at the start of its chain.
-__global__ void __launch_bounds__(kK3Threads, 1)
+// Warp roles: 16 warps drain/convert (warp w owns TMEM lane quarter w % 4 and
+// the 32-column group 32 * (w / 4)); lane 0 of warp 0 additionally issues
+// every tcgen05.mma and TMA prefetch (after waiting, converged, on the same
+// barriers).  Each step's operands are published in two sets so the next
+// step's MMAs start before the epilogue has finished:
+//   set 1 = {A_lo (TMEM), B_hi (SMEM)} -> the 16 lo*hi MMAs may start
+//   set 2 = {A_hi (TMEM), B_lo (SMEM)} -> the 16 hi*lo and 16 hi*hi MMAs
+// (small cross terms still precede the big terms in every accumulator).
+constexpr int kK3Workers = 16;
+constexpr int kK3AllThreads = kK3Workers * 32;
+
+__global__ void __launch_bounds__(kK3AllThreads, 1)
     k3_batched_power(const __grid_constant__ CUtensorMap in_map, int use_tma,
                      const float* __restrict__ in, float* __restrict__ out, int n, long long batch,
                      PlanBits plan, long long* __restrict__ prof) {
     extern __shared__ uint8_t smem_raw[];
-    long long p_load = 0, p_mma = 0, p_epi = 0, p_t = 0;
     uint8_t* smem = align1024(smem_raw);
-    uint64_t* mma_bar = reinterpret_cast<uint64_t*>(smem + 3 * kPlane);
-    uint64_t* load_bar = mma_bar + 1;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 3 * kPlane);
+    uint64_t* mma_bar = bars + 0;   // MMAs of a step complete (tcgen05.commit)
+    uint64_t* set1_bar = bars + 1;  // A_lo + B_hi published (16 warp arrivals)
+    uint64_t* set2_bar = bars + 2;  // A_hi + B_lo published (16 warp arrivals)
+    uint64_t* load_bar = bars + 3;  // TMA staging landed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 3 * kPlane + 64);
 
     const int tid = threadIdx.x;
@@ -137,6 +164,8 @@ __global__ void __launch_bounds__(kK3Threads, 1)
 
     if (tid == 0) {
         mbar_init(mma_bar, 1);
+        mbar_init(set1_bar, kK3Workers);
+        mbar_init(set2_bar, kK3Workers);
         mbar_init(load_bar, 1);
         fence_mbar_init();
         if (use_tma) tma_prefetch(&in_map);
@@ -146,88 +175,108 @@ __global__ void __launch_bounds__(kK3Threads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    uint32_t mma_phase = 0, load_phase = 0;
-
     const uint32_t s_hi = smem_u32(smem), s_lo = s_hi + kPlane, s_stage = s_hi + 2 * kPlane;
-    const int q = warp & 3;             // TMEM lane quarter this warp may access
-    const int colg = (warp >> 2) * 32;  // 32-column group handled by this warp
-    const uint32_t row = q * 32 + lane;
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    const uint32_t t_d0 = lane_base + kColD0, t_d1 = lane_base + kColD1;
-    const uint32_t t_hi = lane_base + kColHi, t_lo = lane_base + kColLo;
     const uint64_t bdesc_hi = mnmajor_desc(s_hi, kChunk), bdesc_lo = mnmajor_desc(s_lo, kChunk);
 
-    auto issue_load = [&](long long mm) {  // one thread
+    auto issue_load = [&](long long mm) {  // warp 0 lane 0
         mbar_expect_tx(load_bar, 4 * kChunk);
 #pragma unroll
         for (int c = 0; c < 4; ++c)
             tma_load_3d(smem + 2 * kPlane + c * kChunk, &in_map, load_bar, 32 * c, 0,
                         static_cast<int32_t>(mm));
     };
+
+    long long p_load = 0, p_mma = 0, p_epi = 0, p_t = 0;
+    const int q = warp & 3;
+    const int colg = (warp >> 2) * 32;
+    const uint32_t row = q * 32 + lane;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t t_d0 = lane_base + kColD0, t_d1 = lane_base + kColD1;
+    const uint32_t t_hi = lane_base + kColHi, t_lo = lane_base + kColLo;
+    uint32_t mma_phase = 0, load_phase = 0, set_phase = 0;
+
+    // Publish one operand set (TMEM stores + SMEM stores done by this warp),
+    // then warp 0 waits for every warp's set and issues the MMAs it enables.
+    auto publish = [&](uint64_t* bar, int which, long long next_load) {
+        tmem_st_wait();
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar);
+        if (warp == 0) {
+            mbar_wait(bar, set_phase);
+            if (lane == 0) {
+                tc_fence_after();
+                const uint32_t a_hi = tmem + kColHi, a_lo = tmem + kColLo;
+                if (which == 1) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const uint32_t d = tmem + ((k & 1) ? kColD1 : kColD0);
+                        mma_tf32_ts(d, a_lo + 8 * k,
+                                    bdesc_hi + static_cast<uint64_t>((k * 1024) >> 4), kIdesc,
+                                    k > 1 ? 1u : 0u);
+                    }
+                } else {
+                    if (next_load >= 0) issue_load(next_load);  // staging consumed
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const uint32_t d = tmem + ((k & 1) ? kColD1 : kColD0);
+                        mma_tf32_ts(d, a_hi + 8 * k,
+                                    bdesc_lo + static_cast<uint64_t>((k * 1024) >> 4), kIdesc, 1u);
+                    }
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const uint32_t d = tmem + ((k & 1) ? kColD1 : kColD0);
+                        mma_tf32_ts(d, a_hi + 8 * k,
+                                    bdesc_hi + static_cast<uint64_t>((k * 1024) >> 4), kIdesc, 1u);
+                    }
+                    mma_commit(mma_bar);
+                }
+            }
+            __syncwarp();
+        }
+        if (which == 2) set_phase ^= 1;
+    };
+
     if (use_tma && tid == 0 && blockIdx.x < batch) issue_load(blockIdx.x);
 
     for (long long m = blockIdx.x; m < batch; m += gridDim.x) {
         const float* src = in + static_cast<size_t>(m) * n * n;
+        const long long next = (use_tma && m + gridDim.x < batch) ? m + gridDim.x : -1;
         if (prof) p_t = clock64();
-        // ---- input -> right operand (SMEM) + left operand (TMEM)
+        // ---- input -> operands (both sets), published like an epilogue
+        uint32_t h[2][16], l[2][16];
         if (use_tma) {
             mbar_wait(load_bar, load_phase);
             load_phase ^= 1;
         }
-#pragma unroll 1
+#pragma unroll
         for (int j = 0; j < 2; ++j) {
-            uint32_t h[16], l[16];
             if (use_tma)
-                k3_stage_row(s_stage, row, colg + 16 * j, h, l);
+                k3_stage_row(s_stage, row, colg + 16 * j, h[j], l[j]);
             else
-                k3_global_row(src, n, row, colg + 16 * j, h, l);
-            k3_put_row(s_hi, s_lo, row, colg + 16 * j, h, l, t_hi, t_lo);
+                k3_global_row(src, n, row, colg + 16 * j, h[j], l[j]);
         }
-        tmem_st_wait();
-        fence_proxy_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        // staging is free again: prefetch the next matrix under this chain
-        if (use_tma && tid == 0 && m + gridDim.x < batch) issue_load(m + gridDim.x);
+        // (a plan starting with MULTIPLY_BASE does not exist: k >= 2 starts with SQUARE)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            tmem_st16(t_lo + colg + 16 * j, l[j]);
+            k3_put_half(s_hi, row, colg + 16 * j, h[j]);
+        }
+        publish(set1_bar, 1, -1);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            tmem_st16(t_hi + colg + 16 * j, h[j]);
+            k3_put_half(s_lo, row, colg + 16 * j, l[j]);
+        }
+        publish(set2_bar, 2, next);
         if (prof) { long long t = clock64(); p_load += t - p_t; p_t = t; }
 
         for (int s = 0; s < plan.len; ++s) {
-            if (plan_is_mult(plan, s)) {
-                // left operand <- base (the resident acc stays the right operand)
-#pragma unroll 1
-                for (int j = 0; j < 2; ++j) {
-                    uint32_t h[16], l[16];
-                    k3_global_row(src, n, row, colg + 16 * j, h, l);
-                    tmem_st16(t_hi + colg + 16 * j, h);
-                    tmem_st16(t_lo + colg + 16 * j, l);
-                }
-                tmem_st_wait();
-                tc_fence_before();
-                __syncthreads();
-            }
-            if (tid == 0) {
-                tc_fence_after();
-                const uint32_t a_hi = tmem + kColHi, a_lo = tmem + kColLo;
-                // small cross terms first, k-steps split by parity over D0/D1
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const uint32_t d = tmem + ((k & 1) ? kColD1 : kColD0);
-                    const uint64_t boff = static_cast<uint64_t>((k * 1024) >> 4);
-                    mma_tf32_ts(d, a_lo + 8 * k, bdesc_hi + boff, kIdesc, k > 1 ? 1u : 0u);
-                    mma_tf32_ts(d, a_hi + 8 * k, bdesc_lo + boff, kIdesc, 1u);
-                }
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const uint32_t d = tmem + ((k & 1) ? kColD1 : kColD0);
-                    const uint64_t boff = static_cast<uint64_t>((k * 1024) >> 4);
-                    mma_tf32_ts(d, a_hi + 8 * k, bdesc_hi + boff, kIdesc, 1u);
-                }
-                mma_commit(mma_bar);
-            }
             mbar_wait(mma_bar, mma_phase);
             mma_phase ^= 1;
-            if (prof) { long long t = clock64(); p_mma += t - p_t; p_t = t; }
             tc_fence_after();
+            if (prof) { long long t = clock64(); p_mma += t - p_t; p_t = t; }
             const bool last = (s == plan.len - 1);
             uint32_t v2[2][16];
             {
@@ -240,43 +289,67 @@ __global__ void __launch_bounds__(kK3Threads, 1)
                     v2[1][i] = __float_as_uint(__fadd_rn(__uint_as_float(v2[1][i]), __uint_as_float(w1[i])));
                 }
             }
+            if (last) {
+                if (row < static_cast<uint32_t>(n)) {
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int col0 = colg + j * 16;
-                const uint32_t (&v)[16] = v2[j];
-                if (last) {
-                    if (row < static_cast<uint32_t>(n)) {
+                    for (int j = 0; j < 2; ++j) {
+                        const int col0 = colg + 16 * j;
                         float* dst = out + static_cast<size_t>(m) * n * n +
                                      static_cast<size_t>(row) * n + col0;
                         if ((n & 3) == 0 && col0 + 16 <= n) {
 #pragma unroll
                             for (int u = 0; u < 4; ++u)
                                 reinterpret_cast<float4*>(dst)[u] = make_float4(
-                                    __uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]),
-                                    __uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3]));
+                                    __uint_as_float(v2[j][4 * u]), __uint_as_float(v2[j][4 * u + 1]),
+                                    __uint_as_float(v2[j][4 * u + 2]), __uint_as_float(v2[j][4 * u + 3]));
                         } else {
                             for (int i = 0; i < 16; ++i)
-                                if (col0 + i < n) dst[i] = __uint_as_float(v[i]);
+                                if (col0 + i < n) dst[i] = __uint_as_float(v2[j][i]);
                         }
                     }
-                } else {
-                    uint32_t h[16], l[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) split_tf32(__uint_as_float(v[i]), h[i], l[i]);
-                    k3_put_row(s_hi, s_lo, row, col0, h, l, t_hi, t_lo);
                 }
+                tc_fence_before();  // D reads done before the next matrix's MMAs
+            } else {
+                const bool next_mult = plan_is_mult(plan, s + 1);
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) split_tf32(__uint_as_float(v2[j][i]), h[j][i], l[j][i]);
+                // left operand of the next step: the new power, or the base
+                // (streamed from global one sub-chunk at a time)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    if (next_mult) {
+                        uint32_t bh[16], bl[16];
+                        k3_global_row(src, n, row, colg + 16 * j, bh, bl);
+                        tmem_st16(t_lo + colg + 16 * j, bl);
+                    } else {
+                        tmem_st16(t_lo + colg + 16 * j, l[j]);
+                    }
+                    k3_put_half(s_hi, row, colg + 16 * j, h[j]);
+                }
+                publish(set1_bar, 1, -1);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    if (next_mult) {
+                        uint32_t bh[16], bl[16];
+                        k3_global_row(src, n, row, colg + 16 * j, bh, bl);
+                        tmem_st16(t_hi + colg + 16 * j, bh);
+                    } else {
+                        tmem_st16(t_hi + colg + 16 * j, h[j]);
+                    }
+                    k3_put_half(s_lo, row, colg + 16 * j, l[j]);
+                }
+                publish(set2_bar, 2, -1);
             }
-            tmem_st_wait();
-            tc_fence_before();
-            fence_proxy_async_smem();
-            __syncthreads();
             if (prof) { long long t = clock64(); p_epi += t - p_t; p_t = t; }
         }
     }
-    __syncthreads();
     if (prof && blockIdx.x == 0 && tid == 0) {
         prof[0] = p_load; prof[1] = p_mma; prof[2] = p_epi;
     }
+    tc_fence_before();
+    __syncthreads();
     if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
@@ -292,8 +365,8 @@ cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
     int use_tma = 0;
     if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0)
         use_tma = encode_batch_map(&map, in, n, batch) ? 1 : 0;
-    k3_batched_power<<<grid, kK3Threads, k3_smem_bytes(), s>>>(map, use_tma, in, out, n, batch,
-                                                               plan, g_k3_prof);
+    k3_batched_power<<<grid, kK3AllThreads, k3_smem_bytes(), s>>>(map, use_tma, in, out, n,
+                                                                  batch, plan, g_k3_prof);
     return cudaGetLastError();
 }
 
