@@ -398,7 +398,9 @@ def main() -> None:
                 "frac": achieved / peak, "traffic": ncu_traffic("k3_batched_power"),
                 "kernel": "k3_batched_power" if w["batch"] > 1 else "k1_gemm_3xtf32 chain",
                 "peak_source": src, "algorithmic_flops_per_launch": fl / max(launches, 1),
-                "bf16_measured_peak": peaks.get("bf16_tflops")}
+                "bf16_measured_peak": peaks.get("bf16_tflops"),
+                "frac_vs_bf16_measured_over_6": (achieved / (peaks["bf16_tflops"] / 6.0)
+                                                 if peaks.get("bf16_tflops") else None)}
     out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,

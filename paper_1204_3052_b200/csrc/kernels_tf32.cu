@@ -144,6 +144,7 @@ size_t k3_smem_bytes() { return 3 * kPlane + 1024 + 256; }
 constexpr int kK3Workers = 16;
 constexpr int kK3AllThreads = kK3Workers * 32;
 
+template <bool kProf>
 __global__ void __launch_bounds__(kK3AllThreads, 1)
     k3_batched_power(const __grid_constant__ CUtensorMap in_map, int use_tma,
                      const float* __restrict__ in, float* __restrict__ out, int n, long long batch,
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(kK3AllThreads, 1)
     for (long long m = blockIdx.x; m < batch; m += gridDim.x) {
         const float* src = in + static_cast<size_t>(m) * n * n;
         const long long next = (use_tma && m + gridDim.x < batch) ? m + gridDim.x : -1;
-        if (prof) p_t = clock64();
+        if (kProf) p_t = clock64();
         // ---- input -> operands (both sets), published like an epilogue
         uint32_t h[2][16], l[2][16];
         if (use_tma) {
@@ -270,13 +271,13 @@ __global__ void __launch_bounds__(kK3AllThreads, 1)
             k3_put_half(s_lo, row, colg + 16 * j, l[j]);
         }
         publish(set2_bar, 2, next);
-        if (prof) { long long t = clock64(); p_load += t - p_t; p_t = t; }
+        if (kProf) { long long t = clock64(); p_load += t - p_t; p_t = t; }
 
         for (int s = 0; s < plan.len; ++s) {
             mbar_wait(mma_bar, mma_phase);
             mma_phase ^= 1;
             tc_fence_after();
-            if (prof) { long long t = clock64(); p_mma += t - p_t; p_t = t; }
+            if (kProf) { long long t = clock64(); p_mma += t - p_t; p_t = t; }
             const bool last = (s == plan.len - 1);
             uint32_t v2[2][16];
             {
@@ -342,10 +343,10 @@ __global__ void __launch_bounds__(kK3AllThreads, 1)
                 }
                 publish(set2_bar, 2, -1);
             }
-            if (prof) { long long t = clock64(); p_epi += t - p_t; p_t = t; }
+            if (kProf) { long long t = clock64(); p_epi += t - p_t; p_t = t; }
         }
     }
-    if (prof && blockIdx.x == 0 && tid == 0) {
+    if (kProf && blockIdx.x == 0 && tid == 0) {
         prof[0] = p_load; prof[1] = p_mma; prof[2] = p_epi;
     }
     tc_fence_before();
@@ -365,8 +366,12 @@ cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
     int use_tma = 0;
     if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0)
         use_tma = encode_batch_map(&map, in, n, batch) ? 1 : 0;
-    k3_batched_power<<<grid, kK3AllThreads, k3_smem_bytes(), s>>>(map, use_tma, in, out, n,
-                                                                  batch, plan, g_k3_prof);
+    if (g_k3_prof != nullptr)
+        k3_batched_power<true><<<grid, kK3AllThreads, k3_smem_bytes(), s>>>(
+            map, use_tma, in, out, n, batch, plan, g_k3_prof);
+    else
+        k3_batched_power<false><<<grid, kK3AllThreads, k3_smem_bytes(), s>>>(
+            map, use_tma, in, out, n, batch, plan, nullptr);
     return cudaGetLastError();
 }
 
@@ -686,8 +691,12 @@ int k1_block_n(int n_pad, int num_sms) {
 }
 
 cudaError_t prepare_tf32_kernels() {
-    cudaError_t e = cudaFuncSetAttribute(k3_batched_power, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k3_batched_power<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(k3_smem_bytes()));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k3_batched_power<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(k3_smem_bytes()));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k1_gemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(K1Cfg::kSmem));
