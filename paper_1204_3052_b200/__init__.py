@@ -22,7 +22,7 @@ from .errors import (
     UnsupportedPowerError,
     ValidationError,
 )
-from .linalg import ErrorMetrics, Matrix, compare, identity, zeros
+from .linalg import ErrorMetrics, Matrix, compare, identity, read_matrix, write_matrix, zeros
 from .tolerances import (
     associativity_tol,
     device_tol,
@@ -55,7 +55,8 @@ __all__ = [
     "DType", "MatexpoError", "InvalidDimensionError", "InvalidRangeError", "ShapeError",
     "UnsupportedPowerError", "BackendStepError", "ConfigError", "ValidationError",
     "UnsupportedError", "DeviceUnavailableError", "DeviceError", "ExtensionNotBuiltError",
-    "Matrix", "ErrorMetrics", "identity", "zeros", "compare", "random_matrix",
+    "Matrix", "ErrorMetrics", "identity", "zeros", "compare", "random_matrix", "read_matrix",
+    "write_matrix",
     "scaled_batch", "scaled_input", "vectorized_tol", "associativity_tol", "oracle_tol",
     "device_tol", "fro_tol", "fro_tol_conditioned", "multiply_count", "Step", "Strategy",
     "ExponentPlan", "plan_exponentiation", "Backend", "CountingBackend", "B200Backend",
@@ -69,7 +70,7 @@ def __getattr__(name):
         from .engine import Engine
 
         return Engine
-    if name in ("engine", "distributed", "build"):
+    if name in ("engine", "distributed", "build", "harness", "cli"):
         import importlib
 
         return importlib.import_module(f".{name}", __name__)

@@ -151,6 +151,30 @@ class Engine:
         self._raise_chain(rc, st, plan_string(k) if k >= 0 else "", "mxp_power_mod")
         return out
 
+    def repeated_power(self, a: np.ndarray, k: int) -> np.ndarray:
+        """A^k by k-1 successive device multiplies acc = acc * A (the REPEATED
+        strategy / F64 oracle of expo.py:142-156 and bench.py:178-180, on the
+        device: one upload, k-1 GEMM launches over ping-pong buffers, one readback)."""
+        if k < 1:
+            raise E.UnsupportedPowerError(f"repeated baseline needs power >= 1, got {k}")
+        a = np.ascontiguousarray(a)
+        mode = _mode_of(a)
+        n = a.shape[0]
+        d_a, d_x, d_y = self.alloc(a.nbytes), self.alloc(a.nbytes), self.alloc(a.nbytes)
+        try:
+            self.upload(d_a, a)
+            self.upload(d_x, a)
+            for _ in range(k - 1):
+                self.gemm_device(d_x, d_a, d_y, n, mode)
+                d_x, d_y = d_y, d_x
+            out = np.empty_like(a)
+            self.download(out, d_x)
+            return out
+        finally:
+            self.free(d_a)
+            self.free(d_x)
+            self.free(d_y)
+
     # ------------------------------------------------------------ device API
     def power_device(self, d_in: int, d_out: int, n: int, k: int, mode: int = _lib.MXP_F32) -> None:
         st = _lib.Stats()

@@ -10,8 +10,9 @@ multiply here: every product goes through the sm_100a engine.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
-from typing import Iterable, Sequence
+from typing import Iterable, Sequence, TextIO, Union
 
 import numpy as np
 
@@ -130,3 +131,47 @@ def compare(result, reference) -> ErrorMetrics:
     fro_diff = float(np.sqrt(np.sum(diff * diff)))
     fro = (0.0 if fro_diff == 0.0 else math.inf) if fro_ref == 0.0 else fro_diff / fro_ref
     return ErrorMetrics(max_abs, max_rel, fro)
+
+
+# --- text file format (linalg.py:235-276) -------------------------------------
+# Line 1: "<n> <dtype>" with dtype in {f32, f64}; then n lines of n decimal
+# values, row-major, shortest round-trip repr; reading back is bitwise exact.
+
+def write_matrix(m, dest: Union[str, os.PathLike, TextIO]) -> None:
+    arr = as_array(m)
+    if hasattr(dest, "write"):
+        _write_stream(arr, dest)
+    else:
+        with open(dest, "w", encoding="utf-8") as fh:
+            _write_stream(arr, fh)
+
+
+def _write_stream(arr: np.ndarray, fh: TextIO) -> None:
+    fh.write(f"{arr.shape[0]} {DType.of(arr).value}\n")
+    for row in arr:
+        fh.write(" ".join(str(v) for v in row))
+        fh.write("\n")
+
+
+def read_matrix(src: Union[str, os.PathLike, TextIO]) -> Matrix:
+    if hasattr(src, "read"):
+        return _read_stream(src)
+    with open(src, "r", encoding="utf-8") as fh:
+        return _read_stream(fh)
+
+
+def _read_stream(fh: TextIO) -> Matrix:
+    header = fh.readline().split()
+    if len(header) != 2:
+        raise ShapeError("matrix file header must be '<n> <dtype>'")
+    n = int(header[0])
+    dtype = DType.parse(header[1])
+    if n < 1:
+        raise InvalidDimensionError(f"matrix order must be >= 1, got {n}")
+    out = np.empty((n, n), dtype=dtype.np)
+    for i in range(n):
+        parts = fh.readline().split()
+        if len(parts) != n:
+            raise ShapeError(f"row {i} has {len(parts)} values, expected {n}")
+        out[i] = [dtype.np(float(tok)) for tok in parts]
+    return Matrix(out, copy=False)

@@ -369,3 +369,23 @@ def test_row_sharded_chain_single_rank_nccl():
         assert np.array_equal(out.cpu().numpy(), mx.exponentiate_batched(batch.cpu().numpy(), 64))
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ harness / CLI / oracle on device
+def test_device_repeated_oracle_and_cli(capsys):
+    from paper_1204_3052_b200 import cli, harness
+
+    eng = mx.Engine(0)
+    a = oracle.random_matrix(16, np.float64, 42)
+    rep = eng.repeated_power(a, 13)
+    ref = oracle.exponentiate(a, 13)
+    assert oracle.compare(rep, ref)[1] <= oracle.oracle_tol(13, 16, np.float64)
+    assert cli.main(["verify", "--size", "64", "--power", "13", "--dtype", "f32"]) == 0
+    out = capsys.readouterr().out
+    assert "verdict=PASS" in out and "backend=b200" in out
+    assert cli.main(["verify", "--size", "512", "--power", "1000", "--dtype", "f32",
+                     "--scaled"]) == 0
+    recs = harness.run_benchmark(harness.BenchConfig(sizes=[64], powers=[16, 13], repetitions=2))
+    assert {(r.strategy.value, r.multiply_count) for r in recs} == {
+        ("repeated", 15), ("squared", 4), ("repeated", 12), ("squared", 5)}
+    assert all(r.max_rel_err is not None and r.max_rel_err < 1e-3 for r in recs)

@@ -171,3 +171,77 @@ def test_wrap_like_reference_matrix_type():
 
     out = wrap_like(Foreign(np.eye(2)), np.ones((2, 2)))
     assert isinstance(out, Foreign)
+
+
+# ------------------------------------------------------------------ text format (linalg.py:235-276)
+UNIFORM_F32_SEED7_TEXT = (  # gpu-backend/test/helpers.ts:51-56 (independent producer)
+    "4 f32\n"
+    "-0.11017025 -0.4832117 0.40076068 0.0829303\n"
+    "-0.047558106 -0.25056848 -0.032046996 -0.17192326\n"
+    "-0.3657417 -0.0868586 -0.39644006 0.45987406\n"
+    "0.4180196 0.37133175 0.36400765 0.048287418\n")
+
+
+def test_text_format_matches_reference_fixture():
+    import io
+
+    m = Matrix(oracle.random_matrix(4, np.float32, 7))
+    buf = io.StringIO()
+    mx.write_matrix(m, buf)
+    assert buf.getvalue() == UNIFORM_F32_SEED7_TEXT
+    back = mx.read_matrix(io.StringIO(UNIFORM_F32_SEED7_TEXT))
+    assert back.array.tobytes() == m.array.tobytes()
+
+
+@given(seed=st.integers(0, 2**20), n=st.integers(1, 8), f64=st.booleans())
+def test_text_round_trip_bitwise(seed, n, f64):
+    import io
+
+    m = Matrix(oracle.random_matrix(n, np.float64 if f64 else np.float32, seed, -100.0, 100.0))
+    buf = io.StringIO()
+    mx.write_matrix(m, buf)
+    back = mx.read_matrix(io.StringIO(buf.getvalue()))
+    assert back.array.tobytes() == m.array.tobytes()
+
+
+def test_text_format_malformed():
+    import io
+
+    with pytest.raises(mx.ShapeError):
+        mx.read_matrix(io.StringIO("2\n1 2\n3 4\n"))
+    with pytest.raises(ValueError):
+        mx.read_matrix(io.StringIO("2 f16\n1 2\n3 4\n"))
+    with pytest.raises(mx.ShapeError):
+        mx.read_matrix(io.StringIO("2 f64\n1 2 3\n4 5 6\n"))
+    with pytest.raises(mx.InvalidDimensionError):
+        mx.read_matrix(io.StringIO("0 f64\n"))
+
+
+# ------------------------------------------------------------------ harness CSV (bench.py:259-305)
+def test_csv_schema_is_the_reference_one():
+    import io
+
+    from paper_1204_3052_b200 import harness
+
+    assert harness.CSV_HEADER == ("size,power,strategy,backend,seconds,multiply_count,"
+                                  "transfer_count,max_rel_err,nonfinite")
+    recs = [harness.BenchmarkRecord(64, 16, Strategy.SQUARED, "b200", 1.5e-5, 4, 2, 3e-7, False,
+                                    1, "f32-3xtf32", 0.01, 0.1),
+            harness.BenchmarkRecord(64, 16, Strategy.REPEATED, "b200", 2e-4, 15, 16, None, True)]
+    for ext in (False, True):
+        buf = io.StringIO()
+        harness.emit_csv(recs, buf, extended=ext)
+        back = harness.read_csv(io.StringIO(buf.getvalue()))
+        assert [(r.power, r.strategy, r.max_rel_err, r.nonfinite) for r in back] == \
+            [(16, Strategy.REPEATED, None, True), (16, Strategy.SQUARED, 3e-7, False)]
+    with pytest.raises(mx.ConfigError):
+        harness.make_backend("naive")
+    with pytest.raises(mx.ConfigError):
+        harness.validate_config(harness.BenchConfig(sizes=[0], powers=[-1]))
+
+
+def test_cli_validation_exit_code():
+    from paper_1204_3052_b200 import cli
+
+    assert cli.main(["verify", "--size", "4"]) == 1  # missing --power: usage error -> 1
+    assert cli.main(["bench", "--sizes", "4", "--powers", "2", "--backend", "naive"]) == 1
