@@ -352,7 +352,7 @@ def main() -> None:
     import torch
 
     dist = None
-    if world > 1:
+    if world > 1 or os.environ.get("BENCH_FORCE_DIST") == "1":
         import torch.distributed as tdist
 
         torch.cuda.set_device(local)

@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
             for (int i = 0; i < 32; ++i) sum[32 + i] = __fadd_rn(sum[32 + i], __uint_as_float(v[i]));
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&cempty[c]);
+            if (lane == 0) mbar_arrive_relaxed(&cempty[c]);
         }
         const int row = m0 + q * 32 + lane;
 #pragma unroll
@@ -632,6 +632,191 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 2) tmem_dealloc<256>(tmem);
+}
+
+// ======================================================================
+// K1P — the same GEMM step on CTA pairs (cta_group::2): a cluster of two
+// CTAs on one TPC computes a 256 x 256 tile with M = 256, N = 256 MMAs issued
+// by the leader.  Each CTA stages its own 128 rows of A and its own 128
+// columns of B (so per-SM shared-memory operand traffic is halved vs K1) and
+// holds its 128 x 256 share of the accumulator in its own TMEM.
+//   warp 0 : TMA producer (both CTAs; bytes complete on the leader's barrier)
+//   warp 1 : MMA issuer (leader only)     warp 2 : TMEM allocator (both)
+//   warps 4-11 : epilogue (both CTAs; lane quarter = warp % 4, 128-column half)
+// Accuracy as K1: per-stage chunk accumulators (two of 256 columns), drained
+// into fp32 register sums with round-to-nearest adds.
+// ======================================================================
+namespace {
+struct K1PCfg {
+    static constexpr int kStages = 3;
+    static constexpr uint32_t kABytes = 128 * 128;        // one plane: 128 rows x 32 fp32
+    static constexpr uint32_t kBBytes = 32 * 128 * 4;     // one plane: 4 chunks x 32 K-rows
+    static constexpr uint32_t kStageBytes = 2 * kABytes + 2 * kBBytes;  // 64 KB per CTA
+    static constexpr size_t kSmem = kStages * kStageBytes + 1024 + 256;
+    static constexpr int kThreads = 384;
+};
+}  // namespace
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K1PCfg::kThreads, 1)
+    k1p_gemm_3xtf32(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
+                    const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
+                    int n_pad, int m_pad, float* __restrict__ out_f32, int n_out, int m_out,
+                    int ld_out, uint32_t* __restrict__ out_hi, uint32_t* __restrict__ out_lo) {
+    using Cfg = K1PCfg;
+    constexpr int S = Cfg::kStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+    uint64_t* empty = full + S;
+    uint64_t* cfull = empty + S;   // [2] chunk accumulator ready (multicast by the leader)
+    uint64_t* cempty = cfull + 2;  // [2] chunk drained (leader's copy counts both CTAs)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = (rank == 0);
+
+    // pair tile raster (grouped along M, as K1)
+    constexpr int kGroupM = 8;
+    const int num_m = m_pad / 256, num_n = n_pad / 256;
+    const int pid = blockIdx.x >> 1;
+    const int per_group = kGroupM * num_n;
+    const int first_m = (pid / per_group) * kGroupM;
+    const int gm = min(num_m - first_m, kGroupM);
+    const int m0 = (first_m + (pid % per_group) % gm) * 256 + static_cast<int>(rank) * 128;
+    const int n0 = ((pid % per_group) / gm) * 256;
+    const int num_kb = n_pad / 32;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&cfull[i], 1);
+            mbar_init(&cempty[i], 16);  // 8 epilogue warps x 2 CTAs
+        }
+        fence_mbar_init();
+        tma_prefetch(&ma_hi);
+        tma_prefetch(&ma_lo);
+        tma_prefetch(&mb_hi);
+        tma_prefetch(&mb_lo);
+    }
+    if (warp == 2) tmem_alloc_pair<512>(tmem_slot);
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        for (int kb = 0; kb < num_kb; ++kb) {
+            const int st = kb % S;
+            const uint32_t ph = (kb / S) & 1;
+            mbar_wait(&empty[st], ph ^ 1);
+            uint8_t* base = smem + st * Cfg::kStageBytes;
+            if (leader) mbar_expect_tx(&full[st], 2 * Cfg::kStageBytes);
+            tma_load_2d_pair(base, &ma_hi, &full[st], kb * 32, m0);
+            tma_load_2d_pair(base + Cfg::kABytes, &ma_lo, &full[st], kb * 32, m0);
+            uint8_t* bh = base + 2 * Cfg::kABytes;
+            uint8_t* bl = bh + Cfg::kBBytes;
+            const int nb = n0 + static_cast<int>(rank) * 128;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                tma_load_2d_pair(bh + j * 4096, &mb_hi, &full[st], nb + 32 * j, kb * 32);
+                tma_load_2d_pair(bl + j * 4096, &mb_lo, &full[st], nb + 32 * j, kb * 32);
+            }
+        }
+    } else if (warp == 1 && lane == 0 && leader) {
+        constexpr uint32_t kIdesc = idesc_tf32_kmaj_mnmaj<256, 256>();
+        const uint32_t s0 = smem_u32(smem);
+        const uint64_t da_hi = kmajor_desc(s0), da_lo = kmajor_desc(s0 + Cfg::kABytes);
+        const uint64_t db_hi = mnmajor_desc(s0 + 2 * Cfg::kABytes, 4096);
+        const uint64_t db_lo = mnmajor_desc(s0 + 2 * Cfg::kABytes + Cfg::kBBytes, 4096);
+        for (int kb = 0; kb < num_kb; ++kb) {
+            const int st = kb % S;
+            const uint32_t ph = (kb / S) & 1;
+            const int c = kb & 1;
+            mbar_wait(&cempty[c], ((kb >> 1) & 1) ^ 1);
+            mbar_wait(&full[st], ph);
+            tc_fence_after();
+            const uint64_t so = static_cast<uint64_t>((st * Cfg::kStageBytes) >> 4);
+            const uint32_t d = tmem + c * 256;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((1024 * k) >> 4);
+                mma_tf32_pair(d, da_lo + ao, db_hi + bo, kIdesc, k > 0 ? 1u : 0u);
+                mma_tf32_pair(d, da_hi + ao, db_lo + bo, kIdesc, 1u);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((1024 * k) >> 4);
+                mma_tf32_pair(d, da_hi + ao, db_hi + bo, kIdesc, 1u);
+            }
+            mma_commit_pair(&empty[st]);
+            mma_commit_pair(&cfull[c]);
+        }
+    } else if (warp >= 4) {
+        const int q = warp & 3;
+        const int ch = ((warp - 4) >> 2) * 128;  // column half of the 256
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        const uint32_t cempty_leader0 = mapa_shared(smem_u32(&cempty[0]), 0);
+        float sum[128];
+#pragma unroll
+        for (int i = 0; i < 128; ++i) sum[i] = 0.f;
+        for (int kb = 0; kb < num_kb; ++kb) {
+            const int c = kb & 1;
+            mbar_wait(&cfull[c], (kb >> 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                uint32_t v[16];
+                tmem_ld16(lane_base + c * 256 + ch + 16 * g, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) sum[16 * g + i] = __fadd_rn(sum[16 * g + i], __uint_as_float(v[i]));
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster_relaxed(cempty_leader0 + 8 * c);
+        }
+        const int row = m0 + q * 32 + lane;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int col = n0 + ch + 32 * h;
+            const float* v = sum + 32 * h;
+            if (out_hi != nullptr) {
+                uint4* dh = reinterpret_cast<uint4*>(out_hi + static_cast<size_t>(row) * n_pad + col);
+                uint4* dl = reinterpret_cast<uint4*>(out_lo + static_cast<size_t>(row) * n_pad + col);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    uint4 hv, lv;
+                    split_tf32(v[4 * u + 0], hv.x, lv.x);
+                    split_tf32(v[4 * u + 1], hv.y, lv.y);
+                    split_tf32(v[4 * u + 2], hv.z, lv.z);
+                    split_tf32(v[4 * u + 3], hv.w, lv.w);
+                    dh[u] = hv;
+                    dl[u] = lv;
+                }
+            }
+            if (out_f32 != nullptr && row < m_out && col < n_out) {
+                float* d = out_f32 + static_cast<size_t>(row) * ld_out + col;
+                if ((ld_out & 3) == 0 && col + 32 <= n_out) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        reinterpret_cast<float4*>(d)[u] =
+                            make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+                } else {
+                    for (int i = 0; i < 32; ++i)
+                        if (col + i < n_out) d[i] = v[i];
+                }
+            }
+        }
+    }
+    // both CTAs done with the pair's TMEM (the peer's epilogue has drained
+    // every chunk the leader's MMAs wrote) before the paired dealloc
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 2) tmem_dealloc_pair<512>(tmem);
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -684,10 +869,11 @@ bool encode_batch_map(CUtensorMap* map, const void* base, int n, int64_t batch) 
     return r == CUDA_SUCCESS;
 }
 
+// 256: the CTA-pair kernel (needs n_pad % 256 == 0; used from 1024 up, where
+// its 256 x 256 pair tiles still give >= 8 clusters); 128: the 1-CTA kernel.
 int k1_block_n(int n_pad, int num_sms) {
-    (void)n_pad;
     (void)num_sms;
-    return K1Cfg::kBN;
+    return (n_pad % 256 == 0 && n_pad >= 1024) ? 256 : K1Cfg::kBN;
 }
 
 cudaError_t prepare_tf32_kernels() {
@@ -700,6 +886,9 @@ cudaError_t prepare_tf32_kernels() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k1_gemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(K1Cfg::kSmem));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k1p_gemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(K1PCfg::kSmem));
     return e;
 }
 
@@ -713,7 +902,13 @@ cudaError_t launch_k1_gemm(const GemmPlanes& m, int n_pad, int block_n, float* o
 cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int block_n,
                                 float* out_f32, int n_out, int m_out, int ld_out, uint32_t* out_hi,
                                 uint32_t* out_lo, cudaStream_t s) {
-    (void)block_n;
+    if (block_n == 256) {  // CTA-pair kernel: n_pad, m_pad multiples of 256
+        dim3 grid(2 * (n_pad / 256) * (m_pad / 256));
+        k1p_gemm_3xtf32<<<grid, K1PCfg::kThreads, K1PCfg::kSmem, s>>>(
+            m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, out_f32, n_out, m_out, ld_out, out_hi,
+            out_lo);
+        return cudaGetLastError();
+    }
     dim3 grid((n_pad / K1Cfg::kBN) * (m_pad / 128));
     k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(
         m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo);

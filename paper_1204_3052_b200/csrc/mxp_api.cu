@@ -575,11 +575,14 @@ int mxp_gemm_rows(mxp_handle h, int mode, int64_t n, int64_t rows, const void* d
     if (rows < 1 || rows > n)
         return fail(MXP_E_VALIDATION, "row block must satisfy 1 <= rows <= n, got %lld", (long long)rows);
     if (!dA || !dB || !dC) return fail(MXP_E_VALIDATION, "null device pointer");
-    const int64_t n_pad = round_up(n, 128), r_pad = round_up(rows, 128);
+    const int64_t n_pad = round_up(n, 128);
+    int64_t r_pad = round_up(rows, 128);
     if (mode == MXP_F32) {
         rc = ensure_ws32(h, n_pad);
         if (rc) return rc;
         const int np = (int)h->ws32_pad;
+        const int bn = k1_block_n(np, h->num_sms);
+        if (bn == 256) r_pad = round_up(rows, 256);  // CTA-pair tiles are 256 rows
         CUtensorMap a_hi, a_lo, b_hi, b_lo;
         if (!encode_plane_map(&a_hi, h->planes[0], np, 32, 128, false, (int)r_pad) ||
             !encode_plane_map(&a_lo, h->planes[1], np, 32, 128, false, (int)r_pad) ||
@@ -593,9 +596,8 @@ int mxp_gemm_rows(mxp_handle h, int mode, int64_t n, int64_t rows, const void* d
                              h->planes[3], np, h->stream);
         if (e != cudaSuccess) return cuda_fail(e, "split");
         GemmPlanes m{a_hi, a_lo, b_hi, b_lo};
-        e = launch_k1_gemm_rows(m, np, (int)r_pad, k1_block_n(np, h->num_sms),
-                                static_cast<float*>(dC), (int)n, (int)rows, (int)n, nullptr, nullptr,
-                                h->stream);
+        e = launch_k1_gemm_rows(m, np, (int)r_pad, bn, static_cast<float*>(dC), (int)n, (int)rows,
+                                (int)n, nullptr, nullptr, h->stream);
         if (e != cudaSuccess) return cuda_fail(e, "k1_gemm_3xtf32");
         return MXP_OK;
     }
