@@ -153,8 +153,6 @@ __global__ void __launch_bounds__(kK3AllThreads, 1)
     uint8_t* smem = align1024(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 3 * kPlane);
     uint64_t* mma_bar = bars + 0;   // MMAs of a step complete (tcgen05.commit)
-    uint64_t* set1_bar = bars + 1;  // A_lo + B_hi published (16 warp arrivals)
-    uint64_t* set2_bar = bars + 2;  // A_hi + B_lo published (16 warp arrivals)
     uint64_t* load_bar = bars + 3;  // TMA staging landed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 3 * kPlane + 64);
 
@@ -165,8 +163,6 @@ __global__ void __launch_bounds__(kK3AllThreads, 1)
 
     if (tid == 0) {
         mbar_init(mma_bar, 1);
-        mbar_init(set1_bar, kK3Workers);
-        mbar_init(set2_bar, kK3Workers);
         mbar_init(load_bar, 1);
         fence_mbar_init();
         if (use_tma) tma_prefetch(&in_map);
@@ -194,18 +190,20 @@ __global__ void __launch_bounds__(kK3AllThreads, 1)
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const uint32_t t_d0 = lane_base + kColD0, t_d1 = lane_base + kColD1;
     const uint32_t t_hi = lane_base + kColHi, t_lo = lane_base + kColLo;
-    uint32_t mma_phase = 0, load_phase = 0, set_phase = 0;
+    uint32_t mma_phase = 0, load_phase = 0;
 
-    // Publish one operand set (TMEM stores + SMEM stores done by this warp),
-    // then warp 0 waits for every warp's set and issues the MMAs it enables.
-    auto publish = [&](uint64_t* bar, int which, long long next_load) {
+    // Publish one operand set (TMEM stores + SMEM stores done by this warp):
+    // workers bar.arrive on named barrier `which`, warp 0 bar.syncs on it (the
+    // hardware barrier drains this CTA's pending st.shared) and its lane 0
+    // issues the MMAs the set enables.
+    auto publish = [&](int which, long long next_load) {
         tmem_st_wait();
         fence_proxy_async_smem();
         tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar);
-        if (warp == 0) {
-            mbar_wait(bar, set_phase);
+        if (warp != 0) {
+            named_bar_arrive(which, kK3AllThreads);
+        } else {
+            named_bar_sync(which, kK3AllThreads);
             if (lane == 0) {
                 tc_fence_after();
                 const uint32_t a_hi = tmem + kColHi, a_lo = tmem + kColLo;
@@ -236,7 +234,6 @@ __global__ void __launch_bounds__(kK3AllThreads, 1)
             }
             __syncwarp();
         }
-        if (which == 2) set_phase ^= 1;
     };
 
     if (use_tma && tid == 0 && blockIdx.x < batch) issue_load(blockIdx.x);
@@ -264,13 +261,13 @@ __global__ void __launch_bounds__(kK3AllThreads, 1)
             tmem_st16(t_lo + colg + 16 * j, l[j]);
             k3_put_half(s_hi, row, colg + 16 * j, h[j]);
         }
-        publish(set1_bar, 1, -1);
+        publish(1, -1);
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             tmem_st16(t_hi + colg + 16 * j, h[j]);
             k3_put_half(s_lo, row, colg + 16 * j, l[j]);
         }
-        publish(set2_bar, 2, next);
+        publish(2, next);
         if (kProf) { long long t = clock64(); p_load += t - p_t; p_t = t; }
 
         for (int s = 0; s < plan.len; ++s) {
@@ -329,7 +326,7 @@ __global__ void __launch_bounds__(kK3AllThreads, 1)
                     }
                     k3_put_half(s_hi, row, colg + 16 * j, h[j]);
                 }
-                publish(set1_bar, 1, -1);
+                publish(1, -1);
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
                     if (next_mult) {
@@ -341,7 +338,7 @@ __global__ void __launch_bounds__(kK3AllThreads, 1)
                     }
                     k3_put_half(s_lo, row, colg + 16 * j, l[j]);
                 }
-                publish(set2_bar, 2, -1);
+                publish(2, -1);
             }
             if (kProf) { long long t = clock64(); p_epi += t - p_t; p_t = t; }
         }
