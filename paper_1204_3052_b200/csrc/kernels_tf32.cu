@@ -477,7 +477,8 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
     k1_gemm_3xtf32(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                    const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
                    int n_pad, int m_pad, float* __restrict__ out_f32, int n_out, int m_out,
-                   int ld_out, uint32_t* __restrict__ out_hi, uint32_t* __restrict__ out_lo) {
+                   int ld_out, uint32_t* __restrict__ out_hi, uint32_t* __restrict__ out_lo,
+                   float* __restrict__ part) {
     using Cfg = K1Cfg;
     constexpr int S = Cfg::kStages;
     constexpr int BN = Cfg::kBN;
@@ -502,7 +503,11 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
     const int gm = min(num_m - first_m, kGroupM);
     const int m0 = (first_m + (pid % per_group) % gm) * 128;
     const int n0 = ((pid % per_group) / gm) * BN;
-    const int num_kb = n_pad / 32;
+    // split-K: blockIdx.y selects a contiguous range of k-blocks
+    const int kb_total = n_pad / 32;
+    const int kb_per = kb_total / gridDim.y;
+    const int kb0 = blockIdx.y * kb_per;
+    const int num_kb = kb_per;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
@@ -532,14 +537,15 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
             mbar_wait(&empty[st], ph ^ 1);
             uint8_t* base = smem + st * Cfg::kStageBytes;
             mbar_expect_tx(&full[st], Cfg::kStageBytes);
-            tma_load_2d(base, &ma_hi, &full[st], kb * 32, m0);
-            tma_load_2d(base + Cfg::kABytes, &ma_lo, &full[st], kb * 32, m0);
+            const int kg = kb0 + kb;  // global k-block
+            tma_load_2d(base, &ma_hi, &full[st], kg * 32, m0);
+            tma_load_2d(base + Cfg::kABytes, &ma_lo, &full[st], kg * 32, m0);
             uint8_t* bh = base + 2 * Cfg::kABytes;
             uint8_t* bl = bh + Cfg::kBBytes;
 #pragma unroll
             for (int j = 0; j < BN / 32; ++j) {
-                tma_load_2d(bh + j * 4096, &mb_hi, &full[st], n0 + 32 * j, kb * 32);
-                tma_load_2d(bl + j * 4096, &mb_lo, &full[st], n0 + 32 * j, kb * 32);
+                tma_load_2d(bh + j * 4096, &mb_hi, &full[st], n0 + 32 * j, kg * 32);
+                tma_load_2d(bl + j * 4096, &mb_lo, &full[st], n0 + 32 * j, kg * 32);
             }
         }
     } else if (warp == 1 && lane == 0) {
@@ -598,6 +604,14 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
         for (int h = 0; h < 2; ++h) {
             const int col = n0 + ch + 32 * h;
             const float* v = sum + 32 * h;
+            if (part != nullptr) {  // split-K partial, reduced by splitk_reduce_kernel
+                float4* d = reinterpret_cast<float4*>(
+                    part + (static_cast<size_t>(blockIdx.y) * m_pad + row) * n_pad + col);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    d[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+                continue;
+            }
             if (out_hi != nullptr) {
                 uint4* dh = reinterpret_cast<uint4*>(out_hi + static_cast<size_t>(row) * n_pad + col);
                 uint4* dl = reinterpret_cast<uint4*>(out_lo + static_cast<size_t>(row) * n_pad + col);
@@ -893,12 +907,76 @@ cudaError_t launch_k1_gemm(const GemmPlanes& m, int n_pad, int block_n, float* o
                            int n_out, int ld_out, uint32_t* out_hi, uint32_t* out_lo,
                            cudaStream_t s) {
     return launch_k1_gemm_rows(m, n_pad, n_pad, block_n, out_f32, n_out, n_out, ld_out, out_hi,
-                               out_lo, s);
+                               out_lo, s, nullptr, 1);
+}
+
+// Deterministic split-K reduction: the S partial products are summed in a
+// fixed order with round-to-nearest fp32 adds, then split into the next
+// step's hi/lo planes (or written as fp32).
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, int n_pad,
+                                     int m_pad, uint32_t* __restrict__ out_hi,
+                                     uint32_t* __restrict__ out_lo, float* __restrict__ out_f32,
+                                     int n_out, int m_out, int ld_out) {
+    const size_t quads = static_cast<size_t>(m_pad) * n_pad / 4;
+    const size_t plane = static_cast<size_t>(m_pad) * n_pad;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < quads;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        float4 a = reinterpret_cast<const float4*>(part)[i];
+        for (int sp = 1; sp < splits; ++sp) {
+            const float4 b = reinterpret_cast<const float4*>(part + sp * plane)[i];
+            a.x = __fadd_rn(a.x, b.x);
+            a.y = __fadd_rn(a.y, b.y);
+            a.z = __fadd_rn(a.z, b.z);
+            a.w = __fadd_rn(a.w, b.w);
+        }
+        if (out_hi != nullptr) {
+            uint4 h, l;
+            split_tf32(a.x, h.x, l.x);
+            split_tf32(a.y, h.y, l.y);
+            split_tf32(a.z, h.z, l.z);
+            split_tf32(a.w, h.w, l.w);
+            reinterpret_cast<uint4*>(out_hi)[i] = h;
+            reinterpret_cast<uint4*>(out_lo)[i] = l;
+        }
+        if (out_f32 != nullptr) {
+            const size_t e = i * 4;
+            const int r = static_cast<int>(e / n_pad), c = static_cast<int>(e % n_pad);
+            if (r < m_out) {
+                const float v[4] = {a.x, a.y, a.z, a.w};
+                for (int k = 0; k < 4; ++k)
+                    if (c + k < n_out) out_f32[static_cast<size_t>(r) * ld_out + c + k] = v[k];
+            }
+        }
+    }
+}
+
+// k-splits for the 1-CTA kernel: enough CTAs to cover the SMs for small n,
+// at least 2 k-blocks (64 k) per split.
+int k1_split_k(int n_pad, int m_pad, int num_sms) {
+    const int tiles = (n_pad / 128) * (m_pad / 128);
+    const int kb = n_pad / 32;
+    int sk = 1;
+    while (tiles * sk * 2 <= num_sms && (kb % (sk * 2)) == 0 && kb / (sk * 2) >= 2) sk *= 2;
+    return sk;
 }
 
 cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int block_n,
                                 float* out_f32, int n_out, int m_out, int ld_out, uint32_t* out_hi,
-                                uint32_t* out_lo, cudaStream_t s) {
+                                uint32_t* out_lo, cudaStream_t s, float* part, int splits) {
+    if (block_n == 128 && splits > 1 && part != nullptr) {
+        dim3 grid((n_pad / K1Cfg::kBN) * (m_pad / 128), splits);
+        k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(
+            m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, nullptr, n_out, m_out, ld_out, nullptr,
+            nullptr, part);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        const size_t quads = static_cast<size_t>(m_pad) * n_pad / 4;
+        int blocks = static_cast<int>((quads + 255) / 256);
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        splitk_reduce_kernel<<<blocks, 256, 0, s>>>(part, splits, n_pad, m_pad, out_hi, out_lo,
+                                                    out_f32, n_out, m_out, ld_out);
+        return cudaGetLastError();
+    }
     if (block_n == 256) {  // CTA-pair kernel: n_pad, m_pad multiples of 256
         dim3 grid(2 * (n_pad / 256) * (m_pad / 256));
         k1p_gemm_3xtf32<<<grid, K1PCfg::kThreads, K1PCfg::kSmem, s>>>(
@@ -906,9 +984,10 @@ cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int b
             out_lo);
         return cudaGetLastError();
     }
-    dim3 grid((n_pad / K1Cfg::kBN) * (m_pad / 128));
+    dim3 grid((n_pad / K1Cfg::kBN) * (m_pad / 128), 1);
     k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(
-        m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo);
+        m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo,
+        nullptr);
     return cudaGetLastError();
 }
 

@@ -95,6 +95,8 @@ struct mxp_handle_s {
     // fp32 single-matrix workspace: 6 tf32 planes (base, ping, pong) x (hi, lo)
     int64_t ws32_pad = 0;
     uint32_t* planes[6] = {};
+    float* part = nullptr;  // split-K workspace (splits x n_pad^2 fp32) for small n
+    int splits = 1;
     CUtensorMap map_a[6], map_b[6];
     // fp64 workspace: base, ping, pong (n_pad^2 doubles)
     int64_t ws64_pad = 0;
@@ -108,10 +110,10 @@ struct mxp_handle_s {
     void* d_in2 = nullptr;
     void* d_out = nullptr;
 
-    std::map<GraphKey, cudaGraphExec_t> graphs;
+    std::map<GraphKey, std::pair<cudaGraphExec_t, int64_t>> graphs;  // exec, kernel launches
 
     void drop_graphs() {
-        for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+        for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
         graphs.clear();
     }
 };
@@ -154,6 +156,12 @@ int ensure_ws32(mxp_handle h, int64_t n_pad) {
     h->ws32_pad = 0;
     const size_t bytes = static_cast<size_t>(n_pad) * n_pad * 4;
     for (auto& p : h->planes) MXP_CUDA(cudaMalloc(&p, bytes));
+    if (h->part) cudaFree(h->part);
+    h->part = nullptr;
+    h->splits = (k1_block_n((int)n_pad, h->num_sms) == 128)
+                    ? k1_split_k((int)n_pad, (int)n_pad, h->num_sms)
+                    : 1;
+    if (h->splits > 1) MXP_CUDA(cudaMalloc(&h->part, bytes * h->splits));
     h->ws32_pad = n_pad;
     return MXP_OK;
 }
@@ -222,14 +230,15 @@ int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float
         m.a_lo = h->map_a[2 * acc + 1];
         m.b_hi = h->map_b[2 * rhs];
         m.b_lo = h->map_b[2 * rhs + 1];
-        e = launch_k1_gemm(m, np, bn, last ? dOut : nullptr, (int)n, (int)n,
-                           last ? nullptr : h->planes[2 * dst],
-                           last ? nullptr : h->planes[2 * dst + 1], h->stream);
+        e = launch_k1_gemm_rows(m, np, np, bn, last ? dOut : nullptr, (int)n, (int)n, (int)n,
+                                last ? nullptr : h->planes[2 * dst],
+                                last ? nullptr : h->planes[2 * dst + 1], h->stream, h->part,
+                                h->splits);
         if (e != cudaSuccess) {
             *failed = s;
             return cuda_fail(e, "k1_gemm_3xtf32");
         }
-        ++*launches;
+        *launches += (bn == 128 && h->splits > 1) ? 2 : 1;
         acc = dst;
     }
     return MXP_OK;
@@ -341,18 +350,11 @@ int run_power_graph(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA
         ce = cudaGraphInstantiate(&ge, g, 0);
         cudaGraphDestroy(g);
         if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
-        it = h->graphs.emplace(key, ge).first;
+        it = h->graphs.emplace(key, std::make_pair(ge, launches)).first;
     }
-    cudaError_t e = cudaGraphLaunch(it->second, h->stream);
+    cudaError_t e = cudaGraphLaunch(it->second.first, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
-    if (st) {
-        // launches inside the graph: recompute from the plan
-        const PlanBits p = make_plan(k);
-        if (mode == MXP_F32)
-            st->launches += (n <= kSmallMax) ? 1 : 1 + p.len;
-        else
-            st->launches += 2 + p.len;
-    }
+    if (st) st->launches += it->second.second;
     return MXP_OK;
 }
 
@@ -445,6 +447,7 @@ int mxp_destroy(mxp_handle h) {
     h->drop_graphs();
     for (auto p : h->planes)
         if (p) cudaFree(p);
+    if (h->part) cudaFree(h->part);
     for (auto p : h->f64buf)
         if (p) cudaFree(p);
     for (auto p : h->modbuf)
@@ -547,8 +550,9 @@ int mxp_gemm(mxp_handle h, int mode, int64_t n, const void* dA, const void* dB, 
                              h->planes[3], np, h->stream);
         if (e != cudaSuccess) return cuda_fail(e, "split");
         GemmPlanes m{h->map_a[0], h->map_a[1], h->map_b[2], h->map_b[3]};
-        e = launch_k1_gemm(m, np, k1_block_n(np, h->num_sms), static_cast<float*>(dC), (int)n,
-                           (int)n, nullptr, nullptr, h->stream);
+        e = launch_k1_gemm_rows(m, np, np, k1_block_n(np, h->num_sms), static_cast<float*>(dC),
+                                (int)n, (int)n, (int)n, nullptr, nullptr, h->stream, h->part,
+                                h->splits);
         if (e != cudaSuccess) return cuda_fail(e, "k1_gemm_3xtf32");
         return MXP_OK;
     }
@@ -596,8 +600,9 @@ int mxp_gemm_rows(mxp_handle h, int mode, int64_t n, int64_t rows, const void* d
                              h->planes[3], np, h->stream);
         if (e != cudaSuccess) return cuda_fail(e, "split");
         GemmPlanes m{a_hi, a_lo, b_hi, b_lo};
+        // same k-split as the full multiply / chain: bitwise-identical rows
         e = launch_k1_gemm_rows(m, np, (int)r_pad, bn, static_cast<float*>(dC), (int)n, (int)rows,
-                                (int)n, nullptr, nullptr, h->stream);
+                                (int)n, nullptr, nullptr, h->stream, h->part, h->splits);
         if (e != cudaSuccess) return cuda_fail(e, "k1_gemm_3xtf32");
         return MXP_OK;
     }

@@ -54,9 +54,13 @@ cudaError_t launch_k1_gemm(const GemmPlanes& maps, int n_pad, int block_n, float
                            int n_out, int ld_out, uint32_t* out_hi, uint32_t* out_lo,
                            cudaStream_t s);
 // Row block: C[m_pad x n_pad] = A[m_pad x n_pad] * B[n_pad x n_pad].
+// part != nullptr and splits > 1: split-K over `splits` k-ranges into the fp32
+// workspace `part` (splits x m_pad x n_pad), then a deterministic reduction.
 cudaError_t launch_k1_gemm_rows(const GemmPlanes& maps, int n_pad, int m_pad, int block_n,
                                 float* out_f32, int n_out, int m_out, int ld_out, uint32_t* out_hi,
-                                uint32_t* out_lo, cudaStream_t s);
+                                uint32_t* out_lo, cudaStream_t s, float* part = nullptr,
+                                int splits = 1);
+int k1_split_k(int n_pad, int m_pad, int num_sms);
 cudaError_t launch_split_rows(const float* in, int n, int ld, int rows, uint32_t* hi, uint32_t* lo,
                               int n_pad, int rows_pad, cudaStream_t s);
 
