@@ -65,7 +65,7 @@ def main():
     for rep in sys.argv[1:]:
         for d in raw(rep):
             name = d.get("Kernel Name", ("?", ""))[0]
-            short = name.split("(")[0].split("::")[-1].split("<")[0]
+            short = name.split("(")[0].split()[-1].split("::")[-1].split("<")[0]
             print(f"## {short}  ({os.path.basename(rep)})\n")
             print(f"`{name}`\n")
             for key in KEYS:
