@@ -716,7 +716,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K1PCfg::kThreads, 1)
     }
     if (warp == 2) tmem_alloc_pair<512>(tmem_slot);
     tc_fence_before();
-    cluster_sync_all();
+    __syncthreads();    // the allocation result in tmem_slot is visible CTA-wide
+    cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA traffic
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 

@@ -1,0 +1,20 @@
+"""Small invocations of every kernel family, for compute-sanitizer runs."""
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import oracle  # noqa: E402
+import paper_1204_3052_b200 as mx  # noqa: E402
+
+eng = mx.Engine(0)
+a = oracle.scaled_input(64, np.float32, 42)
+eng.power(a, 13)                                   # K3 (squares + base multiplies)
+mx.exponentiate_batched(mx.scaled_batch(48, 300, mx.DType.F32, 1), 7)   # K3 batched, n < 128
+mx.exponentiate_batched(mx.scaled_batch(37, 5, mx.DType.F32, 1), 5)    # K3, n % 4 != 0 (no TMA)
+eng.power(oracle.scaled_input(384, np.float32, 42), 13)                 # K1 split-K + reduce
+eng.power(oracle.scaled_input(1024, np.float32, 42), 5)                 # K1P CTA pairs
+eng.power(oracle.scaled_input(256, np.float64, 42), 9)                  # FP64 DMMA
+eng.power_mod(np.arange(100 * 100, dtype=np.uint32).reshape(100, 100), 11, 65521)
+mx.random_matrix(33, mx.DType.F32, 5)
+print("sanitize workload done")
