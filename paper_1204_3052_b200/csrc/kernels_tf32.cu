@@ -5,6 +5,7 @@
 // replaces the reference's scalar ascending-k fp32 loop (linalg.py:151-164,
 // matmul_tiled.cl:91-94); parity is by the relative-Frobenius tolerance of
 // SURVEY §8(d), not bitwise (tensor-core summation order differs).
+#include <cstdlib>
 #include <cstring>
 
 #include "mxp_internal.h"
@@ -355,8 +356,17 @@ __global__ void __launch_bounds__(kK3AllThreads, 1)
 long long* g_k3_prof = nullptr;
 void k3_set_profile(long long* dev_buf) { g_k3_prof = dev_buf; }
 
+static bool k3_use_tf32() {
+    static const bool v = [] {
+        const char* e = std::getenv("MXP_K3");
+        return e != nullptr && std::strcmp(e, "tf32") == 0;
+    }();
+    return v;
+}
+
 cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
                               const PlanBits& plan, int grid, cudaStream_t s) {
+    if (!k3_use_tf32()) return launch_k3b_batched(in, out, n, batch, plan, grid, s);
     if (grid > batch) grid = static_cast<int>(batch);
     CUtensorMap map;
     std::memset(&map, 0, sizeof map);

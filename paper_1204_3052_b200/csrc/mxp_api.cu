@@ -24,6 +24,7 @@ cudaError_t prepare_f64_kernels();
 cudaError_t prepare_kernels() {
     cudaError_t e = prepare_tf32_kernels();
     if (e == cudaSuccess) e = prepare_f64_kernels();
+    if (e == cudaSuccess) e = prepare_k3b_kernel();
     return e;
 }
 

@@ -15,8 +15,11 @@ struct PlanBits {
     uint64_t mult[2];
 };
 PlanBits make_plan(int64_t k);
+// (select, not p.mult[s >> 6]: a runtime index would copy a kernel-parameter
+// PlanBits into local memory)
 __host__ __device__ inline bool plan_is_mult(const PlanBits& p, int s) {
-    return (p.mult[s >> 6] >> (s & 63)) & 1ull;
+    const uint64_t w = s < 64 ? p.mult[0] : p.mult[1];
+    return (w >> (s & 63)) & 1ull;
 }
 
 // Set shared-memory attributes of every kernel on the current device (once
@@ -31,6 +34,12 @@ size_t k3_smem_bytes();
 void k3_set_profile(long long* dev_buf);  // debug: per-phase cycle totals of CTA 0
 cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
                               const PlanBits& plan, int grid, cudaStream_t s);
+// K3B (kernels_k3b.cu): the same contract, two chains per SM, bf16x3 split.
+// launch_k3_batched routes here unless MXP_K3=tf32 is set in the environment.
+size_t k3b_smem_bytes();
+cudaError_t prepare_k3b_kernel();
+cudaError_t launch_k3b_batched(const float* in, float* out, int n, int64_t batch,
+                               const PlanBits& plan, int grid, cudaStream_t s);
 
 // fp32 (n x n, leading dim ld) -> tf32 hi/lo planes (n_pad x n_pad, zero pad).
 cudaError_t launch_split(const float* in, int n, int ld, uint32_t* hi, uint32_t* lo, int n_pad,

@@ -42,6 +42,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Same, but a waiting thread is suspended in hardware (up to `ns`) instead of
+// spinning, so waiting warps leave the issue slots of their SM sub-partition to
+// the warps that work (the MMA issuer above all).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = 1000000) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "MXP_WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra MXP_WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(ns)
+        : "memory");
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -115,6 +128,56 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// kind::f16 (bf16 operands here), SS and TS (A from TMEM: lane = row m, two
+// 16-bit k-consecutive values per 32-bit column, the lower k in the low half —
+// measured with tools/bf16_probe.cu).
+__device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Offset forms: the constant offsets are added INSIDE the asm, so the
+// compiler cannot hoist 48 precomputed descriptors into registers (each then
+// needs an R2UR per MMA); ptxas adds them on the uniform datapath instead.
+template <uint32_t kD, uint32_t kA, uint32_t kB>
+__device__ __forceinline__ void mma_f16_ts_off(uint32_t tbase, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 dt, at;\n\t.reg .b64 bd;\n\t"
+        "add.u32 dt, %0, %4;\n\t"
+        "add.u32 at, %0, %5;\n\t"
+        "add.s64 bd, %1, %6;\n\t"
+        "setp.ne.b32 p, %3, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [dt], [at], bd, %2, p;\n}" ::"r"(tbase),
+        "l"(bdesc), "r"(idesc), "r"(accumulate), "n"(kD), "n"(kA), "n"(kB)
+        : "memory");
+}
+template <uint32_t kD, uint32_t kA, uint32_t kB>
+__device__ __forceinline__ void mma_f16_ss_off(uint32_t tbase, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 dt;\n\t.reg .b64 ad, bd;\n\t"
+        "add.u32 dt, %0, %5;\n\t"
+        "add.s64 ad, %1, %6;\n\t"
+        "add.s64 bd, %2, %7;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [dt], ad, bd, %3, p;\n}" ::"r"(tbase),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "n"(kD), "n"(kA), "n"(kB)
         : "memory");
 }
 // Arrive on an mbarrier once every previously issued tcgen05 op of this
@@ -212,6 +275,13 @@ __device__ __forceinline__ void tmem_ld16x4(uint32_t ta, uint32_t tb, uint32_t t
           "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
         : "r"(ta), "r"(tb), "r"(tc), "r"(td)
         : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                     taddr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+                 "r"(r[7])
+                 : "memory");
 }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
     asm volatile(
@@ -348,6 +418,23 @@ __host__ __device__ constexpr uint32_t idesc_tf32_kmaj_mnmaj() {
     static_assert(N % 16 == 0 && N >= 16 && N <= 256, "N");
     return (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
            (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// Instruction descriptor, kind::f16 with bf16 A/B, fp32 accumulate, A K-major,
+// B MN-major:  [4,6) c_format=1  [7,10) a_format=1 (BF16)  [10,13) b_format=1
+template <int M, int N>
+__host__ __device__ constexpr uint32_t idesc_bf16_kmaj_mnmaj() {
+    static_assert(M == 64 || M == 128, "M");
+    static_assert(N % 16 == 0 && N >= 16 && N <= 256, "N");
+    return (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
+           (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// L2 prefetch of a global range (bulk async, no completion tracking).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)),
+                 "r"(bytes)
+                 : "memory");
 }
 
 // ---------------------------------------------------------------- 3xTF32 split
