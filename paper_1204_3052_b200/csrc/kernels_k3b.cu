@@ -42,6 +42,8 @@
 // does: equal to the reference's acc * base (expo.py:135-136) because acc is
 // a power of the base.  Parity with the reference (linalg.py:151-164 chain,
 // expo.py:121-139) is by the relative-Frobenius tolerance of SURVEY §8(d).
+#include <cstring>
+
 #include "mxp_internal.h"
 #include "ptx.cuh"
 
@@ -55,7 +57,7 @@ constexpr uint32_t kPlane = 128u * 128u * 2u;     // one bf16 plane: 32 KB
 constexpr uint32_t kChainSmem = 3u * kPlane;      // y0, y1, y2 of one chain
 constexpr uint32_t kSOff = 2u * kChainSmem;       // base-b2 scratch
 constexpr uint32_t kBarOff = kSOff + kPlane;      // mbarriers + TMEM slot
-constexpr size_t kSmem = kBarOff + 64 + 1024;     // + alignment slack
+constexpr size_t kSmem = kBarOff + 256 + 1024;    // + alignment slack
 constexpr uint32_t kIdesc = idesc_bf16_kmaj_mnmaj<128, 128>();
 // descriptor address-field advance (16-byte units) per K=16 step
 //   right operand (MN-major): 16 rows of 128 B;  left (K-major): 32 B inside
@@ -149,22 +151,6 @@ __device__ __forceinline__ void store_row(float* __restrict__ dst, int n, int ve
 // for the issuer), so every operand is a compile-time offset from uniform
 // values: chain and step kind are template parameters and TMEM is addressed
 // from column 0 (the CTA owns the SM's whole TMEM, see k3b_batched_power).
-template <uint32_t C, uint32_t kT>  // kT: TS term index (0..4)
-__device__ __forceinline__ void k3b_ts_term(uint32_t tbase, uint64_t ybase) {
-    // (A plane, B plane): x0*y2, x1*y1, x0*y1, x1*y0, x0*y0 — smallest first
-    constexpr uint32_t kA = C * 256u + ((kT == 1 || kT == 3) ? 192u : 128u);
-    constexpr uint32_t kY = kT == 0 ? 2u : (kT <= 2 ? 1u : 0u);
-    constexpr uint32_t kYOff = kY * (kPlane >> 4);
-    mma_f16_ts_off<C * 256u, kA + 0, kYOff + 0 * kBStep>(tbase, ybase, kIdesc, 1u);
-    mma_f16_ts_off<C * 256u, kA + 8, kYOff + 1 * kBStep>(tbase, ybase, kIdesc, 1u);
-    mma_f16_ts_off<C * 256u, kA + 16, kYOff + 2 * kBStep>(tbase, ybase, kIdesc, 1u);
-    mma_f16_ts_off<C * 256u, kA + 24, kYOff + 3 * kBStep>(tbase, ybase, kIdesc, 1u);
-    mma_f16_ts_off<C * 256u, kA + 32, kYOff + 4 * kBStep>(tbase, ybase, kIdesc, 1u);
-    mma_f16_ts_off<C * 256u, kA + 40, kYOff + 5 * kBStep>(tbase, ybase, kIdesc, 1u);
-    mma_f16_ts_off<C * 256u, kA + 48, kYOff + 6 * kBStep>(tbase, ybase, kIdesc, 1u);
-    mma_f16_ts_off<C * 256u, kA + 56, kYOff + 7 * kBStep>(tbase, ybase, kIdesc, 1u);
-}
-
 template <uint32_t C, bool kMult>
 __device__ __forceinline__ void k3b_issue(uint32_t tbase, uint32_t s0, uint64_t* mma_bar,
                                           uint64_t* s_free) {
@@ -172,30 +158,23 @@ __device__ __forceinline__ void k3b_issue(uint32_t tbase, uint32_t s0, uint64_t*
     const uint64_t y0 = smem_desc(s0 + C * kChainSmem, 16384, 1024, 2);
     const uint64_t x2 = kMult ? smem_desc(s0 + kSOff, 16, 1024, 2)
                               : smem_desc(s0 + C * kChainSmem + 2 * kPlane, 16, 1024, 2);
-    constexpr uint32_t D = C * 256u;
-    mma_f16_ss_off<D, 0, 0 * kBStep>(tbase, x2, y0, kIdesc, 0u);
-    mma_f16_ss_off<D, 2, 1 * kBStep>(tbase, x2, y0, kIdesc, 1u);
-    mma_f16_ss_off<D, 4, 2 * kBStep>(tbase, x2, y0, kIdesc, 1u);
-    mma_f16_ss_off<D, 6, 3 * kBStep>(tbase, x2, y0, kIdesc, 1u);
-    mma_f16_ss_off<D, 1024, 4 * kBStep>(tbase, x2, y0, kIdesc, 1u);
-    mma_f16_ss_off<D, 1026, 5 * kBStep>(tbase, x2, y0, kIdesc, 1u);
-    mma_f16_ss_off<D, 1028, 6 * kBStep>(tbase, x2, y0, kIdesc, 1u);
-    mma_f16_ss_off<D, 1030, 7 * kBStep>(tbase, x2, y0, kIdesc, 1u);
-    if (kMult) mma_commit(s_free);
-    k3b_ts_term<C, 0>(tbase, y0);
-    k3b_ts_term<C, 1>(tbase, y0);
-    k3b_ts_term<C, 2>(tbase, y0);
-    k3b_ts_term<C, 3>(tbase, y0);
-    k3b_ts_term<C, 4>(tbase, y0);
-    mma_commit(mma_bar + C);
+    constexpr uint32_t D = C * 256u, X0 = D + 128u, X1 = D + 192u;
+    constexpr uint32_t Y1 = kPlane >> 4, Y2 = 2 * kPlane >> 4;
+    mma_f16_ss_x8<D, 0, kBStep, (16384u >> 4), true>(tbase, x2, y0, kIdesc);  // x2*y0
+    if (kMult) mma_commit_warp(s_free);
+    mma_f16_ts_x8<D, X0, Y2, kBStep>(tbase, y0, kIdesc);  // x0*y2
+    mma_f16_ts_x8<D, X1, Y1, kBStep>(tbase, y0, kIdesc);  // x1*y1
+    mma_f16_ts_x8<D, X0, Y1, kBStep>(tbase, y0, kIdesc);  // x0*y1
+    mma_f16_ts_x8<D, X1, 0, kBStep>(tbase, y0, kIdesc);   // x1*y0
+    mma_f16_ts_x8<D, X0, 0, kBStep>(tbase, y0, kIdesc);   // x0*y0
+    mma_commit_warp(mma_bar + C);
 }
 
-
-// Coalesced global IO (n == 128) through a warp-private 4 KB SMEM tile: the
-// warp's 32 rows x 32 columns, row r at r * 128 B with its 16-byte units XOR
-// r % 8 — conflict-free both for thread-per-row access (the TMEM lane layout)
-// and for 8-lanes-per-row access (each warp instruction then moves four whole
-// 128-byte rows instead of 32 scattered 16-byte pieces).
+// Global IO (n == 128) through a warp-private 4 KB SMEM tile: the warp's 32
+// rows x 32 columns, row r at r * 128 B with its 16-byte units XOR r % 8 —
+// the TMA SWIZZLE_128B box layout, and conflict-free for thread-per-row
+// access (the TMEM lane layout).  TMA moves whole tiles between HBM and SMEM
+// asynchronously, off the epilogue warps' instruction stream.
 __device__ __forceinline__ void tile_put_rows(uint32_t tile, uint32_t lane, const uint32_t (&v)[32]) {
 #pragma unroll
     for (uint32_t u = 0; u < 8; ++u)
@@ -210,47 +189,31 @@ __device__ __forceinline__ void tile_get_rows(uint32_t tile, uint32_t lane, floa
         x[4 * u + 2] = __uint_as_float(w.z); x[4 * u + 3] = __uint_as_float(w.w);
     }
 }
-// blk: element (32q, 32g) of the 128 x 128 row-major matrix
-__device__ __forceinline__ void tile_to_global(uint32_t tile, uint32_t lane, float* blk) {
-    const uint32_t u = lane & 7u;
-#pragma unroll
-    for (uint32_t i = 0; i < 8; ++i) {
-        const uint32_t r = 4 * i + (lane >> 3);
-        const uint4 w = lds128(tile + r * 128u + ((u ^ (r & 7u)) << 4));
-        __stcs(reinterpret_cast<float4*>(blk + r * 128u + 4 * u),
-               make_float4(__uint_as_float(w.x), __uint_as_float(w.y), __uint_as_float(w.z),
-                           __uint_as_float(w.w)));
-    }
-}
-__device__ __forceinline__ void global_rows_load(const float* blk, uint32_t lane, float4 (&w)[8]) {
-#pragma unroll
-    for (uint32_t i = 0; i < 8; ++i)
-        w[i] = __ldg(reinterpret_cast<const float4*>(blk + (4 * i + (lane >> 3)) * 128u + 4 * (lane & 7u)));
-}
-__device__ __forceinline__ void tile_put_loaded(uint32_t tile, uint32_t lane, const float4 (&w)[8]) {
-    const uint32_t u = lane & 7u;
-#pragma unroll
-    for (uint32_t i = 0; i < 8; ++i) {
-        const uint32_t r = 4 * i + (lane >> 3);
-        sts128(tile + r * 128u + ((u ^ (r & 7u)) << 4), __float_as_uint(w[i].x),
-               __float_as_uint(w[i].y), __float_as_uint(w[i].z), __float_as_uint(w[i].w));
-    }
-}
-
 }  // namespace
 
 size_t k3b_smem_bytes() { return kSmem; }
 
-#ifdef K3B_TRACE  // tools/k3b_trace.cu: per-slot clock64 stamps of CTA 0
+#ifdef K3B_TRACE  // tools/k3b_trace.cu: per-phase cycle totals of CTA 0 (warp 0 / issuer lane 0)
 __device__ long long* g_k3b_trace;
-#define K3B_STAMP(idx)                                                   \
-    do {                                                                 \
-        if (blockIdx.x == 0 && lane == 0 && (idx) < (1 << 20))           \
-            g_k3b_trace[idx] = clock64();                                \
+__shared__ long long k3b_acc[16];
+#define K3B_MARK(k)                                                          \
+    do {                                                                     \
+        if (blockIdx.x == 0 && (warp == 0 || warp == kIssueWarp) && lane == 0) { \
+            const long long t_ = clock64();                                  \
+            k3b_acc[k] += t_ - k3b_tprev;                                    \
+            k3b_tprev = t_;                                                  \
+        }                                                                    \
+    } while (0)
+#define K3B_COUNT(k)                                                         \
+    do {                                                                     \
+        if (blockIdx.x == 0 && (warp == 0 || warp == kIssueWarp) && lane == 0) k3b_acc[k] += 1; \
     } while (0)
 #else
-#define K3B_STAMP(idx) \
-    do {               \
+#define K3B_MARK(k) \
+    do {            \
+    } while (0)
+#define K3B_COUNT(k) \
+    do {             \
     } while (0)
 #endif
 
@@ -259,14 +222,16 @@ __device__ long long* g_k3b_trace;
 // run the same deterministic (chain, matrix, step) state machine, so they
 // agree on every publish without exchanging state.
 __global__ void __launch_bounds__(kThreads, 1)
-    k3b_batched_power(const float* __restrict__ in, float* __restrict__ out, int n,
-                      long long batch, PlanBits plan, int vec) {
+    k3b_batched_power(const __grid_constant__ CUtensorMap in_map,
+                      const __grid_constant__ CUtensorMap out_map, const float* __restrict__ in,
+                      float* __restrict__ out, int n, long long batch, PlanBits plan, int vec) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
     uint64_t* mma_bar = bars;     // [2] a chain's step MMAs completed
     uint64_t* s_free = bars + 2;  // the SS MMAs reading S completed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+    uint64_t* io_bar = bars + 8;  // [16] per epilogue warp: its input tile landed (TMA)
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -275,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(mma_bar, 1);
         mbar_init(mma_bar + 1, 1);
         mbar_init(s_free, 1);
+        for (int w = 0; w < kWorkers; ++w) mbar_init(io_bar + w, 1);
         fence_mbar_init();
     }
     if (warp == kIssueWarp) tmem_alloc<512>(tmem_slot);
@@ -292,9 +258,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     long long m_c = blockIdx.x, m_o = static_cast<long long>(blockIdx.x) + G;
     int s_c = -1, s_o = -1;
     bool act_c = m_c < batch, act_o = m_o < batch;
+    // Start-phase skew: chain c of CTA b sits out its first dly slots, so the
+    // chains' input/output steps (64 KB in + 64 KB out each) are spread over
+    // the plan instead of hitting HBM from all 296 chains at once.
+    int dly_c = 0, dly_o = 0;
+    if (batch >= 4 * G && plan.len > 1) {
+        dly_c = (2 * static_cast<int>(blockIdx.x)) % plan.len;
+        dly_o = (2 * static_cast<int>(blockIdx.x) + 1) % plan.len;
+    }
     uint32_t c = 0;
-    int tslot = 0;  // trace slot (K3B_TRACE builds only)
-    (void)tslot;
+#ifdef K3B_TRACE
+    if (tid < 16) k3b_acc[tid] = 0;
+    __syncthreads();
+    long long k3b_tprev = clock64();
+#endif
     auto swap_chains = [&]() {
         const long long tm = m_c;
         m_c = m_o;
@@ -305,13 +282,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool ta = act_c;
         act_c = act_o;
         act_o = ta;
+        const int td = dly_c;
+        dly_c = dly_o;
+        dly_o = td;
         c ^= 1u;
     };
 
     if (warp == kIssueWarp) {
         // ------------------------------------------------------------ MMA issue
         while (act_c || act_o) {
-            if (act_c) {
+            if (act_c && dly_c > 0) {
+                --dly_c;
+            } else if (act_c) {
                 if (s_c == last) {
                     m_c += 2 * G;
                     s_c = -1;
@@ -319,9 +301,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if (act_c) {
                     s_c += 1;
+                    K3B_MARK(10);
                     named_bar_sync(1 + c, kThreads);
-                    K3B_STAMP(tslot * 64 + 48);
-                    if (lane == 0) {
+                    K3B_MARK(8);
+                    {  // the whole warp: the MMA blocks elect one lane themselves
                         tc_fence_after();
                         const bool mult = plan_is_mult(plan, s_c);
                         if (c == 0) {
@@ -331,7 +314,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if (mult) k3b_issue<1, true>(tmem, s0, mma_bar, s_free);
                             else k3b_issue<1, false>(tmem, s0, mma_bar, s_free);
                         }
-                        K3B_STAMP(tslot * 64 + 49);
 #ifndef K3B_X_NOPF
                         if (lane == 0 && vec && s_c == 0 && m_c + 2 * G < batch)
 #else
@@ -341,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         static_cast<uint32_t>(n2 * 4));
                     }
                     __syncwarp();
-                    ++tslot;
+                    K3B_MARK(9);
                 }
             }
             swap_chains();
@@ -391,34 +373,46 @@ __global__ void __launch_bounds__(kThreads, 1)
             emit(cc, 1, x + 16, right, left);
         };
         const uint32_t tile_off = warp * 4096u;  // inside the chain's plane region
-        auto emit_input_tiled = [&](uint32_t cc, const float4 (&pre)[8]) {
+        uint32_t io_ph = 0;
+        // (TMA) the warp's 32 x 32 box of matrix mm into its tile; lane 0 issues
+        auto tile_load = [&](uint32_t tile, long long mm) {
+            if (lane == 0) {
+                mbar_expect_tx(io_bar + warp, 4096);
+                tma_load_2d_s(tile, &in_map, io_bar + warp, static_cast<int32_t>(col0),
+                              static_cast<int32_t>(mm * 128 + q * 32));
+            }
+        };
+        auto emit_input_tiled = [&](uint32_t cc) {
             const uint32_t tile = s0 + cc * kChainSmem + tile_off;
             float x[32];
-            tile_put_loaded(tile, lane, pre);
-            __syncwarp();
+            mbar_wait_sleep(io_bar + warp, io_ph);
+            io_ph ^= 1;
+            K3B_MARK(3);
             tile_get_rows(tile, lane, x);
             named_bar_sync(3, kWorkers * 32);  // every tile read before planes overwrite them
+            K3B_MARK(4);
             emit(cc, 0, x, true, true);
             emit(cc, 1, x + 16, true, true);
+            K3B_MARK(5);
         };
-        auto blk_of = [&](long long mm) { return static_cast<size_t>(mm) * n2 + q * 32u * 128u + col0; };
 
         while (act_c || act_o) {
-            if (act_c) {
+            if (act_c && dly_c > 0) {
+                --dly_c;
+            } else if (act_c) {
                 bool publish = true;
                 if (s_c < 0) {
                     if (vec) {
-                        float4 pre[8];
-                        global_rows_load(in + blk_of(m_c), lane, pre);
-                        emit_input_tiled(c, pre);
+                        tile_load(s0 + c * kChainSmem + tile_off, m_c);
+                        emit_input_tiled(c);
                     } else {
                         emit_input(c, true, true);
                     }
                     s_c = 0;
                 } else {
-                    K3B_STAMP(tslot * 64 + warp);
+                    K3B_MARK(7);
                     mbar_wait_sleep(mma_bar + c, ph_c);
-                    K3B_STAMP(tslot * 64 + 16 + warp);
+                    K3B_MARK(0);
                     ph_c ^= 1;
                     tc_fence_after();
                     uint32_t v[32];
@@ -427,20 +421,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 #else
                     tmem_ld32(lane_base + c * 256u + col0, v);
 #endif
+                    K3B_MARK(1);
                     if (s_c == last) {
                         const long long m_prev = m_c;
                         m_c += 2 * G;
                         act_c = m_c < batch;
                         if (vec) {
+                            // result -> the warp's tile -> TMA store; once the store
+                            // has read the tile, TMA loads the next input into it
                             const uint32_t tile = s0 + c * kChainSmem + tile_off;
                             tile_put_rows(tile, lane, v);
+                            fence_proxy_async_smem();
                             __syncwarp();
-                            tile_to_global(tile, lane, out + blk_of(m_prev));
+                            if (lane == 0) {
+                                tma_store_2d_s(&out_map, tile, static_cast<int32_t>(col0),
+                                               static_cast<int32_t>(m_prev * 128 + q * 32));
+                                bulk_commit_group();
+                                bulk_wait_group_read0();
+                            }
                             __syncwarp();
+                            K3B_MARK(2);
+                            K3B_COUNT(11);
                             if (act_c) {  // (prefetched into L2 one matrix ahead)
-                                float4 pre[8];
-                                global_rows_load(in + blk_of(m_c), lane, pre);
-                                emit_input_tiled(c, pre);
+                                tile_load(tile, m_c);
+                                emit_input_tiled(c);
                             }
                         } else {
                             store_row(out + static_cast<size_t>(m_prev) * n2, n, vec, row, col0, v);
@@ -453,6 +457,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const bool mult = plan_is_mult(plan, s_c);
                         emit(c, 0, reinterpret_cast<const float*>(v), true, !mult);
                         emit(c, 1, reinterpret_cast<const float*>(v) + 16, true, !mult);
+                        K3B_MARK(6);
+                        K3B_COUNT(12);
                         if (mult) {  // left operand = the base: x0, x1 to TMEM, x2 to S
                             if (s_uses > 0) mbar_wait_sleep(s_free, (s_uses - 1) & 1u);
                             emit_input(c, false, true);
@@ -464,9 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_st_wait();
                     fence_proxy_async_smem();
                     tc_fence_before();
-                    K3B_STAMP(tslot * 64 + 32 + warp);
                     named_bar_arrive(1 + c, kThreads);
-                    ++tslot;
                 }
             }
             swap_chains();
@@ -475,8 +479,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             ph_o = tp;
         }
     }
+    if (vec && warp < kWorkers && lane == 0) bulk_wait_group0();  // output stores done
     tc_fence_before();
     __syncthreads();
+#ifdef K3B_TRACE
+    if (blockIdx.x == 0 && tid < 16) g_k3b_trace[tid] = k3b_acc[tid];
+#endif
     if (warp == kIssueWarp) tmem_dealloc<512>(tmem);
 }
 
@@ -489,11 +497,17 @@ cudaError_t launch_k3b_batched(const float* in, float* out, int n, int64_t batch
                                const PlanBits& plan, int grid, cudaStream_t s) {
     if (plan.len < 1 || n < 1 || n > kSmallMax) return cudaErrorInvalidValue;
     if (grid > batch) grid = static_cast<int>(batch);
-    const int vec = (n == 128 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
-                     (reinterpret_cast<uintptr_t>(out) & 15) == 0)
-                        ? 1
-                        : 0;
-    k3b_batched_power<<<grid, kThreads, kSmem, s>>>(in, out, n, batch, plan, vec);
+    CUtensorMap in_map, out_map;
+    std::memset(&in_map, 0, sizeof in_map);
+    std::memset(&out_map, 0, sizeof out_map);
+    int vec = (n == 128 && batch * 128 < (int64_t(1) << 31) &&
+               (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+               (reinterpret_cast<uintptr_t>(out) & 15) == 0)
+                  ? 1
+                  : 0;
+    if (vec && !(encode_tile_map(&in_map, in, batch * 128) && encode_tile_map(&out_map, out, batch * 128)))
+        vec = 0;
+    k3b_batched_power<<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec);
     return cudaGetLastError();
 }
 

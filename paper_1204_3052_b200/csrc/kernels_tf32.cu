@@ -891,6 +891,21 @@ bool encode_batch_map(CUtensorMap* map, const void* base, int n, int64_t batch) 
     return r == CUDA_SUCCESS;
 }
 
+// 2-D map over `rows` rows of 128 fp32 (a batch of 128 x 128 matrices stacked
+// by rows): box {32, 32}, SWIZZLE_128B — the K3B warp-tile layout.
+bool encode_tile_map(CUtensorMap* map, const void* base, int64_t rows) {
+    EncodeTiledFn fn = get_encode_fn();
+    if (fn == nullptr) return false;
+    cuuint64_t dims[2] = {128, static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {128 * 4};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // 256: the CTA-pair kernel (needs n_pad % 256 == 0; used from 1024 up, where
 // its 256 x 256 pair tiles still give >= 8 clusters); 128: the 1-CTA kernel.
 int k1_block_n(int n_pad, int num_sms) {

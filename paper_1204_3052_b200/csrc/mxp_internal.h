@@ -56,6 +56,7 @@ struct GemmPlanes {
     CUtensorMap b_hi, b_lo;  // box {32, 32}, SWIZZLE_128B_ATOM_32B (MN-major right operand)
 };
 bool encode_batch_map(CUtensorMap* map, const void* base, int n, int64_t batch);
+bool encode_tile_map(CUtensorMap* map, const void* base, int64_t rows);
 bool encode_plane_map(CUtensorMap* map, const void* plane, int n_pad, int box_cols, int box_rows,
                       bool right_operand, int rows = 0);
 int k1_block_n(int n_pad, int num_sms);

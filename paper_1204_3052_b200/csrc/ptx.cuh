@@ -75,6 +75,34 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
 }
+// TMA tensor store shared -> global (bulk-group completion), and the group waits.
+// (shared addresses as 32-bit shared-window offsets)
+__device__ __forceinline__ void tma_store_2d_s(const CUtensorMap* map, uint32_t src, int32_t c0,
+                                               int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(src), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_s(uint32_t dst, const CUtensorMap* map, uint64_t* bar,
+                                              int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// the shared-memory sources of all committed bulk stores have been read
+__device__ __forceinline__ void bulk_wait_group_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_group0() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
 // 1-D bulk copy global -> shared (size and addresses 16-byte aligned).
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
                                           uint64_t* bar) {
@@ -178,6 +206,69 @@ __device__ __forceinline__ void mma_f16_ss_off(uint32_t tbase, uint64_t adesc, u
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [dt], ad, bd, %3, p;\n}" ::"r"(tbase),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "n"(kD), "n"(kA), "n"(kB)
+        : "memory");
+}
+// Eight K=16 steps of one term in ONE asm block (one elect/waterfall wrapper
+// for all eight MMAs instead of one per MMA): A from TMEM columns
+// tbase + kA + 8j, B descriptor bdesc + kB + j * kBStep, all accumulating.
+template <uint32_t kD, uint32_t kA, uint32_t kB, uint32_t kBStep>
+__device__ __forceinline__ void mma_f16_ts_x8(uint32_t tbase, uint64_t bdesc, uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 dt, a0, a1, a2, a3, a4, a5, a6, a7;\n\t"
+        ".reg .b64 b0, b1, b2, b3, b4, b5, b6, b7;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.eq.u32 p, 1, 1;\n\t"
+        "add.u32 dt, %0, %3;\n\t"
+        "add.u32 a0, %0, %4;\n\tadd.u32 a1, a0, 8;\n\tadd.u32 a2, a0, 16;\n\tadd.u32 a3, a0, 24;\n\t"
+        "add.u32 a4, a0, 32;\n\tadd.u32 a5, a0, 40;\n\tadd.u32 a6, a0, 48;\n\tadd.u32 a7, a0, 56;\n\t"
+        "add.s64 b0, %1, %5;\n\tadd.s64 b1, b0, %6;\n\tadd.s64 b2, b1, %6;\n\tadd.s64 b3, b2, %6;\n\t"
+        "add.s64 b4, b3, %6;\n\tadd.s64 b5, b4, %6;\n\tadd.s64 b6, b5, %6;\n\tadd.s64 b7, b6, %6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a0], b0, %2, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a1], b1, %2, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a2], b2, %2, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a3], b3, %2, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a4], b4, %2, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a5], b5, %2, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a6], b6, %2, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a7], b7, %2, p;\n}" ::"r"(tbase),
+        "l"(bdesc), "r"(idesc), "n"(kD), "n"(kA), "n"(kB), "n"(kBStep)
+        : "memory");
+}
+// SS: A descriptor adesc + (j/4) * kAChunk + (j%4) * 2 (K-major SW128, 32 B per
+// K=16 step inside the atom), B as above; the first MMA overwrites D when
+// kFirst (accumulate = 0).
+template <uint32_t kD, uint32_t kB, uint32_t kBStep, uint32_t kAChunk, bool kFirst>
+__device__ __forceinline__ void mma_f16_ss_x8(uint32_t tbase, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred p, p0, e;\n\t.reg .b32 dt;\n\t"
+        ".reg .b64 a0, a1, a2, a3, a4, a5, a6, a7, b0, b1, b2, b3, b4, b5, b6, b7;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.eq.u32 p, 1, 1;\n\t"
+        "setp.eq.u32 p0, %7, 0;\n\t"
+        "add.u32 dt, %0, %4;\n\t"
+        "mov.b64 a0, %1;\n\tadd.s64 a1, a0, 2;\n\tadd.s64 a2, a0, 4;\n\tadd.s64 a3, a0, 6;\n\t"
+        "add.s64 a4, a0, %6;\n\tadd.s64 a5, a4, 2;\n\tadd.s64 a6, a4, 4;\n\tadd.s64 a7, a4, 6;\n\t"
+        "add.s64 b0, %2, %5;\n\tadd.s64 b1, b0, %8;\n\tadd.s64 b2, b1, %8;\n\tadd.s64 b3, b2, %8;\n\t"
+        "add.s64 b4, b3, %8;\n\tadd.s64 b5, b4, %8;\n\tadd.s64 b6, b5, %8;\n\tadd.s64 b7, b6, %8;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], a0, b0, %3, p0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], a1, b1, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], a2, b2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], a3, b3, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], a4, b4, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], a5, b5, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], a6, b6, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], a7, b7, %3, p;\n}" ::"r"(tbase),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "n"(kD), "n"(kB), "n"(kAChunk), "n"(kFirst ? 1 : 0),
+        "n"(kBStep)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {  // warp-collective
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
+            smem_u32(bar))
         : "memory");
 }
 // Arrive on an mbarrier once every previously issued tcgen05 op of this
