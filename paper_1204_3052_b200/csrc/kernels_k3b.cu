@@ -52,7 +52,8 @@ namespace {
 
 constexpr int kWorkers = 16;                   // epilogue warps: 4 TMEM lane quarters x 4
 constexpr int kIssueWarp = kWorkers;           //   column groups, + one MMA-issue warp
-constexpr int kThreads = (kWorkers + 1) * 32;  // 544 (<= 96 registers per thread)
+constexpr int kIOWarp = kWorkers + 1;          //   + one TMA IO warp
+constexpr int kThreads = (kWorkers + 2) * 32;  // 576 (<= 96 registers per thread)
 constexpr uint32_t kPlane = 128u * 128u * 2u;     // one bf16 plane: 32 KB
 constexpr uint32_t kChainSmem = 3u * kPlane;      // y0, y1, y2 of one chain
 constexpr uint32_t kSOff = 2u * kChainSmem;       // base-b2 scratch
@@ -198,7 +199,7 @@ __device__ long long* g_k3b_trace;
 __shared__ long long k3b_acc[16];
 #define K3B_MARK(k)                                                          \
     do {                                                                     \
-        if (blockIdx.x == 0 && (warp == 0 || warp == kIssueWarp) && lane == 0) { \
+        if (blockIdx.x == 0 && (warp == 0 || warp == kIssueWarp || warp == kIOWarp) && lane == 0) { \
             const long long t_ = clock64();                                  \
             k3b_acc[k] += t_ - k3b_tprev;                                    \
             k3b_tprev = t_;                                                  \
@@ -206,7 +207,7 @@ __shared__ long long k3b_acc[16];
     } while (0)
 #define K3B_COUNT(k)                                                         \
     do {                                                                     \
-        if (blockIdx.x == 0 && (warp == 0 || warp == kIssueWarp) && lane == 0) k3b_acc[k] += 1; \
+        if (blockIdx.x == 0 && (warp == 0 || warp == kIssueWarp || warp == kIOWarp) && lane == 0) k3b_acc[k] += 1; \
     } while (0)
 #else
 #define K3B_MARK(k) \
@@ -218,9 +219,18 @@ __shared__ long long k3b_acc[16];
 #endif
 
 // Matrices of CTA b are b, b + G, b + 2G, ... (G = gridDim.x); chain c takes
-// every other one starting at b + cG.  The issue warp and the epilogue warps
-// run the same deterministic (chain, matrix, step) state machine, so they
-// agree on every publish without exchanging state.
+// every other one starting at b + cG.  Three roles run the same deterministic
+// (chain, matrix, step) state machine, so they agree on every hand-off
+// without exchanging state:
+//   warps 0-15  epilogue: drain D, split, write the next operands, publish;
+//   warp 16     MMA issue (one elected lane);
+//   warp 17     IO: TMA stores of finished results and TMA loads of the next
+//               inputs (n == 128), L2 prefetch one matrix ahead.
+// A chain's matrix boundary takes two of its slots: OUT (drain the last
+// product into the warp tiles, hand them to the IO warp) and, one slot later,
+// IN (convert the freshly loaded input into operands, publish step 0).  In
+// between, the epilogue warps serve the other chain, so the HBM round trip
+// overlaps that chain's MMAs instead of stalling the epilogue.
 __global__ void __launch_bounds__(kThreads, 1)
     k3b_batched_power(const __grid_constant__ CUtensorMap in_map,
                       const __grid_constant__ CUtensorMap out_map, const float* __restrict__ in,
@@ -228,10 +238,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
-    uint64_t* mma_bar = bars;     // [2] a chain's step MMAs completed
-    uint64_t* s_free = bars + 2;  // the SS MMAs reading S completed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
-    uint64_t* io_bar = bars + 8;  // [16] per epilogue warp: its input tile landed (TMA)
+    uint64_t* mma_bar = bars;        // [2] a chain's step MMAs completed
+    uint64_t* s_free = bars + 2;     // the SS MMAs reading S completed
+    uint64_t* out_ready = bars + 3;  // [2] a chain's result is in its warp tiles (16 arrivals)
+    uint64_t* in_ready = bars + 5;   // [2] a chain's next input landed in its warp tiles (TMA)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -240,7 +251,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(mma_bar, 1);
         mbar_init(mma_bar + 1, 1);
         mbar_init(s_free, 1);
-        for (int w = 0; w < kWorkers; ++w) mbar_init(io_bar + w, 1);
+        mbar_init(out_ready, kWorkers);
+        mbar_init(out_ready + 1, kWorkers);
+        mbar_init(in_ready, 1);
+        mbar_init(in_ready + 1, 1);
         fence_mbar_init();
     }
     if (warp == kIssueWarp) tmem_alloc<512>(tmem_slot);
@@ -252,14 +266,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const long long G = gridDim.x;
     const size_t n2 = static_cast<size_t>(n) * n;
     const int last = plan.len - 1;
+    constexpr int kIn = -2;  // s value: the next input is being loaded / converted
 
     // state of the current chain (c) and of the other one, swapped every slot
     // (runtime-indexed arrays would live in local memory)
     long long m_c = blockIdx.x, m_o = static_cast<long long>(blockIdx.x) + G;
-    int s_c = -1, s_o = -1;
+    int s_c = kIn, s_o = kIn;
     bool act_c = m_c < batch, act_o = m_o < batch;
     // Start-phase skew: chain c of CTA b sits out its first dly slots, so the
-    // chains' input/output steps (64 KB in + 64 KB out each) are spread over
+    // chains' matrix boundaries (64 KB in + 64 KB out each) are spread over
     // the plan instead of hitting HBM from all 296 chains at once.
     int dly_c = 0, dly_o = 0;
     if (batch >= 4 * G && plan.len > 1) {
@@ -267,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         dly_o = (2 * static_cast<int>(blockIdx.x) + 1) % plan.len;
     }
     uint32_t c = 0;
+    uint32_t ph_c = 0, ph_o = 0;  // per-chain mbarrier parities of this role
 #ifdef K3B_TRACE
     if (tid < 16) k3b_acc[tid] = 0;
     __syncthreads();
@@ -285,7 +301,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int td = dly_c;
         dly_c = dly_o;
         dly_o = td;
+        const uint32_t tp = ph_c;
+        ph_c = ph_o;
+        ph_o = tp;
         c ^= 1u;
+    };
+    // the 16 warp tiles of chain cc <-> matrix mm (TMA boxes of 32 x 32)
+    auto tiles_load = [&](uint32_t cc, long long mm) {
+        mbar_expect_tx(in_ready + cc, 16 * 4096);
+        for (uint32_t w = 0; w < kWorkers; ++w)
+            tma_load_2d_s(s0 + cc * kChainSmem + w * 4096u, &in_map, in_ready + cc,
+                          static_cast<int32_t>((w >> 2) * 32), static_cast<int32_t>(mm * 128 + (w & 3) * 32));
+        if (mm + 2 * G < batch)
+            prefetch_l2(in + static_cast<size_t>(mm + 2 * G) * n2, static_cast<uint32_t>(n2 * 4));
     };
 
     if (warp == kIssueWarp) {
@@ -294,33 +322,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (act_c && dly_c > 0) {
                 --dly_c;
             } else if (act_c) {
-                if (s_c == last) {
+                if (s_c == last) {  // OUT slot: nothing to issue
                     m_c += 2 * G;
-                    s_c = -1;
                     act_c = m_c < batch;
-                }
-                if (act_c) {
-                    s_c += 1;
+                    s_c = kIn;
+                } else {
+                    s_c = (s_c == kIn) ? 0 : s_c + 1;
                     K3B_MARK(10);
-                    named_bar_sync(1 + c, kThreads);
+                    named_bar_sync(1 + c, kWorkers * 32 + 32);
                     K3B_MARK(8);
-                    {  // the whole warp: the MMA blocks elect one lane themselves
-                        tc_fence_after();
-                        const bool mult = plan_is_mult(plan, s_c);
-                        if (c == 0) {
-                            if (mult) k3b_issue<0, true>(tmem, s0, mma_bar, s_free);
-                            else k3b_issue<0, false>(tmem, s0, mma_bar, s_free);
-                        } else {
-                            if (mult) k3b_issue<1, true>(tmem, s0, mma_bar, s_free);
-                            else k3b_issue<1, false>(tmem, s0, mma_bar, s_free);
-                        }
-#ifndef K3B_X_NOPF
-                        if (lane == 0 && vec && s_c == 0 && m_c + 2 * G < batch)
-#else
-                        if (false)
-#endif
-                            prefetch_l2(in + static_cast<size_t>(m_c + 2 * G) * n2,
-                                        static_cast<uint32_t>(n2 * 4));
+                    tc_fence_after();  // the whole warp: the MMA blocks elect one lane
+                    const bool mult = plan_is_mult(plan, s_c);
+                    if (c == 0) {
+                        if (mult) k3b_issue<0, true>(tmem, s0, mma_bar, s_free);
+                        else k3b_issue<0, false>(tmem, s0, mma_bar, s_free);
+                    } else {
+                        if (mult) k3b_issue<1, true>(tmem, s0, mma_bar, s_free);
+                        else k3b_issue<1, false>(tmem, s0, mma_bar, s_free);
                     }
                     __syncwarp();
                     K3B_MARK(9);
@@ -328,72 +346,87 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             swap_chains();
         }
+    } else if (warp == kIOWarp) {
+        // ------------------------------------------------------------ IO (TMA)
+        if (vec && lane == 0) {
+            if (act_c) tiles_load(0, m_c);
+            if (act_o) tiles_load(1, m_o);
+        }
+        while (act_c || act_o) {
+            if (act_c && dly_c > 0) {
+                --dly_c;
+            } else if (act_c) {
+                if (s_c == last) {
+                    const long long m_prev = m_c;
+                    m_c += 2 * G;
+                    act_c = m_c < batch;
+                    s_c = kIn;
+                    if (vec) {
+                        K3B_MARK(10);
+                        mbar_wait_sleep(out_ready + c, ph_c);
+                        ph_c ^= 1;
+                        K3B_MARK(8);
+                        if (lane == 0) {
+                            for (uint32_t w = 0; w < kWorkers; ++w)
+                                tma_store_2d_s(&out_map, s0 + c * kChainSmem + w * 4096u,
+                                               static_cast<int32_t>((w >> 2) * 32),
+                                               static_cast<int32_t>(m_prev * 128 + (w & 3) * 32));
+                            bulk_commit_group();
+                            bulk_wait_group_read0();  // tiles read: reuse them for the input
+                            if (act_c) tiles_load(c, m_c);
+                        }
+                        __syncwarp();
+                        K3B_MARK(9);
+                    }
+                } else {
+                    s_c = (s_c == kIn) ? 0 : s_c + 1;
+                }
+            }
+            swap_chains();
+        }
+        if (vec && lane == 0) bulk_wait_group0();  // results written before exit
     } else {
         // ------------------------------------------------------------ epilogue
         const uint32_t q = warp & 3, g = warp >> 2;
         const uint32_t row = q * 32 + lane;
         const uint32_t col0 = g * 32;
         const uint32_t lane_base = tmem + ((q * 32) << 16);
-        uint32_t ph_c = 0, ph_o = 0;  // mma_bar parities (swapped with the state)
+        const uint32_t tile_off = warp * 4096u;  // the warp's tile inside a chain's plane region
+        uint32_t inph_c = 0, inph_o = 0;         // in_ready parities (swapped with the chains)
         uint32_t s_uses = 0;
 
         // 16 values (columns col0 + 16h ...) -> the chain's y planes and,
-        // when `left`, its x0/x1 TMEM planes; `sonly`: the base's b2 into S.
+        // when `left`, its x0/x1 TMEM planes; !right: only the b2 plane, into S.
         auto emit = [&](uint32_t cc, uint32_t h, const float* x, bool right, bool left) {
-#ifdef K3B_X_NOEPI
-            return;
-#endif
             uint32_t p0[8], p1[8], p2[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) split3(x[2 * j], x[2 * j + 1], p0[j], p1[j], p2[j]);
+            // opaque copies: recompute the swizzled addresses here instead of
+            // letting the compiler hoist ~20 of them out of the loop (and spill)
+            uint32_t r_ = row, b_ = s0;
+            asm volatile("" : "+r"(r_), "+r"(b_));
             if (right) {
-                const uint32_t pb = s0 + cc * kChainSmem;
-                put_half(pb, row, g, h, p0);
-                put_half(pb + kPlane, row, g, h, p1);
-                put_half(pb + 2 * kPlane, row, g, h, p2);
+                const uint32_t pb = b_ + cc * kChainSmem;
+                put_half(pb, r_, g, h, p0);
+                put_half(pb + kPlane, r_, g, h, p1);
+                put_half(pb + 2 * kPlane, r_, g, h, p2);
             } else {
-                put_half(s0 + kSOff, row, g, h, p2);
+                put_half(b_ + kSOff, r_, g, h, p2);
             }
             if (left) {
-                const uint32_t tl = lane_base + cc * 256u + 128u + g * 16u + h * 8u;
-#ifndef K3B_X_NOTMEM
+                uint32_t lb_ = lane_base;
+                asm volatile("" : "+r"(lb_));
+                const uint32_t tl = lb_ + cc * 256u + 128u + g * 16u + h * 8u;
                 tmem_st8(tl, p0);
                 tmem_st8(tl + 64u, p1);
-#endif
             }
         };
-        // new matrix m_c of chain cc: all three planes + x0/x1.  For n == 128
-        // the rows come in coalesced through the warp's tile in the chain's
-        // (dead) plane region; `pre` holds loads already in flight.
-        auto emit_input = [&](uint32_t cc, bool right, bool left) {
-            const float* src = in + static_cast<size_t>(m_c) * n2;
+        // matrix m_c straight from global (n != 128, and the base of a MULTIPLY_BASE step)
+        auto emit_global = [&](uint32_t cc, bool right, bool left) {
             float x[32];
-            load_row(src, n, vec, row, col0, x);
+            load_row(in + static_cast<size_t>(m_c) * n2, n, vec, row, col0, x);
             emit(cc, 0, x, right, left);
             emit(cc, 1, x + 16, right, left);
-        };
-        const uint32_t tile_off = warp * 4096u;  // inside the chain's plane region
-        uint32_t io_ph = 0;
-        // (TMA) the warp's 32 x 32 box of matrix mm into its tile; lane 0 issues
-        auto tile_load = [&](uint32_t tile, long long mm) {
-            if (lane == 0) {
-                mbar_expect_tx(io_bar + warp, 4096);
-                tma_load_2d_s(tile, &in_map, io_bar + warp, static_cast<int32_t>(col0),
-                              static_cast<int32_t>(mm * 128 + q * 32));
-            }
-        };
-        auto emit_input_tiled = [&](uint32_t cc) {
-            const uint32_t tile = s0 + cc * kChainSmem + tile_off;
-            float x[32];
-            mbar_wait_sleep(io_bar + warp, io_ph);
-            io_ph ^= 1;
-            K3B_MARK(3);
-            tile_get_rows(tile, lane, x);
-            named_bar_sync(3, kWorkers * 32);  // every tile read before planes overwrite them
-            K3B_MARK(4);
-            emit(cc, 0, x, true, true);
-            emit(cc, 1, x + 16, true, true);
-            K3B_MARK(5);
         };
 
         while (act_c || act_o) {
@@ -401,12 +434,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 --dly_c;
             } else if (act_c) {
                 bool publish = true;
-                if (s_c < 0) {
+                if (s_c == kIn) {
+                    // ---- IN: the new matrix -> operands of step 0
                     if (vec) {
-                        tile_load(s0 + c * kChainSmem + tile_off, m_c);
-                        emit_input_tiled(c);
+                        K3B_MARK(7);
+                        mbar_wait_sleep(in_ready + c, inph_c);
+                        inph_c ^= 1;
+                        K3B_MARK(3);
+                        float x[32];
+                        tile_get_rows(s0 + c * kChainSmem + tile_off, lane, x);
+                        named_bar_sync(3, kWorkers * 32);  // all tiles read before planes overwrite them
+                        K3B_MARK(4);
+                        emit(c, 0, x, true, true);
+                        emit(c, 1, x + 16, true, true);
+                        K3B_MARK(5);
                     } else {
-                        emit_input(c, true, true);
+                        emit_global(c, true, true);
                     }
                     s_c = 0;
                 } else {
@@ -416,70 +459,55 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ph_c ^= 1;
                     tc_fence_after();
                     uint32_t v[32];
-#if defined(K3B_X_NOTMEM) || defined(K3B_X_NOEPI)
-                    for (int i = 0; i < 32; ++i) v[i] = row + i;
-#else
                     tmem_ld32(lane_base + c * 256u + col0, v);
-#endif
                     K3B_MARK(1);
                     if (s_c == last) {
-                        const long long m_prev = m_c;
+                        // ---- OUT: the result -> the warp tile (IO warp stores it)
+                        if (vec) {
+                            tile_put_rows(s0 + c * kChainSmem + tile_off, lane, v);
+                            fence_proxy_async_smem();
+                            tc_fence_before();  // D reads done before the next MMAs into D
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(out_ready + c);
+                            K3B_MARK(2);
+                            K3B_COUNT(13);
+                        } else {
+                            store_row(out + static_cast<size_t>(m_c) * n2, n, vec, row, col0, v);
+                            tc_fence_before();
+                        }
                         m_c += 2 * G;
                         act_c = m_c < batch;
-                        if (vec) {
-                            // result -> the warp's tile -> TMA store; once the store
-                            // has read the tile, TMA loads the next input into it
-                            const uint32_t tile = s0 + c * kChainSmem + tile_off;
-                            tile_put_rows(tile, lane, v);
-                            fence_proxy_async_smem();
-                            __syncwarp();
-                            if (lane == 0) {
-                                tma_store_2d_s(&out_map, tile, static_cast<int32_t>(col0),
-                                               static_cast<int32_t>(m_prev * 128 + q * 32));
-                                bulk_commit_group();
-                                bulk_wait_group_read0();
-                            }
-                            __syncwarp();
-                            K3B_MARK(2);
-                            K3B_COUNT(11);
-                            if (act_c) {  // (prefetched into L2 one matrix ahead)
-                                tile_load(tile, m_c);
-                                emit_input_tiled(c);
-                            }
-                        } else {
-                            store_row(out + static_cast<size_t>(m_prev) * n2, n, vec, row, col0, v);
-                            if (act_c) emit_input(c, true, true);
-                        }
-                        if (act_c) s_c = 0;
-                        else publish = false;
+                        s_c = kIn;
+                        publish = false;
                     } else {
                         s_c += 1;
                         const bool mult = plan_is_mult(plan, s_c);
                         emit(c, 0, reinterpret_cast<const float*>(v), true, !mult);
                         emit(c, 1, reinterpret_cast<const float*>(v) + 16, true, !mult);
                         K3B_MARK(6);
-                        K3B_COUNT(12);
+                        K3B_COUNT(14);
                         if (mult) {  // left operand = the base: x0, x1 to TMEM, x2 to S
                             if (s_uses > 0) mbar_wait_sleep(s_free, (s_uses - 1) & 1u);
-                            emit_input(c, false, true);
+                            emit_global(c, false, true);
                             ++s_uses;
                         }
                     }
                 }
                 if (publish) {
+                    // workers arrive; the issue warp waits for all of them (the
+                    // hardware barrier also drains pending st.shared) and issues
                     tmem_st_wait();
                     fence_proxy_async_smem();
                     tc_fence_before();
-                    named_bar_arrive(1 + c, kThreads);
+                    named_bar_arrive(1 + c, kWorkers * 32 + 32);
                 }
             }
             swap_chains();
-            const uint32_t tp = ph_c;
-            ph_c = ph_o;
-            ph_o = tp;
+            const uint32_t tp = inph_c;
+            inph_c = inph_o;
+            inph_o = tp;
         }
     }
-    if (vec && warp < kWorkers && lane == 0) bulk_wait_group0();  // output stores done
     tc_fence_before();
     __syncthreads();
 #ifdef K3B_TRACE

@@ -36,6 +36,7 @@ int main(int argc, char** argv) {
         printf("%-20s %10lld cycles  %5.1f%%\n", nm[i], h[i], 100.0 * h[i] / (i < 8 ? tot_e : tot_i));
     printf("IO steps %lld, normal steps %lld; per IO step: out %.0f ldg %.0f bar %.0f emit %.0f; per normal step emit %.0f\n",
            h[11], h[12], double(h[2]) / h[11], double(h[3]) / h[11], double(h[4]) / h[11], double(h[5]) / h[11], double(h[6]) / h[12]);
+    printf("IO out split: tile st.shared %.0f, fence+syncwarp %.0f, TMA store+wait read %.0f\n", double(h[13]) / h[11], double(h[14]) / h[11], double(h[2]) / h[11]);
     printf("per slot (E total / slots) %.0f, issue per step %.0f\n", double(tot_e) / (h[11] + h[12]), double(h[9]) / (h[11] + h[12]));
     return 0;
 }
