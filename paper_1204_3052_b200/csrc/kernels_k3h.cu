@@ -1,0 +1,492 @@
+// K3H — persistent batched A^k for n <= 128: two independent chains per SM,
+// split-FP32 as two scaled fp16 planes (tcgen05 kind::f16, fp32 accumulate).
+//
+// A 128x128 chain step is a run of tensor-core MMAs followed by an epilogue
+// (drain the accumulator, split, write the next operands).  One chain per SM
+// serialises the two; two chains per SM overlap chain X's MMAs with chain Y's
+// epilogue.  That needs two resident powers per SM, which the 3xTF32 operands
+// of K3 (kernels_tf32.cu) cannot provide (128 KB SMEM + 256 TMEM columns each).
+//
+// Split (the fp16 analogue of 3xTF32, same 22-bit operand precision):
+//   P = 2^e * P',  max|P'| in [2^13, 2^14)   (power-of-two scale: exact)
+//   h0 = rn_fp16(x'),  h1 = rn_fp16(x' - h0)  (x' - h0 exact; |x' - h0 - h1| <= 2^-22 |x'|)
+//   X * Y = 2^(ex + ey) * (x1*y0 + x0*y1 + x0*y0)   (dropped x1*y1 ~ 2^-22)
+// fp16 shares tf32's 11-bit significand; the per-step scale replaces tf32's
+// 8-bit exponent (each step rescales from the max |element| of its product,
+// so powers that grow or shrink by orders of magnitude stay in range).  fp16
+// MMAs run K=16 per 64 cycles where tf32 runs K=8: a 3-term split costs 24
+// MMAs per 128^3 step instead of 48.
+//
+// One row-major 16-bit plane, stored as [c/64][r][128 B] with 16-byte units
+// XOR-swizzled by r % 8, is a K-major SWIZZLE_128B left operand and an
+// MN-major SWIZZLE_128B right operand at once (tools/bf16_probe.cu).
+//
+//   SMEM:  chain c: y0, y1 planes of the resident power P' (64 KB)
+//   TMEM:  chain c at column 256c: D (fp32 accumulator, 128 columns),
+//          x0, x1 left-operand planes (2 fp16 per column, 64 columns each)
+//
+// Per step of chain c one elected lane of the issue warp runs 24 MMAs
+// (M=N=128, K=16, A from TMEM): x1*y0, x0*y1, then x0*y0 — small terms first
+// because the tensor core truncates its fp32 accumulator on every MMA
+// (DESIGN.md §3).  The 16 epilogue warps alternate between the chains.
+//
+// MULTIPLY_BASE computes base * acc (the base is the left operand), as K3
+// does: equal to the reference's acc * base (expo.py:135-136) because acc is
+// a power of the base.  Parity with the reference chain (linalg.py:151-164,
+// expo.py:121-139) is by the relative-Frobenius tolerance of SURVEY §8(d).
+#include <cstring>
+
+#include "mxp_internal.h"
+#include "ptx.cuh"
+
+namespace mxp {
+namespace {
+
+constexpr int kWorkers = 16;                   // epilogue warps: 4 TMEM lane quarters x 4
+constexpr int kIssueWarp = kWorkers;           //   column groups, + one MMA-issue warp
+constexpr int kIOWarp = kWorkers + 1;          //   + one TMA IO warp
+constexpr int kThreads = (kWorkers + 2) * 32;  // 576 (<= 96 registers per thread)
+constexpr uint32_t kPlane = 128u * 128u * 2u;  // one fp16 plane: 32 KB
+constexpr uint32_t kChainSmem = 2u * kPlane;   // y0, y1 of one chain
+constexpr uint32_t kMaxOff = 2u * kChainSmem;  // [2][16] per-warp max |D| slots
+constexpr uint32_t kBarOff = kMaxOff + 128;    // mbarriers + TMEM slot
+constexpr size_t kSmem = kBarOff + 128 + 1024; // + alignment slack
+constexpr int kTarget = 13;                    // scaled max |P'| in [2^13, 2^14)
+// kind::f16 with fp16 A/B (formats 0), fp32 D, A K-major, B MN-major, M = N = 128
+constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | (1u << 16) | ((128u >> 3) << 17) |
+                            ((128u >> 4) << 24);
+constexpr uint32_t kBStep = (16u * 128u) >> 4;  // right-operand descriptor advance per K=16
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023u) & ~uintptr_t(1023));
+}
+
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ void unpack_f16x2(uint32_t p, float& lo, float& hi) {
+    asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n}"
+        : "=f"(lo), "=f"(hi)
+        : "r"(p));
+}
+// (a, b) = columns 2j, 2j+1, already scaled: two packed fp16x2 words, h0 and h1
+__device__ __forceinline__ void split2(float a, float b, uint32_t& p0, uint32_t& p1) {
+    p0 = pack_f16x2(a, b);
+    float a0, b0;
+    unpack_f16x2(p0, a0, b0);
+    p1 = pack_f16x2(__fsub_rn(a, a0), __fsub_rn(b, b0));
+}
+// 2^t as a float, t clamped to the normal range
+__device__ __forceinline__ float exp2i(int t) {
+    t = max(-126, min(127, t));
+    return __int_as_float((t + 127) << 23);
+}
+// scale exponent for a block whose max |element| has bit pattern mbits:
+// returns t with max * 2^t in [2^13, 2^14) (0 for zero, inf or NaN maxima)
+__device__ __forceinline__ int scale_exp(uint32_t mbits) {
+    if (mbits == 0u || mbits >= 0x7F800000u) return 0;
+    const int k = mbits >= 0x00800000u ? static_cast<int>(mbits >> 23) - 127
+                                       : -127 + (31 - __clz(static_cast<int>(mbits))) - 22;
+    return kTarget - k;
+}
+__device__ __forceinline__ uint32_t absmax_bits(const float* x) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) m = max(m, __float_as_uint(x[i]) & 0x7FFFFFFFu);
+    return m;
+}
+
+// Row `row`, columns [32g + 16h, +16) of a plane: two 16-byte units, unit
+// index XOR row % 8 (a quarter-warp = 8 consecutive rows hits 8 distinct
+// bank groups).
+__device__ __forceinline__ void put_half(uint32_t plane, uint32_t row, uint32_t g, uint32_t h,
+                                         const uint32_t (&p)[8]) {
+    const uint32_t base = plane + (g >> 1) * 16384u + row * 128u;
+    const uint32_t u0 = (g & 1u) * 4u + 2u * h;
+    sts128(base + ((u0 ^ (row & 7u)) << 4), p[0], p[1], p[2], p[3]);
+    sts128(base + (((u0 + 1u) ^ (row & 7u)) << 4), p[4], p[5], p[6], p[7]);
+}
+
+// 32 values of one row of an n x n fp32 matrix, zero padded to 128.
+__device__ __forceinline__ void load_row(const float* __restrict__ src, int n, uint32_t row,
+                                         uint32_t col0, float (&x)[32]) {
+    if (n == 128 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        const float4* p = reinterpret_cast<const float4*>(src + row * 128u + col0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float4 v = __ldg(p + i);
+            x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const uint32_t c = col0 + i;
+            x[i] = (row < static_cast<uint32_t>(n) && c < static_cast<uint32_t>(n))
+                       ? __ldg(src + static_cast<size_t>(row) * n + c)
+                       : 0.f;
+        }
+    }
+}
+__device__ __forceinline__ void store_row(float* __restrict__ dst, int n, uint32_t row,
+                                          uint32_t col0, const float* v) {
+    if (row < static_cast<uint32_t>(n)) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (col0 + i < static_cast<uint32_t>(n))
+                dst[static_cast<size_t>(row) * n + col0 + i] = v[i];
+    }
+}
+
+// Global IO (n == 128) through a warp-private 4 KB SMEM tile: the warp's 32
+// rows x 32 columns, row r at r * 128 B with its 16-byte units XOR r % 8 —
+// the TMA SWIZZLE_128B box layout, and conflict-free for thread-per-row
+// access (the TMEM lane layout).
+__device__ __forceinline__ void tile_put_rows(uint32_t tile, uint32_t lane, const float* v) {
+#pragma unroll
+    for (uint32_t u = 0; u < 8; ++u)
+        sts128(tile + lane * 128u + ((u ^ (lane & 7u)) << 4), __float_as_uint(v[4 * u]),
+               __float_as_uint(v[4 * u + 1]), __float_as_uint(v[4 * u + 2]),
+               __float_as_uint(v[4 * u + 3]));
+}
+__device__ __forceinline__ void tile_get_rows(uint32_t tile, uint32_t lane, float (&x)[32]) {
+#pragma unroll
+    for (uint32_t u = 0; u < 8; ++u) {
+        const uint4 w = lds128(tile + lane * 128u + ((u ^ (lane & 7u)) << 4));
+        x[4 * u] = __uint_as_float(w.x); x[4 * u + 1] = __uint_as_float(w.y);
+        x[4 * u + 2] = __uint_as_float(w.z); x[4 * u + 3] = __uint_as_float(w.w);
+    }
+}
+
+// One chain step: 24 MMAs into D of chain C; the whole issue warp calls it
+// (the asm blocks elect one lane) so descriptors and TMEM addresses stay on
+// the uniform datapath — the issue rate bounds the kernel.
+template <uint32_t C>
+__device__ __forceinline__ void k3h_issue(uint32_t tbase, uint32_t s0, uint64_t* mma_bar) {
+    const uint64_t y0 = smem_desc(s0 + C * kChainSmem, 16384, 1024, 2);
+    constexpr uint32_t D = C * 256u, X0 = D + 128u, X1 = D + 192u;
+    constexpr uint32_t Y1 = kPlane >> 4;
+    mma_f16_ts_x8<D, X1, 0, kBStep, true>(tbase, y0, kIdesc);  // x1*y0 (first: D =)
+    mma_f16_ts_x8<D, X0, Y1, kBStep>(tbase, y0, kIdesc);                // x0*y1
+    mma_f16_ts_x8<D, X0, 0, kBStep>(tbase, y0, kIdesc);                 // x0*y0
+    mma_commit_warp(mma_bar + C);
+}
+
+}  // namespace
+
+size_t k3h_smem_bytes() { return kSmem; }
+
+// Matrices of CTA b are b, b + G, b + 2G, ... (G = gridDim.x); chain c takes
+// every other one starting at b + cG.  Three roles run the same deterministic
+// (chain, matrix, step) state machine, so they agree on every hand-off
+// without exchanging state:
+//   warps 0-15  epilogue: drain D, rescale, split, write the next operands;
+//   warp 16     MMA issue (one elected lane);
+//   warp 17     IO: TMA stores of finished results and TMA loads of the next
+//               inputs (n == 128), L2 prefetch one matrix ahead.
+// A chain's matrix boundary takes two of its slots: OUT (drain the last
+// product into the warp tiles, hand them to the IO warp) and, one slot later,
+// IN (convert the freshly loaded input into operands, publish step 0).  In
+// between the epilogue warps serve the other chain, so the HBM round trip
+// overlaps that chain's MMAs.
+__global__ void __launch_bounds__(kThreads, 1)
+    k3h_batched_power(const __grid_constant__ CUtensorMap in_map,
+                      const __grid_constant__ CUtensorMap out_map, const float* __restrict__ in,
+                      float* __restrict__ out, int n, long long batch, PlanBits plan, int vec) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
+    uint64_t* mma_bar = bars;        // [2] a chain's step MMAs completed
+    uint64_t* out_ready = bars + 2;  // [2] a chain's result is in its warp tiles (16 arrivals)
+    uint64_t* in_ready = bars + 4;   // [2] a chain's next input landed in its warp tiles (TMA)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    if (tid == 0) {
+        mbar_init(mma_bar, 1);
+        mbar_init(mma_bar + 1, 1);
+        mbar_init(out_ready, kWorkers);
+        mbar_init(out_ready + 1, kWorkers);
+        mbar_init(in_ready, 1);
+        mbar_init(in_ready + 1, 1);
+        fence_mbar_init();
+    }
+    if (warp == kIssueWarp) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t s0 = smem_u32(smem);
+    const long long G = gridDim.x;
+    const size_t n2 = static_cast<size_t>(n) * n;
+    const int last = plan.len - 1;
+    constexpr int kIn = -2;  // s value: the next input is being loaded / converted
+
+    // state of the current chain (c) and of the other one, swapped every slot
+    // (runtime-indexed arrays would live in local memory)
+    long long m_c = blockIdx.x, m_o = static_cast<long long>(blockIdx.x) + G;
+    int s_c = kIn, s_o = kIn;
+    bool act_c = m_c < batch, act_o = m_o < batch;
+    // Start-phase skew: chain c of CTA b sits out its first dly slots, so the
+    // chains' matrix boundaries are spread over the plan instead of hitting
+    // HBM from all 296 chains at once.
+    int dly_c = 0, dly_o = 0;
+    if (batch >= 4 * G && plan.len > 1) {
+        dly_c = (2 * static_cast<int>(blockIdx.x)) % plan.len;
+        dly_o = (2 * static_cast<int>(blockIdx.x) + 1) % plan.len;
+    }
+    uint32_t c = 0;
+    uint32_t ph_c = 0, ph_o = 0;  // per-chain mbarrier parities of this role
+    auto swap_chains = [&]() {
+        const long long tm = m_c;
+        m_c = m_o;
+        m_o = tm;
+        const int ts = s_c;
+        s_c = s_o;
+        s_o = ts;
+        const bool ta = act_c;
+        act_c = act_o;
+        act_o = ta;
+        const int td = dly_c;
+        dly_c = dly_o;
+        dly_o = td;
+        const uint32_t tp = ph_c;
+        ph_c = ph_o;
+        ph_o = tp;
+        c ^= 1u;
+    };
+    // the 16 warp tiles of chain cc <-> matrix mm (TMA boxes of 32 x 32)
+    auto tiles_load = [&](uint32_t cc, long long mm) {
+        mbar_expect_tx(in_ready + cc, 16 * 4096);
+        for (uint32_t w = 0; w < kWorkers; ++w)
+            tma_load_2d_s(s0 + cc * kChainSmem + w * 4096u, &in_map, in_ready + cc,
+                          static_cast<int32_t>((w >> 2) * 32),
+                          static_cast<int32_t>(mm * 128 + (w & 3) * 32));
+        if (mm + 2 * G < batch)
+            prefetch_l2(in + static_cast<size_t>(mm + 2 * G) * n2, static_cast<uint32_t>(n2 * 4));
+    };
+
+    if (warp == kIssueWarp) {
+        // ------------------------------------------------------------ MMA issue
+        while (act_c || act_o) {
+            if (act_c && dly_c > 0) {
+                --dly_c;
+            } else if (act_c) {
+                if (s_c == last) {  // OUT slot: nothing to issue
+                    m_c += 2 * G;
+                    act_c = m_c < batch;
+                    s_c = kIn;
+                } else {
+                    s_c = (s_c == kIn) ? 0 : s_c + 1;
+                    named_bar_sync(1 + c, kWorkers * 32 + 32);
+                    tc_fence_after();
+                    if (c == 0) k3h_issue<0>(tmem, s0, mma_bar);
+                    else k3h_issue<1>(tmem, s0, mma_bar);
+                    __syncwarp();
+                }
+            }
+            swap_chains();
+        }
+    } else if (warp == kIOWarp) {
+        // ------------------------------------------------------------ IO (TMA)
+        if (vec && lane == 0) {
+            if (act_c) tiles_load(0, m_c);
+            if (act_o) tiles_load(1, m_o);
+        }
+        while (act_c || act_o) {
+            if (act_c && dly_c > 0) {
+                --dly_c;
+            } else if (act_c) {
+                if (s_c == last) {
+                    const long long m_prev = m_c;
+                    m_c += 2 * G;
+                    act_c = m_c < batch;
+                    s_c = kIn;
+                    if (vec) {
+                        mbar_wait_sleep(out_ready + c, ph_c);
+                        ph_c ^= 1;
+                        if (lane == 0) {
+                            for (uint32_t w = 0; w < kWorkers; ++w)
+                                tma_store_2d_s(&out_map, s0 + c * kChainSmem + w * 4096u,
+                                               static_cast<int32_t>((w >> 2) * 32),
+                                               static_cast<int32_t>(m_prev * 128 + (w & 3) * 32));
+                            bulk_commit_group();
+                            bulk_wait_group_read0();  // tiles read: reuse them for the input
+                            if (act_c) tiles_load(c, m_c);
+                        }
+                        __syncwarp();
+                    }
+                } else {
+                    s_c = (s_c == kIn) ? 0 : s_c + 1;
+                }
+            }
+            swap_chains();
+        }
+        if (vec && lane == 0) bulk_wait_group0();  // results written before exit
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const uint32_t q = warp & 3, g = warp >> 2;
+        const uint32_t row = q * 32 + lane;
+        const uint32_t col0 = g * 32;
+        const uint32_t lane_base = tmem + ((q * 32) << 16);
+        const uint32_t tile_off = warp * 4096u;  // the warp's tile inside a chain's plane region
+        uint32_t inph_c = 0, inph_o = 0;         // in_ready parities (swapped with the chains)
+        int e_c = 0, e_o = 0;                    // P = 2^e * P' (the planes hold P')
+        int eb_c = 0, eb_o = 0;                  // base = 2^eb * base'
+
+        // max |x| over the chain's whole 128 x 128 block: per-warp maxima in
+        // SMEM slot [cc][warp], one barrier among the 16 epilogue warps (it
+        // also orders every warp's tile reads before the plane writes).
+        auto block_max = [&](uint32_t cc, const float* x) -> uint32_t {
+            const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, absmax_bits(x));
+            const uint32_t slots = s0 + kMaxOff + cc * 64u;
+            if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots + warp * 4u), "r"(m) : "memory");
+            named_bar_sync(3, kWorkers * 32);
+            uint32_t r = 0;
+#pragma unroll
+            for (uint32_t i = 0; i < 4; ++i) {
+                const uint4 w4 = lds128(slots + 16u * i);
+                r = max(r, max(max(w4.x, w4.y), max(w4.z, w4.w)));
+            }
+            return r;
+        };
+        // 32 scaled values -> planes y0/y1 of chain cc (right operand) and, if
+        // `left`, x0/x1 in TMEM; !right: only x0/x1 (the base of a MULTIPLY_BASE step)
+        auto emit = [&](uint32_t cc, const float* x, float sc, bool right, bool left) {
+            // opaque copies: recompute the swizzled addresses here instead of
+            // letting the compiler hoist them all out of the loop (and spill)
+            uint32_t r_ = row, b_ = s0, lb_ = lane_base;
+            asm volatile("" : "+r"(r_), "+r"(b_), "+r"(lb_));
+#pragma unroll
+            for (uint32_t h = 0; h < 2; ++h) {
+                uint32_t p0[8], p1[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    split2(__fmul_rn(x[16 * h + 2 * j], sc), __fmul_rn(x[16 * h + 2 * j + 1], sc), p0[j],
+                           p1[j]);
+                if (right) {
+                    const uint32_t pb = b_ + cc * kChainSmem;
+                    put_half(pb, r_, g, h, p0);
+                    put_half(pb + kPlane, r_, g, h, p1);
+                }
+                if (left) {
+                    const uint32_t tl = lb_ + cc * 256u + 128u + g * 16u + h * 8u;
+                    tmem_st8(tl, p0);
+                    tmem_st8(tl + 64u, p1);
+                }
+            }
+        };
+
+        while (act_c || act_o) {
+            if (act_c && dly_c > 0) {
+                --dly_c;
+            } else if (act_c) {
+                bool publish = true;
+                if (s_c == kIn) {
+                    // ---- IN: the new matrix -> scale, operands of step 0
+                    float x[32];
+                    if (vec) {
+                        mbar_wait_sleep(in_ready + c, inph_c);
+                        inph_c ^= 1;
+                        tile_get_rows(s0 + c * kChainSmem + tile_off, lane, x);
+                    } else {
+                        load_row(in + static_cast<size_t>(m_c) * n2, n, row, col0, x);
+                    }
+                    const int t = scale_exp(block_max(c, x));
+                    e_c = -t;
+                    eb_c = -t;
+                    emit(c, x, exp2i(t), true, true);
+                    s_c = 0;
+                } else {
+                    mbar_wait_sleep(mma_bar + c, ph_c);
+                    ph_c ^= 1;
+                    tc_fence_after();
+                    float v[32];
+                    tmem_ld32(lane_base + c * 256u + col0, reinterpret_cast<uint32_t(&)[32]>(v));
+                    // exponent of this step's product: 2^(ex + ey) * D
+                    const int pe = (plan_is_mult(plan, s_c) ? eb_c : e_c) + e_c;
+                    if (s_c == last) {
+                        // ---- OUT: 2^pe * D -> the warp tile (the IO warp stores it)
+                        const float f1 = exp2i(pe / 2), f2 = exp2i(pe - pe / 2);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], f1), f2);
+                        if (vec) {
+                            tile_put_rows(s0 + c * kChainSmem + tile_off, lane, v);
+                            fence_proxy_async_smem();
+                            tc_fence_before();  // D reads done before the next MMAs into D
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(out_ready + c);
+                        } else {
+                            store_row(out + static_cast<size_t>(m_c) * n2, n, row, col0, v);
+                            tc_fence_before();
+                        }
+                        m_c += 2 * G;
+                        act_c = m_c < batch;
+                        s_c = kIn;
+                        publish = false;
+                    } else {
+                        s_c += 1;
+                        const bool mult = plan_is_mult(plan, s_c);
+                        const int t = scale_exp(block_max(c, v));
+                        e_c = pe - t;
+                        emit(c, v, exp2i(t), true, !mult);
+                        if (mult) {  // left operand = the base, rescaled by its input exponent
+                            float x[32];
+                            load_row(in + static_cast<size_t>(m_c) * n2, n, row, col0, x);
+                            emit(c, x, exp2i(-eb_c), false, true);
+                        }
+                    }
+                }
+                if (publish) {
+                    // workers arrive; the issue warp waits for all of them (the
+                    // hardware barrier also drains pending st.shared) and issues
+                    tmem_st_wait();
+                    fence_proxy_async_smem();
+                    tc_fence_before();
+                    named_bar_arrive(1 + c, kWorkers * 32 + 32);
+                }
+            }
+            swap_chains();
+            uint32_t tp = inph_c;
+            inph_c = inph_o;
+            inph_o = tp;
+            int te = e_c;
+            e_c = e_o;
+            e_o = te;
+            te = eb_c;
+            eb_c = eb_o;
+            eb_o = te;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kIssueWarp) tmem_dealloc<512>(tmem);
+}
+
+cudaError_t prepare_k3h_kernel() {
+    return cudaFuncSetAttribute(k3h_batched_power, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kSmem));
+}
+
+cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch,
+                               const PlanBits& plan, int grid, cudaStream_t s) {
+    if (plan.len < 1 || n < 1 || n > kSmallMax) return cudaErrorInvalidValue;
+    if (grid > batch) grid = static_cast<int>(batch);
+    CUtensorMap in_map, out_map;
+    std::memset(&in_map, 0, sizeof in_map);
+    std::memset(&out_map, 0, sizeof out_map);
+    int vec = (n == 128 && batch * 128 < (int64_t(1) << 31) &&
+               (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+               (reinterpret_cast<uintptr_t>(out) & 15) == 0)
+                  ? 1
+                  : 0;
+    if (vec && !(encode_tile_map(&in_map, in, batch * 128) && encode_tile_map(&out_map, out, batch * 128)))
+        vec = 0;
+    k3h_batched_power<<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec);
+    return cudaGetLastError();
+}
+
+}  // namespace mxp

@@ -356,17 +356,23 @@ __global__ void __launch_bounds__(kK3AllThreads, 1)
 long long* g_k3_prof = nullptr;
 void k3_set_profile(long long* dev_buf) { g_k3_prof = dev_buf; }
 
-static bool k3_use_tf32() {
-    static const bool v = [] {
+// MXP_K3 selects the small-n kernel for A/B measurements: "tf32" (this
+// single-chain 3xTF32 kernel), "bf16x3" (K3B); default: K3H (scaled fp16x2).
+static int k3_variant() {
+    static const int v = [] {
         const char* e = std::getenv("MXP_K3");
-        return e != nullptr && std::strcmp(e, "tf32") == 0;
+        if (e != nullptr && std::strcmp(e, "tf32") == 0) return 1;
+        if (e != nullptr && std::strcmp(e, "bf16x3") == 0) return 2;
+        return 0;
     }();
     return v;
 }
 
 cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
                               const PlanBits& plan, int grid, cudaStream_t s) {
-    if (!k3_use_tf32()) return launch_k3b_batched(in, out, n, batch, plan, grid, s);
+    const int variant = k3_variant();
+    if (variant == 0) return launch_k3h_batched(in, out, n, batch, plan, grid, s);
+    if (variant == 2) return launch_k3b_batched(in, out, n, batch, plan, grid, s);
     if (grid > batch) grid = static_cast<int>(batch);
     CUtensorMap map;
     std::memset(&map, 0, sizeof map);

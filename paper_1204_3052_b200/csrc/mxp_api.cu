@@ -25,6 +25,7 @@ cudaError_t prepare_kernels() {
     cudaError_t e = prepare_tf32_kernels();
     if (e == cudaSuccess) e = prepare_f64_kernels();
     if (e == cudaSuccess) e = prepare_k3b_kernel();
+    if (e == cudaSuccess) e = prepare_k3h_kernel();
     return e;
 }
 

@@ -40,6 +40,11 @@ size_t k3b_smem_bytes();
 cudaError_t prepare_k3b_kernel();
 cudaError_t launch_k3b_batched(const float* in, float* out, int n, int64_t batch,
                                const PlanBits& plan, int grid, cudaStream_t s);
+// K3H (kernels_k3h.cu): the same contract, two chains per SM, scaled fp16x2 split.
+size_t k3h_smem_bytes();
+cudaError_t prepare_k3h_kernel();
+cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch,
+                               const PlanBits& plan, int grid, cudaStream_t s);
 
 // fp32 (n x n, leading dim ld) -> tf32 hi/lo planes (n_pad x n_pad, zero pad).
 cudaError_t launch_split(const float* in, int n, int ld, uint32_t* hi, uint32_t* lo, int n_pad,

@@ -211,19 +211,20 @@ __device__ __forceinline__ void mma_f16_ss_off(uint32_t tbase, uint64_t adesc, u
 // Eight K=16 steps of one term in ONE asm block (one elect/waterfall wrapper
 // for all eight MMAs instead of one per MMA): A from TMEM columns
 // tbase + kA + 8j, B descriptor bdesc + kB + j * kBStep, all accumulating.
-template <uint32_t kD, uint32_t kA, uint32_t kB, uint32_t kBStep>
+template <uint32_t kD, uint32_t kA, uint32_t kB, uint32_t kBStep, bool kFirst = false>
 __device__ __forceinline__ void mma_f16_ts_x8(uint32_t tbase, uint64_t bdesc, uint32_t idesc) {
     asm volatile(
-        "{\n\t.reg .pred p, e;\n\t.reg .b32 dt, a0, a1, a2, a3, a4, a5, a6, a7;\n\t"
+        "{\n\t.reg .pred p, p0, e;\n\t.reg .b32 dt, a0, a1, a2, a3, a4, a5, a6, a7;\n\t"
         ".reg .b64 b0, b1, b2, b3, b4, b5, b6, b7;\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
         "setp.eq.u32 p, 1, 1;\n\t"
+        "setp.eq.u32 p0, %7, 0;\n\t"
         "add.u32 dt, %0, %3;\n\t"
         "add.u32 a0, %0, %4;\n\tadd.u32 a1, a0, 8;\n\tadd.u32 a2, a0, 16;\n\tadd.u32 a3, a0, 24;\n\t"
         "add.u32 a4, a0, 32;\n\tadd.u32 a5, a0, 40;\n\tadd.u32 a6, a0, 48;\n\tadd.u32 a7, a0, 56;\n\t"
         "add.s64 b0, %1, %5;\n\tadd.s64 b1, b0, %6;\n\tadd.s64 b2, b1, %6;\n\tadd.s64 b3, b2, %6;\n\t"
         "add.s64 b4, b3, %6;\n\tadd.s64 b5, b4, %6;\n\tadd.s64 b6, b5, %6;\n\tadd.s64 b7, b6, %6;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a0], b0, %2, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a0], b0, %2, p0;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a1], b1, %2, p;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a2], b2, %2, p;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a3], b3, %2, p;\n\t"
@@ -231,7 +232,7 @@ __device__ __forceinline__ void mma_f16_ts_x8(uint32_t tbase, uint64_t bdesc, ui
         "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a5], b5, %2, p;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a6], b6, %2, p;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::f16 [dt], [a7], b7, %2, p;\n}" ::"r"(tbase),
-        "l"(bdesc), "r"(idesc), "n"(kD), "n"(kA), "n"(kB), "n"(kBStep)
+        "l"(bdesc), "r"(idesc), "n"(kD), "n"(kA), "n"(kB), "n"(kBStep), "n"(kFirst ? 1 : 0)
         : "memory");
 }
 // SS: A descriptor adesc + (j/4) * kAChunk + (j%4) * 2 (K-major SW128, 32 B per
