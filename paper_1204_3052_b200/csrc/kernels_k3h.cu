@@ -35,6 +35,7 @@
 // a power of the base.  Parity with the reference chain (linalg.py:151-164,
 // expo.py:121-139) is by the relative-Frobenius tolerance of SURVEY §8(d).
 #include <cstring>
+#include <type_traits>
 
 #include "mxp_internal.h"
 #include "ptx.cuh"
@@ -71,12 +72,28 @@ __device__ __forceinline__ void unpack_f16x2(uint32_t p, float& lo, float& hi) {
         : "=f"(lo), "=f"(hi)
         : "r"(p));
 }
-// (a, b) = columns 2j, 2j+1, already scaled: two packed fp16x2 words, h0 and h1
-__device__ __forceinline__ void split2(float a, float b, uint32_t& p0, uint32_t& p1) {
-    p0 = pack_f16x2(a, b);
-    float a0, b0;
-    unpack_f16x2(p0, a0, b0);
-    p1 = pack_f16x2(__fsub_rn(a, a0), __fsub_rn(b, b0));
+// (a, b) = columns 2j, 2j+1 (unscaled), sc2 = the scale in both halves:
+// two packed fp16x2 words h0 = rn(a', b'), h1 = rn((a', b') - h0).  The
+// scale and the residual use packed fp32x2 arithmetic (FMUL2 / FADD2).
+__device__ __forceinline__ void split2(float a, float b, uint64_t sc2, uint32_t& p0, uint32_t& p1) {
+    uint64_t ab, s2, h2, r2;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ab) : "f"(a), "f"(b));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(s2) : "l"(ab), "l"(sc2));
+    float sa, sb;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(sa), "=f"(sb) : "l"(s2));
+    p0 = pack_f16x2(sa, sb);
+    float ha, hb;
+    unpack_f16x2(p0, ha, hb);
+    asm("mov.b64 %0, {%1, %2};" : "=l"(h2) : "f"(ha), "f"(hb));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r2) : "l"(s2), "l"(h2));
+    float ra, rb;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(ra), "=f"(rb) : "l"(r2));
+    p1 = pack_f16x2(ra, rb);
+}
+__device__ __forceinline__ uint64_t splat2(float x) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
+    return r;
 }
 // 2^t as a float, t clamped to the normal range
 __device__ __forceinline__ float exp2i(int t) {
@@ -91,11 +108,13 @@ __device__ __forceinline__ int scale_exp(uint32_t mbits) {
                                        : -127 + (31 - __clz(static_cast<int>(mbits))) - 22;
     return kTarget - k;
 }
+// max |x_i| as float bits (3-input FMNMX with |.| operands; a NaN is skipped,
+// which is harmless: it propagates through the products anyway)
 __device__ __forceinline__ uint32_t absmax_bits(const float* x) {
-    uint32_t m = 0;
+    float m = 0.f;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) m = max(m, __float_as_uint(x[i]) & 0x7FFFFFFFu);
-    return m;
+    for (int i = 0; i < 32; i += 2) m = fmaxf(fmaxf(m, fabsf(x[i])), fabsf(x[i + 1]));
+    return __float_as_uint(m);
 }
 
 // Row `row`, columns [32g + 16h, +16) of a plane: two 16-byte units, unit
@@ -177,6 +196,45 @@ __device__ __forceinline__ void k3h_issue(uint32_t tbase, uint32_t s0, uint64_t*
 
 size_t k3h_smem_bytes() { return kSmem; }
 
+#ifdef K3H_TRACE  // tools/k3h_trace.cu: per-phase cycle totals of CTA 0 (lane 0 of warps 0, issue, IO)
+__device__ long long* g_k3h_trace;
+__shared__ long long k3h_acc[16];
+#define K3H_MARK(k)                                                                      \
+    do {                                                                                 \
+        if (blockIdx.x == 0 && (warp == 0 || warp == kIssueWarp || warp == kIOWarp) &&   \
+            lane == 0) {                                                                 \
+            const long long t_ = clock64();                                              \
+            k3h_acc[k] += t_ - k3h_tprev;                                                \
+            k3h_tprev = t_;                                                              \
+        }                                                                                \
+    } while (0)
+#define K3H_COUNT(k)                                                                     \
+    do {                                                                                 \
+        if (blockIdx.x == 0 && warp == 0 && lane == 0) k3h_acc[k] += 1;                  \
+    } while (0)
+#else
+#define K3H_MARK(k) \
+    do {            \
+    } while (0)
+#define K3H_COUNT(k) \
+    do {             \
+    } while (0)
+#endif
+
+// Per-chain state of one role.  Two named instances, and the slot code is
+// instantiated per chain (template parameter), so nothing is swapped or
+// indexed at run time.
+struct Chain {
+    long long m;    // current matrix
+    int s;          // step whose MMAs are in flight, or kIn
+    int dly;        // start-phase skew slots still to sit out
+    uint32_t ph;    // mbarrier parity (mma_bar for the epilogue, out_ready for IO)
+    uint32_t inph;  // in_ready parity (epilogue)
+    int e, eb;      // P = 2^e P', base = 2^eb base' (epilogue)
+    bool act;
+};
+constexpr int kIn = -2;  // Chain::s: the next input is being loaded / converted
+
 // Matrices of CTA b are b, b + G, b + 2G, ... (G = gridDim.x); chain c takes
 // every other one starting at b + cG.  Three roles run the same deterministic
 // (chain, matrix, step) state machine, so they agree on every hand-off
@@ -223,41 +281,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     const long long G = gridDim.x;
     const size_t n2 = static_cast<size_t>(n) * n;
     const int last = plan.len - 1;
-    constexpr int kIn = -2;  // s value: the next input is being loaded / converted
 
-    // state of the current chain (c) and of the other one, swapped every slot
-    // (runtime-indexed arrays would live in local memory)
-    long long m_c = blockIdx.x, m_o = static_cast<long long>(blockIdx.x) + G;
-    int s_c = kIn, s_o = kIn;
-    bool act_c = m_c < batch, act_o = m_o < batch;
+    Chain ch0{}, ch1{};
+    ch0.m = blockIdx.x;
+    ch1.m = static_cast<long long>(blockIdx.x) + G;
+    ch0.s = ch1.s = kIn;
+    ch0.act = ch0.m < batch;
+    ch1.act = ch1.m < batch;
     // Start-phase skew: chain c of CTA b sits out its first dly slots, so the
     // chains' matrix boundaries are spread over the plan instead of hitting
     // HBM from all 296 chains at once.
-    int dly_c = 0, dly_o = 0;
     if (batch >= 4 * G && plan.len > 1) {
-        dly_c = (2 * static_cast<int>(blockIdx.x)) % plan.len;
-        dly_o = (2 * static_cast<int>(blockIdx.x) + 1) % plan.len;
+        ch0.dly = (2 * static_cast<int>(blockIdx.x)) % plan.len;
+        ch1.dly = (2 * static_cast<int>(blockIdx.x) + 1) % plan.len;
     }
-    uint32_t c = 0;
-    uint32_t ph_c = 0, ph_o = 0;  // per-chain mbarrier parities of this role
-    auto swap_chains = [&]() {
-        const long long tm = m_c;
-        m_c = m_o;
-        m_o = tm;
-        const int ts = s_c;
-        s_c = s_o;
-        s_o = ts;
-        const bool ta = act_c;
-        act_c = act_o;
-        act_o = ta;
-        const int td = dly_c;
-        dly_c = dly_o;
-        dly_o = td;
-        const uint32_t tp = ph_c;
-        ph_c = ph_o;
-        ph_o = tp;
-        c ^= 1u;
-    };
+#ifdef K3H_TRACE
+    if (tid < 16) k3h_acc[tid] = 0;
+    __syncthreads();
+    long long k3h_tprev = clock64();
+#endif
     // the 16 warp tiles of chain cc <-> matrix mm (TMA boxes of 32 x 32)
     auto tiles_load = [&](uint32_t cc, long long mm) {
         mbar_expect_tx(in_ready + cc, 16 * 4096);
@@ -271,59 +313,70 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == kIssueWarp) {
         // ------------------------------------------------------------ MMA issue
-        while (act_c || act_o) {
-            if (act_c && dly_c > 0) {
-                --dly_c;
-            } else if (act_c) {
-                if (s_c == last) {  // OUT slot: nothing to issue
-                    m_c += 2 * G;
-                    act_c = m_c < batch;
-                    s_c = kIn;
-                } else {
-                    s_c = (s_c == kIn) ? 0 : s_c + 1;
-                    named_bar_sync(1 + c, kWorkers * 32 + 32);
-                    tc_fence_after();
-                    if (c == 0) k3h_issue<0>(tmem, s0, mma_bar);
-                    else k3h_issue<1>(tmem, s0, mma_bar);
-                    __syncwarp();
-                }
+        auto slot = [&](Chain& st, auto cc) {
+            constexpr uint32_t C = decltype(cc)::value;
+            if (!st.act) return;
+            if (st.dly > 0) {
+                --st.dly;
+                return;
             }
-            swap_chains();
+            if (st.s == last) {  // OUT slot: nothing to issue
+                st.m += 2 * G;
+                st.act = st.m < batch;
+                st.s = kIn;
+                return;
+            }
+            st.s = (st.s == kIn) ? 0 : st.s + 1;
+            K3H_MARK(10);
+            named_bar_sync(1 + C, kWorkers * 32 + 32);
+            K3H_MARK(8);
+            tc_fence_after();
+            k3h_issue<C>(tmem, s0, mma_bar);
+            __syncwarp();
+            K3H_MARK(9);
+        };
+        while (ch0.act || ch1.act) {
+            slot(ch0, std::integral_constant<uint32_t, 0>{});
+            slot(ch1, std::integral_constant<uint32_t, 1>{});
         }
     } else if (warp == kIOWarp) {
         // ------------------------------------------------------------ IO (TMA)
         if (vec && lane == 0) {
-            if (act_c) tiles_load(0, m_c);
-            if (act_o) tiles_load(1, m_o);
+            if (ch0.act) tiles_load(0, ch0.m);
+            if (ch1.act) tiles_load(1, ch1.m);
         }
-        while (act_c || act_o) {
-            if (act_c && dly_c > 0) {
-                --dly_c;
-            } else if (act_c) {
-                if (s_c == last) {
-                    const long long m_prev = m_c;
-                    m_c += 2 * G;
-                    act_c = m_c < batch;
-                    s_c = kIn;
-                    if (vec) {
-                        mbar_wait_sleep(out_ready + c, ph_c);
-                        ph_c ^= 1;
-                        if (lane == 0) {
-                            for (uint32_t w = 0; w < kWorkers; ++w)
-                                tma_store_2d_s(&out_map, s0 + c * kChainSmem + w * 4096u,
-                                               static_cast<int32_t>((w >> 2) * 32),
-                                               static_cast<int32_t>(m_prev * 128 + (w & 3) * 32));
-                            bulk_commit_group();
-                            bulk_wait_group_read0();  // tiles read: reuse them for the input
-                            if (act_c) tiles_load(c, m_c);
-                        }
-                        __syncwarp();
-                    }
-                } else {
-                    s_c = (s_c == kIn) ? 0 : s_c + 1;
-                }
+        auto slot = [&](Chain& st, auto cc) {
+            constexpr uint32_t C = decltype(cc)::value;
+            if (!st.act) return;
+            if (st.dly > 0) {
+                --st.dly;
+                return;
             }
-            swap_chains();
+            if (st.s != last) {
+                st.s = (st.s == kIn) ? 0 : st.s + 1;
+                return;
+            }
+            const long long m_prev = st.m;
+            st.m += 2 * G;
+            st.act = st.m < batch;
+            st.s = kIn;
+            if (!vec) return;
+            mbar_wait_sleep(out_ready + C, st.ph);
+            st.ph ^= 1;
+            if (lane == 0) {
+                for (uint32_t w = 0; w < kWorkers; ++w)
+                    tma_store_2d_s(&out_map, s0 + C * kChainSmem + w * 4096u,
+                                   static_cast<int32_t>((w >> 2) * 32),
+                                   static_cast<int32_t>(m_prev * 128 + (w & 3) * 32));
+                bulk_commit_group();
+                bulk_wait_group_read0();  // tiles read: reuse them for the input
+                if (st.act) tiles_load(C, st.m);
+            }
+            __syncwarp();
+        };
+        while (ch0.act || ch1.act) {
+            slot(ch0, std::integral_constant<uint32_t, 0>{});
+            slot(ch1, std::integral_constant<uint32_t, 1>{});
         }
         if (vec && lane == 0) bulk_wait_group0();  // results written before exit
     } else {
@@ -333,9 +386,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t col0 = g * 32;
         const uint32_t lane_base = tmem + ((q * 32) << 16);
         const uint32_t tile_off = warp * 4096u;  // the warp's tile inside a chain's plane region
-        uint32_t inph_c = 0, inph_o = 0;         // in_ready parities (swapped with the chains)
-        int e_c = 0, e_o = 0;                    // P = 2^e * P' (the planes hold P')
-        int eb_c = 0, eb_o = 0;                  // base = 2^eb * base'
 
         // max |x| over the chain's whole 128 x 128 block: per-warp maxima in
         // SMEM slot [cc][warp], one barrier among the 16 epilogue warps (it
@@ -353,20 +403,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             return r;
         };
-        // 32 scaled values -> planes y0/y1 of chain cc (right operand) and, if
-        // `left`, x0/x1 in TMEM; !right: only x0/x1 (the base of a MULTIPLY_BASE step)
+        // 32 values (scaled by sc here) -> planes y0/y1 of chain cc (right
+        // operand) and, if `left`, x0/x1 in TMEM; !right: only x0/x1 (the
+        // base of a MULTIPLY_BASE step)
         auto emit = [&](uint32_t cc, const float* x, float sc, bool right, bool left) {
             // opaque copies: recompute the swizzled addresses here instead of
             // letting the compiler hoist them all out of the loop (and spill)
             uint32_t r_ = row, b_ = s0, lb_ = lane_base;
             asm volatile("" : "+r"(r_), "+r"(b_), "+r"(lb_));
+            const uint64_t sc2 = splat2(sc);
 #pragma unroll
             for (uint32_t h = 0; h < 2; ++h) {
                 uint32_t p0[8], p1[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    split2(__fmul_rn(x[16 * h + 2 * j], sc), __fmul_rn(x[16 * h + 2 * j + 1], sc), p0[j],
-                           p1[j]);
+                for (int j = 0; j < 8; ++j) split2(x[16 * h + 2 * j], x[16 * h + 2 * j + 1], sc2, p0[j], p1[j]);
                 if (right) {
                     const uint32_t pb = b_ + cc * kChainSmem;
                     put_half(pb, r_, g, h, p0);
@@ -380,89 +430,96 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         };
 
-        while (act_c || act_o) {
-            if (act_c && dly_c > 0) {
-                --dly_c;
-            } else if (act_c) {
-                bool publish = true;
-                if (s_c == kIn) {
-                    // ---- IN: the new matrix -> scale, operands of step 0
-                    float x[32];
-                    if (vec) {
-                        mbar_wait_sleep(in_ready + c, inph_c);
-                        inph_c ^= 1;
-                        tile_get_rows(s0 + c * kChainSmem + tile_off, lane, x);
-                    } else {
-                        load_row(in + static_cast<size_t>(m_c) * n2, n, row, col0, x);
-                    }
-                    const int t = scale_exp(block_max(c, x));
-                    e_c = -t;
-                    eb_c = -t;
-                    emit(c, x, exp2i(t), true, true);
-                    s_c = 0;
+        auto slot = [&](Chain& st, auto cc) {
+            constexpr uint32_t C = decltype(cc)::value;
+            if (!st.act) return;
+            if (st.dly > 0) {
+                --st.dly;
+                return;
+            }
+            if (st.s == kIn) {
+                // ---- IN: the new matrix -> scale, operands of step 0
+                float x[32];
+                K3H_MARK(7);
+                if (vec) {
+                    mbar_wait_sleep(in_ready + C, st.inph);
+                    st.inph ^= 1;
+                    K3H_MARK(3);
+                    tile_get_rows(s0 + C * kChainSmem + tile_off, lane, x);
                 } else {
-                    mbar_wait_sleep(mma_bar + c, ph_c);
-                    ph_c ^= 1;
-                    tc_fence_after();
-                    float v[32];
-                    tmem_ld32(lane_base + c * 256u + col0, reinterpret_cast<uint32_t(&)[32]>(v));
-                    // exponent of this step's product: 2^(ex + ey) * D
-                    const int pe = (plan_is_mult(plan, s_c) ? eb_c : e_c) + e_c;
-                    if (s_c == last) {
-                        // ---- OUT: 2^pe * D -> the warp tile (the IO warp stores it)
-                        const float f1 = exp2i(pe / 2), f2 = exp2i(pe - pe / 2);
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], f1), f2);
-                        if (vec) {
-                            tile_put_rows(s0 + c * kChainSmem + tile_off, lane, v);
-                            fence_proxy_async_smem();
-                            tc_fence_before();  // D reads done before the next MMAs into D
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive(out_ready + c);
-                        } else {
-                            store_row(out + static_cast<size_t>(m_c) * n2, n, row, col0, v);
-                            tc_fence_before();
-                        }
-                        m_c += 2 * G;
-                        act_c = m_c < batch;
-                        s_c = kIn;
-                        publish = false;
-                    } else {
-                        s_c += 1;
-                        const bool mult = plan_is_mult(plan, s_c);
-                        const int t = scale_exp(block_max(c, v));
-                        e_c = pe - t;
-                        emit(c, v, exp2i(t), true, !mult);
-                        if (mult) {  // left operand = the base, rescaled by its input exponent
-                            float x[32];
-                            load_row(in + static_cast<size_t>(m_c) * n2, n, row, col0, x);
-                            emit(c, x, exp2i(-eb_c), false, true);
-                        }
-                    }
+                    load_row(in + static_cast<size_t>(st.m) * n2, n, row, col0, x);
                 }
-                if (publish) {
-                    // workers arrive; the issue warp waits for all of them (the
-                    // hardware barrier also drains pending st.shared) and issues
-                    tmem_st_wait();
-                    fence_proxy_async_smem();
-                    tc_fence_before();
-                    named_bar_arrive(1 + c, kWorkers * 32 + 32);
+                const int t = scale_exp(block_max(C, x));
+                K3H_MARK(4);
+                st.e = -t;
+                st.eb = -t;
+                emit(C, x, exp2i(t), true, true);
+                K3H_MARK(5);
+                K3H_COUNT(13);
+                st.s = 0;
+            } else {
+                K3H_MARK(7);
+                mbar_wait_sleep(mma_bar + C, st.ph);
+                K3H_MARK(0);
+                st.ph ^= 1;
+                tc_fence_after();
+                float v[32];
+                tmem_ld32(lane_base + C * 256u + col0, reinterpret_cast<uint32_t(&)[32]>(v));
+                K3H_MARK(1);
+                // exponent of this step's product: 2^(ex + ey) * D
+                const int pe = (plan_is_mult(plan, st.s) ? st.eb : st.e) + st.e;
+                if (st.s == last) {
+                    // ---- OUT: 2^pe * D -> the warp tile (the IO warp stores it)
+                    const float f1 = exp2i(pe / 2), f2 = exp2i(pe - pe / 2);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], f1), f2);
+                    if (vec) {
+                        tile_put_rows(s0 + C * kChainSmem + tile_off, lane, v);
+                        fence_proxy_async_smem();
+                        tc_fence_before();  // D reads done before the next MMAs into D
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(out_ready + C);
+                        K3H_MARK(2);
+                    } else {
+                        store_row(out + static_cast<size_t>(st.m) * n2, n, row, col0, v);
+                        tc_fence_before();
+                    }
+                    st.m += 2 * G;
+                    st.act = st.m < batch;
+                    st.s = kIn;
+                    return;  // no publish: IN follows one slot later
+                }
+                st.s += 1;
+                const bool mult = plan_is_mult(plan, st.s);
+                const int t = scale_exp(block_max(C, v));
+                K3H_MARK(11);
+                st.e = pe - t;
+                emit(C, v, exp2i(t), true, !mult);
+                K3H_MARK(6);
+                K3H_COUNT(14);
+                if (mult) {  // left operand = the base, rescaled by its input exponent
+                    float x[32];
+                    load_row(in + static_cast<size_t>(st.m) * n2, n, row, col0, x);
+                    emit(C, x, exp2i(-st.eb), false, true);
                 }
             }
-            swap_chains();
-            uint32_t tp = inph_c;
-            inph_c = inph_o;
-            inph_o = tp;
-            int te = e_c;
-            e_c = e_o;
-            e_o = te;
-            te = eb_c;
-            eb_c = eb_o;
-            eb_o = te;
+            // workers arrive; the issue warp waits for all of them (the hardware
+            // barrier also drains pending st.shared) and issues the step
+            tmem_st_wait();
+            fence_proxy_async_smem();
+            tc_fence_before();
+            named_bar_arrive(1 + C, kWorkers * 32 + 32);
+        };
+        while (ch0.act || ch1.act) {
+            slot(ch0, std::integral_constant<uint32_t, 0>{});
+            slot(ch1, std::integral_constant<uint32_t, 1>{});
         }
     }
     tc_fence_before();
     __syncthreads();
+#ifdef K3H_TRACE
+    if (blockIdx.x == 0 && tid < 16) g_k3h_trace[tid] = k3h_acc[tid];
+#endif
     if (warp == kIssueWarp) tmem_dealloc<512>(tmem);
 }
 
