@@ -5,6 +5,7 @@
 // replaces the reference's scalar ascending-k fp32 loop (linalg.py:151-164,
 // matmul_tiled.cl:91-94); parity is by the relative-Frobenius tolerance of
 // SURVEY §8(d), not bitwise (tensor-core summation order differs).
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
@@ -370,7 +371,20 @@ static int k3_variant() {
 
 cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
                               const PlanBits& plan, int grid, cudaStream_t s) {
-    const int variant = k3_variant();
+    int variant = k3_variant();
+    if (variant == 0) {
+        // Accuracy guard.  The tensor core truncates its fp32 accumulator on
+        // every MMA, a relative bias per multiply that a chain amplifies
+        // ~(k-1)-fold (tools/bias_check.py: K3H b(n) ~ 2.5e-8 + 1.05e-9 n,
+        // K3B ~ 3.4e-8 + 3.6e-10 n).  When K3H's predicted (k-1) b(n) would
+        // use more than 60% of the relative-Frobenius tolerance
+        // 16 m sqrt(n) 2^-24, run the bf16x3 kernel instead.
+        double k = 1.0;
+        for (int i = 0; i < plan.len; ++i) k = plan_is_mult(plan, i) ? k + 1.0 : 2.0 * k;
+        const double pred = (k - 1.0) * (2.5e-8 + 1.05e-9 * n);
+        const double tol = 16.0 * plan.len * std::sqrt(static_cast<double>(n)) * std::ldexp(1.0, -24);
+        if (pred > 0.6 * tol) variant = 2;
+    }
     if (variant == 0) return launch_k3h_batched(in, out, n, batch, plan, grid, s);
     if (variant == 2) return launch_k3b_batched(in, out, n, batch, plan, grid, s);
     if (grid > batch) grid = static_cast<int>(batch);
