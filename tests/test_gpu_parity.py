@@ -389,3 +389,58 @@ def test_device_repeated_oracle_and_cli(capsys):
     assert {(r.strategy.value, r.multiply_count) for r in recs} == {
         ("repeated", 15), ("squared", 4), ("repeated", 12), ("squared", 5)}
     assert all(r.max_rel_err is not None and r.max_rel_err < 1e-3 for r in recs)
+
+
+# ------------------------------------------------------------------ small-n kernel (K3H) edge cases
+# K3H keeps the running power as 2^e * P' with P' in fp16 pieces; these pin the
+# per-step power-of-two rescaling, the two-chain schedule and the TMA IO path.
+@pytest.mark.parametrize("mag", [1e-15, 1e-6, 1.0, 1e6, 1e15])
+def test_small_n_scaling_extreme_magnitudes(eng, mag):
+    """Results scale exactly with the input's magnitude (power-of-two scales
+    are exact), so huge and tiny inputs meet the same tolerance."""
+    n, k = 64, 2
+    a = (oracle.scaled_input(n, np.float64, 11) * mag).astype(np.float32)
+    got = eng.power(a, k)
+    ref = oracle.exponentiate(a, k)
+    assert np.isfinite(got).all()
+    assert fro(got, ref) <= mx.fro_tol(n, k, "f32"), (mag, fro(got, ref))
+
+
+@pytest.mark.parametrize("growth", [0.5, 2.0])
+def test_small_n_growing_and_shrinking_powers(eng, growth):
+    """A^64 with spectral radius ~0.5 (result ~1e-19) or ~2 (~1e19): every
+    step rescales, nothing under- or overflows in the fp16 planes."""
+    n, k = 128, 64
+    a = (oracle.scaled_input(n, np.float64, 12) * growth).astype(np.float32)
+    got = eng.power(a, k)
+    ref = oracle.exponentiate(a, k)
+    assert np.isfinite(ref).all() and np.isfinite(got).all()
+    assert fro(got, ref) <= mx.fro_tol(n, k, "f32"), fro(got, ref)
+
+
+def test_small_n_zero_and_nan(eng):
+    z = np.zeros((64, 64), dtype=np.float32)
+    assert not eng.power(z, 13).any()
+    a = oracle.scaled_input(32, np.float32, 13)
+    a[3, 5] = np.nan
+    got = eng.power(a, 4)
+    ref = oracle.exponentiate(a, 4)
+    assert np.array_equal(np.isnan(got), np.isnan(ref))
+
+
+def test_batched_mixed_magnitudes_and_schedule_edges():
+    """Per-matrix scales are independent; batch sizes around the CTA / chain
+    boundaries (1, 149, 297) and a skewed large batch with MULTIPLY_BASE steps."""
+    n = 128
+    for batch, k in ((1, 64), (149, 7), (297, 2), (1200, 13), (1200, 3)):
+        stack = mx.scaled_batch(n, batch, mx.DType.F32, 21).astype(np.float64)
+        e_max = max(1, 60 // k)  # |A_i^k| stays within 2^+-60 of the unscaled power
+        scale = 2.0 ** ((np.arange(batch) % (2 * e_max + 1)) - e_max)
+        stack = (stack * scale[:, None, None]).astype(np.float32)
+        out = mx.exponentiate_batched(stack, k)
+        for i in sorted({0, batch // 2, batch - 1, min(148, batch - 1)}):
+            ref = oracle.exponentiate(stack[i], k)
+            assert np.isfinite(out[i]).all()
+            assert fro(out[i], ref) <= mx.fro_tol(n, k, "f32"), (batch, k, i, fro(out[i], ref))
+        # deterministic: a second launch is bitwise identical
+        assert np.array_equal(mx.exponentiate_batched(stack, k), out)
