@@ -44,15 +44,16 @@ namespace mxp {
 namespace {
 
 constexpr int kWorkers = 16;                   // epilogue warps: 4 TMEM lane quarters x 4
-constexpr int kIssueWarp = kWorkers;           //   column groups, + one MMA-issue warp
-constexpr int kIOWarp = kWorkers + 1;          //   + one TMA IO warp
+constexpr int kIssueWarp = kWorkers + 1;       //   column groups, + one MMA-issue warp
+constexpr int kIOWarp = kWorkers;              //   + one TMA IO warp
 constexpr int kThreads = (kWorkers + 2) * 32;  // 576 (<= 96 registers per thread)
 constexpr uint32_t kPlane = 128u * 128u * 2u;  // one fp16 plane: 32 KB
 constexpr uint32_t kChainSmem = 2u * kPlane;   // y0, y1 of one chain
-constexpr uint32_t kMaxOff = 2u * kChainSmem;  // [2][16] per-warp max |D| slots
-constexpr uint32_t kBarOff = kMaxOff + 128;    // mbarriers + TMEM slot
+constexpr uint32_t kMaxOff = 2u * kChainSmem;  // [chain][buffer][16] per-warp max |D| slots
+constexpr uint32_t kBarOff = kMaxOff + 256;    // mbarriers + TMEM slot
 constexpr size_t kSmem = kBarOff + 128 + 1024; // + alignment slack
-constexpr int kTarget = 13;                    // scaled max |P'| in [2^13, 2^14)
+constexpr int kTarget = 13;                    // input: scaled max |A'| in [2^13, 2^14)
+constexpr int kCeil = 14;                      // products: scaled max |D'| < 2^14 guaranteed
 // kind::f16 with fp16 A/B (formats 0), fp32 D, A K-major, B MN-major, M = N = 128
 constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | (1u << 16) | ((128u >> 3) << 17) |
                             ((128u >> 4) << 24);
@@ -74,7 +75,8 @@ __device__ __forceinline__ void unpack_f16x2(uint32_t p, float& lo, float& hi) {
 }
 // (a, b) = columns 2j, 2j+1 (unscaled), sc2 = the scale in both halves:
 // two packed fp16x2 words h0 = rn(a', b'), h1 = rn((a', b') - h0).  The
-// scale and the residual use packed fp32x2 arithmetic (FMUL2 / FADD2).
+// scale and the residual use packed fp32x2 arithmetic (FMUL2 / FADD2); per
+// pair: FMUL2, 2 F2FP, 2 HADD2.F32 (h0 back to fp32), FADD2.
 __device__ __forceinline__ void split2(float a, float b, uint64_t sc2, uint32_t& p0, uint32_t& p1) {
     uint64_t ab, s2, h2, r2;
     asm("mov.b64 %0, {%1, %2};" : "=l"(ab) : "f"(a), "f"(b));
@@ -108,6 +110,13 @@ __device__ __forceinline__ int scale_exp(uint32_t mbits) {
                                        : -127 + (31 - __clz(static_cast<int>(mbits))) - 22;
     return kTarget - k;
 }
+// floor(log2(x)) from the bits of |x| (x finite, > 0); -1000 for 0
+__device__ __forceinline__ int ilogb_bits(uint32_t mbits) {
+    if (mbits == 0u) return -1000;
+    return mbits >= 0x00800000u ? static_cast<int>(mbits >> 23) - 127
+                                : (31 - __clz(static_cast<int>(mbits))) - 149;
+}
+
 // max |x_i| as float bits (3-input FMNMX with |.| operands; a NaN is skipped,
 // which is harmless: it propagates through the products anyway)
 __device__ __forceinline__ uint32_t absmax_bits(const float* x) {
@@ -196,12 +205,16 @@ __device__ __forceinline__ void k3h_issue(uint32_t tbase, uint32_t s0, uint64_t*
 
 size_t k3h_smem_bytes() { return kSmem; }
 
-#ifdef K3H_TRACE  // tools/k3h_trace.cu: per-phase cycle totals of CTA 0 (lane 0 of warps 0, issue, IO)
+#ifdef K3H_TRACE  // tools/k3h_trace.cu: per-phase cycle totals of CTA 0 (lane 0 of one
+                  // epilogue warp, the issue warp and the IO warp)
+#ifndef K3H_TRACE_WARP
+#define K3H_TRACE_WARP 0
+#endif
 __device__ long long* g_k3h_trace;
 __shared__ long long k3h_acc[16];
 #define K3H_MARK(k)                                                                      \
     do {                                                                                 \
-        if (blockIdx.x == 0 && (warp == 0 || warp == kIssueWarp || warp == kIOWarp) &&   \
+        if (blockIdx.x == 0 && (warp == K3H_TRACE_WARP || warp == kIssueWarp || warp == kIOWarp) && \
             lane == 0) {                                                                 \
             const long long t_ = clock64();                                              \
             k3h_acc[k] += t_ - k3h_tprev;                                                \
@@ -210,7 +223,19 @@ __shared__ long long k3h_acc[16];
     } while (0)
 #define K3H_COUNT(k)                                                                     \
     do {                                                                                 \
-        if (blockIdx.x == 0 && warp == 0 && lane == 0) k3h_acc[k] += 1;                  \
+        if (blockIdx.x == 0 && warp == K3H_TRACE_WARP && lane == 0) k3h_acc[k] += 1;                  \
+    } while (0)
+#elif defined(K3H_EVT)
+__device__ long long* g_k3h_evt;  // [role slot][8] stamps of CTA 0
+#define K3H_MARK(k) \
+    do {            \
+    } while (0)
+#define K3H_COUNT(k) \
+    do {             \
+    } while (0)
+#define K3H_EV(slot, k)                                                        \
+    do {                                                                       \
+        if (blockIdx.x == 0 && lane == 0 && (slot) < 4096) evt[(slot) * 8 + (k)] = clock64(); \
     } while (0)
 #else
 #define K3H_MARK(k) \
@@ -231,6 +256,10 @@ struct Chain {
     uint32_t ph;    // mbarrier parity (mma_bar for the epilogue, out_ready for IO)
     uint32_t inph;  // in_ready parity (epilogue)
     int e, eb;      // P = 2^e P', base = 2^eb base' (epilogue)
+    int t_prev;     // scale exponent applied at this chain's previous epilogue
+    int bmax_e;     // floor(log2 max |base'|)
+    uint32_t sb;    // max-slot buffer the next epilogue reads (0/1)
+    uint32_t mph;   // max_bar parities, bit b for buffer b
     bool act;
 };
 constexpr int kIn = -2;  // Chain::s: the next input is being loaded / converted
@@ -258,7 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* mma_bar = bars;        // [2] a chain's step MMAs completed
     uint64_t* out_ready = bars + 2;  // [2] a chain's result is in its warp tiles (16 arrivals)
     uint64_t* in_ready = bars + 4;   // [2] a chain's next input landed in its warp tiles (TMA)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
+    uint64_t* max_bar = bars + 6;    // [chain][buffer] the 16 per-warp maxima are written
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -270,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(out_ready + 1, kWorkers);
         mbar_init(in_ready, 1);
         mbar_init(in_ready + 1, 1);
+        for (int i = 0; i < 4; ++i) mbar_init(max_bar + i, kWorkers);
         fence_mbar_init();
     }
     if (warp == kIssueWarp) tmem_alloc<512>(tmem_slot);
@@ -300,6 +331,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     long long k3h_tprev = clock64();
 #endif
+#ifdef K3H_EVT
+    long long* evt = g_k3h_evt;
+    int evs = 0;  // this role's slot counter
+#else
+#define K3H_EV(slot, k) \
+    do {                \
+    } while (0)
+#endif
     // the 16 warp tiles of chain cc <-> matrix mm (TMA boxes of 32 x 32)
     auto tiles_load = [&](uint32_t cc, long long mm) {
         mbar_expect_tx(in_ready + cc, 16 * 4096);
@@ -328,11 +367,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             st.s = (st.s == kIn) ? 0 : st.s + 1;
             K3H_MARK(10);
+            K3H_EV(evs, 0);
             named_bar_sync(1 + C, kWorkers * 32 + 32);
             K3H_MARK(8);
+            K3H_EV(evs, 1);
             tc_fence_after();
             k3h_issue<C>(tmem, s0, mma_bar);
             __syncwarp();
+            K3H_EV(evs, 2);
+#ifdef K3H_EVT
+            ++evs;
+#endif
             K3H_MARK(9);
         };
         while (ch0.act || ch1.act) {
@@ -387,14 +432,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_base = tmem + ((q * 32) << 16);
         const uint32_t tile_off = warp * 4096u;  // the warp's tile inside a chain's plane region
 
-        // max |x| over the chain's whole 128 x 128 block: per-warp maxima in
-        // SMEM slot [cc][warp], one barrier among the 16 epilogue warps (it
-        // also orders every warp's tile reads before the plane writes).
-        auto block_max = [&](uint32_t cc, const float* x) -> uint32_t {
+        const uint32_t lg_n = 32u - __clz(static_cast<int>(n - 1));  // ceil(log2 n), n >= 2
+        // Per-warp maxima of a chain live in SMEM slots [cc][buffer][warp].
+        // IN: exact max of the new input (one barrier among the 16 epilogue
+        // warps, which also orders every warp's tile reads before the plane
+        // writes); the slots then hold max |A| for the first step's bound.
+        auto block_max_in = [&](uint32_t cc, uint32_t buf, const float* x) -> uint32_t {
             const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, absmax_bits(x));
-            const uint32_t slots = s0 + kMaxOff + cc * 64u;
+            const uint32_t slots = s0 + kMaxOff + cc * 128u + buf * 64u;
             if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots + warp * 4u), "r"(m) : "memory");
             named_bar_sync(3, kWorkers * 32);
+            if (lane == 0) mbar_arrive(max_bar + cc * 2 + buf);  // uniform hand-off to the next step
             uint32_t r = 0;
 #pragma unroll
             for (uint32_t i = 0; i < 4; ++i) {
@@ -403,31 +451,74 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             return r;
         };
-        // 32 values (scaled by sc here) -> planes y0/y1 of chain cc (right
-        // operand) and, if `left`, x0/x1 in TMEM; !right: only x0/x1 (the
-        // base of a MULTIPLY_BASE step)
-        auto emit = [&](uint32_t cc, const float* x, float sc, bool right, bool left) {
-            // opaque copies: recompute the swizzled addresses here instead of
-            // letting the compiler hoist them all out of the loop (and spill)
-            uint32_t r_ = row, b_ = s0, lb_ = lane_base;
-            asm volatile("" : "+r"(r_), "+r"(b_), "+r"(lb_));
+        // max over the 16 slots written at this chain's previous epilogue
+        // (long complete: every warp published since; the mbarrier wait is
+        // the acquire that makes the slots visible)
+        auto slots_max = [&](uint32_t cc, Chain& st) -> uint32_t {
+            mbar_wait_sleep(max_bar + cc * 2 + st.sb, (st.mph >> st.sb) & 1u);
+            st.mph ^= 1u << st.sb;
+            const uint32_t slots = s0 + kMaxOff + cc * 128u + st.sb * 64u;
+            uint32_t r = 0;
+#pragma unroll
+            for (uint32_t i = 0; i < 4; ++i) {
+                const uint4 w4 = lds128(slots + 16u * i);
+                r = max(r, max(max(w4.x, w4.y), max(w4.z, w4.w)));
+            }
+            return r;
+        };
+        // 16 values (columns col0 + 16h ...), scaled by sc2 here -> planes
+        // y0/y1 of chain cc (right operand) and, if `left`, x0/x1 in TMEM;
+        // !right: only x0/x1 (the base of a MULTIPLY_BASE step)
+        // Plane addresses of this thread's 16-byte units: row `row`, unit u of
+        // columns 32g + 8u' lives at (u ^ (row & 7)) << 4.  With u = u0 + j
+        // (u0 even, j = 0/1) that is (u0 ^ (row & 6)) + (j ^ (row & 1)), so
+        // four registers cover both halves and both units; chain and plane
+        // are immediate offsets (compile-time), nothing else is recomputed.
+        uint32_t sa00, sa01, sa10, sa11;
+        {
+            const uint32_t rb = s0 + (g >> 1) * 16384u + row * 128u;
+            const uint32_t u00 = (g & 1u) * 4u, u10 = u00 + 2u;
+            const uint32_t lo0 = (row & 1u) << 4, lo1 = ((row & 1u) ^ 1u) << 4;
+            sa00 = rb + ((u00 ^ (row & 6u)) << 4) + lo0;
+            sa01 = rb + ((u00 ^ (row & 6u)) << 4) + lo1;
+            sa10 = rb + ((u10 ^ (row & 6u)) << 4) + lo0;
+            sa11 = rb + ((u10 ^ (row & 6u)) << 4) + lo1;
+        }
+        // 16 values (columns col0 + 16h ...), scaled by sc2 here -> planes
+        // y0/y1 of chain CC (right operand) and, if `left`, x0/x1 in TMEM
+        auto emit_half = [&](auto cc, const float* x, auto hh, uint64_t sc2, bool left) {
+            constexpr uint32_t CC = decltype(cc)::value, H = decltype(hh)::value;
+            uint32_t p0[8], p1[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) split2(x[2 * j], x[2 * j + 1], sc2, p0[j], p1[j]);
+            const uint32_t a0 = H ? sa10 : sa00, a1 = H ? sa11 : sa01;
+            sts128_imm<CC * kChainSmem>(a0, p0[0], p0[1], p0[2], p0[3]);
+            sts128_imm<CC * kChainSmem>(a1, p0[4], p0[5], p0[6], p0[7]);
+            sts128_imm<CC * kChainSmem + kPlane>(a0, p1[0], p1[1], p1[2], p1[3]);
+            sts128_imm<CC * kChainSmem + kPlane>(a1, p1[4], p1[5], p1[6], p1[7]);
+            if (left) {
+                const uint32_t tl = lane_base + CC * 256u + 128u + g * 16u + H * 8u;
+                tmem_st8(tl, p0);
+                tmem_st8(tl + 64u, p1);
+            }
+        };
+        // the base of a MULTIPLY_BASE step: x0/x1 (TMEM) only
+        auto emit_left = [&](uint32_t cc, const float* x, float sc) {
             const uint64_t sc2 = splat2(sc);
 #pragma unroll
             for (uint32_t h = 0; h < 2; ++h) {
                 uint32_t p0[8], p1[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) split2(x[16 * h + 2 * j], x[16 * h + 2 * j + 1], sc2, p0[j], p1[j]);
-                if (right) {
-                    const uint32_t pb = b_ + cc * kChainSmem;
-                    put_half(pb, r_, g, h, p0);
-                    put_half(pb + kPlane, r_, g, h, p1);
-                }
-                if (left) {
-                    const uint32_t tl = lb_ + cc * 256u + 128u + g * 16u + h * 8u;
-                    tmem_st8(tl, p0);
-                    tmem_st8(tl + 64u, p1);
-                }
+                const uint32_t tl = lane_base + cc * 256u + 128u + g * 16u + h * 8u;
+                tmem_st8(tl, p0);
+                tmem_st8(tl + 64u, p1);
             }
+        };
+        auto emit = [&](auto cc, const float* x, float sc) {  // IN: all planes
+            const uint64_t sc2 = splat2(sc);
+            emit_half(cc, x, std::integral_constant<uint32_t, 0>{}, sc2, true);
+            emit_half(cc, x + 16, std::integral_constant<uint32_t, 1>{}, sc2, true);
         };
 
         auto slot = [&](Chain& st, auto cc) {
@@ -449,11 +540,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else {
                     load_row(in + static_cast<size_t>(st.m) * n2, n, row, col0, x);
                 }
-                const int t = scale_exp(block_max(C, x));
+                st.sb ^= 1u;  // (the other buffer: the current one was read at OUT)
+                const uint32_t mA = block_max_in(C, st.sb, x);
+                const int t = scale_exp(mA);
                 K3H_MARK(4);
                 st.e = -t;
                 st.eb = -t;
-                emit(C, x, exp2i(t), true, true);
+                st.t_prev = t;
+                st.bmax_e = ilogb_bits(mA) + t;
+                emit(cc, x, exp2i(t));
                 K3H_MARK(5);
                 K3H_COUNT(13);
                 st.s = 0;
@@ -461,15 +556,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 K3H_MARK(7);
                 mbar_wait_sleep(mma_bar + C, st.ph);
                 K3H_MARK(0);
+                if (warp == 2) K3H_EV(evs, 3);
                 st.ph ^= 1;
                 tc_fence_after();
-                float v[32];
-                tmem_ld32(lane_base + C * 256u + col0, reinterpret_cast<uint32_t(&)[32]>(v));
-                K3H_MARK(1);
                 // exponent of this step's product: 2^(ex + ey) * D
                 const int pe = (plan_is_mult(plan, st.s) ? st.eb : st.e) + st.e;
                 if (st.s == last) {
                     // ---- OUT: 2^pe * D -> the warp tile (the IO warp stores it)
+                    (void)slots_max(C, st);  // consume the last step's maxima (keeps the parities in step)
+                    float v[32];
+                    tmem_ld32(lane_base + C * 256u + col0, reinterpret_cast<uint32_t(&)[32]>(v));
                     const float f1 = exp2i(pe / 2), f2 = exp2i(pe - pe / 2);
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], f1), f2);
@@ -489,18 +585,59 @@ __global__ void __launch_bounds__(kThreads, 1)
                     st.s = kIn;
                     return;  // no publish: IN follows one slot later
                 }
+                // ---- step: D -> operands of the next step.  Two 16-column
+                // halves; the second TMEM load is in flight while the first
+                // half is split, and the scale is settled under the first load.
+                uint32_t a[16], b[16];
+                tmem_ld16_async(lane_base + C * 256u + col0, a);
+                // Scale for the split, from a bound instead of a barrier:
+                // |D| <= n max|X'| max|Y'|, with max|P'| known exactly one step
+                // late (the previous epilogue's maxima).  The scaled max stays
+                // < 2^14 (no fp16 overflow); it falls below the full-precision
+                // floor (~2^-3) only if one product cancels by more than 2^17
+                // against its bound.
+                const bool was_mult = plan_is_mult(plan, st.s);
+                const uint32_t mprev = slots_max(C, st);
+                const int pmax_e = ilogb_bits(mprev) + st.t_prev;  // floor(log2 max|P'_s|)
+                const int xmax_e = was_mult ? st.bmax_e : pmax_e;
+                int t = kCeil - static_cast<int>(lg_n) - (xmax_e + 1) - (pmax_e + 1);
+                if (mprev == 0u || mprev >= 0x7F800000u) t = 0;  // zero / non-finite operand
+                t = max(-126, min(126, t));
+                st.t_prev = t;
                 st.s += 1;
                 const bool mult = plan_is_mult(plan, st.s);
-                const int t = scale_exp(block_max(C, v));
-                K3H_MARK(11);
                 st.e = pe - t;
-                emit(C, v, exp2i(t), true, !mult);
+                const uint64_t sc2 = splat2(exp2i(t));
+                K3H_MARK(1);
+                tmem_ld_wait_dep(a);
+                tmem_ld16_async(lane_base + C * 256u + col0 + 16u, b);
+                const float* fa = reinterpret_cast<const float*>(a);
+                const float* fb = reinterpret_cast<const float*>(b);
+                float m = 0.f;
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) m = fmaxf(fmaxf(m, fabsf(fa[i])), fabsf(fa[i + 1]));
+                emit_half(cc, fa, std::integral_constant<uint32_t, 0>{}, sc2, !mult);
+                tmem_ld_wait_dep(b);
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) m = fmaxf(fmaxf(m, fabsf(fb[i])), fabsf(fb[i + 1]));
+                emit_half(cc, fb, std::integral_constant<uint32_t, 1>{}, sc2, !mult);
+                {   // this step's maxima, for the next epilogue of this chain
+                    const uint32_t mw = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(m));
+                    const uint32_t nb = st.sb ^ 1u;
+                    if (lane == 0) {
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(s0 + kMaxOff + C * 128u + nb * 64u + warp * 4u),
+                                     "r"(mw)
+                                     : "memory");
+                        mbar_arrive(max_bar + C * 2 + nb);
+                    }
+                    st.sb = nb;
+                }
                 K3H_MARK(6);
                 K3H_COUNT(14);
                 if (mult) {  // left operand = the base, rescaled by its input exponent
                     float x[32];
                     load_row(in + static_cast<size_t>(st.m) * n2, n, row, col0, x);
-                    emit(C, x, exp2i(-st.eb), false, true);
+                    emit_left(C, x, exp2i(-st.eb));
                 }
             }
             // workers arrive; the issue warp waits for all of them (the hardware
@@ -508,6 +645,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st_wait();
             fence_proxy_async_smem();
             tc_fence_before();
+            if (warp == 2) K3H_EV(evs, 4);
+            if (warp == 0) K3H_EV(evs, 5);
+            if (warp == 15) K3H_EV(evs, 6);
+#ifdef K3H_EVT
+            ++evs;
+#endif
             named_bar_arrive(1 + C, kWorkers * 32 + 32);
         };
         while (ch0.act || ch1.act) {
