@@ -593,45 +593,68 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // Scale for the split, from a bound instead of a barrier:
                 // |D| <= n max|X'| max|Y'|, with max|P'| known exactly one step
                 // late (the previous epilogue's maxima).  The scaled max stays
-                // < 2^14 (no fp16 overflow); it falls below the full-precision
-                // floor (~2^-3) only if one product cancels by more than 2^17
-                // against its bound.
+                // < 2^14 (no fp16 overflow).  A product that cancels strongly
+                // against its bound would land low in fp16's range and lose
+                // bits of h1, so the exact path (block max, one barrier) runs
+                // for the first product of every matrix and whenever the
+                // previous product came out more than 2^12 below its bound.
                 const bool was_mult = plan_is_mult(plan, st.s);
                 const uint32_t mprev = slots_max(C, st);
                 const int pmax_e = ilogb_bits(mprev) + st.t_prev;  // floor(log2 max|P'_s|)
+                const bool exact = st.s == 0 || pmax_e < kCeil - 12;
                 const int xmax_e = was_mult ? st.bmax_e : pmax_e;
                 int t = kCeil - static_cast<int>(lg_n) - (xmax_e + 1) - (pmax_e + 1);
                 if (mprev == 0u || mprev >= 0x7F800000u) t = 0;  // zero / non-finite operand
-                t = max(-126, min(126, t));
-                st.t_prev = t;
                 st.s += 1;
                 const bool mult = plan_is_mult(plan, st.s);
-                st.e = pe - t;
-                const uint64_t sc2 = splat2(exp2i(t));
-                K3H_MARK(1);
-                tmem_ld_wait_dep(a);
-                tmem_ld16_async(lane_base + C * 256u + col0 + 16u, b);
                 const float* fa = reinterpret_cast<const float*>(a);
                 const float* fb = reinterpret_cast<const float*>(b);
-                float m = 0.f;
+                const uint32_t nb = st.sb ^ 1u;  // this step's maxima -> slots [nb]
+                const uint32_t slots = s0 + kMaxOff + C * 128u + nb * 64u;
+                auto absmax16 = [](const float* x, float m) {
 #pragma unroll
-                for (int i = 0; i < 16; i += 2) m = fmaxf(fmaxf(m, fabsf(fa[i])), fabsf(fa[i + 1]));
-                emit_half(cc, fa, std::integral_constant<uint32_t, 0>{}, sc2, !mult);
-                tmem_ld_wait_dep(b);
-#pragma unroll
-                for (int i = 0; i < 16; i += 2) m = fmaxf(fmaxf(m, fabsf(fb[i])), fabsf(fb[i + 1]));
-                emit_half(cc, fb, std::integral_constant<uint32_t, 1>{}, sc2, !mult);
-                {   // this step's maxima, for the next epilogue of this chain
+                    for (int i = 0; i < 16; i += 2) m = fmaxf(fmaxf(m, fabsf(x[i])), fabsf(x[i + 1]));
+                    return m;
+                };
+                auto publish_max = [&](float m) {
                     const uint32_t mw = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(m));
-                    const uint32_t nb = st.sb ^ 1u;
                     if (lane == 0) {
-                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(s0 + kMaxOff + C * 128u + nb * 64u + warp * 4u),
-                                     "r"(mw)
-                                     : "memory");
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots + warp * 4u), "r"(mw) : "memory");
                         mbar_arrive(max_bar + C * 2 + nb);
                     }
-                    st.sb = nb;
+                };
+                K3H_MARK(1);
+                if (!exact) {
+                    t = max(-126, min(126, t));
+                    const uint64_t sc2 = splat2(exp2i(t));
+                    tmem_ld_wait_dep(a);
+                    tmem_ld16_async(lane_base + C * 256u + col0 + 16u, b);
+                    float m = absmax16(fa, 0.f);
+                    emit_half(cc, fa, std::integral_constant<uint32_t, 0>{}, sc2, !mult);
+                    tmem_ld_wait_dep(b);
+                    m = absmax16(fb, m);
+                    emit_half(cc, fb, std::integral_constant<uint32_t, 1>{}, sc2, !mult);
+                    publish_max(m);
+                } else {
+                    tmem_ld_wait_dep(a);
+                    tmem_ld16_async(lane_base + C * 256u + col0 + 16u, b);
+                    tmem_ld_wait_dep(b);
+                    publish_max(absmax16(fb, absmax16(fa, 0.f)));
+                    named_bar_sync(3, kWorkers * 32);
+                    uint32_t mx = 0;
+#pragma unroll
+                    for (uint32_t i = 0; i < 4; ++i) {
+                        const uint4 w4 = lds128(slots + 16u * i);
+                        mx = max(mx, max(max(w4.x, w4.y), max(w4.z, w4.w)));
+                    }
+                    t = scale_exp(mx);
+                    const uint64_t sc2 = splat2(exp2i(t));
+                    emit_half(cc, fa, std::integral_constant<uint32_t, 0>{}, sc2, !mult);
+                    emit_half(cc, fb, std::integral_constant<uint32_t, 1>{}, sc2, !mult);
                 }
+                st.sb = nb;
+                st.t_prev = t;
+                st.e = pe - t;
                 K3H_MARK(6);
                 K3H_COUNT(14);
                 if (mult) {  // left operand = the base, rescaled by its input exponent
