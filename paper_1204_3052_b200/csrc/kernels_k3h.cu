@@ -49,7 +49,8 @@ constexpr int kIOWarp = kWorkers;              //   + one TMA IO warp
 constexpr int kThreads = (kWorkers + 2) * 32;  // 576 (<= 96 registers per thread)
 constexpr uint32_t kPlane = 128u * 128u * 2u;  // one fp16 plane: 32 KB
 constexpr uint32_t kChainSmem = 2u * kPlane;   // y0, y1 of one chain
-constexpr uint32_t kMaxOff = 2u * kChainSmem;  // [chain][buffer][16] per-warp max |D| slots
+constexpr uint32_t kROff = 2u * kChainSmem;    // 64 KB: finished results on their way out (TMA)
+constexpr uint32_t kMaxOff = kROff + 65536u;   // [chain][buffer][16] per-warp max |D| slots
 constexpr uint32_t kBarOff = kMaxOff + 256;    // mbarriers + TMEM slot
 constexpr size_t kSmem = kBarOff + 128 + 1024; // + alignment slack
 constexpr int kTarget = 13;                    // input: scaled max |A'| in [2^13, 2^14)
@@ -288,7 +289,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* out_ready = bars + 2;  // [2] a chain's result is in its warp tiles (16 arrivals)
     uint64_t* in_ready = bars + 4;   // [2] a chain's next input landed in its warp tiles (TMA)
     uint64_t* max_bar = bars + 6;    // [chain][buffer] the 16 per-warp maxima are written
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+    uint64_t* r_free = bars + 10;    // the result region's last TMA store has read it
+    uint64_t* planes_free = bars + 11;  // [2] a chain's last step's MMAs are done (OUT)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -301,6 +304,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(in_ready, 1);
         mbar_init(in_ready + 1, 1);
         for (int i = 0; i < 4; ++i) mbar_init(max_bar + i, kWorkers);
+        mbar_init(r_free, 1);
+        mbar_init(planes_free, 1);
+        mbar_init(planes_free + 1, 1);
         fence_mbar_init();
     }
     if (warp == kIssueWarp) tmem_alloc<512>(tmem_slot);
@@ -390,6 +396,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (ch0.act) tiles_load(0, ch0.m);
             if (ch1.act) tiles_load(1, ch1.m);
         }
+        // Matrix boundary of chain C: as soon as the last step's MMAs are done
+        // (its operand planes are dead) the next input is TMA-loaded into
+        // the chain's plane region; the result meanwhile goes out from the
+        // separate region R, so the load does not wait for the store.
         auto slot = [&](Chain& st, auto cc) {
             constexpr uint32_t C = decltype(cc)::value;
             if (!st.act) return;
@@ -406,16 +416,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             st.act = st.m < batch;
             st.s = kIn;
             if (!vec) return;
+            // (signalled by the epilogue, which tracks every mma_bar phase; a
+            // parity wait on mma_bar here could alias a phase the IO warp,
+            // running ahead, has not reached yet)
+            mbar_wait_sleep(planes_free + C, st.inph);
+            st.inph ^= 1;
+            if (lane == 0 && st.act) tiles_load(C, st.m);
             mbar_wait_sleep(out_ready + C, st.ph);
             st.ph ^= 1;
             if (lane == 0) {
                 for (uint32_t w = 0; w < kWorkers; ++w)
-                    tma_store_2d_s(&out_map, s0 + C * kChainSmem + w * 4096u,
-                                   static_cast<int32_t>((w >> 2) * 32),
+                    tma_store_2d_s(&out_map, s0 + kROff + w * 4096u, static_cast<int32_t>((w >> 2) * 32),
                                    static_cast<int32_t>(m_prev * 128 + (w & 3) * 32));
                 bulk_commit_group();
-                bulk_wait_group_read0();  // tiles read: reuse them for the input
-                if (st.act) tiles_load(C, st.m);
+                bulk_wait_group_read0();
+                mbar_arrive(r_free);  // R may take the next result
             }
             __syncwarp();
         };
@@ -430,7 +445,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t row = q * 32 + lane;
         const uint32_t col0 = g * 32;
         const uint32_t lane_base = tmem + ((q * 32) << 16);
-        const uint32_t tile_off = warp * 4096u;  // the warp's tile inside a chain's plane region
+        const uint32_t tile_off = warp * 4096u;  // the warp's tile inside a 64 KB region
+        uint32_t outs = 0;                       // results handed to the IO warp so far (vec)
 
         const uint32_t lg_n = 32u - __clz(static_cast<int>(n - 1));  // ceil(log2 n), n >= 2
         // Per-warp maxima of a chain live in SMEM slots [cc][buffer][warp].
@@ -563,6 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int pe = (plan_is_mult(plan, st.s) ? st.eb : st.e) + st.e;
                 if (st.s == last) {
                     // ---- OUT: 2^pe * D -> the warp tile (the IO warp stores it)
+                    if (warp == 0 && lane == 0 && vec) mbar_arrive(planes_free + C);  // load the next input
                     (void)slots_max(C, st);  // consume the last step's maxima (keeps the parities in step)
                     float v[32];
                     tmem_ld32(lane_base + C * 256u + col0, reinterpret_cast<uint32_t(&)[32]>(v));
@@ -570,7 +587,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], f1), f2);
                     if (vec) {
-                        tile_put_rows(s0 + C * kChainSmem + tile_off, lane, v);
+                        if (outs > 0) mbar_wait_sleep(r_free, (outs - 1u) & 1u);
+                        ++outs;
+                        tile_put_rows(s0 + kROff + tile_off, lane, v);
                         fence_proxy_async_smem();
                         tc_fence_before();  // D reads done before the next MMAs into D
                         __syncwarp();
