@@ -19,6 +19,8 @@
  *                          config 3; no reference counterpart beyond the loop)
  *   mxp_alloc/free,     <- ComputeDevice.createBuffer / releaseBuffer /
  *   mxp_upload/download    writeBuffer / readBuffer  device.ts:25-39
+ *   mxp_gemm_prepare_rhs,  the same, split so several row blocks share one
+ *   mxp_gemm_rows_prepared right-hand side (row-sharded chain)
  *   mxp_gemm            <- ComputeDevice.dispatchMatmul(kernel, n, a, b, c)
  *                          device.ts:33-39 (device pointers, async)
  *   mxp_power_device    <- the gpuExponentiate step loop host.ts:126-131 on
@@ -65,7 +67,8 @@ extern "C" {
 #define MXP_E_NCCL 5               /* collective failure (multi-GPU paths) */
 
 /* element modes */
-#define MXP_F32 0     /* float32 in/out; 3xTF32 on tcgen05 tensor cores */
+#define MXP_F32 0     /* float32 in/out; split-fp32 on tcgen05 tensor cores (3xTF32
+                         for n > 128, scaled fp16x2 / bf16x3 for n <= 128) */
 #define MXP_F64 1     /* float64 in/out; DMMA tensor pipe */
 #define MXP_U32_MOD 2 /* uint32 residues mod p; exact (see mxp_power_mod) */
 
@@ -111,6 +114,16 @@ MXP_API int mxp_gemm(mxp_handle h, int mode, int64_t n, const void* dA, const vo
  * bitwise equal to the single-GPU ones. */
 MXP_API int mxp_gemm_rows(mxp_handle h, int mode, int64_t n, int64_t rows, const void* dA,
                           const void* dB, void* dC);
+/* the row-block multiply in two parts, so a caller can run several row blocks
+ * against one right-hand side (the row-sharded multi-GPU chain computes its
+ * rows in chunks and all-gathers each chunk while the next one computes):
+ * prepare B once (split / pad into the handle's workspace), then any number
+ * of C[rows x n] = A[rows x n] * B.  Any other call that uses the handle's
+ * workspace invalidates the prepared B (E_VALIDATION until prepared again).
+ * Arithmetic per element is identical to mxp_gemm_rows / mxp_gemm. */
+MXP_API int mxp_gemm_prepare_rhs(mxp_handle h, int mode, int64_t n, const void* dB);
+MXP_API int mxp_gemm_rows_prepared(mxp_handle h, int mode, int64_t n, int64_t rows,
+                                   const void* dA, void* dC);
 MXP_API int mxp_multiply(mxp_handle h, int mode, int64_t n, const void* hA, const void* hB, void* hC,
                  mxp_stats* stats);
 

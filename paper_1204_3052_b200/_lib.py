@@ -34,7 +34,7 @@ EXPORTS = (
     "mxp_host_free", "mxp_upload", "mxp_download", "mxp_plan", "mxp_gemm", "mxp_multiply",
     "mxp_power_device", "mxp_power", "mxp_power_batched_device", "mxp_power_batched",
     "mxp_power_mod_device", "mxp_power_mod", "mxp_random_device", "mxp_last_error",
-    "mxp_status_string",
+    "mxp_status_string", "mxp_gemm_prepare_rhs", "mxp_gemm_rows_prepared",
 )
 
 
@@ -93,6 +93,8 @@ def load() -> ctypes.CDLL:
             "mxp_plan": [i64, ctypes.c_char_p, i64, P(i64)],
             "mxp_gemm": [vp, c_int, i64, vp, vp, vp],
             "mxp_gemm_rows": [vp, c_int, i64, i64, vp, vp, vp],
+            "mxp_gemm_prepare_rhs": [vp, c_int, i64, vp],
+            "mxp_gemm_rows_prepared": [vp, c_int, i64, i64, vp, vp],
             "mxp_multiply": [vp, c_int, i64, vp, vp, vp, P(Stats)],
             "mxp_power_device": [vp, c_int, i64, i64, vp, vp, P(Stats)],
             "mxp_power": [vp, c_int, i64, i64, vp, vp, P(Stats)],

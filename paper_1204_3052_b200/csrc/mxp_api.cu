@@ -100,6 +100,10 @@ struct mxp_handle_s {
     float* part = nullptr;  // split-K workspace (splits x n_pad^2 fp32) for small n
     int splits = 1;
     CUtensorMap map_a[6], map_b[6];
+    // right-hand side prepared by mxp_gemm_prepare_rhs (planes[2..3] / f64buf[1]);
+    // any other use of the workspace invalidates it
+    int rhs_mode = -1;
+    int64_t rhs_n = 0;
     // fp64 workspace: base, ping, pong (n_pad^2 doubles)
     int64_t ws64_pad = 0;
     double* f64buf[3] = {};
@@ -149,6 +153,7 @@ void stats_reset(mxp_stats* st) {
 }
 
 int ensure_ws32(mxp_handle h, int64_t n_pad) {
+    h->rhs_mode = -1;
     if (h->ws32_pad >= n_pad) return MXP_OK;
     for (auto& p : h->planes) {
         if (p) cudaFree(p);
@@ -179,6 +184,7 @@ int encode_ws32(mxp_handle h, int64_t n_pad) {
 }
 
 int ensure_ws64(mxp_handle h, int64_t n_pad) {
+    h->rhs_mode = -1;
     if (h->ws64_pad >= n_pad) return MXP_OK;
     for (auto& p : h->f64buf) {
         if (p) cudaFree(p);
@@ -572,20 +578,49 @@ int mxp_gemm(mxp_handle h, int mode, int64_t n, const void* dA, const void* dB, 
     return MXP_OK;
 }
 
-int mxp_gemm_rows(mxp_handle h, int mode, int64_t n, int64_t rows, const void* dA, const void* dB,
-                  void* dC) {
+// The right-hand side of a row-block multiply, prepared once (split into tf32
+// hi/lo planes, or padded for FP64) in the handle's workspace.
+int mxp_gemm_prepare_rhs(mxp_handle h, int mode, int64_t n, const void* dB) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    rc = validate(mode, n, 2);
+    if (rc) return rc;
+    if (!dB) return fail(MXP_E_VALIDATION, "null device pointer");
+    const int64_t n_pad = round_up(n, 128);
+    if (mode == MXP_F32) {
+        rc = ensure_ws32(h, n_pad);
+        if (rc) return rc;
+        cudaError_t e = launch_split(static_cast<const float*>(dB), (int)n, (int)n, h->planes[2],
+                                     h->planes[3], (int)h->ws32_pad, h->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "split");
+    } else {
+        rc = ensure_ws64(h, n_pad);
+        if (rc) return rc;
+        cudaError_t e = launch_f64_pad(static_cast<const double*>(dB), (int)n, h->f64buf[1],
+                                       (int)n_pad, h->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "f64 pad");
+    }
+    h->rhs_mode = mode;
+    h->rhs_n = n;
+    return MXP_OK;
+}
+
+// C[rows x n] = A[rows x n] * (the prepared right-hand side).
+int mxp_gemm_rows_prepared(mxp_handle h, int mode, int64_t n, int64_t rows, const void* dA,
+                           void* dC) {
     int rc = check_handle(h);
     if (rc) return rc;
     rc = validate(mode, n, 2);
     if (rc) return rc;
     if (rows < 1 || rows > n)
         return fail(MXP_E_VALIDATION, "row block must satisfy 1 <= rows <= n, got %lld", (long long)rows);
-    if (!dA || !dB || !dC) return fail(MXP_E_VALIDATION, "null device pointer");
+    if (!dA || !dC) return fail(MXP_E_VALIDATION, "null device pointer");
+    if (h->rhs_mode != mode || h->rhs_n != n)
+        return fail(MXP_E_VALIDATION, "no right-hand side prepared for this mode and n "
+                                      "(call mxp_gemm_prepare_rhs first)");
     const int64_t n_pad = round_up(n, 128);
     int64_t r_pad = round_up(rows, 128);
     if (mode == MXP_F32) {
-        rc = ensure_ws32(h, n_pad);
-        if (rc) return rc;
         const int np = (int)h->ws32_pad;
         const int bn = k1_block_n(np, h->num_sms);
         if (bn == 256) r_pad = round_up(rows, 256);  // CTA-pair tiles are 256 rows
@@ -597,9 +632,6 @@ int mxp_gemm_rows(mxp_handle h, int mode, int64_t n, int64_t rows, const void* d
             return fail(MXP_E_CUDA, "cuTensorMapEncodeTiled failed");
         cudaError_t e = launch_split_rows(static_cast<const float*>(dA), (int)n, (int)n, (int)rows,
                                           h->planes[0], h->planes[1], np, (int)r_pad, h->stream);
-        if (e == cudaSuccess)
-            e = launch_split(static_cast<const float*>(dB), (int)n, (int)n, h->planes[2],
-                             h->planes[3], np, h->stream);
         if (e != cudaSuccess) return cuda_fail(e, "split");
         GemmPlanes m{a_hi, a_lo, b_hi, b_lo};
         // same k-split as the full multiply / chain: bitwise-identical rows
@@ -608,19 +640,27 @@ int mxp_gemm_rows(mxp_handle h, int mode, int64_t n, int64_t rows, const void* d
         if (e != cudaSuccess) return cuda_fail(e, "k1_gemm_3xtf32");
         return MXP_OK;
     }
-    rc = ensure_ws64(h, n_pad);
-    if (rc) return rc;
     double** b = h->f64buf;
     cudaError_t e = launch_f64_pad_rows(static_cast<const double*>(dA), (int)n, (int)rows, b[0],
                                         (int)n_pad, (int)r_pad, h->stream);
-    if (e == cudaSuccess)
-        e = launch_f64_pad(static_cast<const double*>(dB), (int)n, b[1], (int)n_pad, h->stream);
     if (e == cudaSuccess) e = launch_f64_gemm_rows(b[0], b[1], b[2], (int)n_pad, (int)r_pad, h->stream);
     if (e == cudaSuccess)
         e = launch_f64_unpad_rows(b[2], (int)n_pad, static_cast<double*>(dC), (int)n, (int)rows,
                                   h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "f64 gemm rows");
     return MXP_OK;
+}
+
+int mxp_gemm_rows(mxp_handle h, int mode, int64_t n, int64_t rows, const void* dA, const void* dB,
+                  void* dC) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (rows < 1 || rows > n)
+        return fail(MXP_E_VALIDATION, "row block must satisfy 1 <= rows <= n, got %lld", (long long)rows);
+    if (!dA || !dB || !dC) return fail(MXP_E_VALIDATION, "null device pointer");
+    rc = mxp_gemm_prepare_rhs(h, mode, n, dB);
+    if (rc) return rc;
+    return mxp_gemm_rows_prepared(h, mode, n, rows, dA, dC);
 }
 
 int mxp_multiply(mxp_handle h, int mode, int64_t n, const void* hA, const void* hB, void* hC,

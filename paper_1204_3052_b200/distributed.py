@@ -5,13 +5,17 @@ Two strategies:
 * ``exponentiate_batched_sharded`` — independent matrices (config 3): rank r
   takes the contiguous slice ``shard_range(batch, r, world)``; no collective
   on the data path, results are bitwise the single-GPU ones.
-* ``exponentiate_row_sharded`` — one large matrix (config 5): rank g owns
-  rows R_g of the running power.  Each step computes its row block
-  ``P'[R_g, :] = P[R_g, :] @ RHS`` (RHS = P for SQUARE, the replicated base A
-  for MULTIPLY_BASE, accumulator on the left as in expo.py:133-136) and then
-  all-gathers the row blocks (NCCL over NVLink) so every rank holds the full
-  P' for the next squaring.  Every element keeps its full-K dot product on one
-  GPU, so the result is bitwise equal to the single-GPU chain.
+* ``exponentiate_row_sharded`` — one large matrix (config 5): each rank owns
+  a set of row chunks of the running power.  Each step prepares the
+  right-hand side once (RHS = P for SQUARE, the replicated base A for
+  MULTIPLY_BASE, accumulator on the left as in expo.py:133-136), then computes
+  its chunks ``P'[rows, :] = P[rows, :] @ RHS`` one after the other and
+  all-gathers every chunk (NCCL over NVLink, ``async_op``) as soon as it is
+  computed, so the exchange of chunk j overlaps the MMAs of chunk j+1; only
+  the last chunk's gather is exposed.  Chunks are interleaved over the ranks
+  (rank r's chunk j = global rows [(j W + r) c, +c)) so each chunk's gather
+  lands in one contiguous slab of P'.  Every element keeps its full-K dot
+  product on one GPU, so the result is bitwise equal to the single-GPU chain.
 
 The per-step compute is injectable (``ops``) so the host-side sharding and
 collective logic is tested with the gloo backend on CPU (tests/
@@ -59,6 +63,17 @@ class EngineOps:
         self.eng.gemm_rows_device(a_rows.data_ptr(), b.data_ptr(), out.data_ptr(), b.shape[0],
                                   a_rows.shape[0], mode)
 
+    def prepare_rhs(self, b):
+        from . import _lib
+
+        mode = _lib.MXP_F32 if str(b.dtype) == "torch.float32" else _lib.MXP_F64
+        self._n, self._mode = b.shape[0], mode
+        self.eng.gemm_prepare_rhs_device(b.data_ptr(), b.shape[0], mode)
+
+    def gemm_rows_prepared(self, a_rows, out):
+        self.eng.gemm_rows_prepared_device(a_rows.data_ptr(), out.data_ptr(), self._n,
+                                           a_rows.shape[0], self._mode)
+
     def power_batched(self, a, k, out):
         from . import _lib
 
@@ -66,17 +81,26 @@ class EngineOps:
         self.eng.power_batched_device(a.data_ptr(), out.data_ptr(), a.shape[1], a.shape[0], k, mode)
 
 
-def _all_gather_rows(full, local, group, dist):
-    """full[(r*rows):(r+1)*rows] <- local of rank r, on every rank."""
+def _all_gather_slab(slab, local, group, dist, async_op):
+    """slab[(r*c):(r+1)*c] <- local of rank r, on every rank (NCCL: one
+    all_gather_into_tensor; gloo: the list form)."""
     if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(full, local.contiguous(), group=group)
-    else:  # gloo: list form
-        world = dist.get_world_size(group)
-        parts = list(full.chunk(world, dim=0))
-        dist.all_gather(parts, local.contiguous(), group=group)
+        return dist.all_gather_into_tensor(slab, local, group=group, async_op=async_op)
+    world = dist.get_world_size(group)
+    return dist.all_gather(list(slab.chunk(world, dim=0)), local, group=group, async_op=async_op)
 
 
-def exponentiate_row_sharded(a, power: int, group=None, ops=None):
+def chunk_layout(n: int, world: int, chunks: Optional[int] = None) -> tuple[int, int, int]:
+    """(chunks per rank, rows per chunk, padded n) for the row-sharded chain.
+    Rows per chunk are a multiple of 256 (the CTA-pair tile) when n allows."""
+    if chunks is None:
+        chunks = 4 if n >= 1024 * world else (2 if n >= 512 * world else 1)
+    align = 256 if n >= 256 * world * chunks else 1
+    c = math.ceil(n / (world * chunks * align)) * align
+    return chunks, c, c * world * chunks
+
+
+def exponentiate_row_sharded(a, power: int, group=None, ops=None, chunks: Optional[int] = None):
     """A^power for one n x n matrix with its rows sharded over the group.
 
     `a` is the full base matrix (torch tensor, replicated on every rank, on
@@ -93,8 +117,8 @@ def exponentiate_row_sharded(a, power: int, group=None, ops=None):
         return torch.eye(n, dtype=a.dtype, device=a.device)
     if power == 1:
         return a.clone()
-    rows = padded_rows(n, world)
-    n_p = rows * world
+    ck, c, n_p = chunk_layout(n, world, chunks)
+    slab = world * c
     if ops is None:
         from .engine import default_engine
 
@@ -105,14 +129,21 @@ def exponentiate_row_sharded(a, power: int, group=None, ops=None):
         base = torch.zeros((n_p, n_p), dtype=a.dtype, device=a.device)
         base[:n, :n] = a  # zero padding never mixes into the top-left n x n block
         full = base.clone()
-        local = torch.empty((rows, n_p), dtype=a.dtype, device=a.device)
-        r0 = rank * rows
+        nxt = torch.empty_like(full)
+        local = [torch.empty((c, n_p), dtype=a.dtype, device=a.device) for _ in range(ck)]
         for step in plan.steps:
-            rhs = full if step is Step.SQUARE else base
-            ops.gemm_rows(full[r0:r0 + rows], rhs, local)
-            nxt = torch.empty_like(full)
-            _all_gather_rows(nxt, local, group, dist)
-            full = nxt
+            ops.prepare_rhs(full if step is Step.SQUARE else base)
+            pending = []
+            for j in range(ck):
+                g0 = (j * world + rank) * c  # this rank's chunk j
+                ops.gemm_rows_prepared(full[g0:g0 + c], local[j])
+                # issued behind chunk j on the compute stream; chunk j+1's MMAs
+                # are enqueued right away and overlap the transfer
+                pending.append(_all_gather_slab(nxt[j * slab:(j + 1) * slab], local[j], group, dist,
+                                                async_op=True))
+            for work in pending:
+                work.wait()  # the next step reads every row of P'
+            full, nxt = nxt, full
         return full[:n, :n].contiguous()
 
 

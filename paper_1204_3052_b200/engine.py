@@ -202,6 +202,15 @@ class Engine:
         _lib.check(self._L.mxp_gemm(self._h, mode, n, ctypes.c_void_p(d_a), ctypes.c_void_p(d_b),
                                     ctypes.c_void_p(d_c)), "mxp_gemm")
 
+    def gemm_prepare_rhs_device(self, d_b: int, n: int, mode: int = _lib.MXP_F32) -> None:
+        _lib.check(self._L.mxp_gemm_prepare_rhs(self._h, mode, n, ctypes.c_void_p(d_b)),
+                   "mxp_gemm_prepare_rhs")
+
+    def gemm_rows_prepared_device(self, d_a: int, d_c: int, n: int, rows: int,
+                                  mode: int = _lib.MXP_F32) -> None:
+        _lib.check(self._L.mxp_gemm_rows_prepared(self._h, mode, n, rows, ctypes.c_void_p(d_a),
+                                                  ctypes.c_void_p(d_c)), "mxp_gemm_rows_prepared")
+
     def gemm_rows_device(self, d_a: int, d_b: int, d_c: int, n: int, rows: int,
                          mode: int = _lib.MXP_F32) -> None:
         """C[rows x n] = A[rows x n] * B[n x n] on device (row block of one multiply)."""

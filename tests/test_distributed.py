@@ -30,6 +30,12 @@ class OracleOps:
     def power_batched(self, a, k, out):
         out.copy_(torch.from_numpy(oracle.exponentiate_batched(a.numpy(), k, 1)))
 
+    def prepare_rhs(self, b):
+        self._b = b.numpy().copy()
+
+    def gemm_rows_prepared(self, a_rows, out):
+        self.gemm_rows(a_rows, torch.from_numpy(self._b), out)
+
 
 def _free_port():
     s = socket.socket()
@@ -39,13 +45,13 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, n, k, dtype, q):
+def _worker(rank, world, port, n, k, dtype, q, chunks=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         a = torch.from_numpy(oracle.scaled_input(n, dtype, 42))
-        out = D.exponentiate_row_sharded(a, k, ops=OracleOps())
+        out = D.exponentiate_row_sharded(a, k, ops=OracleOps(), chunks=chunks)
         # batched: 5 matrices sharded unevenly over the ranks
         batch = torch.from_numpy(oracle.scaled_batch(16, 5, np.float32, 7))
         lo, hi = D.shard_range(5, rank, world)
@@ -57,14 +63,16 @@ def _worker(rank, world, port, n, k, dtype, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,k,dtype", [(64, 13, np.float32), (37, 1000, np.float32),
-                                       (48, 257, np.float64), (9, 2, np.float32)])
-def test_row_and_batch_sharding_bitwise(n, k, dtype):
+@pytest.mark.parametrize("n,k,dtype,chunks", [(64, 13, np.float32, None), (37, 1000, np.float32, 3),
+                                              (48, 257, np.float64, 2), (9, 2, np.float32, None),
+                                              (70, 7, np.float32, 4)])
+def test_row_and_batch_sharding_bitwise(n, k, dtype, chunks):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, k, dtype, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, k, dtype, q, chunks))
+             for r in range(world)]
     for p in procs:
         p.start()
     got_rows, got_batch = q.get(timeout=120)
@@ -89,3 +97,7 @@ def test_shard_range_covers_exactly():
             sizes = [e - s for s, e in spans]
             assert max(sizes) - min(sizes) <= 1
     assert D.padded_rows(8192, 8) == 1024 and D.padded_rows(37, 2) == 19
+    # C5 layout: 8 ranks x 4 chunks of 256 rows (CTA-pair tiles), no padding
+    assert D.chunk_layout(8192, 8) == (4, 256, 8192)
+    ck, c, n_p = D.chunk_layout(37, 2, 3)
+    assert ck == 3 and n_p == c * 2 * 3 and n_p >= 37

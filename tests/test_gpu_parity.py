@@ -346,6 +346,32 @@ def test_gemm_rows_bitwise_equals_full_multiply(n, rows):
     assert torch.equal(part, full[r0:])
 
 
+@pytest.mark.parametrize("mode_dt", ["f32", "f64"])
+def test_prepared_rhs_chunks_bitwise_and_invalidation(mode_dt):
+    """mxp_gemm_prepare_rhs once + several mxp_gemm_rows_prepared row chunks ==
+    the full multiply's rows, bitwise; any other workspace use invalidates the
+    prepared right-hand side (validation error, not a silent stale result)."""
+    import torch
+
+    dt = np.float32 if mode_dt == "f32" else np.float64
+    mode = _lib.MXP_F32 if mode_dt == "f32" else _lib.MXP_F64
+    n, c = 1024, 256
+    eng = mx.Engine(0)
+    a = torch.from_numpy(oracle.random_matrix(n, dt, 5)).cuda()
+    b = torch.from_numpy(oracle.random_matrix(n, dt, 6)).cuda()
+    full = torch.empty_like(a)
+    eng.gemm_device(a.data_ptr(), b.data_ptr(), full.data_ptr(), n, mode)
+    eng.gemm_prepare_rhs_device(b.data_ptr(), n, mode)
+    parts = [torch.empty((c, n), dtype=a.dtype, device=a.device) for _ in range(n // c)]
+    for j, part in enumerate(parts):
+        eng.gemm_rows_prepared_device(a[j * c:(j + 1) * c].data_ptr(), part.data_ptr(), n, c, mode)
+    eng.synchronize()
+    assert torch.equal(torch.cat(parts), full)
+    eng.gemm_device(a.data_ptr(), b.data_ptr(), full.data_ptr(), n, mode)  # reuses the workspace
+    with pytest.raises(ValueError):
+        eng.gemm_rows_prepared_device(a.data_ptr(), parts[0].data_ptr(), n, c, mode)
+
+
 def test_row_sharded_chain_single_rank_nccl():
     import os
 
