@@ -17,6 +17,12 @@
 #include "../../include/matexpo_b200.h"
 #include "mxp_internal.h"
 
+// host batched pipeline chunk (MB): small enough that the PCIe fill and drain
+// (one chunk each way) stay short, large enough for a full persistent kernel
+#ifndef MXP_E2E_CHUNK_MB
+#define MXP_E2E_CHUNK_MB 64
+#endif
+
 namespace mxp {
 
 cudaError_t prepare_tf32_kernels();
@@ -807,7 +813,7 @@ int mxp_power_batched(mxp_handle h, int mode, int64_t n, int64_t batch, int64_t 
     const size_t mat = static_cast<size_t>(n) * n * elem_size(mode);
     // Pipeline in chunks: H2D (copy_in) | compute (stream) | D2H (copy_out),
     // double-buffered, so PCIe in both directions overlaps the tensor cores.
-    const size_t chunk_target = size_t(256) << 20;
+    const size_t chunk_target = size_t(MXP_E2E_CHUNK_MB) << 20;
     int64_t chunk = static_cast<int64_t>(chunk_target / mat);
     if (chunk < 1) chunk = 1;
     if (chunk > batch) chunk = batch;
