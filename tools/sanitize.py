@@ -9,9 +9,19 @@ import paper_1204_3052_b200 as mx  # noqa: E402
 
 eng = mx.Engine(0)
 a = oracle.scaled_input(64, np.float32, 42)
-eng.power(a, 13)                                   # K3 (squares + base multiplies)
-mx.exponentiate_batched(mx.scaled_batch(48, 300, mx.DType.F32, 1), 7)   # K3 batched, n < 128
-mx.exponentiate_batched(mx.scaled_batch(37, 5, mx.DType.F32, 1), 5)    # K3, n % 4 != 0 (no TMA)
+eng.power(a, 13)                                   # K3H single chain (squares + base multiplies)
+mx.exponentiate_batched(mx.scaled_batch(48, 300, mx.DType.F32, 1), 7)   # K3H batched, n < 128
+mx.exponentiate_batched(mx.scaled_batch(37, 5, mx.DType.F32, 1), 5)    # K3H, n % 4 != 0
+# K3H TMA IO path: n = 128, several matrices per chain, start-phase skew (batch >= 4 x 148)
+mx.exponentiate_batched(mx.scaled_batch(128, 600, mx.DType.F32, 3), 13)
+mx.exponentiate_batched(mx.scaled_batch(128, 300, mx.DType.F32, 3), 64)
+mx.exponentiate_batched(mx.scaled_batch(128, 300, mx.DType.F32, 3), 1000)  # K3B via the bias guard
+import torch  # noqa: E402
+t = torch.from_numpy(oracle.random_matrix(512, np.float32, 9)).cuda()
+o = torch.empty((128, 512), dtype=t.dtype, device=t.device)
+eng.gemm_prepare_rhs_device(t.data_ptr(), 512)                          # prepared right-hand side
+eng.gemm_rows_prepared_device(t[256:384].data_ptr(), o.data_ptr(), 512, 128)
+eng.synchronize()
 eng.power(oracle.scaled_input(384, np.float32, 42), 13)                 # K1 split-K + reduce
 eng.power(oracle.scaled_input(1024, np.float32, 42), 5)                 # K1P CTA pairs
 eng.power(oracle.scaled_input(256, np.float64, 42), 9)                  # FP64 DMMA
