@@ -124,6 +124,24 @@ MXP_API int mxp_gemm_rows(mxp_handle h, int mode, int64_t n, int64_t rows, const
 MXP_API int mxp_gemm_prepare_rhs(mxp_handle h, int mode, int64_t n, const void* dB);
 MXP_API int mxp_gemm_rows_prepared(mxp_handle h, int mode, int64_t n, int64_t rows,
                                    const void* dA, void* dC);
+/* Fused exchange for the row-sharded chain: the CTA-pair GEMM
+ * epilogue stores its output rows straight into every rank's buffers, tile by
+ * tile, instead of a separate all-gather.  Ranks share buffers through CUDA
+ * IPC handles (72 opaque bytes) and order their steps with a flag barrier in
+ * peer-mapped memory.  MXP_F32 only; n % 256 == 0 and n >= 1024; planes are
+ * tf32 hi/lo n x n (mxp_split_planes).  peer_f32 (or NULL): write fp32 rows
+ * (leading dim n) instead of planes — the chain's last step. */
+#define MXP_IPC_HANDLE_BYTES 72 /* cudaIpcMemHandle_t + byte offset in the allocation */
+MXP_API int mxp_ipc_get_handle(mxp_handle h, const void* dptr, void* handle_out);
+MXP_API int mxp_ipc_open_handle(mxp_handle h, const void* handle, void** dptr);
+MXP_API int mxp_ipc_close_handle(mxp_handle h, void* dptr);
+MXP_API int mxp_split_planes(mxp_handle h, int64_t n, const void* dA, void* d_hi, void* d_lo);
+MXP_API int mxp_gemm_rows_planes_peers(mxp_handle h, int64_t n, int64_t rows, int64_t row0,
+                                       const void* a_hi, const void* a_lo, const void* b_hi,
+                                       const void* b_lo, int npeers, void* const* peer_hi,
+                                       void* const* peer_lo, void* const* peer_f32);
+MXP_API int mxp_peer_barrier(mxp_handle h, int rank, int npeers, void* const* peer_flags,
+                             uint32_t epoch);
 MXP_API int mxp_multiply(mxp_handle h, int mode, int64_t n, const void* hA, const void* hB, void* hC,
                  mxp_stats* stats);
 

@@ -35,7 +35,10 @@ EXPORTS = (
     "mxp_power_device", "mxp_power", "mxp_power_batched_device", "mxp_power_batched",
     "mxp_power_mod_device", "mxp_power_mod", "mxp_random_device", "mxp_last_error",
     "mxp_status_string", "mxp_gemm_prepare_rhs", "mxp_gemm_rows_prepared",
+    "mxp_ipc_get_handle", "mxp_ipc_open_handle", "mxp_ipc_close_handle", "mxp_split_planes",
+    "mxp_gemm_rows_planes_peers", "mxp_peer_barrier",
 )
+MXP_IPC_HANDLE_BYTES = 72
 
 
 class Stats(ctypes.Structure):
@@ -95,6 +98,14 @@ def load() -> ctypes.CDLL:
             "mxp_gemm_rows": [vp, c_int, i64, i64, vp, vp, vp],
             "mxp_gemm_prepare_rhs": [vp, c_int, i64, vp],
             "mxp_gemm_rows_prepared": [vp, c_int, i64, i64, vp, vp],
+            "mxp_ipc_get_handle": [vp, vp, vp],
+            "mxp_ipc_open_handle": [vp, vp, ctypes.POINTER(vp)],
+            "mxp_ipc_close_handle": [vp, vp],
+            "mxp_split_planes": [vp, i64, vp, vp, vp],
+            "mxp_gemm_rows_planes_peers": [vp, i64, i64, i64, vp, vp, vp, vp, c_int,
+                                           ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                           ctypes.POINTER(vp)],
+            "mxp_peer_barrier": [vp, c_int, c_int, ctypes.POINTER(vp), ctypes.c_uint32],
             "mxp_multiply": [vp, c_int, i64, vp, vp, vp, P(Stats)],
             "mxp_power_device": [vp, c_int, i64, i64, vp, vp, P(Stats)],
             "mxp_power": [vp, c_int, i64, i64, vp, vp, P(Stats)],

@@ -702,7 +702,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K1PCfg::kThreads, 1)
     k1p_gemm_3xtf32(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                     const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
                     int n_pad, int m_pad, float* __restrict__ out_f32, int n_out, int m_out,
-                    int ld_out, uint32_t* __restrict__ out_hi, uint32_t* __restrict__ out_lo) {
+                    int ld_out, uint32_t* __restrict__ out_hi, uint32_t* __restrict__ out_lo,
+                    const __grid_constant__ PeerOut po) {
     using Cfg = K1PCfg;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -822,8 +823,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K1PCfg::kThreads, 1)
             if (lane == 0) mbar_arrive_cluster_relaxed(cempty_leader0 + 8 * c);
         }
         const int row = m0 + q * 32 + lane;
+        if (po.n > 0) {
+            // fused exchange: this row segment goes straight to every rank
+            // (its own included) while other tiles are still in their MMAs
+            const size_t grow = static_cast<size_t>(po.row0 + row);
+#pragma unroll 1
+            for (int p = 0; p < po.n; ++p) {
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
+                for (int h = 0; h < 4; ++h) {
+                    const int col = n0 + ch + 32 * h;
+                    const float* v = sum + 32 * h;
+                    if (po.f32[p] != nullptr) {
+                        float4* d = reinterpret_cast<float4*>(po.f32[p] + grow * ld_out + col);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            d[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+                    } else {
+                        uint4* dh = reinterpret_cast<uint4*>(po.hi[p] + grow * n_pad + col);
+                        uint4* dl = reinterpret_cast<uint4*>(po.lo[p] + grow * n_pad + col);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            uint4 hv, lv;
+                            split_tf32(v[4 * u + 0], hv.x, lv.x);
+                            split_tf32(v[4 * u + 1], hv.y, lv.y);
+                            split_tf32(v[4 * u + 2], hv.z, lv.z);
+                            split_tf32(v[4 * u + 3], hv.w, lv.w);
+                            dh[u] = hv;
+                            dl[u] = lv;
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 4 && po.n == 0; ++h) {
             const int col = n0 + ch + 32 * h;
             const float* v = sum + 32 * h;
             if (out_hi != nullptr) {
@@ -1006,6 +1039,50 @@ int k1_split_k(int n_pad, int m_pad, int num_sms) {
     return sk;
 }
 
+cudaError_t launch_k1p_gemm_peers(const GemmPlanes& m, int n_pad, int m_pad, int ld_out,
+                                  const PeerOut& po, cudaStream_t s) {
+    if (n_pad % 256 != 0 || m_pad % 256 != 0 || po.n < 1 || po.n > kMaxPeers)
+        return cudaErrorInvalidValue;
+    dim3 grid(2 * (n_pad / 256) * (m_pad / 256));
+    k1p_gemm_3xtf32<<<grid, K1PCfg::kThreads, K1PCfg::kSmem, s>>>(
+        m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, nullptr, n_pad, m_pad, ld_out, nullptr,
+        nullptr, po);
+    return cudaGetLastError();
+}
+
+namespace {
+struct PeerFlags {
+    uint32_t* f[kMaxPeers];
+};
+__global__ void peer_barrier_kernel(PeerFlags pf, int npeers, int rank, uint32_t epoch) {
+    const int t = threadIdx.x;
+    __threadfence_system();  // this rank's earlier peer stores are performed system-wide
+    __syncthreads();
+    if (t < npeers)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pf.f[t] + rank), "r"(epoch)
+                     : "memory");
+    if (t < npeers) {
+        const uint32_t* mine = pf.f[rank] + t;
+        uint32_t v;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+            if (static_cast<int32_t>(v - epoch) >= 0) break;
+            __nanosleep(200);
+        }
+    }
+    __syncthreads();
+}
+}  // namespace
+
+cudaError_t launch_peer_barrier(uint32_t* const* flags, int npeers, int rank, uint32_t epoch,
+                                cudaStream_t s) {
+    if (npeers < 1 || npeers > kMaxPeers || rank < 0 || rank >= npeers) return cudaErrorInvalidValue;
+    PeerFlags pf{};
+    for (int i = 0; i < npeers; ++i) pf.f[i] = flags[i];
+    peer_barrier_kernel<<<1, 32, 0, s>>>(pf, npeers, rank, epoch);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int block_n,
                                 float* out_f32, int n_out, int m_out, int ld_out, uint32_t* out_hi,
                                 uint32_t* out_lo, cudaStream_t s, float* part, int splits) {
@@ -1027,7 +1104,7 @@ cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int b
         dim3 grid(2 * (n_pad / 256) * (m_pad / 256));
         k1p_gemm_3xtf32<<<grid, K1PCfg::kThreads, K1PCfg::kSmem, s>>>(
             m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, out_f32, n_out, m_out, ld_out, out_hi,
-            out_lo);
+            out_lo, PeerOut{});
         return cudaGetLastError();
     }
     dim3 grid((n_pad / K1Cfg::kBN) * (m_pad / 128), 1);

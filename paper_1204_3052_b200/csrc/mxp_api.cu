@@ -657,6 +657,132 @@ int mxp_gemm_rows_prepared(mxp_handle h, int mode, int64_t n, int64_t rows, cons
     return MXP_OK;
 }
 
+// ---------------------------------------------------------------- fused row-sharded exchange
+// cuMemGetAddressRange through the runtime's driver entry point (the library
+// does not link libcuda directly: it must load on machines without a driver).
+static int alloc_base(const void* p, CUdeviceptr* base) {
+    using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static Fn fn = nullptr;
+    if (fn == nullptr) {
+        void* q = nullptr;
+        cudaDriverEntryPointQueryResult r;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &q, cudaEnableDefault, &r) !=
+                cudaSuccess ||
+            r != cudaDriverEntryPointSuccess)
+            return fail(MXP_E_CUDA, "cuMemGetAddressRange unavailable");
+        fn = reinterpret_cast<Fn>(q);
+    }
+    size_t size = 0;
+    if (fn(base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS)
+        return fail(MXP_E_CUDA, "cuMemGetAddressRange failed");
+    return MXP_OK;
+}
+
+// The exported handle is the CUDA IPC handle of the ALLOCATION that contains
+// dptr plus dptr's byte offset inside it (sub-allocated pointers, e.g. from a
+// caching allocator, map to the allocation base on the other side).
+int mxp_ipc_get_handle(mxp_handle h, const void* dptr, void* handle_out) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (!dptr || !handle_out) return fail(MXP_E_VALIDATION, "null pointer");
+    cudaIpcMemHandle_t ih;
+    MXP_CUDA(cudaIpcGetMemHandle(&ih, const_cast<void*>(dptr)));
+    CUdeviceptr base = 0;
+    rc = alloc_base(dptr, &base);
+    if (rc) return rc;
+    const uint64_t off = reinterpret_cast<uint64_t>(dptr) - static_cast<uint64_t>(base);
+    static_assert(sizeof(ih) + sizeof(off) == MXP_IPC_HANDLE_BYTES, "ipc handle size");
+    std::memcpy(handle_out, &ih, sizeof ih);
+    std::memcpy(static_cast<char*>(handle_out) + sizeof ih, &off, sizeof off);
+    return MXP_OK;
+}
+
+int mxp_ipc_open_handle(mxp_handle h, const void* handle, void** dptr) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (!handle || !dptr) return fail(MXP_E_VALIDATION, "null pointer");
+    cudaIpcMemHandle_t ih;
+    uint64_t off = 0;
+    std::memcpy(&ih, handle, sizeof ih);
+    std::memcpy(&off, static_cast<const char*>(handle) + sizeof ih, sizeof off);
+    void* base = nullptr;
+    MXP_CUDA(cudaIpcOpenMemHandle(&base, ih, cudaIpcMemLazyEnablePeerAccess));
+    *dptr = static_cast<char*>(base) + off;
+    return MXP_OK;
+}
+
+int mxp_ipc_close_handle(mxp_handle h, void* dptr) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    CUdeviceptr base = 0;
+    rc = alloc_base(dptr, &base);
+    if (rc) return rc;
+    MXP_CUDA(cudaIpcCloseMemHandle(reinterpret_cast<void*>(base)));
+    return MXP_OK;
+}
+
+int mxp_split_planes(mxp_handle h, int64_t n, const void* dA, void* d_hi, void* d_lo) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (n < 1) return fail(MXP_E_VALIDATION, "n must be >= 1, got %lld", (long long)n);
+    if (!dA || !d_hi || !d_lo) return fail(MXP_E_VALIDATION, "null device pointer");
+    cudaError_t e = launch_split(static_cast<const float*>(dA), (int)n, (int)n,
+                                 static_cast<uint32_t*>(d_hi), static_cast<uint32_t*>(d_lo),
+                                 (int)round_up(n, 128), h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "split");
+    return MXP_OK;
+}
+
+int mxp_gemm_rows_planes_peers(mxp_handle h, int64_t n, int64_t rows, int64_t row0,
+                               const void* a_hi, const void* a_lo, const void* b_hi,
+                               const void* b_lo, int npeers, void* const* peer_hi,
+                               void* const* peer_lo, void* const* peer_f32) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (n < 1024 || n % 256 != 0)
+        return fail(MXP_E_UNSUPPORTED, "fused exchange needs n %% 256 == 0 and n >= 1024, got %lld",
+                    (long long)n);
+    if (rows < 256 || rows % 256 != 0 || row0 < 0 || row0 % 256 != 0 || row0 + rows > n)
+        return fail(MXP_E_VALIDATION, "row block [%lld, +%lld) must be 256-aligned inside n",
+                    (long long)row0, (long long)rows);
+    if (npeers < 1 || npeers > kMaxPeers)
+        return fail(MXP_E_VALIDATION, "1 <= npeers <= %d, got %d", kMaxPeers, npeers);
+    if (!a_hi || !a_lo || !b_hi || !b_lo) return fail(MXP_E_VALIDATION, "null device pointer");
+    PeerOut po;
+    po.n = npeers;
+    po.row0 = static_cast<int>(row0);
+    for (int i = 0; i < npeers; ++i) {
+        po.f32[i] = peer_f32 ? static_cast<float*>(peer_f32[i]) : nullptr;
+        po.hi[i] = peer_hi ? static_cast<uint32_t*>(peer_hi[i]) : nullptr;
+        po.lo[i] = peer_lo ? static_cast<uint32_t*>(peer_lo[i]) : nullptr;
+        if (!po.f32[i] && (!po.hi[i] || !po.lo[i]))
+            return fail(MXP_E_VALIDATION, "peer %d has no destination", i);
+    }
+    const size_t off = static_cast<size_t>(row0) * n;
+    CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
+    if (!encode_plane_map(&ma_hi, static_cast<const uint32_t*>(a_hi) + off, (int)n, 32, 128, false,
+                          (int)rows) ||
+        !encode_plane_map(&ma_lo, static_cast<const uint32_t*>(a_lo) + off, (int)n, 32, 128, false,
+                          (int)rows) ||
+        !encode_plane_map(&mb_hi, b_hi, (int)n, 32, 32, true) ||
+        !encode_plane_map(&mb_lo, b_lo, (int)n, 32, 32, true))
+        return fail(MXP_E_CUDA, "cuTensorMapEncodeTiled failed");
+    GemmPlanes m{ma_hi, ma_lo, mb_hi, mb_lo};
+    cudaError_t e = launch_k1p_gemm_peers(m, (int)n, (int)rows, (int)n, po, h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "k1p_gemm_3xtf32 (fused exchange)");
+    return MXP_OK;
+}
+
+int mxp_peer_barrier(mxp_handle h, int rank, int npeers, void* const* peer_flags, uint32_t epoch) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (!peer_flags) return fail(MXP_E_VALIDATION, "null flag table");
+    cudaError_t e = launch_peer_barrier(reinterpret_cast<uint32_t* const*>(peer_flags), npeers,
+                                        rank, epoch, h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "peer barrier");
+    return MXP_OK;
+}
+
 int mxp_gemm_rows(mxp_handle h, int mode, int64_t n, int64_t rows, const void* dA, const void* dB,
                   void* dC) {
     int rc = check_handle(h);

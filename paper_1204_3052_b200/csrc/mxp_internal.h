@@ -65,6 +65,24 @@ bool encode_tile_map(CUtensorMap* map, const void* base, int64_t rows);
 bool encode_plane_map(CUtensorMap* map, const void* plane, int n_pad, int box_cols, int box_rows,
                       bool right_operand, int rows = 0);
 int k1_block_n(int n_pad, int num_sms);
+// Fused exchange (row-sharded multi-GPU chain): the CTA-pair kernel's epilogue
+// stores its output rows straight into every rank's buffers (peer / IPC
+// pointers), tile by tile, instead of a separate all-gather.
+constexpr int kMaxPeers = 8;
+struct PeerOut {
+    int n = 0;     // destinations (0: the kernel's ordinary outputs)
+    int row0 = 0;  // global row of this launch's row 0
+    uint32_t* hi[kMaxPeers] = {};
+    uint32_t* lo[kMaxPeers] = {};
+    float* f32[kMaxPeers] = {};  // fp32 rows (leading dim ld_out) instead of planes
+};
+cudaError_t launch_k1p_gemm_peers(const GemmPlanes& maps, int n_pad, int m_pad, int ld_out,
+                                  const PeerOut& po, cudaStream_t s);
+// Cross-process barrier over peer-mapped flag words: rank writes `epoch` into
+// slot [rank] of every peer's flags (release, system scope), then waits until
+// all npeers slots of its own flags reach `epoch` (acquire).
+cudaError_t launch_peer_barrier(uint32_t* const* flags, int npeers, int rank, uint32_t epoch,
+                                cudaStream_t s);
 cudaError_t launch_k1_gemm(const GemmPlanes& maps, int n_pad, int block_n, float* out_f32,
                            int n_out, int ld_out, uint32_t* out_hi, uint32_t* out_lo,
                            cudaStream_t s);

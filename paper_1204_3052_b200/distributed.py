@@ -147,6 +147,101 @@ def exponentiate_row_sharded(a, power: int, group=None, ops=None, chunks: Option
         return full[:n, :n].contiguous()
 
 
+def fused_layout(n: int, world: int) -> tuple[int, int]:
+    """(padded n, rows per rank) for the fused exchange: 256-row CTA-pair row
+    blocks per rank and n_p >= 1024 (the CTA-pair kernel's range)."""
+    n_p = max(1024, math.ceil(n / (256 * world)) * 256 * world)
+    return n_p, n_p // world
+
+
+def exponentiate_row_sharded_fused(a, power: int, group=None, engine=None):
+    """A^power for one n x n FP32 matrix, rows sharded over the group, with the
+    exchange fused into the GEMM: every rank's CTA-pair epilogue stores its
+    new rows (tf32 hi/lo planes; fp32 at the last step) straight into every
+    rank's buffers over NVLink (CUDA IPC mappings), tile by tile, so the
+    transfer overlaps the other tiles' MMAs; a flag barrier in peer memory
+    orders the steps.  No collective library on the data path.  Bitwise equal
+    to the single-GPU chain (same CTA-pair kernel, same per-element order).
+
+    `a` is the full base matrix (torch float32, replicated, on this rank's
+    device).  Returns the full A^power on every rank.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = a.shape[0]
+    if power == 0:
+        return torch.eye(n, dtype=a.dtype, device=a.device)
+    if power == 1:
+        return a.clone()
+    if a.dtype != torch.float32:
+        raise ValueError("the fused exchange runs the FP32 (3xTF32) chain")
+    plan = plan_exponentiation(power)
+    n_p, rows = fused_layout(n, world)
+    if engine is None:
+        from .engine import default_engine
+
+        engine = default_engine(a.device.index or 0)
+    eng = engine
+    dev = a.device
+    stream = torch.cuda.ExternalStream(eng.stream)
+    with torch.cuda.stream(stream):
+        planes = {k: torch.empty((n_p, n_p), dtype=torch.int32, device=dev)
+                  for k in ("base_hi", "base_lo", "p0_hi", "p0_lo", "p1_hi", "p1_lo")}
+        out = torch.empty((n_p, n_p), dtype=torch.float32, device=dev)
+        flags = torch.zeros(world, dtype=torch.int32, device=dev)
+        base = torch.zeros((n_p, n_p), dtype=torch.float32, device=dev)
+        base[:n, :n] = a  # zero padding never mixes into the top-left n x n block
+        eng.split_planes_device(base.data_ptr(), planes["base_hi"].data_ptr(),
+                                planes["base_lo"].data_ptr(), n_p)
+        planes["p0_hi"].copy_(planes["base_hi"])
+        planes["p0_lo"].copy_(planes["base_lo"])
+    torch.cuda.current_stream(dev).synchronize()
+    eng.synchronize()
+    # every rank maps every other rank's exchange buffers (its own: the local pointer)
+    shared = ("p0_hi", "p0_lo", "p1_hi", "p1_lo", "out", "flags")
+    local = {k: (planes[k] if k in planes else (out if k == "out" else flags)).data_ptr()
+             for k in shared}
+    mine = {k: eng.ipc_get_handle(local[k]) for k in shared}
+    everyone = [None] * world
+    dist.all_gather_object(everyone, mine, group=group)
+    opened = []
+    peer = {k: [] for k in shared}
+    for r in range(world):
+        for k in shared:
+            if r == rank:
+                peer[k].append(local[k])
+            else:
+                ptr = eng.ipc_open_handle(everyone[r][k])
+                opened.append(ptr)
+                peer[k].append(ptr)
+    dist.barrier(group=group)  # every rank's buffers exist and are mapped
+    try:
+        cur, nxt = "p0", "p1"
+        r0 = rank * rows
+        for s, step in enumerate(plan.steps):
+            last = s == len(plan.steps) - 1
+            b_hi, b_lo = ((local[cur + "_hi"], local[cur + "_lo"]) if step is Step.SQUARE
+                          else (planes["base_hi"].data_ptr(), planes["base_lo"].data_ptr()))
+            eng.gemm_rows_planes_peers(
+                n_p, rows, r0, local[cur + "_hi"], local[cur + "_lo"], b_hi, b_lo,
+                None if last else peer[nxt + "_hi"], None if last else peer[nxt + "_lo"],
+                peer["out"] if last else None)
+            # all ranks' rows have landed everywhere (and nobody still reads
+            # the buffer the next step overwrites) before anyone goes on
+            eng.peer_barrier(rank, peer["flags"], s + 1)
+            cur, nxt = nxt, cur
+        eng.synchronize()
+        result = out[:n, :n].clone()
+    finally:
+        dist.barrier(group=group)  # nobody closes a mapping a peer still writes through
+        for ptr in opened:
+            eng.ipc_close_handle(ptr)
+    return result
+
+
 def exponentiate_batched_sharded(a_local, power: int, ops=None):
     """A_i^power for this rank's shard (independent matrices, no collective)."""
     import torch

@@ -211,6 +211,46 @@ class Engine:
         _lib.check(self._L.mxp_gemm_rows_prepared(self._h, mode, n, rows, ctypes.c_void_p(d_a),
                                                   ctypes.c_void_p(d_c)), "mxp_gemm_rows_prepared")
 
+    # ------------------------------------------------------------ fused row-sharded exchange
+    def ipc_get_handle(self, d_ptr: int) -> bytes:
+        buf = ctypes.create_string_buffer(_lib.MXP_IPC_HANDLE_BYTES)
+        _lib.check(self._L.mxp_ipc_get_handle(self._h, ctypes.c_void_p(d_ptr), buf),
+                   "mxp_ipc_get_handle")
+        return buf.raw
+
+    def ipc_open_handle(self, handle: bytes) -> int:
+        out = ctypes.c_void_p()
+        _lib.check(self._L.mxp_ipc_open_handle(self._h, handle, ctypes.byref(out)),
+                   "mxp_ipc_open_handle")
+        return out.value
+
+    def ipc_close_handle(self, d_ptr: int) -> None:
+        _lib.check(self._L.mxp_ipc_close_handle(self._h, ctypes.c_void_p(d_ptr)),
+                   "mxp_ipc_close_handle")
+
+    def split_planes_device(self, d_a: int, d_hi: int, d_lo: int, n: int) -> None:
+        _lib.check(self._L.mxp_split_planes(self._h, n, ctypes.c_void_p(d_a), ctypes.c_void_p(d_hi),
+                                            ctypes.c_void_p(d_lo)), "mxp_split_planes")
+
+    @staticmethod
+    def _ptr_array(ptrs):
+        if ptrs is None:
+            return None
+        return (ctypes.c_void_p * len(ptrs))(*[ctypes.c_void_p(p) for p in ptrs])
+
+    def gemm_rows_planes_peers(self, n: int, rows: int, row0: int, a_hi: int, a_lo: int,
+                               b_hi: int, b_lo: int, peer_hi, peer_lo, peer_f32=None) -> None:
+        npeers = len(peer_f32 if peer_f32 is not None else peer_hi)
+        _lib.check(self._L.mxp_gemm_rows_planes_peers(
+            self._h, n, rows, row0, ctypes.c_void_p(a_hi), ctypes.c_void_p(a_lo),
+            ctypes.c_void_p(b_hi), ctypes.c_void_p(b_lo), npeers, self._ptr_array(peer_hi),
+            self._ptr_array(peer_lo), self._ptr_array(peer_f32)), "mxp_gemm_rows_planes_peers")
+
+    def peer_barrier(self, rank: int, peer_flags, epoch: int) -> None:
+        _lib.check(self._L.mxp_peer_barrier(self._h, rank, len(peer_flags),
+                                            self._ptr_array(peer_flags), epoch & 0xFFFFFFFF),
+                   "mxp_peer_barrier")
+
     def gemm_rows_device(self, d_a: int, d_b: int, d_c: int, n: int, rows: int,
                          mode: int = _lib.MXP_F32) -> None:
         """C[rows x n] = A[rows x n] * B[n x n] on device (row block of one multiply)."""

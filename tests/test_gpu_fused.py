@@ -1,0 +1,79 @@
+"""Fused row-sharded exchange (CTA-pair epilogue stores into every rank's
+buffers over CUDA IPC, flag barrier in peer memory) — two ranks sharing one
+B200 (the box has one GPU): the IPC mappings, peer stores, row offsets and the
+cross-process barrier are exercised exactly as across GPUs.  The result must be
+BITWISE the single-GPU chain."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n, ks, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    import paper_1204_3052_b200 as mx
+    from paper_1204_3052_b200 import distributed as D
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        eng = mx.Engine(0)
+        a_np = oracle.scaled_input(n, np.float32, 42)
+        a = torch.from_numpy(a_np).cuda()
+        res = {}
+        for k in ks:
+            got = D.exponentiate_row_sharded_fused(a, k, engine=eng).cpu().numpy()
+            res[k] = (got.tobytes(), eng.power(a_np, k).tobytes() if rank == 0 else None)
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_fused_exchange_two_ranks_one_gpu_bitwise():
+    import torch.multiprocessing as mp
+
+    world, n, ks = 2, 1024, (16, 13)  # 13: plan with MULTIPLY_BASE steps
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, ks, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for k in ks:
+        single = results[0][k][1]
+        for r in range(world):
+            assert results[r][k][0] == single, (k, r)
+    ref = oracle.exponentiate(oracle.scaled_input(n, np.float32, 42), 13)
+    got = np.frombuffer(results[1][13][0], dtype=np.float32).reshape(n, n)
+    assert oracle.compare(got, ref)[2] <= 16 * 5 * np.sqrt(n) * 2.0 ** -24
+
+
+def test_fused_layout():
+    from paper_1204_3052_b200 import distributed as D
+
+    assert D.fused_layout(8192, 8) == (8192, 1024)
+    assert D.fused_layout(1000, 2) == (1024, 512)
+    n_p, rows = D.fused_layout(3000, 4)
+    assert rows % 256 == 0 and n_p == 4 * rows and n_p >= 3000
