@@ -154,92 +154,122 @@ def fused_layout(n: int, world: int) -> tuple[int, int]:
     return n_p, n_p // world
 
 
-def exponentiate_row_sharded_fused(a, power: int, group=None, engine=None):
-    """A^power for one n x n FP32 matrix, rows sharded over the group, with the
-    exchange fused into the GEMM: every rank's CTA-pair epilogue stores its
-    new rows (tf32 hi/lo planes; fp32 at the last step) straight into every
-    rank's buffers over NVLink (CUDA IPC mappings), tile by tile, so the
-    transfer overlaps the other tiles' MMAs; a flag barrier in peer memory
-    orders the steps.  No collective library on the data path.  Bitwise equal
-    to the single-GPU chain (same CTA-pair kernel, same per-element order).
+class RowShardedFused:
+    """The fused row-sharded chain for one n x n FP32 matrix shape on a group:
+    every rank's CTA-pair epilogue stores its new rows (tf32 hi/lo planes; fp32
+    at the last step) straight into every rank's buffers over NVLink (CUDA IPC
+    mappings), tile by tile, so the transfer overlaps the other tiles' MMAs; a
+    flag barrier in peer memory orders the steps.  No collective library on
+    the data path.  Bitwise equal to the single-GPU chain (same CTA-pair
+    kernel, same per-element order).  Buffers and peer mappings are set up
+    once (collective over the group) and reused by every ``power`` call;
+    ``close`` (also collective) unmaps them."""
 
-    `a` is the full base matrix (torch float32, replicated, on this rank's
-    device).  Returns the full A^power on every rank.
-    """
-    import torch
-    import torch.distributed as dist
+    _SHARED = ("p0_hi", "p0_lo", "p1_hi", "p1_lo", "out", "flags")
 
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    n = a.shape[0]
-    if power == 0:
-        return torch.eye(n, dtype=a.dtype, device=a.device)
-    if power == 1:
-        return a.clone()
-    if a.dtype != torch.float32:
-        raise ValueError("the fused exchange runs the FP32 (3xTF32) chain")
-    plan = plan_exponentiation(power)
-    n_p, rows = fused_layout(n, world)
-    if engine is None:
-        from .engine import default_engine
+    def __init__(self, n: int, device, group=None, engine=None):
+        import torch
+        import torch.distributed as dist
 
-        engine = default_engine(a.device.index or 0)
-    eng = engine
-    dev = a.device
-    stream = torch.cuda.ExternalStream(eng.stream)
-    with torch.cuda.stream(stream):
-        planes = {k: torch.empty((n_p, n_p), dtype=torch.int32, device=dev)
-                  for k in ("base_hi", "base_lo", "p0_hi", "p0_lo", "p1_hi", "p1_lo")}
-        out = torch.empty((n_p, n_p), dtype=torch.float32, device=dev)
-        flags = torch.zeros(world, dtype=torch.int32, device=dev)
-        base = torch.zeros((n_p, n_p), dtype=torch.float32, device=dev)
-        base[:n, :n] = a  # zero padding never mixes into the top-left n x n block
-        eng.split_planes_device(base.data_ptr(), planes["base_hi"].data_ptr(),
-                                planes["base_lo"].data_ptr(), n_p)
-        planes["p0_hi"].copy_(planes["base_hi"])
-        planes["p0_lo"].copy_(planes["base_lo"])
-    torch.cuda.current_stream(dev).synchronize()
-    eng.synchronize()
-    # every rank maps every other rank's exchange buffers (its own: the local pointer)
-    shared = ("p0_hi", "p0_lo", "p1_hi", "p1_lo", "out", "flags")
-    local = {k: (planes[k] if k in planes else (out if k == "out" else flags)).data_ptr()
-             for k in shared}
-    mine = {k: eng.ipc_get_handle(local[k]) for k in shared}
-    everyone = [None] * world
-    dist.all_gather_object(everyone, mine, group=group)
-    opened = []
-    peer = {k: [] for k in shared}
-    for r in range(world):
-        for k in shared:
-            if r == rank:
-                peer[k].append(local[k])
-            else:
-                ptr = eng.ipc_open_handle(everyone[r][k])
-                opened.append(ptr)
-                peer[k].append(ptr)
-    dist.barrier(group=group)  # every rank's buffers exist and are mapped
-    try:
+        self.dist, self.group = dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.n = n
+        self.n_p, self.rows = fused_layout(n, self.world)
+        if engine is None:
+            from .engine import default_engine
+
+            engine = default_engine(torch.device(device).index or 0)
+        self.eng = engine
+        n_p = self.n_p
+        self.buf = {k: torch.empty((n_p, n_p), dtype=torch.int32, device=device)
+                    for k in ("base_hi", "base_lo", "p0_hi", "p0_lo", "p1_hi", "p1_lo")}
+        self.buf["out"] = torch.empty((n_p, n_p), dtype=torch.float32, device=device)
+        self.buf["flags"] = torch.zeros(self.world, dtype=torch.int32, device=device)
+        self.base = torch.zeros((n_p, n_p), dtype=torch.float32, device=device)
+        torch.cuda.synchronize(device)
+        self.local = {k: self.buf[k].data_ptr() for k in self._SHARED}
+        mine = {k: self.eng.ipc_get_handle(self.local[k]) for k in self._SHARED}
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=group)
+        self.opened = []
+        self.peer = {k: [] for k in self._SHARED}
+        for r in range(self.world):
+            for k in self._SHARED:
+                if r == self.rank:
+                    self.peer[k].append(self.local[k])
+                else:
+                    ptr = self.eng.ipc_open_handle(everyone[r][k])
+                    self.opened.append(ptr)
+                    self.peer[k].append(ptr)
+        self.epoch = 0
+        dist.barrier(group=group)  # every rank's buffers exist and are mapped
+
+    def power(self, a, power: int):
+        """A^power (a: n x n float32 on this rank's device, replicated); the full
+        result on every rank.  Collective: every rank calls it with the same power."""
+        import torch
+
+        n, n_p, rows, eng = self.n, self.n_p, self.rows, self.eng
+        if power == 0:
+            return torch.eye(n, dtype=a.dtype, device=a.device)
+        if power == 1:
+            return a.clone()
+        plan = plan_exponentiation(power)
+        b = self.buf
+        with torch.cuda.stream(torch.cuda.ExternalStream(eng.stream)):
+            self.base[:n, :n] = a  # zero padding never mixes into the top-left n x n block
+        eng.split_planes_device(self.base.data_ptr(), b["base_hi"].data_ptr(),
+                                b["base_lo"].data_ptr(), n_p)
+        eng.split_planes_device(self.base.data_ptr(), b["p0_hi"].data_ptr(),
+                                b["p0_lo"].data_ptr(), n_p)
         cur, nxt = "p0", "p1"
-        r0 = rank * rows
+        r0 = self.rank * rows
         for s, step in enumerate(plan.steps):
             last = s == len(plan.steps) - 1
-            b_hi, b_lo = ((local[cur + "_hi"], local[cur + "_lo"]) if step is Step.SQUARE
-                          else (planes["base_hi"].data_ptr(), planes["base_lo"].data_ptr()))
+            if step is Step.SQUARE:
+                b_hi, b_lo = self.local[cur + "_hi"], self.local[cur + "_lo"]
+            else:
+                b_hi, b_lo = b["base_hi"].data_ptr(), b["base_lo"].data_ptr()
             eng.gemm_rows_planes_peers(
-                n_p, rows, r0, local[cur + "_hi"], local[cur + "_lo"], b_hi, b_lo,
-                None if last else peer[nxt + "_hi"], None if last else peer[nxt + "_lo"],
-                peer["out"] if last else None)
-            # all ranks' rows have landed everywhere (and nobody still reads
-            # the buffer the next step overwrites) before anyone goes on
-            eng.peer_barrier(rank, peer["flags"], s + 1)
+                n_p, rows, r0, self.local[cur + "_hi"], self.local[cur + "_lo"], b_hi, b_lo,
+                None if last else self.peer[nxt + "_hi"], None if last else self.peer[nxt + "_lo"],
+                self.peer["out"] if last else None)
+            # all ranks' rows have landed everywhere (and nobody still reads the
+            # buffer the next step overwrites) before anyone goes on
+            self.epoch += 1
+            eng.peer_barrier(self.rank, self.peer["flags"], self.epoch)
             cur, nxt = nxt, cur
+        out = torch.empty((n, n), dtype=a.dtype, device=a.device)
+        with torch.cuda.stream(torch.cuda.ExternalStream(eng.stream)):
+            out.copy_(b["out"][:n, :n])
         eng.synchronize()
-        result = out[:n, :n].clone()
+        return out
+
+    def close(self):
+        self.eng.synchronize()
+        self.dist.barrier(group=self.group)  # nobody unmaps what a peer still writes through
+        for ptr in self.opened:
+            self.eng.ipc_close_handle(ptr)
+        self.opened = []
+
+
+def exponentiate_row_sharded_fused(a, power: int, group=None, engine=None):
+    """A^power for one n x n FP32 matrix with its rows sharded over the group and
+    the exchange fused into the GEMM epilogue (see RowShardedFused).  `a` is
+    the full base matrix (replicated, on this rank's device); the full A^power
+    is returned on every rank."""
+    import torch
+
+    if a.dtype != torch.float32:
+        raise ValueError("the fused exchange runs the FP32 (3xTF32) chain")
+    if power in (0, 1):
+        return torch.eye(a.shape[0], dtype=a.dtype, device=a.device) if power == 0 else a.clone()
+    ctx = RowShardedFused(a.shape[0], a.device, group=group, engine=engine)
+    try:
+        return ctx.power(a, power)
     finally:
-        dist.barrier(group=group)  # nobody closes a mapping a peer still writes through
-        for ptr in opened:
-            eng.ipc_close_handle(ptr)
-    return result
+        ctx.close()
 
 
 def exponentiate_batched_sharded(a_local, power: int, ops=None):
