@@ -13,7 +13,12 @@ int main(int argc, char** argv) {
     float *din, *dout; long long* tr;
     cudaMalloc(&din, B * n * n * 4); cudaMalloc(&dout, B * n * n * 4);
     cudaMalloc(&tr, 16 * 8); cudaMemset(tr, 0, 16 * 8);
-    cudaMemset(din, 0, B * n * n * 4);
+    {  // random inputs (zeros would take the exact-scale path every step)
+        std::vector<float> hbuf(static_cast<size_t>(B) * n * n);
+        uint32_t x = 12345u;
+        for (auto& v : hbuf) { x = x * 1664525u + 1013904223u; v = (static_cast<float>(x >> 8) / 16777216.0f - 0.5f) * 0.306f; }
+        cudaMemcpy(din, hbuf.data(), hbuf.size() * 4, cudaMemcpyHostToDevice);
+    }
     cudaMemcpyToSymbol(g_k3h_trace, &tr, sizeof(tr));
     prepare_k3h_kernel();
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
