@@ -580,8 +580,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float v[32];
                     tmem_ld32(lane_base + C * 256u + col0, reinterpret_cast<uint32_t(&)[32]>(v));
                     const float f1 = exp2i(pe / 2), f2 = exp2i(pe - pe / 2);
+                    const uint64_t g1 = splat2(f1), g2 = splat2(f2);
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], f1), f2);
+                    for (int i = 0; i < 32; i += 2) {  // two exact-range steps, packed
+                        uint64_t w;
+                        asm("mov.b64 %0, {%1, %2};" : "=l"(w) : "f"(v[i]), "f"(v[i + 1]));
+                        asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(w) : "l"(g1));
+                        asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(w) : "l"(g2));
+                        asm("mov.b64 {%0, %1}, %2;" : "=f"(v[i]), "=f"(v[i + 1]) : "l"(w));
+                    }
                     if (vec) {
                         if (outs > 0) mbar_wait_sleep(r_free, (outs - 1u) & 1u);
                         ++outs;
@@ -611,12 +618,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // < 2^14 (no fp16 overflow).  A product that cancels strongly
                 // against its bound would land low in fp16's range and lose
                 // bits of h1, so the exact path (block max, one barrier) runs
-                // for the first product of every matrix and whenever the
-                // previous product came out more than 2^12 below its bound.
+                // whenever the previous product came out more than 2^12 below
+                // its bound (the input's exact max feeds the first step's bound).
                 const bool was_mult = plan_is_mult(plan, st.s);
                 const uint32_t mprev = slots_max(C, st);
                 const int pmax_e = ilogb_bits(mprev) + st.t_prev;  // floor(log2 max|P'_s|)
-                const bool exact = st.s == 0 || pmax_e < kCeil - 12;
+                const bool exact = pmax_e < kCeil - 12;
                 const int xmax_e = was_mult ? st.bmax_e : pmax_e;
                 int t = kCeil - static_cast<int>(lg_n) - (xmax_e + 1) - (pmax_e + 1);
                 if (mprev == 0u || mprev >= 0x7F800000u) t = 0;  // zero / non-finite operand
