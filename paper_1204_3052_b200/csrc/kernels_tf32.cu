@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
                    const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
                    int n_pad, int m_pad, float* __restrict__ out_f32, int n_out, int m_out,
                    int ld_out, uint32_t* __restrict__ out_hi, uint32_t* __restrict__ out_lo,
-                   float* __restrict__ part) {
+                   float* __restrict__ part, int dsmem_reduce) {
     using Cfg = K1Cfg;
     constexpr int S = Cfg::kStages;
     constexpr int BN = Cfg::kBN;
@@ -634,6 +634,19 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
         for (int h = 0; h < 2; ++h) {
             const int col = n0 + ch + 32 * h;
             const float* v = sum + 32 * h;
+            if (dsmem_reduce) {  // split-K partial -> this CTA's SMEM (stage buffers are free:
+                                 // every MMA has completed), reduced across the cluster below
+                const uint32_t rr = static_cast<uint32_t>(q * 32 + lane);
+                const uint32_t base = smem_u32(smem) + rr * 512u;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t uu = static_cast<uint32_t>((ch + 32 * h) / 4 + u);
+                    sts128(base + ((uu ^ (rr & 7u)) << 4), __float_as_uint(v[4 * u]),
+                           __float_as_uint(v[4 * u + 1]), __float_as_uint(v[4 * u + 2]),
+                           __float_as_uint(v[4 * u + 3]));
+                }
+                continue;
+            }
             if (part != nullptr) {  // split-K partial, reduced by splitk_reduce_kernel
                 float4* d = reinterpret_cast<float4*>(
                     part + (static_cast<size_t>(blockIdx.y) * m_pad + row) * n_pad + col);
@@ -671,7 +684,49 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
         }
     }
     tc_fence_before();
-    __syncthreads();
+    __syncwarp();
+    if (dsmem_reduce) {
+        // Split-K reduction over the cluster (the gridDim.y CTAs of this tile):
+        // CTA r sums rows [r R, (r + 1) R) of the S partials, read from every
+        // CTA's SMEM in split order with round-to-nearest adds — the order
+        // and arithmetic of splitk_reduce_kernel, so results are bitwise the
+        // same — and writes the next step's planes / the fp32 result.
+        cluster_sync_all();  // every partial is in SMEM (release / acquire)
+        const uint32_t S_ = gridDim.y, r = cluster_ctarank();
+        const uint32_t R = 128u / S_;
+        const uint32_t s0 = smem_u32(smem);
+        for (uint32_t i = threadIdx.x; i < R * 32u; i += blockDim.x) {
+            const uint32_t rr = r * R + (i >> 5), u = i & 31u;
+            const uint32_t la = s0 + rr * 512u + ((u ^ (rr & 7u)) << 4);
+            float4 a = ld_dsmem_f4(mapa_shared(la, 0));
+            for (uint32_t p = 1; p < S_; ++p) {
+                const float4 b = ld_dsmem_f4(mapa_shared(la, p));
+                a.x = __fadd_rn(a.x, b.x);
+                a.y = __fadd_rn(a.y, b.y);
+                a.z = __fadd_rn(a.z, b.z);
+                a.w = __fadd_rn(a.w, b.w);
+            }
+            const int grow = m0 + static_cast<int>(rr), col = n0 + static_cast<int>(4u * u);
+            if (out_hi != nullptr) {
+                uint4 hv, lv;
+                split_tf32(a.x, hv.x, lv.x);
+                split_tf32(a.y, hv.y, lv.y);
+                split_tf32(a.z, hv.z, lv.z);
+                split_tf32(a.w, hv.w, lv.w);
+                *reinterpret_cast<uint4*>(out_hi + static_cast<size_t>(grow) * n_pad + col) = hv;
+                *reinterpret_cast<uint4*>(out_lo + static_cast<size_t>(grow) * n_pad + col) = lv;
+            }
+            if (out_f32 != nullptr && grow < m_out) {
+                const float vv[4] = {a.x, a.y, a.z, a.w};
+                float* d = out_f32 + static_cast<size_t>(grow) * ld_out;
+                for (int k = 0; k < 4; ++k)
+                    if (col + k < n_out) d[col + k] = vv[k];
+            }
+        }
+        cluster_sync_all();  // peers are done reading this CTA's SMEM
+    } else {
+        __syncthreads();
+    }
     if (warp == 2) tmem_dealloc<256>(tmem);
 }
 
@@ -1029,13 +1084,60 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits,
     }
 }
 
+// MXP_SPLITK=global: the two-launch split-K (partials through HBM/L2 and
+// splitk_reduce_kernel) instead of the cluster/DSMEM reduction (A/B runs).
+bool k1_split_legacy() {
+    static const int v = [] {
+        const char* e = std::getenv("MXP_SPLITK");
+        return (e != nullptr && std::strcmp(e, "global") == 0) ? 1 : 0;
+    }();
+    return v != 0;
+}
+int k1_split_launches(int splits) { return (splits > 1 && k1_split_legacy()) ? 2 : 1; }
+
+// Clusters of cs K1 CTAs that can be resident at once (one CTA per SM; a
+// cluster must fit in one GPC): 148 / 74 / 33 / 15 for cs = 1 / 2 / 4 / 8 on
+// a B200.  Cached per cluster size.
+static int k1_max_clusters(int cs) {
+    static int cache[9] = {0};
+    if (cs < 1 || cs > 8) return 0;
+    if (cache[cs] == 0) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(1, static_cast<unsigned>(cs));
+        cfg.blockDim = dim3(K1Cfg::kThreads);
+        cfg.dynamicSmemBytes = K1Cfg::kSmem;
+        cudaLaunchAttribute a[1];
+        a[0].id = cudaLaunchAttributeClusterDimension;
+        a[0].val.clusterDim.x = 1;
+        a[0].val.clusterDim.y = static_cast<unsigned>(cs);
+        a[0].val.clusterDim.z = 1;
+        cfg.attrs = a;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k1_gemm_3xtf32, &cfg) != cudaSuccess || n < 1) {
+            cudaGetLastError();
+            n = -1;
+        }
+        cache[cs] = n;
+    }
+    return cache[cs];
+}
+
 // k-splits for the 1-CTA kernel: enough CTAs to cover the SMs for small n,
-// at least 2 k-blocks (64 k) per split.
+// at least 2 k-blocks (64 k) per split, and (cluster reduction) every
+// tile's cluster of splits resident in one wave.  The same split is used by
+// every path of a given n (chain, single multiply, row blocks), so their
+// results agree bitwise.
 int k1_split_k(int n_pad, int m_pad, int num_sms) {
     const int tiles = (n_pad / 128) * (m_pad / 128);
     const int kb = n_pad / 32;
     int sk = 1;
-    while (tiles * sk * 2 <= num_sms && (kb % (sk * 2)) == 0 && kb / (sk * 2) >= 2) sk *= 2;
+    for (;;) {
+        const int nx = 2 * sk;
+        if (nx > 8 || tiles * nx > num_sms || kb % nx != 0 || kb / nx < 2) break;
+        if (!k1_split_legacy() && tiles > k1_max_clusters(nx)) break;
+        sk = nx;
+    }
     return sk;
 }
 
@@ -1086,11 +1188,30 @@ cudaError_t launch_peer_barrier(uint32_t* const* flags, int npeers, int rank, ui
 cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int block_n,
                                 float* out_f32, int n_out, int m_out, int ld_out, uint32_t* out_hi,
                                 uint32_t* out_lo, cudaStream_t s, float* part, int splits) {
+    if (block_n == 128 && splits > 1 && !k1_split_legacy()) {
+        // split-K in one launch: the splits of a tile form a cluster and
+        // reduce through distributed shared memory
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((n_pad / K1Cfg::kBN) * (m_pad / 128), splits);
+        cfg.blockDim = dim3(K1Cfg::kThreads);
+        cfg.dynamicSmemBytes = K1Cfg::kSmem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1;
+        attr[0].val.clusterDim.y = static_cast<unsigned>(splits);
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, k1_gemm_3xtf32, m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad,
+                                  out_f32, n_out, m_out, ld_out, out_hi, out_lo,
+                                  static_cast<float*>(nullptr), 1);
+    }
     if (block_n == 128 && splits > 1 && part != nullptr) {
         dim3 grid((n_pad / K1Cfg::kBN) * (m_pad / 128), splits);
         k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(
             m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, nullptr, n_out, m_out, ld_out, nullptr,
-            nullptr, part);
+            nullptr, part, 0);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         const size_t quads = static_cast<size_t>(m_pad) * n_pad / 4;
@@ -1110,7 +1231,7 @@ cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int b
     dim3 grid((n_pad / K1Cfg::kBN) * (m_pad / 128), 1);
     k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(
         m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo,
-        nullptr);
+        nullptr, 0);
     return cudaGetLastError();
 }
 

@@ -252,7 +252,7 @@ int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float
             *failed = s;
             return cuda_fail(e, "k1_gemm_3xtf32");
         }
-        *launches += (bn == 128 && h->splits > 1) ? 2 : 1;
+        *launches += (bn == 128) ? k1_split_launches(h->splits) : 1;
         acc = dst;
     }
     return MXP_OK;
