@@ -1021,6 +1021,8 @@ int k1_block_n(int n_pad, int num_sms) {
     return (n_pad % 256 == 0 && n_pad >= 1024) ? 256 : K1Cfg::kBN;
 }
 
+static cudaError_t prepare_k1c();  // (after the K1C kernel)
+
 cudaError_t prepare_tf32_kernels() {
     cudaError_t e = cudaFuncSetAttribute(k3_batched_power<false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1031,6 +1033,7 @@ cudaError_t prepare_tf32_kernels() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k1_gemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(K1Cfg::kSmem));
+    if (e == cudaSuccess) e = prepare_k1c();
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k1p_gemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(K1PCfg::kSmem));
@@ -1139,6 +1142,268 @@ int k1_split_k(int n_pad, int m_pad, int num_sms) {
         sk = nx;
     }
     return sk;
+}
+
+// ======================================================================
+// K1C — a whole 3xTF32 chain in ONE launch for the K1 sizes whose split-K
+// clusters are all resident at once (n_pad <= 896: C2's 512^2 A^1000).
+// The grid is K1's split-K grid (tiles x splits, a cluster per tile); each
+// CTA runs K1's pipeline for every plan step, reduces through DSMEM, writes
+// the next step's planes, and meets the other CTAs at a grid barrier
+// instead of a kernel boundary.  Per step: the same MMAs, split and reduction
+// order as a K1 launch, so the results are bitwise the per-step chain's.
+// Launched cooperatively (co-residency guaranteed, or the launch fails and
+// the caller runs the per-step chain).
+// ======================================================================
+struct K1CMaps {
+    CUtensorMap a[6];  // plane pairs 0 base, 1 ping, 2 pong as left operands
+    CUtensorMap b[6];  //                               as right operands
+};
+struct K1CPlanes {
+    uint32_t* p[6];
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();  // this CTA's plane stores are visible GPU-wide
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+        unsigned int v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (v >= target) break;
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(K1Cfg::kThreads, 1)
+    k1c_chain_3xtf32(const __grid_constant__ K1CMaps maps, const __grid_constant__ K1CPlanes pl,
+                     PlanBits plan, int n_pad, float* __restrict__ out_f32, int n_out,
+                     unsigned int* __restrict__ bar_ctr) {
+    using Cfg = K1Cfg;
+    constexpr int S = Cfg::kStages;
+    constexpr int BN = Cfg::kBN;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+    uint64_t* empty = full + S;
+    uint64_t* cfull = empty + S;
+    uint64_t* cempty = cfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    // tile and k-range as K1's split-K grid (num_m = num_n = n_pad / 128)
+    constexpr int kGroupM = 16;
+    const int num_m = n_pad / 128, num_n = n_pad / BN;
+    const int pid = blockIdx.x;
+    const int per_group = kGroupM * num_n;
+    const int first_m = (pid / per_group) * kGroupM;
+    const int gm = min(num_m - first_m, kGroupM);
+    const int m0 = (first_m + (pid % per_group) % gm) * 128;
+    const int n0 = ((pid % per_group) / gm) * BN;
+    const int kb_per = (n_pad / 32) / static_cast<int>(gridDim.y);
+    const int kb0 = static_cast<int>(blockIdx.y) * kb_per;
+    const unsigned int nctas = gridDim.x * gridDim.y;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&cfull[i], 1);
+            mbar_init(&cempty[i], 8);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc<256>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t s0 = smem_u32(smem);
+
+    int acc = 0;  // plane pair holding the running power: 0 base, 1 ping, 2 pong
+    for (int step = 0; step < plan.len; ++step) {
+        const bool mult = plan_is_mult(plan, step);
+        const bool last = step == plan.len - 1;
+        const int dst = (acc == 1) ? 2 : 1;
+        const int rhs = mult ? 0 : acc;
+        const int g0 = step * kb_per;  // pipeline position of this step's first k-block
+        if (warp == 0 && lane == 0) {
+            // the planes this step reads were written by other CTAs' generic
+            // stores before the grid barrier: order them before TMA (async proxy)
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const CUtensorMap* ah = &maps.a[2 * acc];
+            const CUtensorMap* al = &maps.a[2 * acc + 1];
+            const CUtensorMap* bh_m = &maps.b[2 * rhs];
+            const CUtensorMap* bl_m = &maps.b[2 * rhs + 1];
+            for (int kb = 0; kb < kb_per; ++kb) {
+                const int g = g0 + kb;
+                const int st = g % S;
+                const uint32_t ph = (g / S) & 1;
+                mbar_wait(&empty[st], ph ^ 1);
+                uint8_t* base = smem + st * Cfg::kStageBytes;
+                mbar_expect_tx(&full[st], Cfg::kStageBytes);
+                const int kg = kb0 + kb;
+                tma_load_2d(base, ah, &full[st], kg * 32, m0);
+                tma_load_2d(base + Cfg::kABytes, al, &full[st], kg * 32, m0);
+                uint8_t* bh = base + 2 * Cfg::kABytes;
+                uint8_t* bl = bh + Cfg::kBBytes;
+#pragma unroll
+                for (int j = 0; j < BN / 32; ++j) {
+                    tma_load_2d(bh + j * 4096, bh_m, &full[st], n0 + 32 * j, kg * 32);
+                    tma_load_2d(bl + j * 4096, bl_m, &full[st], n0 + 32 * j, kg * 32);
+                }
+            }
+        } else if (warp == 1 && lane == 0) {
+            constexpr uint32_t kIdesc = idesc_tf32_kmaj_mnmaj<128, BN>();
+            const uint64_t da_hi = kmajor_desc(s0), da_lo = kmajor_desc(s0 + Cfg::kABytes);
+            const uint64_t db_hi = mnmajor_desc(s0 + 2 * Cfg::kABytes, 4096);
+            const uint64_t db_lo = mnmajor_desc(s0 + 2 * Cfg::kABytes + Cfg::kBBytes, 4096);
+            for (int kb = 0; kb < kb_per; ++kb) {
+                const int g = g0 + kb;
+                const int st = g % S;
+                const uint32_t ph = (g / S) & 1;
+                const int c = g & 1;
+                mbar_wait(&cempty[c], ((g >> 1) & 1) ^ 1);
+                mbar_wait(&full[st], ph);
+                tc_fence_after();
+                const uint64_t so = static_cast<uint64_t>((st * Cfg::kStageBytes) >> 4);
+                const uint32_t d = tmem + c * BN;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((1024 * k) >> 4);
+                    mma_tf32(d, da_lo + ao, db_hi + bo, kIdesc, k > 0 ? 1u : 0u);
+                    mma_tf32(d, da_hi + ao, db_lo + bo, kIdesc, 1u);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((1024 * k) >> 4);
+                    mma_tf32(d, da_hi + ao, db_hi + bo, kIdesc, 1u);
+                }
+                mma_commit(&empty[st]);
+                mma_commit(&cfull[c]);
+            }
+        } else if (warp >= 4) {
+            const int q = warp & 3;
+            const int ch = ((warp - 4) >> 2) * 64;
+            const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+            float sum[64];
+#pragma unroll
+            for (int i = 0; i < 64; ++i) sum[i] = 0.f;
+            for (int kb = 0; kb < kb_per; ++kb) {
+                const int g = g0 + kb;
+                const int c = g & 1;
+                mbar_wait(&cfull[c], (g >> 1) & 1);
+                tc_fence_after();
+                uint32_t v[32];
+                tmem_ld32(lane_base + c * BN + ch, v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) sum[i] = __fadd_rn(sum[i], __uint_as_float(v[i]));
+                tmem_ld32(lane_base + c * BN + ch + 32, v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) sum[32 + i] = __fadd_rn(sum[32 + i], __uint_as_float(v[i]));
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_relaxed(&cempty[c]);
+            }
+            // partial -> SMEM (every MMA of the step has completed: stages free)
+            const uint32_t rr = static_cast<uint32_t>(q * 32 + lane);
+            const uint32_t base = s0 + rr * 512u;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const uint32_t uu = static_cast<uint32_t>(ch / 4 + u);
+                sts128(base + ((uu ^ (rr & 7u)) << 4), __float_as_uint(sum[4 * u]),
+                       __float_as_uint(sum[4 * u + 1]), __float_as_uint(sum[4 * u + 2]),
+                       __float_as_uint(sum[4 * u + 3]));
+            }
+        }
+        tc_fence_before();
+        __syncwarp();
+        cluster_sync_all();  // every partial of the tile is in SMEM
+        {
+            const uint32_t S_ = gridDim.y, r = cluster_ctarank();
+            const uint32_t R = 128u / S_;
+            uint32_t* out_hi = pl.p[2 * dst];
+            uint32_t* out_lo = pl.p[2 * dst + 1];
+            for (uint32_t i = threadIdx.x; i < R * 32u; i += blockDim.x) {
+                const uint32_t rr = r * R + (i >> 5), u = i & 31u;
+                const uint32_t la = s0 + rr * 512u + ((u ^ (rr & 7u)) << 4);
+                float4 a = ld_dsmem_f4(mapa_shared(la, 0));
+                for (uint32_t p = 1; p < S_; ++p) {
+                    const float4 b = ld_dsmem_f4(mapa_shared(la, p));
+                    a.x = __fadd_rn(a.x, b.x);
+                    a.y = __fadd_rn(a.y, b.y);
+                    a.z = __fadd_rn(a.z, b.z);
+                    a.w = __fadd_rn(a.w, b.w);
+                }
+                const int grow = m0 + static_cast<int>(rr), col = n0 + static_cast<int>(4u * u);
+                if (!last) {
+                    uint4 hv, lv;
+                    split_tf32(a.x, hv.x, lv.x);
+                    split_tf32(a.y, hv.y, lv.y);
+                    split_tf32(a.z, hv.z, lv.z);
+                    split_tf32(a.w, hv.w, lv.w);
+                    *reinterpret_cast<uint4*>(out_hi + static_cast<size_t>(grow) * n_pad + col) = hv;
+                    *reinterpret_cast<uint4*>(out_lo + static_cast<size_t>(grow) * n_pad + col) = lv;
+                } else if (grow < n_out) {
+                    const float vv[4] = {a.x, a.y, a.z, a.w};
+                    float* d = out_f32 + static_cast<size_t>(grow) * n_out;
+                    for (int k = 0; k < 4; ++k)
+                        if (col + k < n_out) d[col + k] = vv[k];
+                }
+            }
+        }
+        cluster_sync_all();  // peers are done reading this CTA's SMEM
+        if (!last) grid_barrier(bar_ctr, nctas * static_cast<unsigned int>(step + 1));
+        acc = dst;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) tmem_dealloc<256>(tmem);
+}
+
+static cudaError_t prepare_k1c() {
+    return cudaFuncSetAttribute(k1c_chain_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(K1Cfg::kSmem));
+}
+
+// One cooperative launch for the whole chain; cudaErrorCooperativeLaunchTooLarge
+// (or any launch error) tells the caller to run the per-step chain instead.
+cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
+                             uint32_t* const* planes, const PlanBits& plan, int n_pad, int splits,
+                             float* out_f32, int n_out, unsigned int* bar_ctr, cudaStream_t s) {
+    if (splits < 1 || splits > 8 || n_pad % 128 != 0 || k1_split_legacy()) return cudaErrorNotSupported;
+    const int tiles = (n_pad / 128) * (n_pad / 128);
+    if (tiles > k1_max_clusters(splits)) return cudaErrorNotSupported;
+    K1CMaps maps;
+    K1CPlanes pl;
+    for (int i = 0; i < 6; ++i) {
+        maps.a[i] = map_a[i];
+        maps.b[i] = map_b[i];
+        pl.p[i] = planes[i];
+    }
+    cudaError_t e = cudaMemsetAsync(bar_ctr, 0, sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(tiles, splits);
+    cfg.blockDim = dim3(K1Cfg::kThreads);
+    cfg.dynamicSmemBytes = K1Cfg::kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = static_cast<unsigned>(splits);
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, k1c_chain_3xtf32, maps, pl, plan, n_pad, out_f32, n_out, bar_ctr);
 }
 
 cudaError_t launch_k1p_gemm_peers(const GemmPlanes& m, int n_pad, int m_pad, int ld_out,

@@ -7,6 +7,7 @@
 // over ping-pong buffers in HBM; the graph is cached per (mode, n, k, in, out)
 // and replayed.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -105,6 +106,7 @@ struct mxp_handle_s {
     uint32_t* planes[6] = {};
     float* part = nullptr;  // split-K workspace (splits x n_pad^2 fp32) for small n
     int splits = 1;
+    unsigned int* bar_ctr = nullptr;  // grid-barrier counter of the one-launch chain (K1C)
     CUtensorMap map_a[6], map_b[6];
     // right-hand side prepared by mxp_gemm_prepare_rhs (planes[2..3] / f64buf[1]);
     // any other use of the workspace invalidates it
@@ -220,6 +222,15 @@ int ensure_io(mxp_handle h, size_t bytes) {
 
 // ---- enqueue helpers (no validation; stream = h->stream) -----------------
 
+// MXP_K1C=0: run the K1 chain as one launch per step (A/B runs).
+bool k1c_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("MXP_K1C");
+        return !(v != nullptr && std::strcmp(v, "0") == 0);
+    }();
+    return on;
+}
+
 // 3xTF32 chain for n > kSmallMax through K1, planes padded to 128.
 int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float* dA,
                       float* dOut, int64_t* launches, int64_t* failed) {
@@ -233,6 +244,16 @@ int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float
     if (e != cudaSuccess) return cuda_fail(e, "split");
     ++*launches;
     const int bn = k1_block_n(np, h->num_sms);
+    if (bn == 128 && k1c_enabled()) {
+        // the whole chain in one launch when every split-K cluster fits at once
+        e = launch_k1c_chain(h->map_a, h->map_b, h->planes, plan, np, h->splits, dOut, (int)n,
+                             h->bar_ctr, h->stream);
+        if (e == cudaSuccess) {
+            ++*launches;
+            return MXP_OK;
+        }
+        if (e != cudaErrorNotSupported) return cuda_fail(e, "k1c_chain_3xtf32");
+    }
     int acc = 0;  // plane pair index: 0 base, 1 ping, 2 pong
     for (int s = 0; s < plan.len; ++s) {
         const bool mult = plan_is_mult(plan, s);
@@ -446,6 +467,7 @@ int mxp_create(int device, mxp_handle* out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->copy_out, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
+    if (e == cudaSuccess) e = cudaMalloc(&h->bar_ctr, 256);
     if (e != cudaSuccess) {
         delete h;
         return cuda_fail(e, "stream/event creation");
@@ -462,6 +484,7 @@ int mxp_destroy(mxp_handle h) {
     for (auto p : h->planes)
         if (p) cudaFree(p);
     if (h->part) cudaFree(h->part);
+    if (h->bar_ctr) cudaFree(h->bar_ctr);
     for (auto p : h->f64buf)
         if (p) cudaFree(p);
     for (auto p : h->modbuf)

@@ -94,7 +94,12 @@ cudaError_t launch_k1_gemm_rows(const GemmPlanes& maps, int n_pad, int m_pad, in
                                 uint32_t* out_lo, cudaStream_t s, float* part = nullptr,
                                 int splits = 1);
 int k1_split_k(int n_pad, int m_pad, int num_sms);
-int k1_split_launches(int splits);  // kernel launches one split-K multiply takes
+int k1_split_launches(int splits);
+// K1C: the whole 3xTF32 chain in one cooperative launch (kernels_tf32.cu);
+// cudaErrorNotSupported / a launch error => run the per-step chain
+cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
+                             uint32_t* const* planes, const PlanBits& plan, int n_pad, int splits,
+                             float* out_f32, int n_out, unsigned int* bar_ctr, cudaStream_t s);  // kernel launches one split-K multiply takes
 cudaError_t launch_split_rows(const float* in, int n, int ld, int rows, uint32_t* hi, uint32_t* lo,
                               int n_pad, int rows_pad, cudaStream_t s);
 
