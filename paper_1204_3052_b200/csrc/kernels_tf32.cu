@@ -503,6 +503,37 @@ struct K1Cfg {
 };
 }  // namespace
 
+// Split-K partial sums of one 128 x 128 tile held in the SMEM of the S CTAs
+// of a cluster (row r at r * 512 B, 16-byte unit u at (u ^ (r & 7)) << 4):
+// CTA `rank` reduces rows [rank R, (rank + 1) R), R = 128 / S, in split order
+// with round-to-nearest adds (splitk_reduce_kernel's order and arithmetic),
+// and hands each 4-column group to emit(row, unit, sum).  Up to 8 loads per
+// group are in flight before the adds.
+template <typename Emit>
+__device__ __forceinline__ void cluster_reduce_tile(uint32_t s0, uint32_t S_, uint32_t rank,
+                                                    Emit&& emit) {
+    const uint32_t R = 128u / S_;
+    for (uint32_t i = threadIdx.x; i < R * 32u; i += blockDim.x) {
+        const uint32_t rr = rank * R + (i >> 5), u = i & 31u;
+        const uint32_t la = s0 + rr * 512u + ((u ^ (rr & 7u)) << 4);
+        float4 v[8];
+#pragma unroll
+        for (uint32_t p = 0; p < 8; ++p)
+            if (p < S_) v[p] = ld_dsmem_f4(mapa_shared(la, p));
+        float4 a = v[0];
+#pragma unroll
+        for (uint32_t p = 1; p < 8; ++p) {
+            if (p < S_) {
+                a.x = __fadd_rn(a.x, v[p].x);
+                a.y = __fadd_rn(a.y, v[p].y);
+                a.z = __fadd_rn(a.z, v[p].z);
+                a.w = __fadd_rn(a.w, v[p].w);
+            }
+        }
+        emit(rr, u, a);
+    }
+}
+
 __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
     k1_gemm_3xtf32(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                    const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
@@ -692,20 +723,8 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
         // and arithmetic of splitk_reduce_kernel, so results are bitwise the
         // same — and writes the next step's planes / the fp32 result.
         cluster_sync_all();  // every partial is in SMEM (release / acquire)
-        const uint32_t S_ = gridDim.y, r = cluster_ctarank();
-        const uint32_t R = 128u / S_;
-        const uint32_t s0 = smem_u32(smem);
-        for (uint32_t i = threadIdx.x; i < R * 32u; i += blockDim.x) {
-            const uint32_t rr = r * R + (i >> 5), u = i & 31u;
-            const uint32_t la = s0 + rr * 512u + ((u ^ (rr & 7u)) << 4);
-            float4 a = ld_dsmem_f4(mapa_shared(la, 0));
-            for (uint32_t p = 1; p < S_; ++p) {
-                const float4 b = ld_dsmem_f4(mapa_shared(la, p));
-                a.x = __fadd_rn(a.x, b.x);
-                a.y = __fadd_rn(a.y, b.y);
-                a.z = __fadd_rn(a.z, b.z);
-                a.w = __fadd_rn(a.w, b.w);
-            }
+        cluster_reduce_tile(smem_u32(smem), gridDim.y, cluster_ctarank(),
+                            [&](uint32_t rr, uint32_t u, float4 a) {
             const int grow = m0 + static_cast<int>(rr), col = n0 + static_cast<int>(4u * u);
             if (out_hi != nullptr) {
                 uint4 hv, lv;
@@ -722,7 +741,7 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
                 for (int k = 0; k < 4; ++k)
                     if (col + k < n_out) d[col + k] = vv[k];
             }
-        }
+        });
         cluster_sync_all();  // peers are done reading this CTA's SMEM
     } else {
         __syncthreads();
@@ -1163,6 +1182,19 @@ struct K1CPlanes {
     uint32_t* p[6];
 };
 
+#ifdef K1C_TRACE  // tools/k1c_trace.cu: per-step phase stamps of CTA (0, 0)
+__device__ long long* g_k1c_trace;  // [step][8]
+#define K1C_STAMP(k)                                                                       \
+    do {                                                                                   \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && step < 64)    \
+            g_k1c_trace[step * 8 + (k)] = clock64();                                       \
+    } while (0)
+#else
+#define K1C_STAMP(k) \
+    do {             \
+    } while (0)
+#endif
+
 __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int target) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1233,6 +1265,7 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
         const int dst = (acc == 1) ? 2 : 1;
         const int rhs = mult ? 0 : acc;
         const int g0 = step * kb_per;  // pipeline position of this step's first k-block
+        if (warp == 4) K1C_STAMP(0);
         if (warp == 0 && lane == 0) {
             // the planes this step reads were written by other CTAs' generic
             // stores before the grid barrier: order them before TMA (async proxy)
@@ -1311,6 +1344,7 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive_relaxed(&cempty[c]);
             }
+            if (warp == 4) K1C_STAMP(1);
             // partial -> SMEM (every MMA of the step has completed: stages free)
             const uint32_t rr = static_cast<uint32_t>(q * 32 + lane);
             const uint32_t base = s0 + rr * 512u;
@@ -1324,23 +1358,13 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
+        if (warp == 4) K1C_STAMP(2);
         cluster_sync_all();  // every partial of the tile is in SMEM
+        if (warp == 4) K1C_STAMP(3);
         {
-            const uint32_t S_ = gridDim.y, r = cluster_ctarank();
-            const uint32_t R = 128u / S_;
             uint32_t* out_hi = pl.p[2 * dst];
             uint32_t* out_lo = pl.p[2 * dst + 1];
-            for (uint32_t i = threadIdx.x; i < R * 32u; i += blockDim.x) {
-                const uint32_t rr = r * R + (i >> 5), u = i & 31u;
-                const uint32_t la = s0 + rr * 512u + ((u ^ (rr & 7u)) << 4);
-                float4 a = ld_dsmem_f4(mapa_shared(la, 0));
-                for (uint32_t p = 1; p < S_; ++p) {
-                    const float4 b = ld_dsmem_f4(mapa_shared(la, p));
-                    a.x = __fadd_rn(a.x, b.x);
-                    a.y = __fadd_rn(a.y, b.y);
-                    a.z = __fadd_rn(a.z, b.z);
-                    a.w = __fadd_rn(a.w, b.w);
-                }
+            cluster_reduce_tile(s0, gridDim.y, cluster_ctarank(), [&](uint32_t rr, uint32_t u, float4 a) {
                 const int grow = m0 + static_cast<int>(rr), col = n0 + static_cast<int>(4u * u);
                 if (!last) {
                     uint4 hv, lv;
@@ -1356,10 +1380,17 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
                     for (int k = 0; k < 4; ++k)
                         if (col + k < n_out) d[col + k] = vv[k];
                 }
-            }
+            });
         }
-        cluster_sync_all();  // peers are done reading this CTA's SMEM
+        if (warp == 4) K1C_STAMP(4);
+        // The grid barrier also tells every CTA that its peers have finished
+        // reading its SMEM (their reduce precedes their arrival), so the next
+        // step's TMA loads may overwrite it; after the last step a cluster
+        // barrier does that before exit.
+        if (last) cluster_sync_all();
+        if (warp == 4) K1C_STAMP(5);
         if (!last) grid_barrier(bar_ctr, nctas * static_cast<unsigned int>(step + 1));
+        if (warp == 4) K1C_STAMP(6);
         acc = dst;
     }
     tc_fence_before();
