@@ -22,7 +22,8 @@ o = torch.empty((128, 512), dtype=t.dtype, device=t.device)
 eng.gemm_prepare_rhs_device(t.data_ptr(), 512)                          # prepared right-hand side
 eng.gemm_rows_prepared_device(t[256:384].data_ptr(), o.data_ptr(), 512, 128)
 eng.synchronize()
-eng.power(oracle.scaled_input(384, np.float32, 42), 13)                 # K1 split-K + reduce
+eng.power(oracle.scaled_input(384, np.float32, 42), 13)                 # K1C one-launch chain
+eng.multiply(oracle.scaled_input(256, np.float32, 1), oracle.scaled_input(256, np.float32, 2))  # K1 cluster split-K
 eng.power(oracle.scaled_input(1024, np.float32, 42), 5)                 # K1P CTA pairs
 eng.power(oracle.scaled_input(256, np.float64, 42), 9)                  # FP64 DMMA
 eng.power_mod(np.arange(100 * 100, dtype=np.uint32).reshape(100, 100), 11, 65521)
