@@ -123,17 +123,6 @@ __device__ __forceinline__ uint32_t absmax_bits(const float* x) {
     return __float_as_uint(m);
 }
 
-// Row `row`, columns [32g + 16h, +16) of a plane: two 16-byte units, unit
-// index XOR row % 8 (a quarter-warp = 8 consecutive rows hits 8 distinct
-// bank groups).
-__device__ __forceinline__ void put_half(uint32_t plane, uint32_t row, uint32_t g, uint32_t h,
-                                         const uint32_t (&p)[8]) {
-    const uint32_t base = plane + (g >> 1) * 16384u + row * 128u;
-    const uint32_t u0 = (g & 1u) * 4u + 2u * h;
-    sts128(base + ((u0 ^ (row & 7u)) << 4), p[0], p[1], p[2], p[3]);
-    sts128(base + (((u0 + 1u) ^ (row & 7u)) << 4), p[4], p[5], p[6], p[7]);
-}
-
 // 32 values of one row of an n x n fp32 matrix, zero padded to 128.
 __device__ __forceinline__ void load_row(const float* __restrict__ src, int n, uint32_t row,
                                          uint32_t col0, float (&x)[32]) {

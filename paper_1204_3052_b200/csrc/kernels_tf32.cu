@@ -46,34 +46,10 @@ namespace mxp {
 namespace {
 constexpr uint32_t kChunk = 128u * 128u;  // one 32-column chunk: 128 rows x 128 B
 constexpr uint32_t kPlane = 4u * kChunk;  // 64 KB
-constexpr int kK3Threads = 512;  // 16 warps: 4 lane quarters x 4 column groups
 constexpr uint32_t kColD0 = 0, kColD1 = 128, kColHi = 256, kColLo = 384;
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023u) & ~uintptr_t(1023));
-}
-
-// Write 16 split values (row `row`, columns [col0, col0+16), col0 % 16 == 0)
-// into the SMEM right operand (MN-major SW128_BASE32B).  The 16-byte unit
-// order is flipped for rows with (row >> 2) odd so the 8 rows of a
-// quarter-warp hit 8 distinct 16-byte bank groups (no conflicts).
-__device__ __forceinline__ void k3_put_right(uint32_t s_hi, uint32_t s_lo, uint32_t row, int col0,
-                                             const uint32_t (&h)[16], const uint32_t (&l)[16]) {
-    const uint32_t flip = (row >> 2) & 1u;
-    const uint32_t base = (col0 >> 5) * kChunk + row * 128u;
-    const uint32_t u0 = (col0 & 31) >> 2;  // first 16-byte unit of this sub-chunk (0 or 4)
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int ua = u, ub = u ^ 1;
-        const uint32_t unit = u0 + (static_cast<uint32_t>(u) ^ flip);
-        const uint32_t off = base + ((((unit >> 1) ^ (row & 3u)) << 1 | (unit & 1u)) << 4);
-        uint32_t h0 = flip ? h[4 * ub] : h[4 * ua], h1 = flip ? h[4 * ub + 1] : h[4 * ua + 1];
-        uint32_t h2 = flip ? h[4 * ub + 2] : h[4 * ua + 2], h3 = flip ? h[4 * ub + 3] : h[4 * ua + 3];
-        uint32_t l0 = flip ? l[4 * ub] : l[4 * ua], l1 = flip ? l[4 * ub + 1] : l[4 * ua + 1];
-        uint32_t l2 = flip ? l[4 * ub + 2] : l[4 * ua + 2], l3 = flip ? l[4 * ub + 3] : l[4 * ua + 3];
-        sts128(s_hi + off, h0, h1, h2, h3);
-        sts128(s_lo + off, l0, l1, l2, l3);
-    }
 }
 
 // One plane only (16 values of row `row`, columns [col0, col0+16)).
@@ -91,15 +67,6 @@ __device__ __forceinline__ void k3_put_half(uint32_t s_plane, uint32_t row, int 
         uint32_t h2 = flip ? h[4 * ub + 2] : h[4 * ua + 2], h3 = flip ? h[4 * ub + 3] : h[4 * ua + 3];
         sts128(s_plane + off, h0, h1, h2, h3);
     }
-}
-
-// ... and the same values into the TMEM left operand as well.
-__device__ __forceinline__ void k3_put_row(uint32_t s_hi, uint32_t s_lo, uint32_t row, int col0,
-                                           const uint32_t (&h)[16], const uint32_t (&l)[16],
-                                           uint32_t t_hi, uint32_t t_lo) {
-    tmem_st16(t_hi + col0, h);
-    tmem_st16(t_lo + col0, l);
-    k3_put_right(s_hi, s_lo, row, col0, h, l);
 }
 
 // Row `row`, columns [col0, col0+16) of the staged input (TMA SWIZZLE_128B
@@ -485,13 +452,6 @@ cudaError_t launch_identity_f64(double* out, int n, cudaStream_t s) {
 // chunk, ~310 cycles) hides under the chunk's 12 MMAs (~768 cycles).
 // ======================================================================
 namespace {
-// 3 MMAs per k-step, small cross terms first.
-__device__ __forceinline__ void mma3(uint32_t tmem, uint64_t a_hi, uint64_t a_lo, uint64_t b_hi,
-                                     uint64_t b_lo, uint32_t idesc, uint32_t acc) {
-    mma_tf32(tmem, a_lo, b_hi, idesc, acc);
-    mma_tf32(tmem, a_hi, b_lo, idesc, 1u);
-    mma_tf32(tmem, a_hi, b_hi, idesc, 1u);
-}
 struct K1Cfg {
     static constexpr int kBN = 128;
     static constexpr int kStages = 3;
