@@ -52,7 +52,10 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023u) & ~uintptr_t(1023));
 }
 
-// One plane only (16 values of row `row`, columns [col0, col0+16)).
+// 16 split values (row `row`, columns [col0, col0+16), col0 % 16 == 0) into
+// one SMEM right-operand plane (MN-major SW128_BASE32B).  The 16-byte unit
+// order is flipped for rows with (row >> 2) odd so the 8 rows of a
+// quarter-warp hit 8 distinct 16-byte bank groups (no conflicts).
 __device__ __forceinline__ void k3_put_half(uint32_t s_plane, uint32_t row, int col0,
                                             const uint32_t (&h)[16]) {
     const uint32_t flip = (row >> 2) & 1u;
