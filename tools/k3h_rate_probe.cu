@@ -9,7 +9,20 @@
 #include <cstdio>
 #include "../paper_1204_3052_b200/csrc/kernels_k3h.cu"
 using namespace mxp;
-__global__ void __launch_bounds__(kThreads, 1) rate(int steps, int mode, int fill, long long* cyc, uint32_t* sink) {
+// the same step with both operands from SMEM (SS): the plane is the K-major
+// left operand and the MN-major right operand at once
+template <uint32_t C>
+__device__ __forceinline__ void k3h_issue_ss(uint32_t tbase, uint32_t s0, uint64_t* mma_bar) {
+    const uint32_t pl = s0 + C * kChainSmem;
+    const uint64_t y0 = smem_desc(pl, 16384, 1024, 2), y1 = smem_desc(pl + kPlane, 16384, 1024, 2);
+    const uint64_t x0 = smem_desc(pl, 16, 1024, 2), x1 = smem_desc(pl + kPlane, 16, 1024, 2);
+    constexpr uint32_t D = C * 256u;
+    mma_f16_ss_x8<D, 0, kBStep, (16384u >> 4), true>(tbase, x1, y0, kIdescNegA);
+    mma_f16_ss_x8<D, 0, kBStep, (16384u >> 4), false>(tbase, x0, y1, kIdescNegB);
+    mma_f16_ss_x8<D, 0, kBStep, (16384u >> 4), false>(tbase, x0, y0, kIdesc);
+    mma_commit_warp(mma_bar + C);
+}
+__global__ void __launch_bounds__(kThreads, 1) rate(int steps, int mode, int fill, int ss, long long* cyc, uint32_t* sink) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
@@ -58,8 +71,13 @@ __global__ void __launch_bounds__(kThreads, 1) rate(int steps, int mode, int fil
     long long t0 = clock64();
     if (warp == kIssueWarp) {
         for (int s = 0; s < steps; ++s) {
-            if (s & 1) k3h_issue<1>(tmem, s0, bars);
-            else k3h_issue<0>(tmem, s0, bars);
+            if (ss) {
+                if (s & 1) k3h_issue_ss<1>(tmem, s0, bars);
+                else k3h_issue_ss<0>(tmem, s0, bars);
+            } else {
+                if (s & 1) k3h_issue<1>(tmem, s0, bars);
+                else k3h_issue<0>(tmem, s0, bars);
+            }
         }
         mma_commit_warp(bars + 2);
         mbar_wait_sleep(bars + 2, 0);
@@ -94,6 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1) rate(int steps, int mode, int fil
             }
             ++it;
             if (mode == 0) __nanosleep(200);
+            if (mode & 8) __nanosleep(1000);  // ~64 KB of st.shared per ~2000 cycles (the epilogue's rate)
         }
         tmem_st_wait();
     }
@@ -109,17 +128,18 @@ int main() {
     cudaMalloc(&sink, 64);
     cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
     const int steps = 2000;
-    for (int fill = 0; fill < 3; ++fill)
-    for (int mode : {0, 7}) {
+    for (int ss = 0; ss < 2; ++ss)
+    for (int fill = 1; fill < 2; ++fill)
+    for (int mode : {0, 2, 10, 7, 15}) {
         for (int grid : {148}) {
-            rate<<<grid, kThreads, kSmem>>>(steps, mode, fill, cyc, sink);
+            rate<<<grid, kThreads, kSmem>>>(steps, mode, fill, ss, cyc, sink);
             cudaError_t e = cudaDeviceSynchronize();
             long long h[148];
             cudaMemcpy(h, cyc, grid * 8, cudaMemcpyDeviceToHost);
             double avg = 0;
             for (int i = 0; i < grid; ++i) avg += h[i];
             avg /= grid;
-            printf("fill %d mode %d (ld %d sts %d st %d) grid %3d err=%s: %.1f cycles/step = %.1f per MMA\n", fill, mode, mode & 1,
+            printf("%s fill %d mode %d (ld %d sts %d st %d) grid %3d err=%s: %.1f cycles/step = %.1f per MMA\n", ss ? "SS" : "TS", fill, mode, mode & 1,
                    (mode >> 1) & 1, (mode >> 2) & 1, grid, cudaGetErrorString(e), avg / steps, avg / steps / 24);
         }
     }
