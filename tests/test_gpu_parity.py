@@ -470,3 +470,56 @@ def test_batched_mixed_magnitudes_and_schedule_edges():
             assert fro(out[i], ref) <= mx.fro_tol(n, k, "f32"), (batch, k, i, fro(out[i], ref))
         # deterministic: a second launch is bitwise identical
         assert np.array_equal(mx.exponentiate_batched(stack, k), out)
+
+
+# ------------------------------------------------- one-launch chain (K1C) A/B
+_AB_SCRIPT = r"""
+import hashlib, math, sys
+import numpy as np
+sys.path.insert(0, ".")
+import oracle, paper_1204_3052_b200 as mx
+eng = mx.Engine(0)
+out = []
+for n, k in ((130, 7), (256, 64), (384, 33), (512, 1000), (896, 9)):
+    r = eng.power(oracle.scaled_input(n, np.float32, 42), k)
+    out.append(hashlib.sha256(np.ascontiguousarray(r).tobytes()).hexdigest())
+    out.append(str(eng.last_stats.launches))
+r = eng.multiply(oracle.scaled_input(512, np.float32, 1), oracle.scaled_input(512, np.float32, 2))
+out.append(hashlib.sha256(np.ascontiguousarray(r).tobytes()).hexdigest())
+print(" ".join(out))
+"""
+
+
+def _run_ab(env_extra):
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ)
+    env.update(env_extra)
+    res = subprocess.run([sys.executable, "-c", _AB_SCRIPT], env=env, capture_output=True, text=True,
+                         timeout=600, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert res.returncode == 0, res.stderr[-2000:]
+    return res.stdout.split()
+
+
+def test_one_launch_chain_bitwise_equals_per_step_chain():
+    """K1C (whole chain in one cooperative launch) against the same chain run
+    one K1 launch per step (MXP_K1C=0): bitwise equal, fewer launches."""
+    k1c = _run_ab({})
+    per_step = _run_ab({"MXP_K1C": "0"})
+    for i in range(0, 10, 2):
+        assert k1c[i] == per_step[i], f"chain {i // 2}"
+        assert int(k1c[i + 1]) == 2 and int(per_step[i + 1]) > 2
+    assert k1c[10] == per_step[10]
+
+
+def test_cluster_split_k_bitwise_equals_two_launch_split_k():
+    """K1 split-K with the cluster/DSMEM reduction against the two-launch form
+    (partials through a workspace + splitk_reduce_kernel) at the same split:
+    bitwise equal for chains and single multiplies (n where both pick the
+    same split: the cluster cap does not bind below 512)."""
+    a = _run_ab({"MXP_K1C": "0"})
+    b = _run_ab({"MXP_K1C": "0", "MXP_SPLITK": "global"})
+    for i in (0, 2, 4, 8):  # n = 130, 256, 384, 896
+        assert a[i] == b[i], f"chain {i // 2}"
