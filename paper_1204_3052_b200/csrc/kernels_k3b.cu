@@ -60,6 +60,9 @@ constexpr uint32_t kSOff = 2u * kChainSmem;       // base-b2 scratch
 constexpr uint32_t kBarOff = kSOff + kPlane;      // mbarriers + TMEM slot
 constexpr size_t kSmem = kBarOff + 256 + 1024;    // + alignment slack
 constexpr uint32_t kIdesc = idesc_bf16_kmaj_mnmaj<128, 128>();
+// plane 1 holds -b1 (split3): x1*y0 negates A, x0*y1 negates B
+constexpr uint32_t kIdescNegA = kIdesc | (1u << 13);
+constexpr uint32_t kIdescNegB = kIdesc | (1u << 14);
 // descriptor address-field advance (16-byte units) per K=16 step
 //   right operand (MN-major): 16 rows of 128 B;  left (K-major): 32 B inside
 //   the 128-byte atom row, next 64-column chunk every 4 steps
@@ -69,22 +72,26 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023u) & ~uintptr_t(1023));
 }
 
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-    uint32_t r;
-    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-    return r;
-}
-__device__ __forceinline__ float bf_lo(uint32_t p) { return __uint_as_float(p << 16); }
-__device__ __forceinline__ float bf_hi(uint32_t p) { return __uint_as_float(p & 0xFFFF0000u); }
-
 // Split the pair (a = column 2j, b = column 2j+1) into three packed bf16x2
-// words; every subtraction is exact.
+// words p0 = b0, p1 = -b1, p2 = b2 (x = b0 + b1 + b2); every subtraction is
+// exact.  The residuals come from mixed bf16-fp32 subtractions that read the
+// bf16 half in place (FHADD.BF16): n1 = b0 - x = -r1, p1 = rn(n1) = -b1,
+// r2 = p1 - n1 = r1 - b1 — 7 instructions per pair instead of 11 (unpacking
+// each bf16 half first).  The MMAs that read p1 against a positive plane set
+// the instruction descriptor's negate bit; x1*y1 needs none.
 __device__ __forceinline__ void split3(float a, float b, uint32_t& p0, uint32_t& p1, uint32_t& p2) {
-    p0 = pack_bf16x2(a, b);
-    const float a1 = __fsub_rn(a, bf_lo(p0)), b1 = __fsub_rn(b, bf_hi(p0));
-    p1 = pack_bf16x2(a1, b1);
-    const float a2 = __fsub_rn(a1, bf_lo(p1)), b2 = __fsub_rn(b1, bf_hi(p1));
-    p2 = pack_bf16x2(a2, b2);
+    asm("{\n\t.reg .b16 l0, h0, l1, h1;\n\t.reg .f32 a1, b1, a2, b2;\n\t"
+        "cvt.rn.bf16x2.f32 %0, %4, %3;\n\t"
+        "mov.b32 {l0, h0}, %0;\n\t"
+        "sub.f32.bf16 a1, l0, %3;\n\t"
+        "sub.f32.bf16 b1, h0, %4;\n\t"
+        "cvt.rn.bf16x2.f32 %1, b1, a1;\n\t"
+        "mov.b32 {l1, h1}, %1;\n\t"
+        "sub.f32.bf16 a2, l1, a1;\n\t"
+        "sub.f32.bf16 b2, h1, b1;\n\t"
+        "cvt.rn.bf16x2.f32 %2, b2, a2;\n\t}"
+        : "=r"(p0), "=r"(p1), "=r"(p2)
+        : "f"(a), "f"(b));
 }
 
 // Row `row`, columns [32g + 16h, +16) of a plane: two 16-byte units, unit
@@ -164,9 +171,9 @@ __device__ __forceinline__ void k3b_issue(uint32_t tbase, uint32_t s0, uint64_t*
     mma_f16_ss_x8<D, 0, kBStep, (16384u >> 4), true>(tbase, x2, y0, kIdesc);  // x2*y0
     if (kMult) mma_commit_warp(s_free);
     mma_f16_ts_x8<D, X0, Y2, kBStep>(tbase, y0, kIdesc);  // x0*y2
-    mma_f16_ts_x8<D, X1, Y1, kBStep>(tbase, y0, kIdesc);  // x1*y1
-    mma_f16_ts_x8<D, X0, Y1, kBStep>(tbase, y0, kIdesc);  // x0*y1
-    mma_f16_ts_x8<D, X1, 0, kBStep>(tbase, y0, kIdesc);   // x1*y0
+    mma_f16_ts_x8<D, X1, Y1, kBStep>(tbase, y0, kIdesc);      // x1*y1 ((-b1)(-b1))
+    mma_f16_ts_x8<D, X0, Y1, kBStep>(tbase, y0, kIdescNegB);  // x0*y1
+    mma_f16_ts_x8<D, X1, 0, kBStep>(tbase, y0, kIdescNegA);   // x1*y0
     mma_f16_ts_x8<D, X0, 0, kBStep>(tbase, y0, kIdesc);   // x0*y0
     mma_commit_warp(mma_bar + C);
 }
