@@ -263,6 +263,10 @@ constexpr int kIn = -2;  // Chain::s: the next input is being loaded / converted
 // IN (convert the freshly loaded input into operands, publish step 0).  In
 // between the epilogue warps serve the other chain, so the HBM round trip
 // overlaps that chain's MMAs.
+// kMults: the plan has MULTIPLY_BASE steps.  Square-only plans (k a power
+// of two) run the kMults = false instance, which drops every base-operand
+// path from the epilogue.
+template <bool kMults>
 __global__ void __launch_bounds__(kThreads, 1)
     k3h_batched_power(const __grid_constant__ CUtensorMap in_map,
                       const __grid_constant__ CUtensorMap out_map, const float* __restrict__ in,
@@ -303,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const long long G = gridDim.x;
     const size_t n2 = static_cast<size_t>(n) * n;
     const int last = plan.len - 1;
+    auto is_mult = [&](int step) { return kMults && plan_is_mult(plan, step); };
 
     Chain ch0{}, ch1{};
     ch0.m = blockIdx.x;
@@ -561,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 st.ph ^= 1;
                 tc_fence_after();
                 // exponent of this step's product: 2^(ex + ey) * D
-                const int pe = (plan_is_mult(plan, st.s) ? st.eb : st.e) + st.e;
+                const int pe = (is_mult(st.s) ? st.eb : st.e) + st.e;
                 if (st.s == last) {
                     // ---- OUT: 2^pe * D -> the warp tile (the IO warp stores it)
                     if (warp == 0 && lane == 0 && vec) mbar_arrive(planes_free + C);  // load the next input
@@ -609,7 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // bits of h1, so the exact path (block max, one barrier) runs
                 // whenever the previous product came out more than 2^12 below
                 // its bound (the input's exact max feeds the first step's bound).
-                const bool was_mult = plan_is_mult(plan, st.s);
+                const bool was_mult = is_mult(st.s);
                 const uint32_t mprev = slots_max(C, st);
                 const int pmax_e = ilogb_bits(mprev) + st.t_prev;  // floor(log2 max|P'_s|)
                 const bool exact = pmax_e < kCeil - 12;
@@ -617,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int t = kCeil - static_cast<int>(lg_n) - (xmax_e + 1) - (pmax_e + 1);
                 if (mprev == 0u || mprev >= 0x7F800000u) t = 0;  // zero / non-finite operand
                 st.s += 1;
-                const bool mult = plan_is_mult(plan, st.s);
+                const bool mult = is_mult(st.s);
                 const float* fa = reinterpret_cast<const float*>(a);
                 const float* fb = reinterpret_cast<const float*>(b);
                 const uint32_t nb = st.sb ^ 1u;  // this step's maxima -> slots [nb]
@@ -701,8 +706,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 cudaError_t prepare_k3h_kernel() {
-    return cudaFuncSetAttribute(k3h_batched_power, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kSmem));
+    cudaError_t e = cudaFuncSetAttribute(k3h_batched_power<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmem));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k3h_batched_power<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kSmem));
+    return e;
 }
 
 cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch,
@@ -719,7 +729,10 @@ cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch
                   : 0;
     if (vec && !(encode_tile_map(&in_map, in, batch * 128) && encode_tile_map(&out_map, out, batch * 128)))
         vec = 0;
-    k3h_batched_power<<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec);
+    if (plan.mult[0] | plan.mult[1])
+        k3h_batched_power<true><<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec);
+    else
+        k3h_batched_power<false><<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec);
     return cudaGetLastError();
 }
 
