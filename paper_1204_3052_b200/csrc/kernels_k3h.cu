@@ -439,6 +439,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t outs = 0;                       // results handed to the IO warp so far (vec)
 
         const uint32_t lg_n = 32u - __clz(static_cast<int>(n - 1));  // ceil(log2 n), n >= 2
+        // max of the 16 per-warp slots at `slots`: lane i < 16 reads slot i, one
+        // warp reduction (2 instructions instead of 4 LDS.128 + 9 max)
+        auto max16 = [&](uint32_t slots) -> uint32_t {
+            uint32_t v = 0;
+            if (lane < 16) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(slots + lane * 4u) : "memory");
+            return __reduce_max_sync(0xFFFFFFFFu, v);
+        };
         // Per-warp maxima of a chain live in SMEM slots [cc][buffer][warp].
         // IN: exact max of the new input (one barrier among the 16 epilogue
         // warps, which also orders every warp's tile reads before the plane
@@ -449,13 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots + warp * 4u), "r"(m) : "memory");
             named_bar_sync(3, kWorkers * 32);
             if (lane == 0) mbar_arrive(max_bar + cc * 2 + buf);  // uniform hand-off to the next step
-            uint32_t r = 0;
-#pragma unroll
-            for (uint32_t i = 0; i < 4; ++i) {
-                const uint4 w4 = lds128(slots + 16u * i);
-                r = max(r, max(max(w4.x, w4.y), max(w4.z, w4.w)));
-            }
-            return r;
+            return max16(slots);
         };
         // max over the 16 slots written at this chain's previous epilogue
         // (long complete: every warp published since; the mbarrier wait is
@@ -464,13 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait_sleep(max_bar + cc * 2 + st.sb, (st.mph >> st.sb) & 1u);
             st.mph ^= 1u << st.sb;
             const uint32_t slots = s0 + kMaxOff + cc * 128u + st.sb * 64u;
-            uint32_t r = 0;
-#pragma unroll
-            for (uint32_t i = 0; i < 4; ++i) {
-                const uint4 w4 = lds128(slots + 16u * i);
-                r = max(r, max(max(w4.x, w4.y), max(w4.z, w4.w)));
-            }
-            return r;
+            return max16(slots);
         };
         // 16 values (columns col0 + 16h ...), scaled by sc2 here -> planes
         // y0/y1 of chain cc (right operand) and, if `left`, x0/x1 in TMEM;
@@ -657,13 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_ld_wait_dep(b);
                     publish_max(absmax16(fb, absmax16(fa, 0.f)));
                     named_bar_sync(3, kWorkers * 32);
-                    uint32_t mx = 0;
-#pragma unroll
-                    for (uint32_t i = 0; i < 4; ++i) {
-                        const uint4 w4 = lds128(slots + 16u * i);
-                        mx = max(mx, max(max(w4.x, w4.y), max(w4.z, w4.w)));
-                    }
-                    t = scale_exp(mx);
+                    t = scale_exp(max16(slots));
                     const uint64_t sc2 = splat2(exp2i(t));
                     emit_half(cc, fa, std::integral_constant<uint32_t, 0>{}, sc2, !mult);
                     emit_half(cc, fb, std::integral_constant<uint32_t, 1>{}, sc2, !mult);
