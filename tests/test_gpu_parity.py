@@ -523,3 +523,18 @@ def test_cluster_split_k_bitwise_equals_two_launch_split_k():
     b = _run_ab({"MXP_K1C": "0", "MXP_SPLITK": "global"})
     for i in (0, 2, 4, 8):  # n = 130, 256, 384, 896
         assert a[i] == b[i], f"chain {i // 2}"
+
+
+@pytest.mark.parametrize("n", [129, 200, 255, 257, 384, 511, 640, 768, 896])
+@pytest.mark.parametrize("k", [2, 3, 13])
+def test_one_launch_chain_sizes_vs_exact(eng, n, k):
+    """K1C over its whole size range (ragged n, split-K S = 1/2/4, plans with
+    and without MULTIPLY_BASE steps) against the exact product in f64, within
+    the chain tolerance."""
+    a = oracle.scaled_input(n, np.float32, 7)
+    got = eng.power(a, k)
+    exact = np.linalg.matrix_power(a.astype(np.float64), k)
+    assert np.isfinite(got).all()
+    assert fro(got, exact) <= mx.fro_tol(n, k, "f32"), (n, k, fro(got, exact))
+    assert eng.last_stats.launches == 2
+    assert eng.last_stats.multiply_count == mx.plan_exponentiation(k).multiply_count
