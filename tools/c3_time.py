@@ -29,4 +29,5 @@ for _ in range(reps):
     ts.append(e0.elapsed_time(e1))
 ts.sort()
 fl = 2.0 * n ** 3 * 6 * B  # 6 multiplies for A^64
-print(f"C3 B={B} median {ts[len(ts)//2]:.3f} ms min {ts[0]:.3f} -> {fl / ts[len(ts)//2] / 1e9:.1f} TFLOP/s")
+mean = sum(ts) / len(ts)
+print(f"C3 B={B} median {ts[len(ts)//2]:.3f} ms mean {mean:.3f} min {ts[0]:.3f} -> {fl / ts[len(ts)//2] / 1e9:.1f} TFLOP/s")
