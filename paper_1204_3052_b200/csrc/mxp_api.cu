@@ -102,7 +102,9 @@ struct mxp_handle_s {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
     // fp32 single-matrix workspace: 6 tf32 planes (base, ping, pong) x (hi, lo)
-    int64_t ws32_pad = 0;
+    int64_t ws32_pad = 0;  // padded order the planes are currently laid out for
+    int64_t ws32_cap = 0;  // padded order they are allocated for (>= ws32_pad)
+    size_t part_bytes = 0;
     uint32_t* planes[6] = {};
     float* part = nullptr;  // split-K workspace (splits x n_pad^2 fp32) for small n
     int splits = 1;
@@ -160,24 +162,40 @@ void stats_reset(mxp_stats* st) {
     st->failed_step = -1;
 }
 
+// The fp32 workspace for padded order n_pad: 6 planes (allocated for the
+// largest order seen, used with stride n_pad), the split-K factor of n_pad
+// (and, for the two-launch split-K, its partial-sum buffer).  Every call
+// runs at its own n_pad, whatever larger order the handle served before, so
+// a result does not depend on the handle's history.
 int ensure_ws32(mxp_handle h, int64_t n_pad) {
     h->rhs_mode = -1;
-    if (h->ws32_pad >= n_pad) return MXP_OK;
-    for (auto& p : h->planes) {
-        if (p) cudaFree(p);
-        p = nullptr;
+    if (h->ws32_cap < n_pad) {
+        for (auto& p : h->planes) {
+            if (p) cudaFree(p);
+            p = nullptr;
+        }
+        h->drop_graphs();
+        h->ws32_cap = 0;
+        h->ws32_pad = 0;
+        const size_t bytes = static_cast<size_t>(n_pad) * n_pad * 4;
+        for (auto& p : h->planes) MXP_CUDA(cudaMalloc(&p, bytes));
+        h->ws32_cap = n_pad;
     }
-    h->drop_graphs();
-    h->ws32_pad = 0;
-    const size_t bytes = static_cast<size_t>(n_pad) * n_pad * 4;
-    for (auto& p : h->planes) MXP_CUDA(cudaMalloc(&p, bytes));
-    if (h->part) cudaFree(h->part);
-    h->part = nullptr;
-    h->splits = (k1_block_n((int)n_pad, h->num_sms) == 128)
-                    ? k1_split_k((int)n_pad, (int)n_pad, h->num_sms)
-                    : 1;
-    if (h->splits > 1) MXP_CUDA(cudaMalloc(&h->part, bytes * h->splits));
-    h->ws32_pad = n_pad;
+    if (h->ws32_pad != n_pad) {
+        h->splits = (k1_block_n((int)n_pad, h->num_sms) == 128)
+                        ? k1_split_k((int)n_pad, (int)n_pad, h->num_sms)
+                        : 1;
+        const size_t need = h->splits > 1 ? static_cast<size_t>(n_pad) * n_pad * 4 * h->splits : 0;
+        if (need > h->part_bytes) {
+            h->drop_graphs();
+            if (h->part) cudaFree(h->part);
+            h->part = nullptr;
+            h->part_bytes = 0;
+            MXP_CUDA(cudaMalloc(&h->part, need));
+            h->part_bytes = need;
+        }
+        h->ws32_pad = n_pad;
+    }
     return MXP_OK;
 }
 

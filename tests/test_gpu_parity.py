@@ -538,3 +538,20 @@ def test_one_launch_chain_sizes_vs_exact(eng, n, k):
     assert fro(got, exact) <= mx.fro_tol(n, k, "f32"), (n, k, fro(got, exact))
     assert eng.last_stats.launches == 2
     assert eng.last_stats.multiply_count == mx.plan_exponentiation(k).multiply_count
+
+
+def test_result_independent_of_handle_history():
+    """A handle that served a larger order first must run a small chain at the
+    small order: same bits and same launch count as a fresh handle (the
+    workspace is reused, never the larger padding)."""
+    a = oracle.scaled_input(200, np.float32, 11)
+    fresh = Engine(0)
+    want = fresh.power(a, 13)
+    want_launches = fresh.last_stats.launches
+    fresh.close()
+    used = Engine(0)
+    used.multiply(oracle.scaled_input(1024, np.float32, 1), oracle.scaled_input(1024, np.float32, 2))
+    got = used.power(a, 13)
+    assert used.last_stats.launches == want_launches
+    used.close()
+    assert sha(got) == sha(want)
