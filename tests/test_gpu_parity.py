@@ -525,7 +525,7 @@ def test_cluster_split_k_bitwise_equals_two_launch_split_k():
         assert a[i] == b[i], f"chain {i // 2}"
 
 
-@pytest.mark.parametrize("n", [129, 200, 255, 257, 384, 511, 640, 768, 896])
+@pytest.mark.parametrize("n", [129, 200, 255, 257, 384, 511, 640, 768, 896, 1100, 1300])
 @pytest.mark.parametrize("k", [2, 3, 13])
 def test_one_launch_chain_sizes_vs_exact(eng, n, k):
     """K1C over its whole size range (ragged n, split-K S = 1/2/4, plans with
