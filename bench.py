@@ -166,7 +166,9 @@ def cpu_sample(w: dict, budget_s: float = 12.0) -> dict:
 
     import oracle
 
-    threads = oracle.max_threads()
+    # every host core this process may run on (torchrun sets OMP_NUM_THREADS=1
+    # for its ranks; the reference arm runs on rank 0 alone and uses them all)
+    threads = max(oracle.max_threads(), len(os.sched_getaffinity(0)))
     n, k = w["n"], w["k"]
     dt = np.float32 if w["dtype"] == "f32" else np.float64
     m = mults(k)
@@ -388,11 +390,20 @@ def main() -> None:
     import torch
 
     dist = None
+    # Test knob: BENCH_SHARE_GPU=1 maps every rank onto the visible GPUs
+    # round-robin and uses gloo, so the multi-rank path (per-rank seeds,
+    # barriers, max over ranks) runs on a one-GPU box (numbers meaningless).
+    share = os.environ.get("BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % max(torch.cuda.device_count(), 1)
     if world > 1 or os.environ.get("BENCH_FORCE_DIST") == "1":
         import torch.distributed as tdist
 
         torch.cuda.set_device(local)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = tdist
     else:
         torch.cuda.set_device(local)
