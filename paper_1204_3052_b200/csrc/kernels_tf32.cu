@@ -472,13 +472,14 @@ struct K1Cfg {
 // with round-to-nearest adds (splitk_reduce_kernel's order and arithmetic),
 // and hands each 4-column group to emit(row, unit, sum).  Up to 8 loads per
 // group are in flight before the adds.
-template <typename Emit>
+template <uint32_t kUnits = 32, typename Emit>
 __device__ __forceinline__ void cluster_reduce_tile(uint32_t s0, uint32_t S_, uint32_t rank,
                                                     Emit&& emit) {
+    // kUnits 16-byte units per partial row (row stride kUnits * 16 B)
     const uint32_t R = 128u / S_;
-    for (uint32_t i = threadIdx.x; i < R * 32u; i += blockDim.x) {
-        const uint32_t rr = rank * R + (i >> 5), u = i & 31u;
-        const uint32_t la = s0 + rr * 512u + ((u ^ (rr & 7u)) << 4);
+    for (uint32_t i = threadIdx.x; i < R * kUnits; i += blockDim.x) {
+        const uint32_t rr = rank * R + i / kUnits, u = i % kUnits;
+        const uint32_t la = s0 + rr * (kUnits * 16u) + ((u ^ (rr & 7u)) << 4);
         float4 v[8];
 #pragma unroll
         for (uint32_t p = 0; p < 8; ++p)
@@ -1079,6 +1080,14 @@ bool k1_split_legacy() {
     return v != 0;
 }
 int k1_split_launches(int splits) { return (splits > 1 && k1_split_legacy()) ? 2 : 1; }
+// MXP_K1C_NARROW=0: K1C keeps K1's 128-column tiles (A/B runs).
+static bool k1c_narrow_enabled() {
+    static const int v = [] {
+        const char* e = std::getenv("MXP_K1C_NARROW");
+        return (e != nullptr && std::strcmp(e, "0") == 0) ? 0 : 1;
+    }();
+    return v != 0;
+}
 
 // Clusters of cs K1 CTAs that can be resident at once (one CTA per SM; a
 // cluster must fit in one GPC): 148 / 74 / 33 / 15 for cs = 1 / 2 / 4 / 8 on
@@ -1173,13 +1182,29 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int tar
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(K1Cfg::kThreads, 1)
+// K1C tile width: 128 (K1's tiles) or 64 (twice the CTAs for the same split,
+// half the B operand and partial per CTA: the step is load- and
+// latency-bound at these sizes, not MMA-bound).
+template <int kBN_>
+struct K1CCfg {
+    static constexpr int kBN = kBN_;
+    static constexpr int kStages = kBN_ == 64 ? 4 : 3;
+    static constexpr uint32_t kABytes = 128 * 128;
+    static constexpr uint32_t kBBytes = 32 * 128 * (kBN_ / 32);
+    static constexpr uint32_t kStageBytes = 2 * kABytes + 2 * kBBytes;
+    static constexpr size_t kSmem = kStages * kStageBytes + 1024 + 256;
+    static constexpr int kThreads = 384;
+};
+
+template <int kBN_>
+__global__ void __launch_bounds__(384, 1)
     k1c_chain_3xtf32(const __grid_constant__ K1CMaps maps, const __grid_constant__ K1CPlanes pl,
                      PlanBits plan, int n_pad, float* __restrict__ out_f32, int n_out,
                      unsigned int* __restrict__ bar_ctr) {
-    using Cfg = K1Cfg;
+    using Cfg = K1CCfg<kBN_>;
     constexpr int S = Cfg::kStages;
     constexpr int BN = Cfg::kBN;
+    constexpr uint32_t kUnits = BN / 4;  // 16-byte units per partial row
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
@@ -1214,7 +1239,7 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
         }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc<256>(tmem_slot);
+    if (warp == 2) tmem_alloc<2 * BN>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1285,24 +1310,26 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
                 mma_commit(&cfull[c]);
             }
         } else if (warp >= 4) {
+            constexpr int kCols = BN / 2;  // columns per epilogue warp
             const int q = warp & 3;
-            const int ch = ((warp - 4) >> 2) * 64;
+            const int ch = ((warp - 4) >> 2) * kCols;
             const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
-            float sum[64];
+            float sum[kCols];
 #pragma unroll
-            for (int i = 0; i < 64; ++i) sum[i] = 0.f;
+            for (int i = 0; i < kCols; ++i) sum[i] = 0.f;
             for (int kb = 0; kb < kb_per; ++kb) {
                 const int g = g0 + kb;
                 const int c = g & 1;
                 mbar_wait(&cfull[c], (g >> 1) & 1);
                 tc_fence_after();
-                uint32_t v[32];
-                tmem_ld32(lane_base + c * BN + ch, v);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) sum[i] = __fadd_rn(sum[i], __uint_as_float(v[i]));
-                tmem_ld32(lane_base + c * BN + ch + 32, v);
+                for (int h = 0; h < kCols / 32; ++h) {
+                    uint32_t v[32];
+                    tmem_ld32(lane_base + c * BN + ch + 32 * h, v);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) sum[32 + i] = __fadd_rn(sum[32 + i], __uint_as_float(v[i]));
+                    for (int i = 0; i < 32; ++i)
+                        sum[32 * h + i] = __fadd_rn(sum[32 * h + i], __uint_as_float(v[i]));
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_relaxed(&cempty[c]);
@@ -1310,9 +1337,9 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
             if (warp == 4) K1C_STAMP(1);
             // partial -> SMEM (every MMA of the step has completed: stages free)
             const uint32_t rr = static_cast<uint32_t>(q * 32 + lane);
-            const uint32_t base = s0 + rr * 512u;
+            const uint32_t base = s0 + rr * (kUnits * 16u);
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
+            for (int u = 0; u < kCols / 4; ++u) {
                 const uint32_t uu = static_cast<uint32_t>(ch / 4 + u);
                 sts128(base + ((uu ^ (rr & 7u)) << 4), __float_as_uint(sum[4 * u]),
                        __float_as_uint(sum[4 * u + 1]), __float_as_uint(sum[4 * u + 2]),
@@ -1327,7 +1354,7 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
         {
             uint32_t* out_hi = pl.p[2 * dst];
             uint32_t* out_lo = pl.p[2 * dst + 1];
-            cluster_reduce_tile(s0, gridDim.y, cluster_ctarank(), [&](uint32_t rr, uint32_t u, float4 a) {
+            cluster_reduce_tile<kUnits>(s0, gridDim.y, cluster_ctarank(), [&](uint32_t rr, uint32_t u, float4 a) {
                 const int grow = m0 + static_cast<int>(rr), col = n0 + static_cast<int>(4u * u);
                 if (!last) {
                     uint4 hv, lv;
@@ -1358,12 +1385,17 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) tmem_dealloc<256>(tmem);
+    if (warp == 2) tmem_dealloc<2 * BN>(tmem);
 }
 
 static cudaError_t prepare_k1c() {
-    return cudaFuncSetAttribute(k1c_chain_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(K1Cfg::kSmem));
+    cudaError_t e = cudaFuncSetAttribute(k1c_chain_3xtf32<128>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(K1CCfg<128>::kSmem));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k1c_chain_3xtf32<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(K1CCfg<64>::kSmem));
+    return e;
 }
 
 // One cooperative launch for the whole chain; cudaErrorCooperativeLaunchTooLarge
@@ -1374,6 +1406,11 @@ cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
     if (splits < 1 || splits > 8 || n_pad % 128 != 0 || k1_split_legacy()) return cudaErrorNotSupported;
     const int tiles = (n_pad / 128) * (n_pad / 128);
     if (tiles > k1_max_clusters(splits)) return cudaErrorNotSupported;
+    // 64-column tiles when twice the clusters still fit one wave
+    int num_sms = 0;
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0);
+    const bool narrow = k1c_narrow_enabled() && 2 * tiles <= k1_max_clusters(splits) &&
+                        2 * tiles * splits <= num_sms;
     K1CMaps maps;
     K1CPlanes pl;
     for (int i = 0; i < 6; ++i) {
@@ -1384,9 +1421,9 @@ cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
     cudaError_t e = cudaMemsetAsync(bar_ctr, 0, sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(tiles, splits);
-    cfg.blockDim = dim3(K1Cfg::kThreads);
-    cfg.dynamicSmemBytes = K1Cfg::kSmem;
+    cfg.gridDim = dim3(narrow ? 2 * tiles : tiles, splits);
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = narrow ? K1CCfg<64>::kSmem : K1CCfg<128>::kSmem;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1397,7 +1434,11 @@ cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
     attr[1].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, k1c_chain_3xtf32, maps, pl, plan, n_pad, out_f32, n_out, bar_ctr);
+    if (narrow)
+        return cudaLaunchKernelEx(&cfg, k1c_chain_3xtf32<64>, maps, pl, plan, n_pad, out_f32, n_out,
+                                  bar_ctr);
+    return cudaLaunchKernelEx(&cfg, k1c_chain_3xtf32<128>, maps, pl, plan, n_pad, out_f32, n_out,
+                              bar_ctr);
 }
 
 cudaError_t launch_k1p_gemm_peers(const GemmPlanes& m, int n_pad, int m_pad, int ld_out,
