@@ -1407,8 +1407,9 @@ cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
     const int tiles = (n_pad / 128) * (n_pad / 128);
     if (tiles > k1_max_clusters(splits)) return cudaErrorNotSupported;
     // 64-column tiles when twice the clusters still fit one wave
-    int num_sms = 0;
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0);
+    int dev = 0, num_sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     const bool narrow = k1c_narrow_enabled() && 2 * tiles <= k1_max_clusters(splits) &&
                         2 * tiles * splits <= num_sms;
     K1CMaps maps;
