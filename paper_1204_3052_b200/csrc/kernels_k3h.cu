@@ -28,7 +28,7 @@
 // Per step of chain c one elected lane of the issue warp runs 24 MMAs
 // (M=N=128, K=16, A from TMEM): x1*y0, x0*y1, then x0*y0 — small terms first
 // because the tensor core truncates its fp32 accumulator on every MMA
-// (DESIGN.md §3).  The 16 epilogue warps alternate between the chains.
+// (DESIGN.md §3).  The 8 epilogue warps alternate between the chains.
 //
 // MULTIPLY_BASE computes base * acc (the base is the left operand), as K3
 // does: equal to the reference's acc * base (expo.py:135-136) because acc is
@@ -43,14 +43,14 @@
 namespace mxp {
 namespace {
 
-constexpr int kWorkers = 16;                   // epilogue warps: 4 TMEM lane quarters x 4
-constexpr int kIssueWarp = kWorkers + 1;       //   column groups, + one MMA-issue warp
+constexpr int kWorkers = 8;                    // epilogue warps: 4 TMEM lane quarters x 2
+constexpr int kIssueWarp = kWorkers + 1;       //   column halves, + one MMA-issue warp
 constexpr int kIOWarp = kWorkers;              //   + one TMA IO warp
-constexpr int kThreads = (kWorkers + 2) * 32;  // 576 (<= 96 registers per thread)
+constexpr int kThreads = (kWorkers + 2) * 32;  // 320 (<= 168 registers per thread)
 constexpr uint32_t kPlane = 128u * 128u * 2u;  // one fp16 plane: 32 KB
 constexpr uint32_t kChainSmem = 2u * kPlane;   // y0, y1 of one chain
 constexpr uint32_t kROff = 2u * kChainSmem;    // 64 KB: finished results on their way out (TMA)
-constexpr uint32_t kMaxOff = kROff + 65536u;   // [chain][buffer][16] per-warp max |D| slots
+constexpr uint32_t kMaxOff = kROff + 65536u;   // [chain][buffer][8] per-warp max |D| slots
 constexpr uint32_t kBarOff = kMaxOff + 256;    // mbarriers + TMEM slot
 constexpr size_t kSmem = kBarOff + 128 + 1024; // + alignment slack
 constexpr int kTarget = 13;                    // input: scaled max |A'| in [2^13, 2^14)
@@ -254,10 +254,13 @@ constexpr int kIn = -2;  // Chain::s: the next input is being loaded / converted
 // every other one starting at b + cG.  Three roles run the same deterministic
 // (chain, matrix, step) state machine, so they agree on every hand-off
 // without exchanging state:
-//   warps 0-15  epilogue: drain D, rescale, split, write the next operands;
-//   warp 16     MMA issue (one elected lane);
-//   warp 17     IO: TMA stores of finished results and TMA loads of the next
-//               inputs (n == 128), L2 prefetch one matrix ahead.
+//   warps 0-7   epilogue: drain D, rescale, split, write the next operands
+//               (a thread owns one row x 64 columns: 8 warps with 168
+//               registers each beat 16 with 96 — the per-step control and
+//               synchronisation cost is paid once per 64 values, not 32);
+//   warp 8      IO: TMA stores of finished results and TMA loads of the next
+//               inputs (n == 128), L2 prefetch one matrix ahead;
+//   warp 9      MMA issue (one elected lane).
 // A chain's matrix boundary takes two of its slots: OUT (drain the last
 // product into the warp tiles, hand them to the IO warp) and, one slot later,
 // IN (convert the freshly loaded input into operands, publish step 0).  In
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the 16 warp tiles of chain cc <-> matrix mm (TMA boxes of 32 x 32)
     auto tiles_load = [&](uint32_t cc, long long mm) {
         mbar_expect_tx(in_ready + cc, 16 * 4096);
-        for (uint32_t w = 0; w < kWorkers; ++w)
+        for (uint32_t w = 0; w < 16; ++w)
             tma_load_2d_s(s0 + cc * kChainSmem + w * 4096u, &in_map, in_ready + cc,
                           static_cast<int32_t>((w >> 2) * 32),
                           static_cast<int32_t>(mm * 128 + (w & 3) * 32));
@@ -415,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait_sleep(out_ready + C, st.ph);
             st.ph ^= 1;
             if (lane == 0) {
-                for (uint32_t w = 0; w < kWorkers; ++w)
+                for (uint32_t w = 0; w < 16; ++w)
                     tma_store_2d_s(&out_map, s0 + kROff + w * 4096u, static_cast<int32_t>((w >> 2) * 32),
                                    static_cast<int32_t>(m_prev * 128 + (w & 3) * 32));
                 bulk_commit_group();
@@ -431,95 +434,93 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (vec && lane == 0) bulk_wait_group0();  // results written before exit
     } else {
         // ------------------------------------------------------------ epilogue
+        // 8 warps: 4 TMEM lane quarters x 2 column halves; a thread owns row
+        // `row`, columns 64g .. 64g + 63 (four 16-column chunks)
         const uint32_t q = warp & 3, g = warp >> 2;
         const uint32_t row = q * 32 + lane;
-        const uint32_t col0 = g * 32;
+        const uint32_t col0 = g * 64;
         const uint32_t lane_base = tmem + ((q * 32) << 16);
-        const uint32_t tile_off = warp * 4096u;  // the warp's tile inside a 64 KB region
-        uint32_t outs = 0;                       // results handed to the IO warp so far (vec)
+        // its two 32 x 32 IO tiles (TMA boxes 8g + q and 8g + 4 + q of a region)
+        const uint32_t tile0 = (8u * g + q) * 4096u, tile1 = tile0 + 4u * 4096u;
+        uint32_t outs = 0;  // results handed to the IO warp so far (vec)
 
         const uint32_t lg_n = 32u - __clz(static_cast<int>(n - 1));  // ceil(log2 n), n >= 2
-        // max of the 16 per-warp slots at `slots`: lane i < 16 reads slot i, one
-        // warp reduction (2 instructions instead of 4 LDS.128 + 9 max)
-        auto max16 = [&](uint32_t slots) -> uint32_t {
+        // max of the 8 per-warp slots at `slots` (lane i < 8 reads slot i)
+        auto max8 = [&](uint32_t slots) -> uint32_t {
             uint32_t v = 0;
-            if (lane < 16) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(slots + lane * 4u) : "memory");
+            if (lane < kWorkers) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(slots + lane * 4u) : "memory");
             return __reduce_max_sync(0xFFFFFFFFu, v);
         };
+        auto absmax64 = [](const float* x) {
+            float m = 0.f;
+#pragma unroll
+            for (int i = 0; i < 64; i += 2) m = fmaxf(fmaxf(m, fabsf(x[i])), fabsf(x[i + 1]));
+            return __float_as_uint(m);
+        };
         // Per-warp maxima of a chain live in SMEM slots [cc][buffer][warp].
-        // IN: exact max of the new input (one barrier among the 16 epilogue
+        // IN: exact max of the new input (one barrier among the epilogue
         // warps, which also orders every warp's tile reads before the plane
         // writes); the slots then hold max |A| for the first step's bound.
         auto block_max_in = [&](uint32_t cc, uint32_t buf, const float* x) -> uint32_t {
-            const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, absmax_bits(x));
-            const uint32_t slots = s0 + kMaxOff + cc * 128u + buf * 64u;
+            const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, absmax64(x));
+            const uint32_t slots = s0 + kMaxOff + cc * 64u + buf * 32u;
             if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots + warp * 4u), "r"(m) : "memory");
             named_bar_sync(3, kWorkers * 32);
             if (lane == 0) mbar_arrive(max_bar + cc * 2 + buf);  // uniform hand-off to the next step
-            return max16(slots);
+            return max8(slots);
         };
-        // max over the 16 slots written at this chain's previous epilogue
-        // (long complete: every warp published since; the mbarrier wait is
-        // the acquire that makes the slots visible)
+        // max over the slots written at this chain's previous epilogue (the
+        // mbarrier wait is the acquire that makes them visible)
         auto slots_max = [&](uint32_t cc, Chain& st) -> uint32_t {
             mbar_wait_sleep(max_bar + cc * 2 + st.sb, (st.mph >> st.sb) & 1u);
             st.mph ^= 1u << st.sb;
-            const uint32_t slots = s0 + kMaxOff + cc * 128u + st.sb * 64u;
-            return max16(slots);
+            return max8(s0 + kMaxOff + cc * 64u + st.sb * 32u);
         };
-        // 16 values (columns col0 + 16h ...), scaled by sc2 here -> planes
-        // y0/y1 of chain cc (right operand) and, if `left`, x0/x1 in TMEM;
-        // !right: only x0/x1 (the base of a MULTIPLY_BASE step)
-        // Plane addresses of this thread's 16-byte units: row `row`, unit u of
-        // columns 32g + 8u' lives at (u ^ (row & 7)) << 4.  With u = u0 + j
-        // (u0 even, j = 0/1) that is (u0 ^ (row & 6)) + (j ^ (row & 1)), so
-        // four registers cover both halves and both units; chain and plane
-        // are immediate offsets (compile-time), nothing else is recomputed.
-        uint32_t sa00, sa01, sa10, sa11;
-        {
-            const uint32_t rb = s0 + (g >> 1) * 16384u + row * 128u;
-            const uint32_t u00 = (g & 1u) * 4u, u10 = u00 + 2u;
-            const uint32_t lo0 = (row & 1u) << 4, lo1 = ((row & 1u) ^ 1u) << 4;
-            sa00 = rb + ((u00 ^ (row & 6u)) << 4) + lo0;
-            sa01 = rb + ((u00 ^ (row & 6u)) << 4) + lo1;
-            sa10 = rb + ((u10 ^ (row & 6u)) << 4) + lo0;
-            sa11 = rb + ((u10 ^ (row & 6u)) << 4) + lo1;
-        }
-        // 16 values (columns col0 + 16h ...), scaled by sc2 here -> planes
+        // Plane addresses: row `row` of panel g, 16-byte unit u at
+        // (u ^ (row & 7)) << 4.  Chunk k (units 2k, 2k+1): unit 2k + i sits at
+        // pa_i ^ (k << 5); chain and plane are immediate offsets.
+        const uint32_t pa0 = s0 + g * 16384u + row * 128u + ((row & 6u) << 4) + ((row & 1u) << 4);
+        // chunk k (16 values, columns col0 + 16k ...), scaled by sc2 -> planes
         // y0/y1 of chain CC (right operand) and, if `left`, x0/x1 in TMEM
-        auto emit_half = [&](auto cc, const float* x, auto hh, uint64_t sc2, bool left) {
-            constexpr uint32_t CC = decltype(cc)::value, H = decltype(hh)::value;
+        auto emit_chunk = [&](auto cc, auto kk, const float* x, uint64_t sc2, bool left) {
+            constexpr uint32_t CC = decltype(cc)::value, K = decltype(kk)::value;
             uint32_t p0[8], p1[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) split2(x[2 * j], x[2 * j + 1], sc2, p0[j], p1[j]);
-            const uint32_t a0 = H ? sa10 : sa00, a1 = H ? sa11 : sa01;
+            const uint32_t a0 = pa0 ^ (K << 5), a1 = (pa0 ^ 16u) ^ (K << 5);
             sts128_imm<CC * kChainSmem>(a0, p0[0], p0[1], p0[2], p0[3]);
             sts128_imm<CC * kChainSmem>(a1, p0[4], p0[5], p0[6], p0[7]);
             sts128_imm<CC * kChainSmem + kPlane>(a0, p1[0], p1[1], p1[2], p1[3]);
             sts128_imm<CC * kChainSmem + kPlane>(a1, p1[4], p1[5], p1[6], p1[7]);
             if (left) {
-                const uint32_t tl = lane_base + CC * 256u + 128u + g * 16u + H * 8u;
+                const uint32_t tl = lane_base + CC * 256u + 128u + g * 32u + K * 8u;
                 tmem_st8(tl, p0);
                 tmem_st8(tl + 64u, p1);
             }
+        };
+        auto emit64 = [&](auto cc, const float* x, uint64_t sc2, bool left) {
+            emit_chunk(cc, std::integral_constant<uint32_t, 0>{}, x, sc2, left);
+            emit_chunk(cc, std::integral_constant<uint32_t, 1>{}, x + 16, sc2, left);
+            emit_chunk(cc, std::integral_constant<uint32_t, 2>{}, x + 32, sc2, left);
+            emit_chunk(cc, std::integral_constant<uint32_t, 3>{}, x + 48, sc2, left);
         };
         // the base of a MULTIPLY_BASE step: x0/x1 (TMEM) only
         auto emit_left = [&](uint32_t cc, const float* x, float sc) {
             const uint64_t sc2 = splat2(sc);
 #pragma unroll
-            for (uint32_t h = 0; h < 2; ++h) {
+            for (uint32_t k = 0; k < 4; ++k) {
                 uint32_t p0[8], p1[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) split2(x[16 * h + 2 * j], x[16 * h + 2 * j + 1], sc2, p0[j], p1[j]);
-                const uint32_t tl = lane_base + cc * 256u + 128u + g * 16u + h * 8u;
+                for (int j = 0; j < 8; ++j) split2(x[16 * k + 2 * j], x[16 * k + 2 * j + 1], sc2, p0[j], p1[j]);
+                const uint32_t tl = lane_base + cc * 256u + 128u + g * 32u + k * 8u;
                 tmem_st8(tl, p0);
                 tmem_st8(tl + 64u, p1);
             }
         };
-        auto emit = [&](auto cc, const float* x, float sc) {  // IN: all planes
-            const uint64_t sc2 = splat2(sc);
-            emit_half(cc, x, std::integral_constant<uint32_t, 0>{}, sc2, true);
-            emit_half(cc, x + 16, std::integral_constant<uint32_t, 1>{}, sc2, true);
+        auto load_row64 = [&](long long m, float (&x)[64]) {
+            const float* src = in + static_cast<size_t>(m) * n2;
+            load_row(src, n, row, col0, *reinterpret_cast<float(*)[32]>(x));
+            load_row(src, n, row, col0 + 32u, *reinterpret_cast<float(*)[32]>(x + 32));
         };
 
         auto slot = [&](Chain& st, auto cc) {
@@ -531,15 +532,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (st.s == kIn) {
                 // ---- IN: the new matrix -> scale, operands of step 0
-                float x[32];
+                float x[64];
                 K3H_MARK(7);
                 if (vec) {
                     mbar_wait_sleep(in_ready + C, st.inph);
                     st.inph ^= 1;
                     K3H_MARK(3);
-                    tile_get_rows(s0 + C * kChainSmem + tile_off, lane, x);
+                    tile_get_rows(s0 + C * kChainSmem + tile0, lane, *reinterpret_cast<float(*)[32]>(x));
+                    tile_get_rows(s0 + C * kChainSmem + tile1, lane, *reinterpret_cast<float(*)[32]>(x + 32));
                 } else {
-                    load_row(in + static_cast<size_t>(st.m) * n2, n, row, col0, x);
+                    load_row64(st.m, x);
                 }
                 st.sb ^= 1u;  // (the other buffer: the current one was read at OUT)
                 const uint32_t mA = block_max_in(C, st.sb, x);
@@ -549,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 st.eb = -t;
                 st.t_prev = t;
                 st.bmax_e = ilogb_bits(mA) + t;
-                emit(cc, x, exp2i(t));
+                emit64(cc, x, splat2(exp2i(t)), true);
                 K3H_MARK(5);
                 K3H_COUNT(13);
                 st.s = 0;
@@ -563,32 +565,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // exponent of this step's product: 2^(ex + ey) * D
                 const int pe = (is_mult(st.s) ? st.eb : st.e) + st.e;
                 if (st.s == last) {
-                    // ---- OUT: 2^pe * D -> the warp tile (the IO warp stores it)
+                    // ---- OUT: 2^pe * D -> the warp tiles (the IO warp stores them)
                     if (warp == 0 && lane == 0 && vec) mbar_arrive(planes_free + C);  // load the next input
                     (void)slots_max(C, st);  // consume the last step's maxima (keeps the parities in step)
-                    float v[32];
-                    tmem_ld32(lane_base + C * 256u + col0, reinterpret_cast<uint32_t(&)[32]>(v));
-                    const float f1 = exp2i(pe / 2), f2 = exp2i(pe - pe / 2);
-                    const uint64_t g1 = splat2(f1), g2 = splat2(f2);
+                    const uint64_t g1 = splat2(exp2i(pe / 2)), g2 = splat2(exp2i(pe - pe / 2));
+                    if (vec && outs > 0) mbar_wait_sleep(r_free, (outs - 1u) & 1u);
 #pragma unroll
-                    for (int i = 0; i < 32; i += 2) {  // two exact-range steps, packed
-                        uint64_t w;
-                        asm("mov.b64 %0, {%1, %2};" : "=l"(w) : "f"(v[i]), "f"(v[i + 1]));
-                        asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(w) : "l"(g1));
-                        asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(w) : "l"(g2));
-                        asm("mov.b64 {%0, %1}, %2;" : "=f"(v[i]), "=f"(v[i + 1]) : "l"(w));
+                    for (uint32_t h = 0; h < 2; ++h) {
+                        float v[32];
+                        tmem_ld32(lane_base + C * 256u + col0 + 32u * h, reinterpret_cast<uint32_t(&)[32]>(v));
+#pragma unroll
+                        for (int i = 0; i < 32; i += 2) {  // two exact-range steps, packed
+                            uint64_t w;
+                            asm("mov.b64 %0, {%1, %2};" : "=l"(w) : "f"(v[i]), "f"(v[i + 1]));
+                            asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(w) : "l"(g1));
+                            asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(w) : "l"(g2));
+                            asm("mov.b64 {%0, %1}, %2;" : "=f"(v[i]), "=f"(v[i + 1]) : "l"(w));
+                        }
+                        if (vec) tile_put_rows(s0 + kROff + (h ? tile1 : tile0), lane, v);
+                        else store_row(out + static_cast<size_t>(st.m) * n2, n, row, col0 + 32u * h, v);
                     }
                     if (vec) {
-                        if (outs > 0) mbar_wait_sleep(r_free, (outs - 1u) & 1u);
                         ++outs;
-                        tile_put_rows(s0 + kROff + tile_off, lane, v);
                         fence_proxy_async_smem();
                         tc_fence_before();  // D reads done before the next MMAs into D
                         __syncwarp();
                         if (lane == 0) mbar_arrive(out_ready + C);
                         K3H_MARK(2);
                     } else {
-                        store_row(out + static_cast<size_t>(st.m) * n2, n, row, col0, v);
                         tc_fence_before();
                     }
                     st.m += 2 * G;
@@ -596,11 +600,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     st.s = kIn;
                     return;  // no publish: IN follows one slot later
                 }
-                // ---- step: D -> operands of the next step.  Two 16-column
-                // halves; the second TMEM load is in flight while the first
-                // half is split, and the scale is settled under the first load.
-                uint32_t a[16], b[16];
-                tmem_ld16_async(lane_base + C * 256u + col0, a);
+                // ---- step: D -> operands of the next step.  All four 16-column
+                // TMEM loads are issued at once; the scale is settled under them.
                 // Scale for the split, from a bound instead of a barrier:
                 // |D| <= n max|X'| max|Y'|, with max|P'| known exactly one step
                 // late (the previous epilogue's maxima).  The scaled max stays
@@ -609,6 +610,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // bits of h1, so the exact path (block max, one barrier) runs
                 // whenever the previous product came out more than 2^12 below
                 // its bound (the input's exact max feeds the first step's bound).
+                uint32_t d0[16], d1[16], d2[16], d3[16];
+                tmem_ld16_async(lane_base + C * 256u + col0, d0);
+                tmem_ld16_async(lane_base + C * 256u + col0 + 16u, d1);
+                tmem_ld16_async(lane_base + C * 256u + col0 + 32u, d2);
+                tmem_ld16_async(lane_base + C * 256u + col0 + 48u, d3);
                 const bool was_mult = is_mult(st.s);
                 const uint32_t mprev = slots_max(C, st);
                 const int pmax_e = ilogb_bits(mprev) + st.t_prev;  // floor(log2 max|P'_s|)
@@ -618,53 +624,50 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (mprev == 0u || mprev >= 0x7F800000u) t = 0;  // zero / non-finite operand
                 st.s += 1;
                 const bool mult = is_mult(st.s);
-                const float* fa = reinterpret_cast<const float*>(a);
-                const float* fb = reinterpret_cast<const float*>(b);
                 const uint32_t nb = st.sb ^ 1u;  // this step's maxima -> slots [nb]
-                const uint32_t slots = s0 + kMaxOff + C * 128u + nb * 64u;
-                auto absmax16 = [](const float* x, float m) {
+                const uint32_t slots = s0 + kMaxOff + C * 64u + nb * 32u;
+                tmem_ld_wait_dep(d0);
+                tmem_ld_wait_dep(d1);
+                tmem_ld_wait_dep(d2);
+                tmem_ld_wait_dep(d3);
+                const float* f0 = reinterpret_cast<const float*>(d0);
+                const float* f1 = reinterpret_cast<const float*>(d1);
+                const float* f2 = reinterpret_cast<const float*>(d2);
+                const float* f3 = reinterpret_cast<const float*>(d3);
+                float m = 0.f;
 #pragma unroll
-                    for (int i = 0; i < 16; i += 2) m = fmaxf(fmaxf(m, fabsf(x[i])), fabsf(x[i + 1]));
-                    return m;
-                };
-                auto publish_max = [&](float m) {
-                    const uint32_t mw = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(m));
-                    if (lane == 0) {
-                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots + warp * 4u), "r"(mw) : "memory");
-                        mbar_arrive(max_bar + C * 2 + nb);
-                    }
-                };
-                K3H_MARK(1);
-                if (!exact) {
-                    t = max(-126, min(126, t));
-                    const uint64_t sc2 = splat2(exp2i(t));
-                    tmem_ld_wait_dep(a);
-                    tmem_ld16_async(lane_base + C * 256u + col0 + 16u, b);
-                    float m = absmax16(fa, 0.f);
-                    emit_half(cc, fa, std::integral_constant<uint32_t, 0>{}, sc2, !mult);
-                    tmem_ld_wait_dep(b);
-                    m = absmax16(fb, m);
-                    emit_half(cc, fb, std::integral_constant<uint32_t, 1>{}, sc2, !mult);
-                    publish_max(m);
-                } else {
-                    tmem_ld_wait_dep(a);
-                    tmem_ld16_async(lane_base + C * 256u + col0 + 16u, b);
-                    tmem_ld_wait_dep(b);
-                    publish_max(absmax16(fb, absmax16(fa, 0.f)));
-                    named_bar_sync(3, kWorkers * 32);
-                    t = scale_exp(max16(slots));
-                    const uint64_t sc2 = splat2(exp2i(t));
-                    emit_half(cc, fa, std::integral_constant<uint32_t, 0>{}, sc2, !mult);
-                    emit_half(cc, fb, std::integral_constant<uint32_t, 1>{}, sc2, !mult);
+                for (int i = 0; i < 16; i += 2) {
+                    m = fmaxf(fmaxf(m, fabsf(f0[i])), fabsf(f0[i + 1]));
+                    m = fmaxf(fmaxf(m, fabsf(f1[i])), fabsf(f1[i + 1]));
+                    m = fmaxf(fmaxf(m, fabsf(f2[i])), fabsf(f2[i + 1]));
+                    m = fmaxf(fmaxf(m, fabsf(f3[i])), fabsf(f3[i + 1]));
                 }
+                const uint32_t mw = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(m));
+                if (lane == 0) {
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots + warp * 4u), "r"(mw) : "memory");
+                    if (!exact) mbar_arrive(max_bar + C * 2 + nb);
+                }
+                K3H_MARK(1);
+                if (exact) {
+                    named_bar_sync(3, kWorkers * 32);
+                    if (lane == 0) mbar_arrive(max_bar + C * 2 + nb);
+                    t = scale_exp(max8(slots));
+                } else {
+                    t = max(-126, min(126, t));
+                }
+                const uint64_t sc2 = splat2(exp2i(t));
+                emit_chunk(cc, std::integral_constant<uint32_t, 0>{}, f0, sc2, !mult);
+                emit_chunk(cc, std::integral_constant<uint32_t, 1>{}, f1, sc2, !mult);
+                emit_chunk(cc, std::integral_constant<uint32_t, 2>{}, f2, sc2, !mult);
+                emit_chunk(cc, std::integral_constant<uint32_t, 3>{}, f3, sc2, !mult);
                 st.sb = nb;
                 st.t_prev = t;
                 st.e = pe - t;
                 K3H_MARK(6);
                 K3H_COUNT(14);
                 if (mult) {  // left operand = the base, rescaled by its input exponent
-                    float x[32];
-                    load_row(in + static_cast<size_t>(st.m) * n2, n, row, col0, x);
+                    float x[64];
+                    load_row64(st.m, x);
                     emit_left(C, x, exp2i(-st.eb));
                 }
             }
@@ -675,7 +678,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             if (warp == 2) K3H_EV(evs, 4);
             if (warp == 0) K3H_EV(evs, 5);
-            if (warp == 15) K3H_EV(evs, 6);
+            if (warp == 7) K3H_EV(evs, 6);
 #ifdef K3H_EVT
             ++evs;
 #endif
