@@ -613,8 +613,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t d0[16], d1[16], d2[16], d3[16];
                 tmem_ld16_async(lane_base + C * 256u + col0, d0);
                 tmem_ld16_async(lane_base + C * 256u + col0 + 16u, d1);
-                tmem_ld16_async(lane_base + C * 256u + col0 + 32u, d2);
-                tmem_ld16_async(lane_base + C * 256u + col0 + 48u, d3);
                 const bool was_mult = is_mult(st.s);
                 const uint32_t mprev = slots_max(C, st);
                 const int pmax_e = ilogb_bits(mprev) + st.t_prev;  // floor(log2 max|P'_s|)
@@ -626,40 +624,55 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool mult = is_mult(st.s);
                 const uint32_t nb = st.sb ^ 1u;  // this step's maxima -> slots [nb]
                 const uint32_t slots = s0 + kMaxOff + C * 64u + nb * 32u;
-                tmem_ld_wait_dep(d0);
-                tmem_ld_wait_dep(d1);
-                tmem_ld_wait_dep(d2);
-                tmem_ld_wait_dep(d3);
                 const float* f0 = reinterpret_cast<const float*>(d0);
                 const float* f1 = reinterpret_cast<const float*>(d1);
                 const float* f2 = reinterpret_cast<const float*>(d2);
                 const float* f3 = reinterpret_cast<const float*>(d3);
-                float m = 0.f;
+                auto absmax32 = [](const float* x, const float* y, float m) {
 #pragma unroll
-                for (int i = 0; i < 16; i += 2) {
-                    m = fmaxf(fmaxf(m, fabsf(f0[i])), fabsf(f0[i + 1]));
-                    m = fmaxf(fmaxf(m, fabsf(f1[i])), fabsf(f1[i + 1]));
-                    m = fmaxf(fmaxf(m, fabsf(f2[i])), fabsf(f2[i + 1]));
-                    m = fmaxf(fmaxf(m, fabsf(f3[i])), fabsf(f3[i + 1]));
-                }
-                const uint32_t mw = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(m));
-                if (lane == 0) {
-                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots + warp * 4u), "r"(mw) : "memory");
-                    if (!exact) mbar_arrive(max_bar + C * 2 + nb);
-                }
+                    for (int i = 0; i < 16; i += 2) {
+                        m = fmaxf(fmaxf(m, fabsf(x[i])), fabsf(x[i + 1]));
+                        m = fmaxf(fmaxf(m, fabsf(y[i])), fabsf(y[i + 1]));
+                    }
+                    return m;
+                };
+                // columns 0-31 land, columns 32-63 are loaded while they are split
+                tmem_ld_wait_dep(d0);
+                tmem_ld_wait_dep(d1);
+                tmem_ld16_async(lane_base + C * 256u + col0 + 32u, d2);
+                tmem_ld16_async(lane_base + C * 256u + col0 + 48u, d3);
+                float m = absmax32(f0, f1, 0.f);
                 K3H_MARK(1);
-                if (exact) {
+                if (!exact) {
+                    t = max(-126, min(126, t));
+                    const uint64_t sc2 = splat2(exp2i(t));
+                    emit_chunk(cc, std::integral_constant<uint32_t, 0>{}, f0, sc2, !mult);
+                    emit_chunk(cc, std::integral_constant<uint32_t, 1>{}, f1, sc2, !mult);
+                    tmem_ld_wait_dep(d2);
+                    tmem_ld_wait_dep(d3);
+                    m = absmax32(f2, f3, m);
+                    const uint32_t mw = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(m));
+                    if (lane == 0) {
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots + warp * 4u), "r"(mw) : "memory");
+                        mbar_arrive(max_bar + C * 2 + nb);
+                    }
+                    emit_chunk(cc, std::integral_constant<uint32_t, 2>{}, f2, sc2, !mult);
+                    emit_chunk(cc, std::integral_constant<uint32_t, 3>{}, f3, sc2, !mult);
+                } else {
+                    tmem_ld_wait_dep(d2);
+                    tmem_ld_wait_dep(d3);
+                    m = absmax32(f2, f3, m);
+                    const uint32_t mw = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(m));
+                    if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots + warp * 4u), "r"(mw) : "memory");
                     named_bar_sync(3, kWorkers * 32);
                     if (lane == 0) mbar_arrive(max_bar + C * 2 + nb);
                     t = scale_exp(max8(slots));
-                } else {
-                    t = max(-126, min(126, t));
+                    const uint64_t sc2 = splat2(exp2i(t));
+                    emit_chunk(cc, std::integral_constant<uint32_t, 0>{}, f0, sc2, !mult);
+                    emit_chunk(cc, std::integral_constant<uint32_t, 1>{}, f1, sc2, !mult);
+                    emit_chunk(cc, std::integral_constant<uint32_t, 2>{}, f2, sc2, !mult);
+                    emit_chunk(cc, std::integral_constant<uint32_t, 3>{}, f3, sc2, !mult);
                 }
-                const uint64_t sc2 = splat2(exp2i(t));
-                emit_chunk(cc, std::integral_constant<uint32_t, 0>{}, f0, sc2, !mult);
-                emit_chunk(cc, std::integral_constant<uint32_t, 1>{}, f1, sc2, !mult);
-                emit_chunk(cc, std::integral_constant<uint32_t, 2>{}, f2, sc2, !mult);
-                emit_chunk(cc, std::integral_constant<uint32_t, 3>{}, f3, sc2, !mult);
                 st.sb = nb;
                 st.t_prev = t;
                 st.e = pe - t;
