@@ -49,8 +49,7 @@ constexpr int kIOWarp = kWorkers;              //   + one TMA IO warp
 constexpr int kThreads = (kWorkers + 2) * 32;  // 320 (<= 168 registers per thread)
 constexpr uint32_t kPlane = 128u * 128u * 2u;  // one fp16 plane: 32 KB
 constexpr uint32_t kChainSmem = 2u * kPlane;   // y0, y1 of one chain
-constexpr uint32_t kROff = 2u * kChainSmem;    // 64 KB: finished results on their way out (TMA)
-constexpr uint32_t kMaxOff = kROff + 65536u;   // [chain][buffer][8] per-warp max |D| slots
+constexpr uint32_t kMaxOff = 3u * kChainSmem;  // after 3 regions: [chain][buffer][8] max slots
 constexpr uint32_t kBarOff = kMaxOff + 256;    // mbarriers + TMEM slot
 constexpr size_t kSmem = kBarOff + 128 + 1024; // + alignment slack
 constexpr int kTarget = 13;                    // input: scaled max |A'| in [2^13, 2^14)
@@ -177,8 +176,8 @@ __device__ __forceinline__ void tile_get_rows(uint32_t tile, uint32_t lane, floa
 // (the asm blocks elect one lane) so descriptors and TMEM addresses stay on
 // the uniform datapath — the issue rate bounds the kernel.
 template <uint32_t C>
-__device__ __forceinline__ void k3h_issue(uint32_t tbase, uint32_t s0, uint64_t* mma_bar) {
-    const uint64_t y0 = smem_desc(s0 + C * kChainSmem, 16384, 1024, 2);
+__device__ __forceinline__ void k3h_issue(uint32_t tbase, uint32_t region, uint64_t* mma_bar) {
+    const uint64_t y0 = smem_desc(region, 16384, 1024, 2);
     constexpr uint32_t D = C * 256u, X0 = D + 128u, X1 = D + 192u;
     constexpr uint32_t Y1 = kPlane >> 4;
     mma_f16_ts_x8<D, X1, 0, kBStep, true>(tbase, y0, kIdescNegA);  // x1*y0 (first: D =)
@@ -246,6 +245,7 @@ struct Chain {
     int bmax_e;     // floor(log2 max |base'|)
     uint32_t sb;    // max-slot buffer the next epilogue reads (0/1)
     uint32_t mph;   // max_bar parities, bit b for buffer b
+    uint32_t home;  // SMEM region (0..2) holding the chain's operand planes
     bool act;
 };
 constexpr int kIn = -2;  // Chain::s: the next input is being loaded / converted
@@ -261,11 +261,13 @@ constexpr int kIn = -2;  // Chain::s: the next input is being loaded / converted
 //   warp 8      IO: TMA stores of finished results and TMA loads of the next
 //               inputs (n == 128), L2 prefetch one matrix ahead;
 //   warp 9      MMA issue (one elected lane).
-// A chain's matrix boundary takes two of its slots: OUT (drain the last
-// product into the warp tiles, hand them to the IO warp) and, one slot later,
-// IN (convert the freshly loaded input into operands, publish step 0).  In
-// between the epilogue warps serve the other chain, so the HBM round trip
-// overlaps that chain's MMAs.
+// SMEM holds three 64 KB regions: each chain's operand planes (its home) and
+// a spare that the IO warp fills, ahead of time, with the next input of
+// whichever chain reaches a matrix boundary next.  A boundary is one slot:
+// the last product goes out through the old home (fp32 tiles, TMA store),
+// the next input is converted in place in the spare, which becomes the new
+// home, and step 0 is published — the chain's MMAs resume one slot later,
+// never waiting for HBM.
 // kMults: the plan has MULTIPLY_BASE steps.  Square-only plans (k a power
 // of two) run the kMults = false instance, which drops every base-operand
 // path from the epilogue.
@@ -278,12 +280,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = align1024(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
     uint64_t* mma_bar = bars;        // [2] a chain's step MMAs completed
-    uint64_t* out_ready = bars + 2;  // [2] a chain's result is in its warp tiles (16 arrivals)
-    uint64_t* in_ready = bars + 4;   // [2] a chain's next input landed in its warp tiles (TMA)
-    uint64_t* max_bar = bars + 6;    // [chain][buffer] the 16 per-warp maxima are written
-    uint64_t* r_free = bars + 10;    // the result region's last TMA store has read it
-    uint64_t* planes_free = bars + 11;  // [2] a chain's last step's MMAs are done (OUT)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+    uint64_t* out_ready = bars + 2;  // [2] a chain's result is in its old home (8 arrivals)
+    uint64_t* in_ready = bars + 4;   // [3] an input landed in region r (TMA)
+    uint64_t* max_bar = bars + 7;    // [chain][buffer] the 8 per-warp maxima are written
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -293,12 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(mma_bar + 1, 1);
         mbar_init(out_ready, kWorkers);
         mbar_init(out_ready + 1, kWorkers);
-        mbar_init(in_ready, 1);
-        mbar_init(in_ready + 1, 1);
+        for (int i = 0; i < 3; ++i) mbar_init(in_ready + i, 1);
         for (int i = 0; i < 4; ++i) mbar_init(max_bar + i, kWorkers);
-        mbar_init(r_free, 1);
-        mbar_init(planes_free, 1);
-        mbar_init(planes_free + 1, 1);
         fence_mbar_init();
     }
     if (warp == kIssueWarp) tmem_alloc<512>(tmem_slot);
@@ -318,13 +314,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     ch0.s = ch1.s = kIn;
     ch0.act = ch0.m < batch;
     ch1.act = ch1.m < batch;
+    ch0.home = 0;
+    ch1.home = 1;
+    uint32_t spare = 2;  // every role tracks the region rotation identically
     // Start-phase skew: chain c of CTA b sits out its first dly slots, so the
-    // chains' matrix boundaries are spread over the plan instead of hitting
-    // HBM from all 296 chains at once.
+    // CTAs' matrix boundaries are spread over the plan (HBM bursts), and the
+    // two chains of a CTA are half a plan apart (the spare is refilled
+    // between their boundaries).
     if (batch >= 4 * G && plan.len > 1) {
         ch0.dly = (2 * static_cast<int>(blockIdx.x)) % plan.len;
-        ch1.dly = (2 * static_cast<int>(blockIdx.x) + 1) % plan.len;
+        ch1.dly = ch0.dly + plan.len / 2;
     }
+    auto has_next = [&](const Chain& st) { return st.m + 2 * G < batch; };
 #ifdef K3H_TRACE
     if (tid < 16) k3h_acc[tid] = 0;
     __syncthreads();
@@ -338,11 +339,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     do {                \
     } while (0)
 #endif
-    // the 16 warp tiles of chain cc <-> matrix mm (TMA boxes of 32 x 32)
-    auto tiles_load = [&](uint32_t cc, long long mm) {
-        mbar_expect_tx(in_ready + cc, 16 * 4096);
+    // the 16 warp tiles of region rg <-> matrix mm (TMA boxes of 32 x 32)
+    auto tiles_load = [&](uint32_t rg, long long mm) {
+        mbar_expect_tx(in_ready + rg, 16 * 4096);
         for (uint32_t w = 0; w < 16; ++w)
-            tma_load_2d_s(s0 + cc * kChainSmem + w * 4096u, &in_map, in_ready + cc,
+            tma_load_2d_s(s0 + rg * kChainSmem + w * 4096u, &in_map, in_ready + rg,
                           static_cast<int32_t>((w >> 2) * 32),
                           static_cast<int32_t>(mm * 128 + (w & 3) * 32));
         if (mm + 2 * G < batch)
@@ -358,20 +359,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                 --st.dly;
                 return;
             }
-            if (st.s == last) {  // OUT slot: nothing to issue
+            if (st.s == last) {  // boundary: step 0 of the next matrix, in the spare
+                const bool more = has_next(st);
                 st.m += 2 * G;
-                st.act = st.m < batch;
-                st.s = kIn;
-                return;
+                st.act = more;
+                if (!more) return;
+                const uint32_t h = st.home;
+                st.home = spare;
+                spare = h;
+                st.s = 0;
+            } else {
+                st.s = (st.s == kIn) ? 0 : st.s + 1;
             }
-            st.s = (st.s == kIn) ? 0 : st.s + 1;
             K3H_MARK(10);
             K3H_EV(evs, 0);
             named_bar_sync(1 + C, kWorkers * 32 + 32);
             K3H_MARK(8);
             K3H_EV(evs, 1);
             tc_fence_after();
-            k3h_issue<C>(tmem, s0, mma_bar);
+            k3h_issue<C>(tmem, s0 + st.home * kChainSmem, mma_bar);
             __syncwarp();
             K3H_EV(evs, 2);
 #ifdef K3H_EVT
@@ -385,14 +391,43 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == kIOWarp) {
         // ------------------------------------------------------------ IO (TMA)
+        // Which chain reaches its next boundary first with a matrix after it,
+        // and that matrix: replays the shared state machine from the slot
+        // after chain `from`'s.
+        auto next_boundary = [&](uint32_t from, long long& mm) -> int {
+            Chain a = ch0, b = ch1;
+            for (int it = 0; it < 4 * (plan.len + 2) + 8; ++it) {
+                for (uint32_t k = 0; k < 2; ++k) {
+                    const uint32_t c = (from + 1 + k) & 1u;
+                    Chain& st = c == 0 ? a : b;
+                    if (!st.act) continue;
+                    if (st.dly > 0) {
+                        --st.dly;
+                        continue;
+                    }
+                    if (st.s == last) {
+                        if (has_next(st)) {
+                            mm = st.m + 2 * G;
+                            return static_cast<int>(c);
+                        }
+                        st.act = false;
+                        continue;
+                    }
+                    st.s = (st.s == kIn) ? 0 : st.s + 1;
+                }
+                if (!a.act && !b.act) break;
+            }
+            return -1;
+        };
         if (vec && lane == 0) {
-            if (ch0.act) tiles_load(0, ch0.m);
-            if (ch1.act) tiles_load(1, ch1.m);
+            if (ch0.act) tiles_load(ch0.home, ch0.m);
+            if (ch1.act) tiles_load(ch1.home, ch1.m);
+            long long mm = 0;
+            if (next_boundary(1, mm) >= 0) tiles_load(spare, mm);
         }
-        // Matrix boundary of chain C: as soon as the last step's MMAs are done
-        // (its operand planes are dead) the next input is TMA-loaded into
-        // the chain's plane region; the result meanwhile goes out from the
-        // separate region R, so the load does not wait for the store.
+        // Boundary of chain C: its result is in the old home once the
+        // epilogue says so; store it, and when the store has read the region,
+        // fill it (the new spare) with the input of the next boundary.
         auto slot = [&](Chain& st, auto cc) {
             constexpr uint32_t C = decltype(cc)::value;
             if (!st.act) return;
@@ -405,25 +440,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                 return;
             }
             const long long m_prev = st.m;
+            const bool more = has_next(st);
+            const uint32_t old_home = st.home;
             st.m += 2 * G;
-            st.act = st.m < batch;
-            st.s = kIn;
+            st.act = more;
+            if (more) {
+                st.home = spare;
+                spare = old_home;
+                st.s = 0;
+            }
             if (!vec) return;
-            // (signalled by the epilogue, which tracks every mma_bar phase; a
-            // parity wait on mma_bar here could alias a phase the IO warp,
-            // running ahead, has not reached yet)
-            mbar_wait_sleep(planes_free + C, st.inph);
-            st.inph ^= 1;
-            if (lane == 0 && st.act) tiles_load(C, st.m);
             mbar_wait_sleep(out_ready + C, st.ph);
             st.ph ^= 1;
             if (lane == 0) {
                 for (uint32_t w = 0; w < 16; ++w)
-                    tma_store_2d_s(&out_map, s0 + kROff + w * 4096u, static_cast<int32_t>((w >> 2) * 32),
+                    tma_store_2d_s(&out_map, s0 + old_home * kChainSmem + w * 4096u,
+                                   static_cast<int32_t>((w >> 2) * 32),
                                    static_cast<int32_t>(m_prev * 128 + (w & 3) * 32));
                 bulk_commit_group();
-                bulk_wait_group_read0();
-                mbar_arrive(r_free);  // R may take the next result
+                if (more) {
+                    bulk_wait_group_read0();  // the old home is the new spare
+                    long long mm = 0;
+                    if (next_boundary(C, mm) >= 0) tiles_load(spare, mm);
+                }
             }
             __syncwarp();
         };
@@ -442,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_base = tmem + ((q * 32) << 16);
         // its two 32 x 32 IO tiles (TMA boxes 8g + q and 8g + 4 + q of a region)
         const uint32_t tile0 = (8u * g + q) * 4096u, tile1 = tile0 + 4u * 4096u;
-        uint32_t outs = 0;  // results handed to the IO warp so far (vec)
+        uint32_t rph = 0;   // in_ready parities, bit r for region r
 
         const uint32_t lg_n = 32u - __clz(static_cast<int>(n - 1));  // ceil(log2 n), n >= 2
         // max of the 8 per-warp slots at `slots` (lane i < 8 reads slot i)
@@ -479,30 +518,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Plane addresses: row `row` of panel g, 16-byte unit u at
         // (u ^ (row & 7)) << 4.  Chunk k (units 2k, 2k+1): unit 2k + i sits at
         // pa_i ^ (k << 5); chain and plane are immediate offsets.
-        const uint32_t pa0 = s0 + g * 16384u + row * 128u + ((row & 6u) << 4) + ((row & 1u) << 4);
+        const uint32_t pa0 = g * 16384u + row * 128u + ((row & 6u) << 4) + ((row & 1u) << 4);
         // chunk k (16 values, columns col0 + 16k ...), scaled by sc2 -> planes
-        // y0/y1 of chain CC (right operand) and, if `left`, x0/x1 in TMEM
-        auto emit_chunk = [&](auto cc, auto kk, const float* x, uint64_t sc2, bool left) {
+        // y0/y1 in the region whose row base is ra = region + pa0 (right
+        // operand) and, if `left`, x0/x1 of chain CC in TMEM
+        auto emit_chunk = [&](auto cc, auto kk, uint32_t ra, const float* x, uint64_t sc2, bool left) {
             constexpr uint32_t CC = decltype(cc)::value, K = decltype(kk)::value;
             uint32_t p0[8], p1[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) split2(x[2 * j], x[2 * j + 1], sc2, p0[j], p1[j]);
-            const uint32_t a0 = pa0 ^ (K << 5), a1 = (pa0 ^ 16u) ^ (K << 5);
-            sts128_imm<CC * kChainSmem>(a0, p0[0], p0[1], p0[2], p0[3]);
-            sts128_imm<CC * kChainSmem>(a1, p0[4], p0[5], p0[6], p0[7]);
-            sts128_imm<CC * kChainSmem + kPlane>(a0, p1[0], p1[1], p1[2], p1[3]);
-            sts128_imm<CC * kChainSmem + kPlane>(a1, p1[4], p1[5], p1[6], p1[7]);
+            const uint32_t a0 = ra ^ (K << 5), a1 = (ra ^ 16u) ^ (K << 5);
+            sts128_imm<0>(a0, p0[0], p0[1], p0[2], p0[3]);
+            sts128_imm<0>(a1, p0[4], p0[5], p0[6], p0[7]);
+            sts128_imm<kPlane>(a0, p1[0], p1[1], p1[2], p1[3]);
+            sts128_imm<kPlane>(a1, p1[4], p1[5], p1[6], p1[7]);
             if (left) {
                 const uint32_t tl = lane_base + CC * 256u + 128u + g * 32u + K * 8u;
                 tmem_st8(tl, p0);
                 tmem_st8(tl + 64u, p1);
             }
         };
-        auto emit64 = [&](auto cc, const float* x, uint64_t sc2, bool left) {
-            emit_chunk(cc, std::integral_constant<uint32_t, 0>{}, x, sc2, left);
-            emit_chunk(cc, std::integral_constant<uint32_t, 1>{}, x + 16, sc2, left);
-            emit_chunk(cc, std::integral_constant<uint32_t, 2>{}, x + 32, sc2, left);
-            emit_chunk(cc, std::integral_constant<uint32_t, 3>{}, x + 48, sc2, left);
+        auto emit64 = [&](auto cc, uint32_t ra, const float* x, uint64_t sc2, bool left) {
+            emit_chunk(cc, std::integral_constant<uint32_t, 0>{}, ra, x, sc2, left);
+            emit_chunk(cc, std::integral_constant<uint32_t, 1>{}, ra, x + 16, sc2, left);
+            emit_chunk(cc, std::integral_constant<uint32_t, 2>{}, ra, x + 32, sc2, left);
+            emit_chunk(cc, std::integral_constant<uint32_t, 3>{}, ra, x + 48, sc2, left);
         };
         // the base of a MULTIPLY_BASE step: x0/x1 (TMEM) only
         auto emit_left = [&](uint32_t cc, const float* x, float sc) {
@@ -523,6 +563,35 @@ __global__ void __launch_bounds__(kThreads, 1)
             load_row(src, n, row, col0 + 32u, *reinterpret_cast<float(*)[32]>(x + 32));
         };
 
+        // a new matrix (in the chain's home region) -> exact scale, operands
+        // of step 0
+        auto convert_input = [&](auto cc, Chain& st) {
+            constexpr uint32_t C = decltype(cc)::value;
+            float x[64];
+            const uint32_t rg = st.home;
+            if (vec) {
+                mbar_wait_sleep(in_ready + rg, (rph >> rg) & 1u);
+                rph ^= 1u << rg;
+                K3H_MARK(3);
+                tile_get_rows(s0 + rg * kChainSmem + tile0, lane, *reinterpret_cast<float(*)[32]>(x));
+                tile_get_rows(s0 + rg * kChainSmem + tile1, lane, *reinterpret_cast<float(*)[32]>(x + 32));
+            } else {
+                load_row64(st.m, x);
+            }
+            st.sb ^= 1u;  // (the other buffer: the current one was read at the boundary)
+            const uint32_t mA = block_max_in(C, st.sb, x);  // (also orders tile reads before plane writes)
+            const int t = scale_exp(mA);
+            K3H_MARK(4);
+            st.e = -t;
+            st.eb = -t;
+            st.t_prev = t;
+            st.bmax_e = ilogb_bits(mA) + t;
+            emit64(cc, s0 + rg * kChainSmem + pa0, x, splat2(exp2i(t)), true);
+            K3H_MARK(5);
+            K3H_COUNT(13);
+            st.s = 0;
+        };
+
         auto slot = [&](Chain& st, auto cc) {
             constexpr uint32_t C = decltype(cc)::value;
             if (!st.act) return;
@@ -531,30 +600,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 return;
             }
             if (st.s == kIn) {
-                // ---- IN: the new matrix -> scale, operands of step 0
-                float x[64];
+                // ---- the chain's first matrix, converted in its home region
                 K3H_MARK(7);
-                if (vec) {
-                    mbar_wait_sleep(in_ready + C, st.inph);
-                    st.inph ^= 1;
-                    K3H_MARK(3);
-                    tile_get_rows(s0 + C * kChainSmem + tile0, lane, *reinterpret_cast<float(*)[32]>(x));
-                    tile_get_rows(s0 + C * kChainSmem + tile1, lane, *reinterpret_cast<float(*)[32]>(x + 32));
-                } else {
-                    load_row64(st.m, x);
-                }
-                st.sb ^= 1u;  // (the other buffer: the current one was read at OUT)
-                const uint32_t mA = block_max_in(C, st.sb, x);
-                const int t = scale_exp(mA);
-                K3H_MARK(4);
-                st.e = -t;
-                st.eb = -t;
-                st.t_prev = t;
-                st.bmax_e = ilogb_bits(mA) + t;
-                emit64(cc, x, splat2(exp2i(t)), true);
-                K3H_MARK(5);
-                K3H_COUNT(13);
-                st.s = 0;
+                convert_input(cc, st);
             } else {
                 K3H_MARK(7);
                 mbar_wait_sleep(mma_bar + C, st.ph);
@@ -565,11 +613,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // exponent of this step's product: 2^(ex + ey) * D
                 const int pe = (is_mult(st.s) ? st.eb : st.e) + st.e;
                 if (st.s == last) {
-                    // ---- OUT: 2^pe * D -> the warp tiles (the IO warp stores them)
-                    if (warp == 0 && lane == 0 && vec) mbar_arrive(planes_free + C);  // load the next input
+                    // ---- boundary: 2^pe * D -> the old home's tiles (its planes
+                    // are dead; the IO warp stores them), then the next input,
+                    // already in the spare, -> step 0 there
                     (void)slots_max(C, st);  // consume the last step's maxima (keeps the parities in step)
                     const uint64_t g1 = splat2(exp2i(pe / 2)), g2 = splat2(exp2i(pe - pe / 2));
-                    if (vec && outs > 0) mbar_wait_sleep(r_free, (outs - 1u) & 1u);
+                    const uint32_t old_region = s0 + st.home * kChainSmem;
 #pragma unroll
                     for (uint32_t h = 0; h < 2; ++h) {
                         float v[32];
@@ -582,11 +631,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(w) : "l"(g2));
                             asm("mov.b64 {%0, %1}, %2;" : "=f"(v[i]), "=f"(v[i + 1]) : "l"(w));
                         }
-                        if (vec) tile_put_rows(s0 + kROff + (h ? tile1 : tile0), lane, v);
+                        if (vec) tile_put_rows(old_region + (h ? tile1 : tile0), lane, v);
                         else store_row(out + static_cast<size_t>(st.m) * n2, n, row, col0 + 32u * h, v);
                     }
                     if (vec) {
-                        ++outs;
                         fence_proxy_async_smem();
                         tc_fence_before();  // D reads done before the next MMAs into D
                         __syncwarp();
@@ -595,11 +643,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     } else {
                         tc_fence_before();
                     }
+                    const bool more = has_next(st);
                     st.m += 2 * G;
-                    st.act = st.m < batch;
-                    st.s = kIn;
-                    return;  // no publish: IN follows one slot later
-                }
+                    st.act = more;
+                    if (!more) return;  // the chain is done: nothing to publish
+                    const uint32_t h = st.home;
+                    st.home = spare;
+                    spare = h;
+                    convert_input(cc, st);
+                } else {
                 // ---- step: D -> operands of the next step.  All four 16-column
                 // TMEM loads are issued at once; the scale is settled under them.
                 // Scale for the split, from a bound instead of a barrier:
@@ -610,6 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // bits of h1, so the exact path (block max, one barrier) runs
                 // whenever the previous product came out more than 2^12 below
                 // its bound (the input's exact max feeds the first step's bound).
+                const uint32_t ra = s0 + st.home * kChainSmem + pa0;
                 uint32_t d0[16], d1[16], d2[16], d3[16];
                 tmem_ld16_async(lane_base + C * 256u + col0, d0);
                 tmem_ld16_async(lane_base + C * 256u + col0 + 16u, d1);
@@ -646,8 +699,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (!exact) {
                     t = max(-126, min(126, t));
                     const uint64_t sc2 = splat2(exp2i(t));
-                    emit_chunk(cc, std::integral_constant<uint32_t, 0>{}, f0, sc2, !mult);
-                    emit_chunk(cc, std::integral_constant<uint32_t, 1>{}, f1, sc2, !mult);
+                    emit_chunk(cc, std::integral_constant<uint32_t, 0>{}, ra, f0, sc2, !mult);
+                    emit_chunk(cc, std::integral_constant<uint32_t, 1>{}, ra, f1, sc2, !mult);
                     tmem_ld_wait_dep(d2);
                     tmem_ld_wait_dep(d3);
                     m = absmax32(f2, f3, m);
@@ -656,8 +709,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots + warp * 4u), "r"(mw) : "memory");
                         mbar_arrive(max_bar + C * 2 + nb);
                     }
-                    emit_chunk(cc, std::integral_constant<uint32_t, 2>{}, f2, sc2, !mult);
-                    emit_chunk(cc, std::integral_constant<uint32_t, 3>{}, f3, sc2, !mult);
+                    emit_chunk(cc, std::integral_constant<uint32_t, 2>{}, ra, f2, sc2, !mult);
+                    emit_chunk(cc, std::integral_constant<uint32_t, 3>{}, ra, f3, sc2, !mult);
                 } else {
                     tmem_ld_wait_dep(d2);
                     tmem_ld_wait_dep(d3);
@@ -668,10 +721,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0) mbar_arrive(max_bar + C * 2 + nb);
                     t = scale_exp(max8(slots));
                     const uint64_t sc2 = splat2(exp2i(t));
-                    emit_chunk(cc, std::integral_constant<uint32_t, 0>{}, f0, sc2, !mult);
-                    emit_chunk(cc, std::integral_constant<uint32_t, 1>{}, f1, sc2, !mult);
-                    emit_chunk(cc, std::integral_constant<uint32_t, 2>{}, f2, sc2, !mult);
-                    emit_chunk(cc, std::integral_constant<uint32_t, 3>{}, f3, sc2, !mult);
+                    emit_chunk(cc, std::integral_constant<uint32_t, 0>{}, ra, f0, sc2, !mult);
+                    emit_chunk(cc, std::integral_constant<uint32_t, 1>{}, ra, f1, sc2, !mult);
+                    emit_chunk(cc, std::integral_constant<uint32_t, 2>{}, ra, f2, sc2, !mult);
+                    emit_chunk(cc, std::integral_constant<uint32_t, 3>{}, ra, f3, sc2, !mult);
                 }
                 st.sb = nb;
                 st.t_prev = t;
@@ -682,6 +735,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float x[64];
                     load_row64(st.m, x);
                     emit_left(C, x, exp2i(-st.eb));
+                }
                 }
             }
             // workers arrive; the issue warp waits for all of them (the hardware
