@@ -21,7 +21,8 @@
 // XOR-swizzled by r % 8, is a K-major SWIZZLE_128B left operand and an
 // MN-major SWIZZLE_128B right operand at once (tools/bf16_probe.cu).
 //
-//   SMEM:  chain c: y0, y1 planes of the resident power P' (64 KB)
+//   SMEM:  three 64 KB regions: each chain's home (y0, y1 planes of its
+//          resident power P') and a spare (the next input, pre-loaded)
 //   TMEM:  chain c at column 256c: D (fp32 accumulator, 128 columns),
 //          x0, x1 left-operand planes (2 fp16 per column, 64 columns each)
 //
