@@ -1158,8 +1158,11 @@ struct K1CPlanes {
 __device__ long long* g_k1c_trace;  // [step][8]
 #define K1C_STAMP(k)                                                                       \
     do {                                                                                   \
-        if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && step < 64)    \
-            g_k1c_trace[step * 8 + (k)] = clock64();                                       \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && step < 64) {  \
+            long long t_;                                                                  \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_) : : "memory");              \
+            g_k1c_trace[step * 8 + (k)] = t_;                                              \
+        }                                                                                  \
     } while (0)
 #else
 #define K1C_STAMP(k) \
@@ -1382,6 +1385,7 @@ __global__ void __launch_bounds__(384, 1)
         if (!last) grid_barrier(bar_ctr, nctas * static_cast<unsigned int>(step + 1));
         if (warp == 4) K1C_STAMP(6);
         acc = dst;
+        if (warp == 4) K1C_STAMP(7);
     }
     tc_fence_before();
     __syncthreads();

@@ -1,6 +1,8 @@
 // K1C per-step phase timeline of CTA (0, 0), epilogue warp 4 (cycles):
 //   0 step start, 1 last chunk drained, 2 partial in SMEM, 3 after cluster
-//   sync, 4 reduce written, 5 after cluster sync, 6 after the grid barrier.
+//   sync, 4 reduce written, 5 after cluster sync, 6 after the grid barrier's
+//   (non-blocking, deferred) BAR.SYNC, 7 end of the step: 6 -> 7 is where the
+//   grid barrier's wait actually lands.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -DK1C_TRACE
 //   -I paper_1204_3052_b200/csrc tools/k1c_trace.cu paper_1204_3052_b200/csrc/kernels_k3b.cu
 //   paper_1204_3052_b200/csrc/kernels_k3h.cu -o k1c_trace -lcuda
@@ -45,11 +47,12 @@ int main(int argc, char** argv) {
     printf("n=%d splits=%d err=%s chain %.1f us (%.2f us/step)\n", n, splits, cudaGetErrorString(e), ms * 1e3, ms * 1e3 / 14);
     std::vector<long long> t(64 * 8);
     cudaMemcpy(t.data(), tr, t.size() * 8, cudaMemcpyDeviceToHost);
-    printf("step: mainloop | partial->smem | csync1 | reduce | csync2 | grid barrier | total (cycles)\n");
+    printf("step: mainloop | partial->smem | csync1 | reduce | csync2 | grid barrier | (6->7) (7->next 0) | total (cycles)\n");
     for (int s = 0; s < 14; ++s) {
         const long long* r = &t[s * 8];
-        printf("%2d %c: %6lld %6lld %6lld %6lld %6lld %6lld | %6lld\n", s, pat[s], r[1] - r[0], r[2] - r[1], r[3] - r[2],
-               r[4] - r[3], r[5] - r[4], s < 13 ? r[6] - r[5] : 0, s < 13 ? t[(s + 1) * 8] - r[0] : r[5] - r[0]);
+        printf("%2d %c: %6lld %6lld %6lld %6lld %6lld %6lld | %6lld %6lld | %6lld\n", s, pat[s], r[1] - r[0], r[2] - r[1], r[3] - r[2],
+               r[4] - r[3], r[5] - r[4], s < 13 ? r[6] - r[5] : 0, r[7] - r[6], s < 13 ? t[(s + 1) * 8] - r[7] : 0,
+               s < 13 ? t[(s + 1) * 8] - r[0] : r[5] - r[0]);
     }
     return 0;
 }
