@@ -555,3 +555,20 @@ def test_result_independent_of_handle_history():
     assert used.last_stats.launches == want_launches
     used.close()
     assert sha(got) == sha(want)
+
+
+@pytest.mark.parametrize("batch,k", [(1200, 2), (1200, 4), (900, 5), (600, 64), (445, 3), (2000, 16)])
+def test_batched_every_matrix_vs_oracle(batch, k):
+    """Every matrix of the batch (not a sample) against the oracle: the K3H
+    region rotation, the IO warp's next-boundary prediction and the skewed
+    schedules must put every result in its place (plans of length 1-6, with
+    and without MULTIPLY_BASE steps, batches around 3G and 4G)."""
+    n = 128
+    stack = mx.scaled_batch(n, batch, mx.DType.F32, 5)
+    out = mx.exponentiate_batched(stack, k)
+    ref = oracle.exponentiate_batched(stack, k, oracle.max_threads())
+    tol = mx.fro_tol(n, k, "f32")
+    diff = np.linalg.norm((out.astype(np.float64) - ref).reshape(batch, -1), axis=1)
+    rel = diff / np.linalg.norm(ref.astype(np.float64).reshape(batch, -1), axis=1)
+    assert np.isfinite(out).all()
+    assert rel.max() <= tol, (batch, k, int(rel.argmax()), float(rel.max()), tol)
