@@ -101,19 +101,13 @@ __device__ __forceinline__ void put_half(uint32_t plane, uint32_t row, uint32_t 
                                          const uint32_t (&p)[8]) {
     const uint32_t base = plane + (g >> 1) * 16384u + row * 128u;
     const uint32_t u0 = (g & 1u) * 4u + 2u * h;
-#ifndef K3B_X_NOSTS
     sts128(base + ((u0 ^ (row & 7u)) << 4), p[0], p[1], p[2], p[3]);
     sts128(base + (((u0 + 1u) ^ (row & 7u)) << 4), p[4], p[5], p[6], p[7]);
-#endif
 }
 
 // 32 values of one row of an n x n fp32 matrix, zero padded to 128.
 __device__ __forceinline__ void load_row(const float* __restrict__ src, int n, int vec,
                                          uint32_t row, uint32_t col0, float (&x)[32]) {
-#ifdef K3B_X_NOLDG
-    for (int i = 0; i < 32; ++i) x[i] = (row + i) * 1e-3f;
-    return;
-#endif
     if (vec) {  // n == 128, 16-byte aligned
         const float4* p = reinterpret_cast<const float4*>(src + row * 128u + col0);
 #pragma unroll
@@ -134,10 +128,6 @@ __device__ __forceinline__ void load_row(const float* __restrict__ src, int n, i
 
 __device__ __forceinline__ void store_row(float* __restrict__ dst, int n, int vec, uint32_t row,
                                           uint32_t col0, const uint32_t (&v)[32]) {
-#ifdef K3B_X_NOSTG
-    if (v[0] == 0x7fc00001u) dst[row] = 0.f;
-    return;
-#endif
     if (vec) {
         float4* p = reinterpret_cast<float4*>(dst + row * 128u + col0);
 #pragma unroll
