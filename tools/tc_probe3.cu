@@ -7,7 +7,7 @@
 #include "ptx.cuh"
 using namespace mxp;
 
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+__device__ __forceinline__ void probe_tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
         "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -20,7 +20,7 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         : "memory");
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void probe_mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc) : "memory");
 }
@@ -42,13 +42,13 @@ __global__ void probe(const uint4* img, const uint32_t* atm, int ts, uint64_t ad
     if (ts && warp < 4) {
         uint32_t v[32];
         for (int i = 0; i < 32; ++i) v[i] = atm[(warp * 32 + lane) * 32 + i];
-        tmem_st32(tmem + ((warp * 32) << 16) + 256, v);
+        probe_tmem_st32(tmem + ((warp * 32) << 16) + 256, v);
     }
     tc_fence_before(); __syncthreads(); tc_fence_after();
     if (tid == 0) {
         uint64_t a = (uint64_t(smem_u32(smem)) >> 4) | adesc_rest;
         uint64_t b = (uint64_t(smem_u32(smem + 16384)) >> 4) | bdesc_rest;
-        if (ts) mma_tf32_ts(tmem, tmem + 256, b, idesc, 0);
+        if (ts) probe_mma_tf32_ts(tmem, tmem + 256, b, idesc, 0);
         else mma_tf32(tmem, a, b, idesc, 0);
         mma_commit(bar);
     }
