@@ -483,6 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // its two 32 x 32 IO tiles (TMA boxes 8g + q and 8g + 4 + q of a region)
         const uint32_t tile0 = (8u * g + q) * 4096u, tile1 = tile0 + 4u * 4096u;
         uint32_t rph = 0;   // in_ready parities, bit r for region r
+        bool out_pending = false;  // a result in the old home awaits the IO warp
 
         const uint32_t lg_n = 32u - __clz(static_cast<int>(n - 1));  // ceil(log2 n), n >= 2
         // max of the 8 per-warp slots at `slots` (lane i < 8 reads slot i)
@@ -635,23 +636,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (vec) tile_put_rows(old_region + (h ? tile1 : tile0), lane, v);
                         else store_row(out + static_cast<size_t>(st.m) * n2, n, row, col0 + 32u * h, v);
                     }
-                    if (vec) {
-                        fence_proxy_async_smem();
-                        tc_fence_before();  // D reads done before the next MMAs into D
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(out_ready + C);
-                        K3H_MARK(2);
-                    } else {
-                        tc_fence_before();
-                    }
                     const bool more = has_next(st);
                     st.m += 2 * G;
                     st.act = more;
-                    if (!more) return;  // the chain is done: nothing to publish
+                    if (!more) {  // the chain is done: hand the result over, nothing to publish
+                        if (vec) fence_proxy_async_smem();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (vec && lane == 0) mbar_arrive(out_ready + C);
+                        return;
+                    }
                     const uint32_t h = st.home;
                     st.home = spare;
                     spare = h;
                     convert_input(cc, st);
+                    // the result tiles are handed to the IO warp together with
+                    // the publish below (one proxy fence for both)
+                    out_pending = vec != 0;
                 } else {
                 // ---- step: D -> operands of the next step.  All four 16-column
                 // TMEM loads are issued at once; the scale is settled under them.
@@ -744,6 +745,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st_wait();
             fence_proxy_async_smem();
             tc_fence_before();
+            if (out_pending) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(out_ready + C);
+                out_pending = false;
+            }
             if (warp == 2) K3H_EV(evs, 4);
             if (warp == 0) K3H_EV(evs, 5);
             if (warp == 7) K3H_EV(evs, 6);
