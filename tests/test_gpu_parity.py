@@ -572,3 +572,21 @@ def test_batched_every_matrix_vs_oracle(batch, k):
     rel = diff / np.linalg.norm(ref.astype(np.float64).reshape(batch, -1), axis=1)
     assert np.isfinite(out).all()
     assert rel.max() <= tol, (batch, k, int(rel.argmax()), float(rel.max()), tol)
+
+
+def test_batched_unaligned_device_pointers_take_the_scalar_path(eng):
+    """n = 128 with 4-byte-misaligned device buffers: no TMA (the epilogue
+    reads inputs and writes results itself); results bitwise equal to the
+    aligned (TMA) run."""
+    import torch
+
+    n, batch, k = 128, 600, 13
+    stack = mx.scaled_batch(n, batch, mx.DType.F32, 9)
+    want = mx.exponentiate_batched(stack, k)
+    src = torch.empty(batch * n * n + 1, dtype=torch.float32, device="cuda")
+    dst = torch.empty(batch * n * n + 1, dtype=torch.float32, device="cuda")
+    src[1:].copy_(torch.from_numpy(stack.reshape(-1)))
+    eng.power_batched_device(src[1:].data_ptr(), dst[1:].data_ptr(), n, batch, k)
+    eng.synchronize()
+    got = dst[1:].cpu().numpy().reshape(batch, n, n)
+    assert np.array_equal(got, want)
