@@ -114,15 +114,6 @@ __device__ __forceinline__ int ilogb_bits(uint32_t mbits) {
                                 : (31 - __clz(static_cast<int>(mbits))) - 149;
 }
 
-// max |x_i| as float bits (3-input FMNMX with |.| operands; a NaN is skipped,
-// which is harmless: it propagates through the products anyway)
-__device__ __forceinline__ uint32_t absmax_bits(const float* x) {
-    float m = 0.f;
-#pragma unroll
-    for (int i = 0; i < 32; i += 2) m = fmaxf(fmaxf(m, fabsf(x[i])), fabsf(x[i + 1]));
-    return __float_as_uint(m);
-}
-
 // 32 values of one row of an n x n fp32 matrix, zero padded to 128.
 __device__ __forceinline__ void load_row(const float* __restrict__ src, int n, uint32_t row,
                                          uint32_t col0, float (&x)[32]) {
@@ -492,6 +483,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane < kWorkers) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(slots + lane * 4u) : "memory");
             return __reduce_max_sync(0xFFFFFFFFu, v);
         };
+        // max |x_i| (3-input FMNMX with |.| operands; a NaN is skipped, which is
+        // harmless: it propagates through the products anyway)
         auto absmax64 = [](const float* x) {
             float m = 0.f;
 #pragma unroll
