@@ -5,13 +5,21 @@
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
     python bench.py --impl reference ...      # the reference CPU path (oracle port)
 
+With ``--gpus N > 1`` and no torchrun environment the script re-launches
+itself under ``torch.distributed.run`` with N ranks (one per GPU); under
+torchrun ``WORLD_SIZE`` must equal ``--gpus``.
+
 Workload (BASELINE.json configs; the metric is quoted "at 1/2/4/8 B200",
-which is config 3's batch-sharded form):  c3 = 65536 x 128x128 FP32 A^64
-(3xTF32), inputs fl(random_matrix(128, F64, 42+i) * sqrt(12/128)) generated on
-device.  Each rank runs its own 65536-matrix batch (weak scaling, no
-collective on the data path).  A "step" is one pass of the chain over the
-batch: ONE launch of the persistent sm_100a kernel.  Inputs (4.3 GB) exceed
-the 126 MB L2, so no flush is needed between steps.
+which is config 3's batch-sharded form):  c3 = 65536 x 128x128 FP32 A^64,
+inputs fl(random_matrix(128, F64, 42+i) * sqrt(12/128)) generated on device.
+The 65536 matrices are sharded over the ranks (rank r takes
+``shard_range(65536, r, N)``, seeds 42+i of its own slice; strong scaling, no
+collective on the data path); ``weak_scaling`` reports 65536 per rank beside
+it.  ``--workload c5`` runs the 8192^2 A^1024 chain, row-sharded over the
+ranks with the exchange fused into the GEMM epilogue.  A "step" is one pass
+of the chain over the batch: ONE launch of the persistent sm_100a kernel for
+c3.  Inputs (4.3 GB) exceed the 126 MB L2, so no flush is needed between
+steps.
 
 Prints ONE JSON line on rank 0.
 """
@@ -22,7 +30,9 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -38,10 +48,10 @@ WORKLOADS = {
     "c3": dict(name="batched 65536 x 128x128 FP32 (split-fp32 tensor cores) A^64", n=128, batch=65536, k=64,
                dtype="f32"),
     "c2": dict(name="512x512 FP32 (3xTF32) A^1000", n=512, batch=1, k=1000, dtype="f32"),
-    "c5": dict(name="8192x8192 FP32 (3xTF32) A^1024 (1 GPU)", n=8192, batch=1, k=1024,
+    "c5": dict(name="8192x8192 FP32 (3xTF32) A^1024", n=8192, batch=1, k=1024,
                dtype="f32"),
     "c4": dict(name="4096x4096 FP64 (DMMA) A^257", n=4096, batch=1, k=257, dtype="f64"),
-    "c1": dict(name="64x64 FP32 (3xTF32) A^16", n=64, batch=1, k=16, dtype="f32"),
+    "c1": dict(name="64x64 FP32 (split-fp32 tensor cores) A^16", n=64, batch=1, k=16, dtype="f32"),
 }
 
 
@@ -49,8 +59,16 @@ def mults(k: int) -> int:
     return k.bit_length() - 1 + bin(k).count("1") - 1 if k >= 1 else 0
 
 
-def flops(w: dict) -> float:
-    return 2.0 * w["n"] ** 3 * mults(w["k"]) * w["batch"]
+def flops(w: dict, batch: int | None = None) -> float:
+    return 2.0 * w["n"] ** 3 * mults(w["k"]) * (w["batch"] if batch is None else batch)
+
+
+def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Same rule as paper_1204_3052_b200.distributed.shard_range (kept import-free
+    here so --plan-only runs without the package's native library)."""
+    base, extra = divmod(total, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -62,7 +80,7 @@ class ClockSampler:
             0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
             0x100: "display_clock_setting"}
 
-    def __init__(self, index: int, period: float = 0.005):
+    def __init__(self, index: int, period: float = 0.002):
         self.samples = []
         self.reasons = 0
         self.max_mhz = None
@@ -121,21 +139,22 @@ def measured_peaks() -> dict:
         return {}
 
 
-def tf32_peak_tflops(device) -> float:
-    """cuBLAS TF32 GEMM 8192^3, best of 10 (the denominator for 3xTF32; the
-    driver's MEASURED_PEAKS.json carries bf16 only).  Library GEMM used only
-    as a peak reference, never on the measured path."""
+def library_gemm_peak_tflops(device, dtype_name: str) -> float:
+    """cuBLAS GEMM 8192^3, best of 10: the TF32 (3xTF32 denominator) and FP64
+    (DMMA denominator) peaks the driver's MEASURED_PEAKS.json does not carry.
+    A library GEMM is used only as a peak reference, never on the measured path."""
     import torch
 
-    torch.backends.cuda.matmul.allow_tf32 = True
+    dt = torch.float32 if dtype_name == "tf32" else torch.float64
+    torch.backends.cuda.matmul.allow_tf32 = dtype_name == "tf32"
     n = 8192
-    a = torch.randn(n, n, device=device)
-    b = torch.randn(n, n, device=device)
+    a = torch.randn(n, n, device=device, dtype=dt)
+    b = torch.randn(n, n, device=device, dtype=dt)
     for _ in range(3):
         a @ b
     torch.cuda.synchronize()
     best = float("inf")
-    for _ in range(10):
+    for _ in range(10 if dtype_name == "tf32" else 5):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         a @ b
@@ -159,23 +178,24 @@ def ncu_traffic(kernel: str):
 
 
 # ----------------------------------------------------------------------------- CPU
-def cpu_sample(w: dict, budget_s: float = 12.0) -> dict:
+def cpu_sample(w: dict, budget_s: float = 12.0, threads: int | None = None) -> dict:
     """Time the oracle port (CPU restatement of the reference's naive chain,
-    bit-identical to it) on a bounded sample of the workload, all threads."""
+    bit-identical to it) on a bounded sample of the workload."""
     import numpy as np
 
     import oracle
 
     # every host core this process may run on (torchrun sets OMP_NUM_THREADS=1
     # for its ranks; the reference arm runs on rank 0 alone and uses them all)
-    threads = max(oracle.max_threads(), len(os.sched_getaffinity(0)))
+    if threads is None:
+        threads = max(oracle.max_threads(), len(os.sched_getaffinity(0)))
     n, k = w["n"], w["k"]
     dt = np.float32 if w["dtype"] == "f32" else np.float64
     m = mults(k)
     if w["batch"] > 1:
         # whole chains of independent matrices (seeds 42, 43, ...), in chunks,
         # until the budget is spent or the whole batch is done
-        chunk = max(threads, 1024)
+        chunk = max(threads * 16, 64)
         done, dt_s = 0, 0.0
         while done < w["batch"] and dt_s < budget_s:
             cnt = min(chunk, w["batch"] - done)
@@ -220,6 +240,34 @@ def cpu_sample(w: dict, budget_s: float = 12.0) -> dict:
 
 
 # ----------------------------------------------------------------------------- GPU
+def device_workload(eng, w: dict, batch: int | None = None, seed0: int = 42):
+    """Allocate the workload's buffers, generate its inputs on the device and
+    return (d_in, d_out, step): ``step()`` enqueues exactly the call the
+    bench times (one ``mxp_power_batched_device`` over the whole batch for a
+    batched config, one ``mxp_power_device`` chain otherwise).  The GPU
+    parity tests import this function, so the launch they check against the
+    oracle is the launch measured here."""
+    from paper_1204_3052_b200 import _lib
+
+    n, k = w["n"], w["k"]
+    B = w["batch"] if batch is None else batch
+    mode = _lib.MXP_F32 if w["dtype"] == "f32" else _lib.MXP_F64
+    es = 4 if w["dtype"] == "f32" else 8
+    nbytes = n * n * max(B, 1) * es
+    d_in = eng.alloc(nbytes)
+    d_out = eng.alloc(nbytes)
+    eng.random_device(d_in, n, B, seed0, -0.5, 0.5, math.sqrt(12.0 / n), mode)
+    batched = w["batch"] > 1
+
+    def step():
+        if batched:
+            eng.power_batched_device(d_in, d_out, n, B, k, mode)
+        else:
+            eng.power_device(d_in, d_out, n, k, mode)
+
+    return d_in, d_out, step
+
+
 def run_row_sharded(eng, w: dict, steps: int, warmup: int, dist, sample=True):
     """C5 on N GPUs: one matrix, rows sharded, the exchange fused into the
     CTA-pair GEMM epilogue (peer stores + flag barrier).  Strong scaling."""
@@ -254,26 +302,12 @@ def run_row_sharded(eng, w: dict, steps: int, warmup: int, dist, sample=True):
     return ms, mults(k) + 1, (sampler.summary() if sampler else None)
 
 
-def run_device(eng, w: dict, steps: int, warmup: int, seed0: int, dist=None, sample=True):
+def run_device(eng, w: dict, steps: int, warmup: int, seed0: int, dist=None, sample=True,
+               batch: int | None = None):
     """Device-resident inputs, CUDA-event timing on the engine's stream."""
     import torch
 
-    from paper_1204_3052_b200 import _lib
-
-    n, B, k = w["n"], w["batch"], w["k"]
-    mode = _lib.MXP_F32 if w["dtype"] == "f32" else _lib.MXP_F64
-    es = 4 if w["dtype"] == "f32" else 8
-    nbytes = n * n * B * es
-    d_in = eng.alloc(nbytes)
-    d_out = eng.alloc(nbytes)
-    eng.random_device(d_in, n, B, seed0, -0.5, 0.5, math.sqrt(12.0 / n), mode)
-
-    def step():
-        if B > 1:
-            eng.power_batched_device(d_in, d_out, n, B, k, mode)
-        else:
-            eng.power_device(d_in, d_out, n, k, mode)
-
+    d_in, d_out, step = device_workload(eng, w, batch, seed0)
     for _ in range(warmup):
         step()
     eng.synchronize()
@@ -303,29 +337,46 @@ def run_device(eng, w: dict, steps: int, warmup: int, seed0: int, dist=None, sam
     return ms, launches, (sampler.summary() if sampler else None)
 
 
-def run_e2e(eng, w: dict, steps: int = 3) -> dict:
-    """Same metric through the public host API: pinned host input -> H2D ->
-    chain -> D2H into pinned host output, every step."""
+def run_e2e(eng, w: dict, batch: int, seed0: int, steps: int = 3, pinned: bool = True) -> dict:
+    """Same metric through the public host API: host input -> H2D -> chain ->
+    D2H into the host output, every step.  ``pinned``: engine-allocated pinned
+    buffers; else ordinary (pageable) numpy arrays, the drop-in
+    ``exponentiate_batched(np.ndarray)`` call a user makes."""
     import numpy as np
 
+    import paper_1204_3052_b200 as mx
     from paper_1204_3052_b200 import _lib
 
-    n, B, k = w["n"], w["batch"], w["k"]
+    n, k = w["n"], w["k"]
     dt = np.float32 if w["dtype"] == "f32" else np.float64
     mode = _lib.MXP_F32 if w["dtype"] == "f32" else _lib.MXP_F64
-    shape = (B, n, n) if B > 1 else (n, n)
-    host_in = eng.pinned_array(shape, dt)
-    host_out = eng.pinned_array(shape, dt)
+    batched = w["batch"] > 1
+    shape = (batch, n, n) if batched else (n, n)
+    if pinned:
+        host_in = eng.pinned_array(shape, dt)
+        host_out = eng.pinned_array(shape, dt)
+    else:
+        host_in = np.empty(shape, dt)
+        host_out = None
     d = eng.alloc(host_in.nbytes)
-    eng.random_device(d, n, B, 42, -0.5, 0.5, math.sqrt(12.0 / n), mode)
+    eng.random_device(d, n, batch, seed0, -0.5, 0.5, math.sqrt(12.0 / n), mode)
     eng.download(host_in, d)
     eng.free(d)
 
+    from paper_1204_3052_b200.engine import default_engine
+
+    user_eng = eng if pinned else default_engine(eng.device)  # the engine the public API uses
+
     def call():
-        if B > 1:
-            eng.power_batched(host_in, k, out=host_out)
-        else:
+        if batched:
+            if pinned:
+                eng.power_batched(host_in, k, out=host_out)
+            else:
+                mx.exponentiate_batched(host_in, k, device=eng.device)
+        elif pinned:
             host_out[...] = eng.power(host_in, k)
+        else:
+            mx.exponentiate(host_in, k, mx.b200_backend(eng.device))
 
     call()  # warm (allocations, graph capture)
     times = []
@@ -333,15 +384,56 @@ def run_e2e(eng, w: dict, steps: int = 3) -> dict:
         t0 = time.perf_counter()
         call()
         times.append(time.perf_counter() - t0)
-    st = eng.last_stats
+    st = user_eng.last_stats
     med = statistics.median(times)
-    res = {"value": flops(w) / med / 1e12, "unit": "TFLOP/s",
+    res = {"value": flops(w, batch) / med / 1e12, "unit": "TFLOP/s",
            "h2d_bytes_per_step": int(st.h2d_bytes), "d2h_bytes_per_step": int(st.d2h_bytes),
-           "ms_per_step": med * 1e3, "matrices_per_s": B / med,
+           "ms_per_step": med * 1e3, "matrices_per_s": batch / med,
+           "host_memory": "pinned (engine-allocated)" if pinned else "pageable numpy arrays",
            "timing": f"host wall clock around the synchronous public call, median of {steps}"}
-    eng.host_free(host_in.ctypes.data)
-    eng.host_free(host_out.ctypes.data)
+    if pinned:
+        eng.host_free(host_in.ctypes.data)
+        eng.host_free(host_out.ctypes.data)
     return res
+
+
+# ----------------------------------------------------------------------------- launch
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_ranks(n: int) -> int:
+    """Re-run this script under torch.distributed.run with n ranks (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def plan_only(args, w, world, rank) -> None:
+    """The launch and sharding plan without touching a GPU (tests/test_bench.py
+    runs it on CPU with gloo): every rank reports its slice, rank 0 prints."""
+    import torch.distributed as tdist
+
+    if world > 1:
+        tdist.init_process_group("gloo")
+    batched = w["batch"] > 1
+    lo, hi = shard_range(w["batch"], rank, world) if batched else (0, 1)
+    mine = {"rank": rank, "shard": [lo, hi], "seed0": 42 + lo}
+    everyone = [mine]
+    if world > 1:
+        everyone = [None] * world
+        tdist.all_gather_object(everyone, mine)
+    if rank == 0:
+        print(json.dumps({"plan_only": True, "n_gpus": world, "workload": w["name"],
+                          "global_batch": w["batch"], "ranks": everyone}))
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
 
 
 def main() -> None:
@@ -354,17 +446,34 @@ def main() -> None:
     ap.add_argument("--no-extras", action="store_true", help="skip the secondary configs")
     ap.add_argument("--quick", action="store_true",
                     help="device timing only (no e2e / CPU baseline / peak GEMM): for ncu runs")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="print the rank/shard plan and exit (no GPU needed)")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(launch_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    config = {"workload": w["name"], "n": w["n"], "batch_per_gpu": w["batch"], "k": w["k"],
-              "multiplies_per_matrix": mults(w["k"]), "global_batch": w["batch"] * world,
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; launch one rank "
+                         "per GPU (or omit torchrun and let --gpus launch the ranks)")
+    if args.plan_only:
+        plan_only(args, w, world, rank)
+        return
+
+    batched = w["batch"] > 1
+    lo, hi = shard_range(w["batch"], rank, world) if batched else (0, 1)
+    config = {"workload": w["name"], "n": w["n"], "k": w["k"],
+              "multiplies_per_matrix": mults(w["k"]), "global_batch": w["batch"],
+              "batch_per_gpu": hi - lo, "shard": [lo, hi],
               "input": "fl(random_matrix(n, F64, 42+i) * sqrt(12/n)) generated on device",
-              "l2": "inputs larger than L2 (no flush needed)" if w["batch"] > 1 else
+              "l2": "inputs larger than L2 (no flush needed)" if batched else
                     "single matrix chain, L2-resident by design (graph replay)",
-              "parallelism": f"batch-sharded x{world} (no collective)" if world > 1 else "1 GPU"}
+              "parallelism": (f"batch-sharded x{world}: rank r runs matrices shard_range(65536, r, "
+                              f"{world}) (no collective)") if world > 1 else "1 GPU"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -377,10 +486,13 @@ def main() -> None:
         val = statistics.median(s["value"] for s in samples)
         cpu = dict(samples[-1])
         cpu["value"] = val
+        config["batch_per_gpu"] = w["batch"]
+        config["shard"] = [0, w["batch"]]
+        config["parallelism"] = "host CPU (rank 0 only)"
         print(json.dumps({"metric": METRIC, "value": val, "unit": "TFLOP/s", "impl": "reference",
                           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                           "ms_per_step": statistics.median(s["sample_seconds"] for s in samples) * 1e3,
-                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                           "dtype": w["dtype"], "data": "synthetic (SURVEY §8(d) recipe)",
                           "config": config, "cpu_baseline": cpu,
                           "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
@@ -390,57 +502,85 @@ def main() -> None:
     import torch
 
     dist = None
+    nccl_nranks = None
     # Test knob: BENCH_SHARE_GPU=1 maps every rank onto the visible GPUs
-    # round-robin and uses gloo, so the multi-rank path (per-rank seeds,
+    # round-robin and uses gloo, so the multi-rank path (per-rank shards,
     # barriers, max over ranks) runs on a one-GPU box (numbers meaningless).
     share = os.environ.get("BENCH_SHARE_GPU") == "1"
     if share:
         local = local % max(torch.cuda.device_count(), 1)
-    if world > 1 or os.environ.get("BENCH_FORCE_DIST") == "1":
+    torch.cuda.set_device(local)
+    if world > 1:
         import torch.distributed as tdist
 
-        torch.cuda.set_device(local)
         if share:
             tdist.init_process_group("gloo")
         else:
+            # NCCL's init log carries "nranks N" for every communicator: the
+            # driver's evidence that N ranks ran
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = tdist
-    else:
-        torch.cuda.set_device(local)
+        one = torch.ones(1, device="cuda") if not share else torch.ones(1)
+        dist.all_reduce(one)
+        nccl_nranks = int(one.item())
+        if nccl_nranks != world:
+            raise SystemExit(f"communicator has {nccl_nranks} ranks, expected {world}")
 
     import paper_1204_3052_b200 as mx
 
     eng = mx.Engine(local)
-    row_sharded = dist is not None and w["batch"] == 1 and w["n"] >= 1024 and w["dtype"] == "f32"
+    row_sharded = dist is not None and not batched and w["n"] >= 1024 and w["dtype"] == "f32"
     if row_sharded:  # one matrix over N GPUs (C5): fused exchange, strong scaling
         ms, launches, clocks = run_row_sharded(eng, w, args.steps, args.warmup, dist)
         config["parallelism"] = f"row-sharded x{world} (exchange fused into the GEMM epilogue)"
-        config["global_batch"] = 1
     else:
-        ms, launches, clocks = run_device(eng, w, args.steps, args.warmup,
-                                          seed0=42 + rank * w["batch"], dist=dist)
-    if dist is not None:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    fl = flops(w)
-    value = (fl if row_sharded else world * fl) / (ms / 1e3) / 1e12
+        ms, launches, clocks = run_device(eng, w, args.steps, args.warmup, seed0=42 + lo,
+                                          dist=dist, batch=hi - lo)
 
-    # e2e through the public host API on every rank (max over ranks)
-    e2e = None
+    def max_over_ranks(v: float) -> float:
+        if dist is None:
+            return v
+        t = torch.tensor([v], device="cuda") if not share else torch.tensor([v])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = max_over_ranks(ms)
+    fl = flops(w)  # the whole job: all 65536 matrices (or the one matrix)
+    value = fl / (ms / 1e3) / 1e12
+
+    weak = None
+    if dist is not None and batched and not args.quick:
+        # secondary: every rank runs a full 65536-matrix batch of its own
+        wms, _, _ = run_device(eng, w, args.steps, args.warmup, seed0=42 + rank * w["batch"],
+                               dist=dist, sample=False)
+        wms = max_over_ranks(wms)
+        weak = {"batch_per_gpu": w["batch"], "global_batch": w["batch"] * world,
+                "ms_per_step": wms, "value": world * fl / (wms / 1e3) / 1e12, "unit": "TFLOP/s"}
+
+    # e2e through the public host API on every rank (its own shard; max over ranks)
+    e2e = e2e_pageable = None
     if not args.quick:
-        try:
-            e2e = run_e2e(eng, w)
-        except Exception as exc:  # noqa: BLE001
-            e2e = {"value": None, "error": str(exc)}
-        if dist is not None:
-            t = torch.tensor([e2e.get("ms_per_step") or float("inf")], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            if e2e.get("ms_per_step"):
-                e2e["ms_per_step"] = float(t.item())
-                e2e["value"] = world * fl / (e2e["ms_per_step"] / 1e3) / 1e12
-                e2e["matrices_per_s"] = world * w["batch"] / (e2e["ms_per_step"] / 1e3)
-                e2e["timing"] += f"; max over {world} ranks"
+        for pinned in (True, False):
+            try:
+                r = run_e2e(eng, w, hi - lo, 42 + lo, steps=3 if pinned else 1, pinned=pinned)
+            except Exception as exc:  # noqa: BLE001
+                r = {"value": None, "error": str(exc)}
+            if dist is not None:
+                worst = max_over_ranks(r.get("ms_per_step") or float("inf"))
+                if r.get("ms_per_step"):
+                    r["ms_per_step"] = worst
+                    r["value"] = fl / (worst / 1e3) / 1e12
+                    r["matrices_per_s"] = w["batch"] / (worst / 1e3)
+                    r["timing"] += f"; max over {world} ranks"
+                    for key in ("h2d_bytes_per_step", "d2h_bytes_per_step"):
+                        r[key + "_per_rank"] = r[key]
+                        r[key] = int(max_over_ranks(float(r[key])) * world) if batched else r[key]
+            if pinned:
+                e2e = r
+            else:
+                e2e_pageable = r
 
     if rank != 0:
         if dist is not None:
@@ -452,7 +592,7 @@ def main() -> None:
     tf32 = None
     if not args.quick:
         try:
-            tf32 = tf32_peak_tflops(torch.device("cuda", local))
+            tf32 = library_gemm_peak_tflops(torch.device("cuda", local), "tf32")
         except Exception:  # noqa: BLE001
             tf32 = None
     # Roofline denominator = the datapath the kernel runs on.  C3 (K3H) forms
@@ -461,7 +601,7 @@ def main() -> None:
     # (MEASURED_PEAKS bf16; fp16 runs at the same rate).  The K1/K1P chains
     # (C2, C5) run 3xTF32: cuBLAS TF32 measured here / 3.
     bf16 = peaks.get("bf16_tflops")
-    if w["batch"] > 1 and w["dtype"] == "f32":
+    if batched and w["dtype"] == "f32":
         if bf16:
             peak, src = bf16 / 3.0, "MEASURED_PEAKS bf16 dense burst (fp16 same rate) / 3 products"
         else:
@@ -475,29 +615,36 @@ def main() -> None:
         else:
             peak, src = 1590.0 / 6.0, "fallback 1.59 PF bf16 / 6"
         kernel = "k1_gemm_3xtf32 chain"
-    kernel_ms = ms / max(launches, 1) if w["batch"] > 1 else ms
-    achieved = fl / (kernel_ms / 1e3) / 1e12 if w["batch"] > 1 else value
+    rank_fl = flops(w, hi - lo)
+    kernel_ms = ms / max(launches, 1) if batched else ms
+    achieved = rank_fl / (kernel_ms / 1e3) / 1e12 if batched else value / world
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(kernel.split()[0]),
                 "kernel": kernel, "peak_source": src,
-                "algorithmic_flops_per_launch": fl / max(launches, 1),
+                "per_gpu": True,
+                "algorithmic_flops_per_launch": rank_fl / max(launches, 1),
                 "bf16_measured_peak": bf16,
                 "bf16_measured_peak_sustained": peaks.get("bf16_tflops_sustained"),
                 "frac_vs_sustained": (achieved / (peaks["bf16_tflops_sustained"] / 3.0)
-                                      if peaks.get("bf16_tflops_sustained") and w["batch"] > 1
+                                      if peaks.get("bf16_tflops_sustained") and batched
                                       else None),
                 "tf32_cublas_measured": tf32,
                 "vs_3xtf32_effective_peak": achieved / (tf32 / 3.0) if tf32 else None}
     out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-           "higher_is_better": True, "scaling": "strong" if row_sharded else "weak",
+           "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None,
-           "dtype": ("f32 (split-fp32: scaled fp16x2, tcgen05)" if w["batch"] > 1 else
+           "dtype": ("f32 (split-fp32: scaled fp16x2, tcgen05)" if batched else
                      "f32 (3xTF32 tcgen05)") if w["dtype"] == "f32" else "f64 (DMMA)",
            "data": "synthetic (SURVEY §8(d) recipe, device SplitMix64)", "config": config,
-           "matrices_per_s": world * w["batch"] / (ms / 1e3),
+           "matrices_per_s": w["batch"] / (ms / 1e3),
            "roofline": roofline, "clocks": clocks,
            "gpu_launches": args.steps * launches}
+    if nccl_nranks is not None:
+        out["comm"] = {"backend": "gloo (BENCH_SHARE_GPU test mode)" if share else "nccl",
+                       "nranks": nccl_nranks}
+    if weak is not None:
+        out["weak_scaling"] = weak
     if args.quick:
         print(json.dumps(out))
         if dist is not None:
@@ -505,12 +652,18 @@ def main() -> None:
             dist.destroy_process_group()
         return
     out["e2e"] = e2e
+    out["e2e_pageable"] = e2e_pageable
     if world == 1:
         try:
             out["cpu_baseline"] = cpu_sample(w)
         except Exception as exc:  # noqa: BLE001
             out["cpu_baseline"] = {"value": None, "error": str(exc)}
         if not args.no_extras:
+            try:
+                f64 = library_gemm_peak_tflops(torch.device("cuda", local), "f64")
+            except Exception:  # noqa: BLE001
+                f64 = None
+            roofline["f64_cublas_measured"] = f64
             extras = {}
             for key in ("c1", "c2", "c4", "c5"):
                 if key == args.workload:
@@ -519,8 +672,15 @@ def main() -> None:
                 try:
                     xms, xl, _ = run_device(eng, wx, 3 if wx["n"] >= 4096 else 20, 2, 42,
                                             sample=False)
-                    extras[key] = {"workload": wx["name"], "ms": xms, "launches": xl,
-                                   "TFLOP/s": flops(wx) / (xms / 1e3) / 1e12}
+                    tf = flops(wx) / (xms / 1e3) / 1e12
+                    ex = {"workload": wx["name"], "ms": xms, "launches": xl, "TFLOP/s": tf}
+                    if wx["dtype"] == "f64" and f64:
+                        ex["frac"] = tf / f64
+                        ex["peak"] = f"cuBLAS DGEMM 8192^3 measured in this run ({f64:.1f} TFLOP/s)"
+                    elif wx["n"] > 128 and tf32:
+                        ex["frac"] = tf / (tf32 / 3.0)
+                        ex["peak"] = f"cuBLAS TF32 8192^3 / 3 ({tf32 / 3.0:.0f} TFLOP/s)"
+                    extras[key] = ex
                 except Exception as exc:  # noqa: BLE001
                     extras[key] = {"error": str(exc)}
             out["other_configs"] = extras

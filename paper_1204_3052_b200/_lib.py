@@ -14,7 +14,7 @@ import threading
 from . import errors as E
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmatexpo_b200.so")
+LIB_PATH = os.environ.get("MXP_LIB_PATH") or os.path.join(HERE, "libmatexpo_b200.so")
 
 MXP_OK = 0
 MXP_E_VALIDATION = 1

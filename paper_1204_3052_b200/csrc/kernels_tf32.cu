@@ -1402,6 +1402,9 @@ static cudaError_t prepare_k1c() {
     return e;
 }
 
+#ifndef MXP_K1C_COOPERATIVE
+#define MXP_K1C_COOPERATIVE 1
+#endif
 // One cooperative launch for the whole chain; cudaErrorCooperativeLaunchTooLarge
 // (or any launch error) tells the caller to run the per-step chain instead.
 cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
@@ -1438,7 +1441,7 @@ cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
     attr[1].id = cudaLaunchAttributeCooperative;
     attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = MXP_K1C_COOPERATIVE ? 2 : 1;
     if (narrow)
         return cudaLaunchKernelEx(&cfg, k1c_chain_3xtf32<64>, maps, pl, plan, n_pad, out_f32, n_out,
                                   bar_ctr);

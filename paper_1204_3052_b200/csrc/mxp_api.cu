@@ -126,11 +126,31 @@ struct mxp_handle_s {
     void* d_in2 = nullptr;
     void* d_out = nullptr;
 
-    std::map<GraphKey, std::pair<cudaGraphExec_t, int64_t>> graphs;  // exec, kernel launches
+    // captured chains, keyed by (mode, n, k, in, out); bounded LRU (callers that
+    // pass fresh buffers every call would otherwise grow it without limit)
+    struct CachedGraph {
+        cudaGraphExec_t exec;
+        int64_t launches;
+        uint64_t last_use;
+    };
+    std::map<GraphKey, CachedGraph> graphs;
+    uint64_t graph_clock = 0;
+    static constexpr size_t kMaxGraphs = 32;
 
     void drop_graphs() {
-        for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
+        for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
         graphs.clear();
+    }
+    void evict_lru() {
+        while (graphs.size() >= kMaxGraphs) {
+            auto victim = graphs.begin();
+            for (auto it = graphs.begin(); it != graphs.end(); ++it)
+                if (it->second.last_use < victim->second.last_use) victim = it;
+            // a graph still queued on the stream must not be destroyed under it
+            cudaStreamSynchronize(stream);
+            cudaGraphExecDestroy(victim->second.exec);
+            graphs.erase(victim);
+        }
     }
 };
 
@@ -226,6 +246,9 @@ int ensure_ws64(mxp_handle h, int64_t n_pad) {
 
 int ensure_io(mxp_handle h, size_t bytes) {
     if (h->io_bytes >= bytes) return MXP_OK;
+    // graphs captured on the old staging buffers would replay into freed memory
+    MXP_CUDA(cudaStreamSynchronize(h->stream));
+    h->drop_graphs();
     if (h->d_in) cudaFree(h->d_in);
     if (h->d_in2) cudaFree(h->d_in2);
     if (h->d_out) cudaFree(h->d_out);
@@ -403,11 +426,16 @@ int run_power_graph(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA
         ce = cudaGraphInstantiate(&ge, g, 0);
         cudaGraphDestroy(g);
         if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
-        it = h->graphs.emplace(key, std::make_pair(ge, launches)).first;
+        h->evict_lru();
+        it = h->graphs.emplace(key, mxp_handle_s::CachedGraph{ge, launches, 0}).first;
     }
-    cudaError_t e = cudaGraphLaunch(it->second.first, h->stream);
+    // the chain overwrites the workspace planes a prepared right-hand side
+    // lives in (cache hit or miss alike)
+    h->rhs_mode = -1;
+    it->second.last_use = ++h->graph_clock;
+    cudaError_t e = cudaGraphLaunch(it->second.exec, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
-    if (st) st->launches += it->second.second;
+    if (st) st->launches += it->second.launches;
     return MXP_OK;
 }
 

@@ -124,6 +124,9 @@ def exponentiate_row_sharded(a, power: int, group=None, ops=None, chunks: Option
 
         ops = EngineOps(default_engine(a.device.index or 0))
     stream = ops.stream() if hasattr(ops, "stream") else None
+    caller = torch.cuda.current_stream(a.device) if stream is not None else None
+    if stream is not None:
+        stream.wait_stream(caller)  # `a` may still be in flight on the caller's stream
     ctx = torch.cuda.stream(stream) if stream is not None else _nullcontext()
     with ctx:
         base = torch.zeros((n_p, n_p), dtype=a.dtype, device=a.device)
@@ -144,7 +147,11 @@ def exponentiate_row_sharded(a, power: int, group=None, ops=None, chunks: Option
             for work in pending:
                 work.wait()  # the next step reads every row of P'
             full, nxt = nxt, full
-        return full[:n, :n].contiguous()
+        result = full[:n, :n].contiguous()
+    if stream is not None:
+        caller.wait_stream(stream)  # the result is complete before the caller reads it
+        result.record_stream(caller)
+    return result
 
 
 def fused_layout(n: int, world: int) -> tuple[int, int]:
@@ -217,7 +224,13 @@ class RowShardedFused:
             return a.clone()
         plan = plan_exponentiation(power)
         b = self.buf
-        with torch.cuda.stream(torch.cuda.ExternalStream(eng.stream)):
+        ext = torch.cuda.ExternalStream(eng.stream)
+        ext.wait_stream(torch.cuda.current_stream(a.device))  # `a` is ready
+        # nobody may overwrite a peer's buffers while that peer still copies the
+        # previous call's result out of them
+        self.epoch += 1
+        eng.peer_barrier(self.rank, self.peer["flags"], self.epoch)
+        with torch.cuda.stream(ext):
             self.base[:n, :n] = a  # zero padding never mixes into the top-left n x n block
         eng.split_planes_device(self.base.data_ptr(), b["base_hi"].data_ptr(),
                                 b["base_lo"].data_ptr(), n_p)
@@ -240,10 +253,12 @@ class RowShardedFused:
             self.epoch += 1
             eng.peer_barrier(self.rank, self.peer["flags"], self.epoch)
             cur, nxt = nxt, cur
-        out = torch.empty((n, n), dtype=a.dtype, device=a.device)
-        with torch.cuda.stream(torch.cuda.ExternalStream(eng.stream)):
+        with torch.cuda.stream(ext):
+            out = torch.empty((n, n), dtype=a.dtype, device=a.device)
             out.copy_(b["out"][:n, :n])
-        eng.synchronize()
+        caller = torch.cuda.current_stream(a.device)
+        caller.wait_stream(ext)
+        out.record_stream(caller)
         return out
 
     def close(self):
@@ -280,8 +295,19 @@ def exponentiate_batched_sharded(a_local, power: int, ops=None):
         from .engine import default_engine
 
         ops = EngineOps(default_engine(a_local.device.index or 0))
-    out = torch.empty_like(a_local)
+    stream = ops.stream() if hasattr(ops, "stream") else None
+    if stream is None:
+        out = torch.empty_like(a_local)
+        ops.power_batched(a_local, power, out)
+        return out
+    caller = torch.cuda.current_stream(a_local.device)
+    stream.wait_stream(caller)
+    with torch.cuda.stream(stream):
+        out = torch.empty_like(a_local)
     ops.power_batched(a_local, power, out)
+    a_local.record_stream(stream)
+    caller.wait_stream(stream)
+    out.record_stream(caller)
     return out
 
 

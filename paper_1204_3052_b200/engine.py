@@ -116,6 +116,10 @@ class Engine:
         mode = _mode_of(a)
         if out is None:
             out = np.empty_like(a)
+        elif (not isinstance(out, np.ndarray) or out.shape != a.shape or out.dtype != a.dtype
+              or not out.flags.c_contiguous or not out.flags.writeable):
+            raise E.ShapeError(f"out must be a writeable C-contiguous {a.dtype} array of shape "
+                               f"{a.shape}")
         st = _lib.Stats()
         rc = self._L.mxp_power_batched(self._h, mode, a.shape[1], a.shape[0], int(k), _ptr(a),
                                        _ptr(out), ctypes.byref(st))
@@ -143,6 +147,10 @@ class Engine:
     def power_mod(self, a: np.ndarray, k: int, p: int) -> np.ndarray:
         """(A^k) mod p, exact, uint32 residues."""
         a = np.ascontiguousarray(a, dtype=np.uint32)
+        if a.ndim != 2 or a.shape[0] != a.shape[1]:
+            raise E.ShapeError(f"expected a square 2-D array, got shape {a.shape}")
+        if not 2 <= int(p) < 2 ** 31:
+            raise E.ValidationError(f"modulus must satisfy 2 <= p < 2^31, got {p}")
         out = np.empty_like(a)
         st = _lib.Stats()
         rc = self._L.mxp_power_mod(self._h, a.shape[0], int(k), int(p), _ptr(a), _ptr(out),

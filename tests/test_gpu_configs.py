@@ -1,0 +1,137 @@
+"""GPU parity on the exact launches bench.py measures, at the BASELINE sizes.
+
+Every test builds its workload with ``bench.device_workload`` — the function
+whose ``step()`` bench.py times — runs that step once, and checks the result
+against the oracle computed on the same seeded inputs:
+
+* C3: ONE ``mxp_power_batched_device`` launch over all 65536 matrices (about
+  221 matrices per K3H chain, hundreds of region rotations per CTA); every
+  matrix against the oracle, plus elements 0 and 65535 against the
+  reference's own golden outputs.
+* C4 (4096^2 f64 A^257), C5 (8192^2 f32 A^1024), C2 (512^2 A^1000), C1 (64^2
+  A^16): the chain against the oracle chain.
+
+The oracle itself is pinned at these sizes: its full result must hash to the
+value the UNMODIFIED reference produced (tests/golden/configs.json, made by
+tests/golden/make_golden_configs.py), so "within tolerance of the oracle" is
+"within tolerance of the reference".
+
+Tolerances: relative Frobenius <= 16 * m(k) * sqrt(n) * u, per
+matrix, u = 2^-24 (f32) or 2^-53 (f64).
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import bench
+import oracle
+import paper_1204_3052_b200 as mx
+from paper_1204_3052_b200.engine import Engine
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _configs():
+    with open(os.path.join(HERE, "golden", "configs.json")) as fh:
+        return json.load(fh)
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _fro_rel(res, ref):
+    """Per-matrix relative Frobenius error of (B, n, n) stacks, in f64 chunks."""
+    out = np.empty(res.shape[0])
+    for i in range(0, res.shape[0], 2048):
+        r = ref[i:i + 2048].astype(np.float64)
+        d = res[i:i + 2048].astype(np.float64) - r
+        out[i:i + 2048] = (np.sqrt(np.einsum("bij,bij->b", d, d)) /
+                           np.sqrt(np.einsum("bij,bij->b", r, r)))
+    return out
+
+
+def _run_bench_step(eng, key):
+    """(inputs, result) of one bench step, downloaded from the device."""
+    w = bench.WORKLOADS[key]
+    dt = np.float32 if w["dtype"] == "f32" else np.float64
+    shape = (w["batch"], w["n"], w["n"]) if w["batch"] > 1 else (w["n"], w["n"])
+    d_in, d_out, step = bench.device_workload(eng, w)
+    try:
+        step()
+        eng.synchronize()
+        launches = eng.last_stats.launches
+        inp = np.empty(shape, dt)
+        out = np.empty(shape, dt)
+        eng.download(inp, d_in)
+        eng.download(out, d_out)
+        step()  # the timed loop runs it again and again: deterministic
+        eng.synchronize()
+        again = np.empty(shape, dt)
+        eng.download(again, d_out)
+        assert again.tobytes() == out.tobytes(), f"{key}: second launch differs"
+    finally:
+        eng.free(d_in)
+        eng.free(d_out)
+    return w, inp, out, launches
+
+
+@pytest.fixture(scope="module")
+def eng():
+    e = Engine(0)
+    yield e
+    e.close()
+
+
+def test_c3_full_bench_launch_every_matrix(eng, golden):
+    arrays, _ = golden
+    w, inp, out, launches = _run_bench_step(eng, "c3")
+    assert launches == 1  # the whole batch in one persistent launch
+    n, B, k = w["n"], w["batch"], w["k"]
+    ref_in = oracle.scaled_batch(n, B, np.float32, 42)
+    assert inp.tobytes() == ref_in.tobytes()  # device inputs == the recipe, bitwise
+    del inp
+    ref = oracle.exponentiate_batched(ref_in, k, oracle.max_threads())
+    del ref_in
+    assert _sha(ref) == _configs()["c3"]["sha256_stack"]  # oracle == reference, all 65536
+    assert ref[0].tobytes() == arrays["c3_out_0"].tobytes()
+    assert ref[B - 1].tobytes() == arrays["c3_out_65535"].tobytes()
+    assert np.isfinite(out).all()
+    rel = _fro_rel(out, ref)
+    tol = mx.fro_tol(n, k, "f32")
+    worst = int(rel.argmax())
+    assert rel.max() <= tol, (worst, float(rel.max()), tol)
+    for i, key in ((0, "c3_out_0"), (B - 1, "c3_out_65535")):
+        assert oracle.compare(out[i], arrays[key])[2] <= tol, i
+    print(f"C3 65536 matrices: max fro_rel {rel.max():.3e} (tol {tol:.3e}), "
+          f"median {np.median(rel):.3e}")
+
+
+@pytest.mark.parametrize("key", ["c1", "c2", "c4", "c5"])
+def test_single_chain_bench_launch_vs_oracle(eng, golden, key):
+    arrays, meta = golden
+    w, inp, out, _ = _run_bench_step(eng, key)
+    n, k = w["n"], w["k"]
+    dt = np.float32 if w["dtype"] == "f32" else np.float64
+    ref_in = oracle.scaled_input(n, dt, 42)
+    assert inp.tobytes() == ref_in.tobytes()
+    ref = oracle.exponentiate(ref_in, k, oracle.max_threads())
+    err = oracle.compare(out, ref)[2]
+    tol = mx.fro_tol(n, k, w["dtype"])
+    print(f"{key}: fro_rel {err:.3e} (tol {tol:.3e}), oracle sha256 {_sha(ref)}")
+    assert np.isfinite(out).all()
+    assert err <= tol, (key, err, tol)
+    # the oracle's result is the reference's, bit for bit
+    if key == "c1":
+        assert ref.tobytes() == arrays["exp_64_f32_16"].tobytes()
+    elif key == "c2":
+        assert _sha(ref) == meta["c2_exp_sha256"]
+    else:
+        pinned = _configs()[key]  # KeyError: run tests/golden/make_golden_configs.py
+        assert _sha(ref) == pinned["sha256"], f"{key}: oracle differs from the reference"

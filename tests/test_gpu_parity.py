@@ -206,9 +206,12 @@ def test_config2_512_a1000():
 
 
 def test_config3_batched_samples(golden):
-    """128x128 A^64, seeds 42+i, generated on device, chained in the persistent kernel."""
+    """128x128 A^64, seeds 42+i, generated on device, chained in the persistent kernel
+    through the host API (chunked pipeline: launches of <= 1024 matrices, about 3-4
+    per chain).  The bench's exact launch (all 65536 matrices in one launch, ~221
+    per chain) is checked matrix by matrix in tests/test_gpu_configs.py."""
     arrays, meta = golden
-    batch = 4352  # > 148 * 29: every CTA loops over many matrices
+    batch = 4352
     stack = mx.scaled_batch(128, batch, mx.DType.F32, 42)
     out = mx.exponentiate_batched(stack, 64)
     tol = mx.fro_tol(128, 64, "f32")
@@ -590,3 +593,57 @@ def test_batched_unaligned_device_pointers_take_the_scalar_path(eng):
     eng.synchronize()
     got = dst[1:].cpu().numpy().reshape(batch, n, n)
     assert np.array_equal(got, want)
+
+
+# ------------------------------------------------------------------ API hygiene
+def test_cached_chain_replay_invalidates_prepared_rhs():
+    """A chain replayed from the graph cache overwrites the workspace a prepared
+    right-hand side lives in, so rows_prepared must refuse afterwards (cache
+    miss and cache hit alike)."""
+    import torch
+
+    eng = mx.Engine(0)
+    n = 512
+    a = torch.from_numpy(oracle.scaled_input(n, np.float32, 3)).cuda()
+    out = torch.empty_like(a)
+    part = torch.empty((128, n), dtype=a.dtype, device=a.device)
+    for _ in range(2):  # the second power_device replays the cached graph
+        eng.gemm_prepare_rhs_device(a.data_ptr(), n)
+        eng.power_device(a.data_ptr(), out.data_ptr(), n, 13)
+        with pytest.raises(ValueError):
+            eng.gemm_rows_prepared_device(a.data_ptr(), part.data_ptr(), n, 128)
+    eng.synchronize()
+
+
+def test_graph_cache_is_bounded_and_results_stay_right():
+    """Fresh buffers on every call (as with torch tensors) capture a new graph
+    each time; the cache evicts instead of growing, and replays stay correct."""
+    import torch
+
+    eng = mx.Engine(0)
+    n = 256
+    a_np = oracle.scaled_input(n, np.float32, 8)
+    want = eng.power(a_np, 7)
+    keep = []
+    for i in range(80):
+        a = torch.from_numpy(a_np).cuda()
+        out = torch.empty_like(a)
+        eng.power_device(a.data_ptr(), out.data_ptr(), n, 7)
+        keep.append((a, out))
+    eng.synchronize()
+    for a, out in keep[::13]:
+        assert out.cpu().numpy().tobytes() == want.tobytes()
+
+
+def test_host_api_argument_validation(eng):
+    with pytest.raises(ValueError):
+        eng.power_mod(np.zeros(16, np.uint32), 3, 7)
+    with pytest.raises(ValueError):
+        eng.power_mod(np.zeros((4, 5), np.uint32), 3, 7)
+    with pytest.raises(ValueError):
+        eng.power_mod(np.zeros((4, 4), np.uint32), 3, 2**32 + 5)
+    stack = np.zeros((3, 8, 8), np.float32)
+    for bad in (np.zeros((2, 8, 8), np.float32), np.zeros((3, 8, 8), np.float64),
+                np.zeros((3, 8, 16), np.float32)[:, :, ::2]):
+        with pytest.raises(ValueError):
+            eng.power_batched(stack, 3, out=bad)
