@@ -171,6 +171,18 @@ MXP_API int mxp_power_mod(mxp_handle h, int64_t n, int64_t k, uint32_t p, const 
 MXP_API int mxp_random_device(mxp_handle h, int mode, int64_t n, int64_t batch, uint64_t seed0,
                               double lo, double hi, double scale, void* dOut);
 
+/* the raw SplitMix64 stream (linalg.py:117-124 splitmix64(seed, count)):
+ * count uint64 draws of `seed` into dOut.  Async on the handle stream. */
+MXP_API int mxp_splitmix64_device(mxp_handle h, uint64_t seed, int64_t count, void* dOut);
+
+/* Test hook (fault injection): chains captured after this call trap at plan
+ * step `step` (-1 disables), so tests can check that an asynchronous device
+ * fault inside a graph-replayed chain is reported with the right step index
+ * (mxp_stats.failed_step -> BackendStepError, errors.py:43-49; the reference's
+ * own test is test_expo.py:123-137).  The trap kills the CUDA context: use it
+ * in a throw-away process. */
+MXP_API int mxp_debug_inject_fault(mxp_handle h, int64_t step);
+
 /* error reporting */
 MXP_API int mxp_last_error(char* buf, size_t len); /* copies the thread's last message */
 MXP_API const char* mxp_status_string(int status);

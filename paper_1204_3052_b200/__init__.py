@@ -47,7 +47,7 @@ from .expo import (
     plan_exponentiation,
     repeated_exponentiate,
 )
-from .generate import random_matrix, scaled_batch, scaled_input
+from .generate import random_matrix, scaled_batch, scaled_input, splitmix64
 
 __version__ = "0.1.0"
 
@@ -56,7 +56,7 @@ __all__ = [
     "UnsupportedPowerError", "BackendStepError", "ConfigError", "ValidationError",
     "UnsupportedError", "DeviceUnavailableError", "DeviceError", "ExtensionNotBuiltError",
     "Matrix", "ErrorMetrics", "identity", "zeros", "compare", "random_matrix", "read_matrix",
-    "write_matrix",
+    "write_matrix", "splitmix64",
     "scaled_batch", "scaled_input", "vectorized_tol", "associativity_tol", "oracle_tol",
     "device_tol", "fro_tol", "fro_tol_conditioned", "multiply_count", "Step", "Strategy",
     "ExponentPlan", "plan_exponentiation", "Backend", "CountingBackend", "B200Backend",

@@ -36,7 +36,8 @@ EXPORTS = (
     "mxp_power_mod_device", "mxp_power_mod", "mxp_random_device", "mxp_last_error",
     "mxp_status_string", "mxp_gemm_prepare_rhs", "mxp_gemm_rows_prepared",
     "mxp_ipc_get_handle", "mxp_ipc_open_handle", "mxp_ipc_close_handle", "mxp_split_planes",
-    "mxp_gemm_rows_planes_peers", "mxp_peer_barrier",
+    "mxp_gemm_rows_planes_peers", "mxp_peer_barrier", "mxp_debug_inject_fault",
+    "mxp_splitmix64_device",
 )
 MXP_IPC_HANDLE_BYTES = 72
 
@@ -117,6 +118,8 @@ def load() -> ctypes.CDLL:
                                   ctypes.c_double, ctypes.c_double, vp],
             "mxp_last_error": [ctypes.c_char_p, sz],
             "mxp_status_string": [c_int],
+            "mxp_debug_inject_fault": [vp, i64],
+            "mxp_splitmix64_device": [vp, ctypes.c_uint64, i64, vp],
         }
         for name, args in sig.items():
             fn = getattr(L, name)

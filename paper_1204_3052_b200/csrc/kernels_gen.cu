@@ -41,6 +41,21 @@ __global__ void random_kernel(T* __restrict__ out, int64_t n2, int64_t batch, ui
     }
 }
 
+// The raw stream (linalg.py:117-124: splitmix64(seed, count)), draw k at out[k].
+__global__ void splitmix64_kernel(uint64_t* __restrict__ out, int64_t count, uint64_t seed) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = sm64(seed, static_cast<uint64_t>(i));
+}
+
+cudaError_t launch_splitmix64(uint64_t seed, int64_t count, uint64_t* out, cudaStream_t s) {
+    int blocks = static_cast<int>((count + 255) / 256);
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks < 1) blocks = 1;
+    splitmix64_kernel<<<blocks, 256, 0, s>>>(out, count, seed);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_random(int mode, int64_t n, int64_t batch, uint64_t seed0, double lo, double hi,
                           double scale, void* out, cudaStream_t s) {
     const double span = hi - lo;

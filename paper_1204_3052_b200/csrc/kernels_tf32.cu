@@ -1203,7 +1203,7 @@ template <int kBN_>
 __global__ void __launch_bounds__(384, 1)
     k1c_chain_3xtf32(const __grid_constant__ K1CMaps maps, const __grid_constant__ K1CPlanes pl,
                      PlanBits plan, int n_pad, float* __restrict__ out_f32, int n_out,
-                     unsigned int* __restrict__ bar_ctr) {
+                     unsigned int* __restrict__ bar_ctr, uint32_t* progress, int fault_step) {
     using Cfg = K1CCfg<kBN_>;
     constexpr int S = Cfg::kStages;
     constexpr int BN = Cfg::kBN;
@@ -1256,6 +1256,15 @@ __global__ void __launch_bounds__(384, 1)
         const int dst = (acc == 1) ? 2 : 1;
         const int rhs = mult ? 0 : acc;
         const int g0 = step * kb_per;  // pipeline position of this step's first k-block
+        if (threadIdx.x == 0 && progress != nullptr) {
+            // every CTA has passed the previous step's grid barrier: a fault
+            // from here on belongs to this step (the host reads the mark back)
+            *reinterpret_cast<volatile uint32_t*>(progress) = static_cast<uint32_t>(step + 1);
+            if (step == fault_step && blockIdx.x == 0 && blockIdx.y == 0) {
+                __threadfence_system();
+                __trap();
+            }
+        }
         if (warp == 4) K1C_STAMP(0);
         if (warp == 0 && lane == 0) {
             // the planes this step reads were written by other CTAs' generic
@@ -1402,14 +1411,20 @@ static cudaError_t prepare_k1c() {
     return e;
 }
 
-#ifndef MXP_K1C_COOPERATIVE
-#define MXP_K1C_COOPERATIVE 1
-#endif
-// One cooperative launch for the whole chain; cudaErrorCooperativeLaunchTooLarge
-// (or any launch error) tells the caller to run the per-step chain instead.
+// One launch for the whole chain.  Its grid barrier needs every CTA resident
+// at once: guaranteed by construction (tiles x splits clusters <= one wave of
+// cudaOccupancyMaxActiveClusters, one CTA per SM, checked above).  The
+// launch is deliberately NOT cooperative: ncu's kernel replay faults
+// (cudaErrorIllegalAddress) on a cooperative cluster launch captured in a
+// graph, while the plain cluster launch profiles and runs bitwise the same
+// (profiles/r02_k1c_ncu_coop_vs_plain.txt).  A kernel running concurrently on
+// another stream can only delay the late CTAs (they start when it retires).
+// cudaErrorNotSupported (or any launch error) tells the caller to run the
+// per-step chain instead.
 cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
                              uint32_t* const* planes, const PlanBits& plan, int n_pad, int splits,
-                             float* out_f32, int n_out, unsigned int* bar_ctr, cudaStream_t s) {
+                             float* out_f32, int n_out, unsigned int* bar_ctr, uint32_t* progress,
+                             int fault_step, cudaStream_t s) {
     if (splits < 1 || splits > 8 || n_pad % 128 != 0 || k1_split_legacy()) return cudaErrorNotSupported;
     const int tiles = (n_pad / 128) * (n_pad / 128);
     if (tiles > k1_max_clusters(splits)) return cudaErrorNotSupported;
@@ -1433,20 +1448,33 @@ cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
     cfg.blockDim = dim3(384);
     cfg.dynamicSmemBytes = narrow ? K1CCfg<64>::kSmem : K1CCfg<128>::kSmem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = static_cast<unsigned>(splits);
     attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeCooperative;
-    attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = MXP_K1C_COOPERATIVE ? 2 : 1;
+    cfg.numAttrs = 1;
     if (narrow)
         return cudaLaunchKernelEx(&cfg, k1c_chain_3xtf32<64>, maps, pl, plan, n_pad, out_f32, n_out,
-                                  bar_ctr);
+                                  bar_ctr, progress, fault_step);
     return cudaLaunchKernelEx(&cfg, k1c_chain_3xtf32<128>, maps, pl, plan, n_pad, out_f32, n_out,
-                              bar_ctr);
+                              bar_ctr, progress, fault_step);
+}
+
+namespace {
+__global__ void progress_mark_kernel(uint32_t* progress, uint32_t value, int trap) {
+    *reinterpret_cast<volatile uint32_t*>(progress) = value;
+    if (trap) {
+        __threadfence_system();
+        __trap();
+    }
+}
+}  // namespace
+
+cudaError_t launch_progress_mark(uint32_t* progress, uint32_t value, int trap, cudaStream_t s) {
+    progress_mark_kernel<<<1, 1, 0, s>>>(progress, value, trap);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_k1p_gemm_peers(const GemmPlanes& m, int n_pad, int m_pad, int ld_out,

@@ -120,6 +120,12 @@ struct mxp_handle_s {
     // modular workspace: base limbs (3), acc limbs (3), T0..T2 (3), n_pad^2 doubles each
     int64_t wsmod_pad = 0;
     double* modbuf[9] = {};
+    // plan-step progress of the running chain (pinned, mapped): kernels store
+    // step+1 at the start of each step, so after an asynchronous device fault
+    // the host still reads which step failed (BackendStepError, errors.py:43-49)
+    uint32_t* progress_host = nullptr;
+    uint32_t* progress_dev = nullptr;
+    int fault_step = -1;  // test hook (mxp_debug_inject_fault): trap at this step
     // host-API staging device buffers
     size_t io_bytes = 0;
     void* d_in = nullptr;
@@ -288,7 +294,7 @@ int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float
     if (bn == 128 && k1c_enabled()) {
         // the whole chain in one launch when every split-K cluster fits at once
         e = launch_k1c_chain(h->map_a, h->map_b, h->planes, plan, np, h->splits, dOut, (int)n,
-                             h->bar_ctr, h->stream);
+                             h->bar_ctr, h->progress_dev, h->fault_step, h->stream);
         if (e == cudaSuccess) {
             ++*launches;
             return MXP_OK;
@@ -301,6 +307,13 @@ int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float
         const bool last = (s == plan.len - 1);
         const int dst = (acc == 1) ? 2 : 1;
         const int rhs = mult ? 0 : acc;
+        e = launch_progress_mark(h->progress_dev, static_cast<uint32_t>(s + 1), s == h->fault_step,
+                                 h->stream);
+        if (e != cudaSuccess) {
+            *failed = s;
+            return cuda_fail(e, "progress mark");
+        }
+        ++*launches;
         GemmPlanes m;
         m.a_hi = h->map_a[2 * acc];
         m.a_lo = h->map_a[2 * acc + 1];
@@ -333,12 +346,15 @@ int enqueue_chain_f64(mxp_handle h, int64_t n, const PlanBits& plan, const doubl
     for (int s = 0; s < plan.len; ++s) {
         const bool mult = plan_is_mult(plan, s);
         const int dst = (acc == 1) ? 2 : 1;
-        e = launch_f64_gemm(b[acc], mult ? b[0] : b[acc], b[dst], (int)n_pad, h->stream);
+        e = launch_progress_mark(h->progress_dev, static_cast<uint32_t>(s + 1), s == h->fault_step,
+                                 h->stream);
+        if (e == cudaSuccess)
+            e = launch_f64_gemm(b[acc], mult ? b[0] : b[acc], b[dst], (int)n_pad, h->stream);
         if (e != cudaSuccess) {
             *failed = s;
             return cuda_fail(e, "f64_gemm");
         }
-        ++*launches;
+        *launches += 2;
         acc = dst;
     }
     e = launch_f64_unpad(b[acc], (int)n_pad, dOut, (int)n, h->stream);
@@ -388,6 +404,11 @@ int enqueue_trivial(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA
         }
     }
     return MXP_OK;
+}
+
+// plan step index of the last progress mark (-1: none this call)
+int64_t progress_step(mxp_handle h) {
+    return static_cast<int64_t>(*reinterpret_cast<volatile uint32_t*>(h->progress_host)) - 1;
 }
 
 void fill_plan_stats(mxp_stats* st, int64_t k, int64_t batch) {
@@ -443,6 +464,16 @@ int run_power_graph(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA
 
 // =====================================================================
 extern "C" {
+
+int mxp_debug_inject_fault(mxp_handle h, int64_t step) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (step < -1 || step > 127) return fail(MXP_E_VALIDATION, "fault step must be in [-1, 127]");
+    MXP_CUDA(cudaStreamSynchronize(h->stream));
+    h->drop_graphs();  // captured chains carry the old setting
+    h->fault_step = static_cast<int>(step);
+    return MXP_OK;
+}
 
 int mxp_version(int* major, int* minor) {
     if (major) *major = 0;
@@ -514,6 +545,10 @@ int mxp_create(int device, mxp_handle* out) {
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
     if (e == cudaSuccess) e = cudaMalloc(&h->bar_ctr, 256);
+    if (e == cudaSuccess)
+        e = cudaHostAlloc(reinterpret_cast<void**>(&h->progress_host), 64, cudaHostAllocMapped);
+    if (e == cudaSuccess)
+        e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->progress_dev), h->progress_host, 0);
     if (e != cudaSuccess) {
         delete h;
         return cuda_fail(e, "stream/event creation");
@@ -531,6 +566,7 @@ int mxp_destroy(mxp_handle h) {
         if (p) cudaFree(p);
     if (h->part) cudaFree(h->part);
     if (h->bar_ctr) cudaFree(h->bar_ctr);
+    if (h->progress_host) cudaFreeHost(h->progress_host);
     for (auto p : h->f64buf)
         if (p) cudaFree(p);
     for (auto p : h->modbuf)
@@ -926,6 +962,8 @@ int mxp_power(mxp_handle h, int mode, int64_t n, int64_t k, const void* hA, void
     const size_t bytes = static_cast<size_t>(n) * n * elem_size(mode);
     rc = ensure_io(h, bytes);
     if (rc) return rc;
+    MXP_CUDA(cudaStreamSynchronize(h->stream));  // no earlier chain still writes progress marks
+    *reinterpret_cast<volatile uint32_t*>(h->progress_host) = 0;
     MXP_CUDA(cudaMemcpyAsync(h->d_in, hA, bytes, cudaMemcpyHostToDevice, h->stream));
     MXP_CUDA(cudaEventRecord(h->ev0, h->stream));
     mxp_stats inner;
@@ -938,7 +976,9 @@ int mxp_power(mxp_handle h, int mode, int64_t n, int64_t k, const void* hA, void
     MXP_CUDA(cudaMemcpyAsync(hOut, h->d_out, bytes, cudaMemcpyDeviceToHost, h->stream));
     cudaError_t e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) {
-        if (st) st->failed_step = 0;
+        // the last step a kernel of this chain started (0: before the first step;
+        // the n <= 128 kernels run a whole chain per CTA and leave no marks)
+        if (st) st->failed_step = static_cast<int64_t>(progress_step(h));
         return cuda_fail(e, "power chain");
     }
     if (st) {
@@ -1089,6 +1129,17 @@ int mxp_random_device(mxp_handle h, int mode, int64_t n, int64_t batch, uint64_t
     return MXP_OK;
 }
 
+int mxp_splitmix64_device(mxp_handle h, uint64_t seed, int64_t count, void* dOut) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (count < 0) return fail(MXP_E_VALIDATION, "count must be >= 0, got %lld", (long long)count);
+    if (count == 0) return MXP_OK;
+    if (!dOut) return fail(MXP_E_VALIDATION, "null device pointer");
+    cudaError_t e = launch_splitmix64(seed, count, static_cast<uint64_t*>(dOut), h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "splitmix64_kernel");
+    return MXP_OK;
+}
+
 int mxp_power_mod_device(mxp_handle h, int64_t n, int64_t k, uint32_t p, const void* dA,
                          void* dOut, mxp_stats* st) {
     stats_reset(st);
@@ -1132,7 +1183,10 @@ int mxp_power_mod_device(mxp_handle h, int64_t n, int64_t k, uint32_t p, const v
     for (int s = 0; s < plan.len; ++s) {
         const int rhs = plan_is_mult(plan, s) ? 0 : acc;
         const bool last = (s == plan.len - 1);
-        e = launch_f64_gemm(B[acc + 1], B[rhs + 1], B[7], np, h->stream);           // T1
+        e = launch_progress_mark(h->progress_dev, static_cast<uint32_t>(s + 1), s == h->fault_step,
+                                 h->stream);
+        if (e == cudaSuccess)
+            e = launch_f64_gemm(B[acc + 1], B[rhs + 1], B[7], np, h->stream);  // T1
         if (e == cudaSuccess) e = launch_f64_gemm(B[acc], B[rhs], B[6], np, h->stream);  // T0
         if (e == cudaSuccess) e = launch_f64_gemm(B[acc + 2], B[rhs + 2], B[8], np, h->stream);
         if (e == cudaSuccess)
@@ -1142,7 +1196,7 @@ int mxp_power_mod_device(mxp_handle h, int64_t n, int64_t k, uint32_t p, const v
             if (st) st->failed_step = s;
             return cuda_fail(e, "modular multiply");
         }
-        launches += 4;
+        launches += 5;
         acc = 3;
     }
     if (st) st->launches = launches;
@@ -1159,6 +1213,8 @@ int mxp_power_mod(mxp_handle h, int64_t n, int64_t k, uint32_t p, const void* hA
     const size_t bytes = static_cast<size_t>(n) * n * 4;
     rc = ensure_io(h, bytes);
     if (rc) return rc;
+    MXP_CUDA(cudaStreamSynchronize(h->stream));
+    *reinterpret_cast<volatile uint32_t*>(h->progress_host) = 0;
     MXP_CUDA(cudaMemcpyAsync(h->d_in, hA, bytes, cudaMemcpyHostToDevice, h->stream));
     MXP_CUDA(cudaEventRecord(h->ev0, h->stream));
     mxp_stats inner;
@@ -1170,7 +1226,10 @@ int mxp_power_mod(mxp_handle h, int64_t n, int64_t k, uint32_t p, const void* hA
     MXP_CUDA(cudaEventRecord(h->ev1, h->stream));
     MXP_CUDA(cudaMemcpyAsync(hOut, h->d_out, bytes, cudaMemcpyDeviceToHost, h->stream));
     cudaError_t e = cudaStreamSynchronize(h->stream);
-    if (e != cudaSuccess) return cuda_fail(e, "modular power");
+    if (e != cudaSuccess) {
+        if (st) st->failed_step = progress_step(h);
+        return cuda_fail(e, "modular power");
+    }
     if (st) {
         *st = inner;
         float ms = 0.f;

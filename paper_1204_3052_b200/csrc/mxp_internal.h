@@ -97,9 +97,16 @@ int k1_split_k(int n_pad, int m_pad, int num_sms);
 int k1_split_launches(int splits);
 // K1C: the whole 3xTF32 chain in one cooperative launch (kernels_tf32.cu);
 // cudaErrorNotSupported / a launch error => run the per-step chain
+// progress (host-mapped, may be null): every CTA stores step+1 at the start of
+// each plan step; fault_step >= 0 makes CTA (0,0) trap there (test hook).
 cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
                              uint32_t* const* planes, const PlanBits& plan, int n_pad, int splits,
-                             float* out_f32, int n_out, unsigned int* bar_ctr, cudaStream_t s);  // kernel launches one split-K multiply takes
+                             float* out_f32, int n_out, unsigned int* bar_ctr, uint32_t* progress,
+                             int fault_step, cudaStream_t s);
+// one-thread kernel: *progress = value (host-mapped memory, survives a sticky
+// device fault so the host can name the failing plan step); trap != 0 then
+// executes a trap (the fault-injection test hook)
+cudaError_t launch_progress_mark(uint32_t* progress, uint32_t value, int trap, cudaStream_t s);  // kernel launches one split-K multiply takes
 cudaError_t launch_split_rows(const float* in, int n, int ld, int rows, uint32_t* hi, uint32_t* lo,
                               int n_pad, int rows_pad, cudaStream_t s);
 
@@ -107,6 +114,7 @@ cudaError_t launch_split_rows(const float* in, int n, int ld, int rows, uint32_t
 // Reference random_matrix (linalg.py:127-148) on device; scale != 0 selects
 // the scaled recipe fl(random_matrix(n, F64, seed, lo, hi) * scale).
 // Matrix b of the batch uses seed seed0 + b.
+cudaError_t launch_splitmix64(uint64_t seed, int64_t count, uint64_t* out, cudaStream_t s);
 cudaError_t launch_random(int mode, int64_t n, int64_t batch, uint64_t seed0, double lo, double hi,
                           double scale, void* out, cudaStream_t s);
 

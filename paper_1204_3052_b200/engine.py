@@ -80,6 +80,11 @@ class Engine:
     def synchronize(self) -> None:
         _lib.check(self._L.mxp_synchronize(self._h), "mxp_synchronize")
 
+    def debug_inject_fault(self, step: int) -> None:
+        """Test hook: chains captured from now on trap at plan step `step` (-1
+        disables).  The trap kills the CUDA context (use a throw-away process)."""
+        _lib.check(self._L.mxp_debug_inject_fault(self._h, int(step)), "mxp_debug_inject_fault")
+
     # ------------------------------------------------------------ errors
     def _raise_chain(self, status: int, stats: _lib.Stats, plan: str, what: str) -> None:
         """Map a failed chain to BackendStepError (errors.py:43-49) when the
@@ -272,6 +277,11 @@ class Engine:
         _lib.check(self._L.mxp_random_device(self._h, mode, n, batch,
                                              ctypes.c_uint64(seed0 & (2**64 - 1)), lo, hi, scale,
                                              ctypes.c_void_p(d_out)), "mxp_random_device")
+
+    def splitmix64_device(self, d_out: int, seed: int, count: int) -> None:
+        _lib.check(self._L.mxp_splitmix64_device(self._h, ctypes.c_uint64(seed & (2**64 - 1)),
+                                                 int(count), ctypes.c_void_p(d_out)),
+                   "mxp_splitmix64_device")
 
     # ------------------------------------------------------------ memory
     def alloc(self, nbytes: int) -> int:

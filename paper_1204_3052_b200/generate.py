@@ -37,6 +37,26 @@ def _gen(n: int, batch: int, dtype: DType, seed0: int, lo: float, hi: float, sca
     return out
 
 
+def splitmix64(seed: int, count: int, device: int = 0) -> np.ndarray:
+    """First ``count`` outputs of SplitMix64 seeded with ``seed`` (linalg.py:117-124),
+    as uint64, generated on the device; bit-identical to the reference."""
+    if count < 0:
+        raise InvalidDimensionError(f"count must be >= 0, got {count}")
+    from .engine import default_engine
+
+    out = np.empty(count, dtype=np.uint64)
+    if count == 0:
+        return out
+    eng = default_engine(device)
+    d = eng.alloc(out.nbytes)
+    try:
+        eng.splitmix64_device(d, seed, count)
+        eng.download(out, d)
+    finally:
+        eng.free(d)
+    return out
+
+
 def random_matrix(n: int, dtype: DType = DType.F64, seed: int = 0, lo: float = -0.5,
                   hi: float = 0.5, device: int = 0) -> Matrix:
     """Deterministic uniform matrix in [lo, hi) (linalg.py:127-148), bit-exact."""

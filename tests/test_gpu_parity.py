@@ -55,6 +55,23 @@ def test_device_random_matrix_bitexact(golden):
         assert sha(mx.random_matrix(int(n), dtype, int(seed)).array) == digest, key
 
 
+def test_splitmix64_exported_and_bitexact(golden):
+    """splitmix64 is public API in the reference (linalg.py:117-124, __all__); its
+    frozen KATs (test_linalg.py:28-45) and the golden streams, through ours."""
+    arrays, _ = golden
+    kats = {0: (0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F, 0xF88BB8A8724C81EC),
+            42: (0xBDD732262FEB6E95, 0x28EFE333B266F103, 0x47526757130F9F52, 0x581CE1FF0E4AE394),
+            2024: (0x9F6D8FECF88EECD5, 0x18E430BB1511F2D2, 0x4C6F7CBF58DBA57F, 0x1DBE69E0AE9BB859)}
+    for seed, want in kats.items():
+        got = mx.splitmix64(seed, 4)
+        assert got.dtype == np.uint64 and tuple(int(v) for v in got) == want
+    for seed in (0, 42, 2024, 7, 2**64 - 1):
+        assert np.array_equal(mx.splitmix64(seed, 16), arrays[f"sm64_{seed}"])
+    big = mx.splitmix64(123, 1 << 20)
+    assert np.array_equal(big, oracle.splitmix64(123, 1 << 20))
+    assert mx.splitmix64(5, 0).shape == (0,)
+
+
 def test_device_scaled_recipe_bitexact(golden):
     _, meta = golden
     for key, digest in meta["scaled_sha256"].items():

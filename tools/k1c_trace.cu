@@ -35,12 +35,12 @@ int main(int argc, char** argv) {
     const int splits = k1_split_k(np, np, sms);
     for (int r = 0; r < 3; ++r) {
         launch_split(a, n, n, planes[0], planes[1], np, 0);
-        cudaError_t e = launch_k1c_chain(ma, mb, planes, plan, np, splits, out, n, ctr, 0);
+        cudaError_t e = launch_k1c_chain(ma, mb, planes, plan, np, splits, out, n, ctr, nullptr, -1, 0);
         if (e != cudaSuccess) { printf("launch: %s\n", cudaGetErrorString(e)); return 1; }
     }
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    launch_k1c_chain(ma, mb, planes, plan, np, splits, out, n, ctr, 0);
+    launch_k1c_chain(ma, mb, planes, plan, np, splits, out, n, ctr, nullptr, -1, 0);
     cudaEventRecord(e1);
     cudaError_t e = cudaDeviceSynchronize();
     float ms; cudaEventElapsedTime(&ms, e0, e1);
