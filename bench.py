@@ -178,7 +178,8 @@ def ncu_traffic(kernel: str):
 
 
 # ----------------------------------------------------------------------------- CPU
-def cpu_sample(w: dict, budget_s: float = 12.0, threads: int | None = None) -> dict:
+def cpu_sample(w: dict, budget_s: float = 12.0, threads: int | None = None,
+               one_core: bool = True) -> dict:
     """Time the oracle port (CPU restatement of the reference's naive chain,
     bit-identical to it) on a bounded sample of the workload."""
     import numpy as np
@@ -234,9 +235,15 @@ def cpu_sample(w: dict, budget_s: float = 12.0, threads: int | None = None) -> d
         sample = (f"{rows} rows of one {n}x{n} multiply on {threads} threads, extrapolated "
                   f"x{n / rows:.0f} rows x{m} multiplies")
         full_s = dt_s * (n / rows) * m
-    return {"value": fl / dt_s / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
-            "sample": sample, "sample_seconds": dt_s, "est_full_workload_seconds": full_s,
-            "matrices_per_s": w["batch"] / full_s if w["batch"] > 1 else 1.0 / full_s}
+    res = {"value": fl / dt_s / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+           "sample": sample, "sample_seconds": dt_s, "est_full_workload_seconds": full_s,
+           "matrices_per_s": w["batch"] / full_s if w["batch"] > 1 else 1.0 / full_s}
+    if threads > 1 and one_core:
+        # BASELINE.md §3 asks for the 1-core figure beside the N-core one
+        one = cpu_sample(w, budget_s=min(budget_s, 3.0), threads=1, one_core=False)
+        res["one_core"] = {k: one[k] for k in ("value", "unit", "cores", "sample",
+                                               "sample_seconds", "est_full_workload_seconds")}
+    return res
 
 
 # ----------------------------------------------------------------------------- GPU
@@ -332,9 +339,20 @@ def run_device(eng, w: dict, steps: int, warmup: int, seed0: int, dist=None, sam
     if dist is not None:
         dist.barrier()
     ms = start.elapsed_time(end) / steps
+    clocks = sampler.summary() if sampler else None
+    if clocks is not None and w["batch"] > 1:
+        # the SM clock inside the last timed launch (clock64 / globaltimer of
+        # CTA 0): NVML's samples can miss or smear a few-ms kernel
+        try:
+            mhz, kms = eng.last_kernel_clock()
+            clocks["sm_mhz_in_kernel"] = mhz
+            clocks["in_kernel_ms"] = kms
+            clocks["sm_mhz_source"] = "NVML median over the timed region; sm_mhz_in_kernel from the kernel"
+        except Exception:  # noqa: BLE001 - K3B launches carry no stamps
+            pass
     eng.free(d_in)
     eng.free(d_out)
-    return ms, launches, (sampler.summary() if sampler else None)
+    return ms, launches, clocks
 
 
 def run_e2e(eng, w: dict, batch: int, seed0: int, steps: int = 3, pinned: bool = True) -> dict:
@@ -480,7 +498,7 @@ def main() -> None:
             return
         samples = []
         for i in range(args.warmup + args.steps):
-            r = cpu_sample(w, budget_s=2.0)
+            r = cpu_sample(w, budget_s=2.0, one_core=False)
             if i >= args.warmup:
                 samples.append(r)
         val = statistics.median(s["value"] for s in samples)

@@ -175,6 +175,12 @@ MXP_API int mxp_random_device(mxp_handle h, int mode, int64_t n, int64_t batch, 
  * count uint64 draws of `seed` into dOut.  Async on the handle stream. */
 MXP_API int mxp_splitmix64_device(mxp_handle h, uint64_t seed, int64_t count, void* dOut);
 
+/* The SM clock the last batched n <= 128 launch (K3H) actually ran at:
+ * clock64 and globaltimer stamped by CTA 0 at its start and end, so
+ * *sm_mhz = cycles / ns (NVML samples miss short kernels).  Synchronizes
+ * the handle's stream.  MXP_E_UNSUPPORTED if no such launch happened. */
+MXP_API int mxp_last_kernel_clock(mxp_handle h, double* sm_mhz, double* kernel_ms);
+
 /* Test hook (fault injection): chains captured after this call trap at plan
  * step `step` (-1 disables), so tests can check that an asynchronous device
  * fault inside a graph-replayed chain is reported with the right step index

@@ -18,6 +18,7 @@ from .errors import (
     InvalidRangeError,
     MatexpoError,
     ShapeError,
+    TableError,
     UnsupportedError,
     UnsupportedPowerError,
     ValidationError,
@@ -54,7 +55,7 @@ __version__ = "0.1.0"
 __all__ = [
     "DType", "MatexpoError", "InvalidDimensionError", "InvalidRangeError", "ShapeError",
     "UnsupportedPowerError", "BackendStepError", "ConfigError", "ValidationError",
-    "UnsupportedError", "DeviceUnavailableError", "DeviceError", "ExtensionNotBuiltError",
+    "UnsupportedError", "TableError", "DeviceUnavailableError", "DeviceError", "ExtensionNotBuiltError",
     "Matrix", "ErrorMetrics", "identity", "zeros", "compare", "random_matrix", "read_matrix",
     "write_matrix", "splitmix64",
     "scaled_batch", "scaled_input", "vectorized_tol", "associativity_tol", "oracle_tol",

@@ -37,7 +37,7 @@ EXPORTS = (
     "mxp_status_string", "mxp_gemm_prepare_rhs", "mxp_gemm_rows_prepared",
     "mxp_ipc_get_handle", "mxp_ipc_open_handle", "mxp_ipc_close_handle", "mxp_split_planes",
     "mxp_gemm_rows_planes_peers", "mxp_peer_barrier", "mxp_debug_inject_fault",
-    "mxp_splitmix64_device",
+    "mxp_splitmix64_device", "mxp_last_kernel_clock",
 )
 MXP_IPC_HANDLE_BYTES = 72
 
@@ -120,6 +120,7 @@ def load() -> ctypes.CDLL:
             "mxp_status_string": [c_int],
             "mxp_debug_inject_fault": [vp, i64],
             "mxp_splitmix64_device": [vp, ctypes.c_uint64, i64, vp],
+            "mxp_last_kernel_clock": [vp, P(ctypes.c_double), P(ctypes.c_double)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)

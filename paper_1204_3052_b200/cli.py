@@ -42,6 +42,9 @@ def build_parser() -> argparse.ArgumentParser:
     bench.add_argument("--no-oracle", action="store_true")
     bench.add_argument("--extended", action="store_true", help="append the B200 CSV columns")
     bench.add_argument("--csv", default="-", help="CSV output path, or - for stdout")
+    bench.add_argument("--table", help="the paper's comparison table: output path, or - for stdout")
+    bench.add_argument("--baseline-csv", help="CSV with the reference's naive (sequential CPU) "
+                       "rows for --table, written by the reference CLI")
     bench.set_defaults(func=cmd_bench)
     verify = sub.add_parser("verify", help="oracle comparison for one grid point")
     verify.add_argument("--size", type=int, required=True)
@@ -65,11 +68,24 @@ def cmd_bench(args) -> int:
                               strategies=[Strategy.parse(s) for s in args.strategies],
                               backends=args.backends, dtype=DType.parse(args.dtype),
                               seed=args.seed, repetitions=args.reps, oracle=not args.no_oracle)
+    if args.table and not args.baseline_csv:
+        raise ValueError("--table needs --baseline-csv (the reference's naive rows)")
     records = harness.run_benchmark(cfg)
     if args.csv == "-":
-        harness.emit_csv(records, sys.stdout, args.extended)
+        if not args.table:
+            harness.emit_csv(records, sys.stdout, args.extended)
     else:
         harness.emit_csv(records, args.csv, args.extended)
+    if args.table:
+        base = [r for r in harness.read_csv(args.baseline_csv) if r.backend == "naive"]
+        texts = [harness.emit_table([r for r in records + base if r.size == size])
+                 for size in sorted({r.size for r in records})]
+        text = "\n".join(texts)
+        if args.table == "-":
+            sys.stdout.write(text)
+        else:
+            with open(args.table, "w", encoding="utf-8") as fh:
+                fh.write(text)
     return 0
 
 

@@ -267,7 +267,8 @@ template <bool kMults>
 __global__ void __launch_bounds__(kThreads, 1)
     k3h_batched_power(const __grid_constant__ CUtensorMap in_map,
                       const __grid_constant__ CUtensorMap out_map, const float* __restrict__ in,
-                      float* __restrict__ out, int n, long long batch, PlanBits plan, int vec) {
+                      float* __restrict__ out, int n, long long batch, PlanBits plan, int vec,
+                      unsigned long long* stamps) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
@@ -296,6 +297,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_slot;
     const uint32_t s0 = smem_u32(smem);
     const long long G = gridDim.x;
+    if (stamps != nullptr && blockIdx.x == 0 && tid == 0) {
+        stamps[0] = clock64();
+        stamps[1] = globaltimer_ns();
+    }
     const size_t n2 = static_cast<size_t>(n) * n;
     const int last = plan.len - 1;
     auto is_mult = [&](int step) { return kMults && plan_is_mult(plan, step); };
@@ -758,6 +763,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (stamps != nullptr && blockIdx.x == 0 && tid == 0) {
+        stamps[2] = clock64();
+        stamps[3] = globaltimer_ns();
+    }
 #ifdef K3H_TRACE
     if (blockIdx.x == 0 && tid < 16) g_k3h_trace[tid] = k3h_acc[tid];
 #endif
@@ -775,7 +784,8 @@ cudaError_t prepare_k3h_kernel() {
 }
 
 cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch,
-                               const PlanBits& plan, int grid, cudaStream_t s) {
+                               const PlanBits& plan, int grid, unsigned long long* stamps,
+                               cudaStream_t s) {
     if (plan.len < 1 || n < 1 || n > kSmallMax) return cudaErrorInvalidValue;
     if (grid > batch) grid = static_cast<int>(batch);
     CUtensorMap in_map, out_map;
@@ -789,9 +799,11 @@ cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch
     if (vec && !(encode_tile_map(&in_map, in, batch * 128) && encode_tile_map(&out_map, out, batch * 128)))
         vec = 0;
     if (plan.mult[0] | plan.mult[1])
-        k3h_batched_power<true><<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec);
+        k3h_batched_power<true><<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec,
+                                                               stamps);
     else
-        k3h_batched_power<false><<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec);
+        k3h_batched_power<false><<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan,
+                                                                vec, stamps);
     return cudaGetLastError();
 }
 

@@ -15,361 +15,38 @@
 namespace mxp {
 
 // ======================================================================
-// K3 — persistent batched chain, n <= 128, one matrix per CTA at a time,
-// the running power P resident on chip for the whole chain.
-//
-//   TMEM (512 columns):  [0,128) D0, [128,256) D1 fp32 accumulators
-//                        (lane = row); [256,384) P_hi, [384,512) P_lo as the
-//                        LEFT operand (lane = row m, column = k)
-//   SMEM (128 KB):       P_hi, P_lo as the RIGHT operand, MN-major
-//                        SW128_BASE32B: [n/32][k][32] with 128-byte rows
-//
-// Per step one thread issues 16 k-steps x 3 tcgen05.mma (M=N=128, K=8,
-// A from TMEM, B from SMEM) and commits to an mbarrier; 8 warps then drain
-// D0 + D1 (tcgen05.ld, round-to-nearest fp32 add), split each value into
-// tf32 hi/lo, and write the next power back both into TMEM (tcgen05.st, left
-// operand) and SMEM (right operand) — or, on the last step, fp32 to global.
-//
-// Accuracy: the tensor core truncates its fp32 accumulator on every MMA
-// (measured: a bias that grows linearly with the number of MMAs into one
-// accumulator, tools/probe.py "acc"), and a chain amplifies a systematic
-// per-multiply bias ~k-fold.  So the small cross terms (lo*hi, hi*lo) are
-// accumulated first (their truncation is 2^-11 smaller), the k-steps are
-// split by parity over two accumulators (8 big-term MMAs each), and the two
-// partial sums are combined with an IEEE round-to-nearest add.
-//
-// MULTIPLY_BASE computes base*acc instead of the reference's acc*base
-// (expo.py:135-136): both are A^(e+1) because acc is a power of the base; the
-// resident power stays the right operand and the base is loaded into the
-// TMEM left operand for that step only.
+// n <= 128: the persistent batched chain kernels K3H (kernels_k3h.cu, scaled
+// fp16x2 split, the default) and K3B (kernels_k3b.cu, bf16x3 split, for
+// chains whose accumulated truncation bias K3H could not keep inside the
+// tolerance).
 // ======================================================================
 namespace {
-constexpr uint32_t kChunk = 128u * 128u;  // one 32-column chunk: 128 rows x 128 B
-constexpr uint32_t kPlane = 4u * kChunk;  // 64 KB
-constexpr uint32_t kColD0 = 0, kColD1 = 128, kColHi = 256, kColLo = 384;
-
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023u) & ~uintptr_t(1023));
 }
-
-// 16 split values (row `row`, columns [col0, col0+16), col0 % 16 == 0) into
-// one SMEM right-operand plane (MN-major SW128_BASE32B).  The 16-byte unit
-// order is flipped for rows with (row >> 2) odd so the 8 rows of a
-// quarter-warp hit 8 distinct 16-byte bank groups (no conflicts).
-__device__ __forceinline__ void k3_put_half(uint32_t s_plane, uint32_t row, int col0,
-                                            const uint32_t (&h)[16]) {
-    const uint32_t flip = (row >> 2) & 1u;
-    const uint32_t base = (col0 >> 5) * kChunk + row * 128u;
-    const uint32_t u0 = (col0 & 31) >> 2;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int ua = u, ub = u ^ 1;
-        const uint32_t unit = u0 + (static_cast<uint32_t>(u) ^ flip);
-        const uint32_t off = base + ((((unit >> 1) ^ (row & 3u)) << 1 | (unit & 1u)) << 4);
-        uint32_t h0 = flip ? h[4 * ub] : h[4 * ua], h1 = flip ? h[4 * ub + 1] : h[4 * ua + 1];
-        uint32_t h2 = flip ? h[4 * ub + 2] : h[4 * ua + 2], h3 = flip ? h[4 * ub + 3] : h[4 * ua + 3];
-        sts128(s_plane + off, h0, h1, h2, h3);
-    }
-}
-
-// Row `row`, columns [col0, col0+16) of the staged input (TMA SWIZZLE_128B
-// layout: chunk c = 128 rows x 128 B, 16-byte unit u of row r at u ^ (r%8)).
-__device__ __forceinline__ void k3_stage_row(uint32_t s_stage, uint32_t row, int col0,
-                                             uint32_t (&h)[16], uint32_t (&l)[16]) {
-    const uint32_t base = s_stage + (col0 >> 5) * kChunk + row * 128u;
-    const uint32_t u0 = (col0 & 31) >> 2;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const uint4 x = lds128(base + (((u0 + u) ^ (row & 7u)) << 4));
-        split_tf32(__uint_as_float(x.x), h[4 * u], l[4 * u]);
-        split_tf32(__uint_as_float(x.y), h[4 * u + 1], l[4 * u + 1]);
-        split_tf32(__uint_as_float(x.z), h[4 * u + 2], l[4 * u + 2]);
-        split_tf32(__uint_as_float(x.w), h[4 * u + 3], l[4 * u + 3]);
-    }
-}
-
-// Fallback for n % 4 != 0 (no TMA map) and for MULTIPLY_BASE steps: row from
-// global, zero padded.
-__device__ __forceinline__ void k3_global_row(const float* __restrict__ src, int n, uint32_t row,
-                                              int col0, uint32_t (&h)[16], uint32_t (&l)[16]) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        const int c = col0 + i;
-        const float v = (row < static_cast<uint32_t>(n) && c < n)
-                            ? __ldg(src + static_cast<size_t>(row) * n + c)
-                            : 0.f;
-        split_tf32(v, h[i], l[i]);
-    }
-}
 }  // namespace
 
-size_t k3_smem_bytes() { return 3 * kPlane + 1024 + 256; }
-
-// Warp roles: 16 warps drain/convert (warp w owns TMEM lane quarter w % 4 and
-// the 32-column group 32 * (w / 4)); lane 0 of warp 0 additionally issues
-// every tcgen05.mma and TMA prefetch (after waiting, converged, on the same
-// barriers).  Each step's operands are published in two sets so the next
-// step's MMAs start before the epilogue has finished:
-//   set 1 = {A_lo (TMEM), B_hi (SMEM)} -> the 16 lo*hi MMAs may start
-//   set 2 = {A_hi (TMEM), B_lo (SMEM)} -> the 16 hi*lo and 16 hi*hi MMAs
-// (small cross terms still precede the big terms in every accumulator).
-constexpr int kK3Workers = 16;
-constexpr int kK3AllThreads = kK3Workers * 32;
-
-template <bool kProf>
-__global__ void __launch_bounds__(kK3AllThreads, 1)
-    k3_batched_power(const __grid_constant__ CUtensorMap in_map, int use_tma,
-                     const float* __restrict__ in, float* __restrict__ out, int n, long long batch,
-                     PlanBits plan, long long* __restrict__ prof) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = align1024(smem_raw);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 3 * kPlane);
-    uint64_t* mma_bar = bars + 0;   // MMAs of a step complete (tcgen05.commit)
-    uint64_t* load_bar = bars + 3;  // TMA staging landed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 3 * kPlane + 64);
-
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int lane = tid & 31;
-    constexpr uint32_t kIdesc = idesc_tf32_kmaj_mnmaj<128, 128>();
-
-    if (tid == 0) {
-        mbar_init(mma_bar, 1);
-        mbar_init(load_bar, 1);
-        fence_mbar_init();
-        if (use_tma) tma_prefetch(&in_map);
-    }
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t s_hi = smem_u32(smem), s_lo = s_hi + kPlane, s_stage = s_hi + 2 * kPlane;
-    const uint64_t bdesc_hi = mnmajor_desc(s_hi, kChunk), bdesc_lo = mnmajor_desc(s_lo, kChunk);
-
-    auto issue_load = [&](long long mm) {  // warp 0 lane 0
-        mbar_expect_tx(load_bar, 4 * kChunk);
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-            tma_load_3d(smem + 2 * kPlane + c * kChunk, &in_map, load_bar, 32 * c, 0,
-                        static_cast<int32_t>(mm));
-    };
-
-    long long p_load = 0, p_mma = 0, p_epi = 0, p_t = 0;
-    const int q = warp & 3;
-    const int colg = (warp >> 2) * 32;
-    const uint32_t row = q * 32 + lane;
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    const uint32_t t_d0 = lane_base + kColD0, t_d1 = lane_base + kColD1;
-    const uint32_t t_hi = lane_base + kColHi, t_lo = lane_base + kColLo;
-    uint32_t mma_phase = 0, load_phase = 0;
-
-    // Publish one operand set (TMEM stores + SMEM stores done by this warp):
-    // workers bar.arrive on named barrier `which`, warp 0 bar.syncs on it (the
-    // hardware barrier drains this CTA's pending st.shared) and its lane 0
-    // issues the MMAs the set enables.
-    auto publish = [&](int which, long long next_load) {
-        tmem_st_wait();
-        fence_proxy_async_smem();
-        tc_fence_before();
-        if (warp != 0) {
-            named_bar_arrive(which, kK3AllThreads);
-        } else {
-            named_bar_sync(which, kK3AllThreads);
-            if (lane == 0) {
-                tc_fence_after();
-                const uint32_t a_hi = tmem + kColHi, a_lo = tmem + kColLo;
-                if (which == 1) {
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const uint32_t d = tmem + ((k & 1) ? kColD1 : kColD0);
-                        mma_tf32_ts(d, a_lo + 8 * k,
-                                    bdesc_hi + static_cast<uint64_t>((k * 1024) >> 4), kIdesc,
-                                    k > 1 ? 1u : 0u);
-                    }
-                } else {
-                    if (next_load >= 0) issue_load(next_load);  // staging consumed
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const uint32_t d = tmem + ((k & 1) ? kColD1 : kColD0);
-                        mma_tf32_ts(d, a_hi + 8 * k,
-                                    bdesc_lo + static_cast<uint64_t>((k * 1024) >> 4), kIdesc, 1u);
-                    }
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const uint32_t d = tmem + ((k & 1) ? kColD1 : kColD0);
-                        mma_tf32_ts(d, a_hi + 8 * k,
-                                    bdesc_hi + static_cast<uint64_t>((k * 1024) >> 4), kIdesc, 1u);
-                    }
-                    mma_commit(mma_bar);
-                }
-            }
-            __syncwarp();
-        }
-    };
-
-    if (use_tma && tid == 0 && blockIdx.x < batch) issue_load(blockIdx.x);
-
-    for (long long m = blockIdx.x; m < batch; m += gridDim.x) {
-        const float* src = in + static_cast<size_t>(m) * n * n;
-        const long long next = (use_tma && m + gridDim.x < batch) ? m + gridDim.x : -1;
-        if (kProf) p_t = clock64();
-        // ---- input -> operands (both sets), published like an epilogue
-        uint32_t h[2][16], l[2][16];
-        if (use_tma) {
-            mbar_wait(load_bar, load_phase);
-            load_phase ^= 1;
-        }
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            if (use_tma)
-                k3_stage_row(s_stage, row, colg + 16 * j, h[j], l[j]);
-            else
-                k3_global_row(src, n, row, colg + 16 * j, h[j], l[j]);
-        }
-        // (a plan starting with MULTIPLY_BASE does not exist: k >= 2 starts with SQUARE)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            tmem_st16(t_lo + colg + 16 * j, l[j]);
-            k3_put_half(s_hi, row, colg + 16 * j, h[j]);
-        }
-        publish(1, -1);
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            tmem_st16(t_hi + colg + 16 * j, h[j]);
-            k3_put_half(s_lo, row, colg + 16 * j, l[j]);
-        }
-        publish(2, next);
-        if (kProf) { long long t = clock64(); p_load += t - p_t; p_t = t; }
-
-        for (int s = 0; s < plan.len; ++s) {
-            mbar_wait(mma_bar, mma_phase);
-            mma_phase ^= 1;
-            tc_fence_after();
-            if (kProf) { long long t = clock64(); p_mma += t - p_t; p_t = t; }
-            const bool last = (s == plan.len - 1);
-            uint32_t v2[2][16];
-            {
-                uint32_t w0[16], w1[16];
-                tmem_ld16x4(t_d0 + colg, t_d1 + colg, t_d0 + colg + 16, t_d1 + colg + 16, v2[0], w0,
-                            v2[1], w1);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    v2[0][i] = __float_as_uint(__fadd_rn(__uint_as_float(v2[0][i]), __uint_as_float(w0[i])));
-                    v2[1][i] = __float_as_uint(__fadd_rn(__uint_as_float(v2[1][i]), __uint_as_float(w1[i])));
-                }
-            }
-            if (last) {
-                if (row < static_cast<uint32_t>(n)) {
-#pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        const int col0 = colg + 16 * j;
-                        float* dst = out + static_cast<size_t>(m) * n * n +
-                                     static_cast<size_t>(row) * n + col0;
-                        if ((n & 3) == 0 && col0 + 16 <= n) {
-#pragma unroll
-                            for (int u = 0; u < 4; ++u)
-                                reinterpret_cast<float4*>(dst)[u] = make_float4(
-                                    __uint_as_float(v2[j][4 * u]), __uint_as_float(v2[j][4 * u + 1]),
-                                    __uint_as_float(v2[j][4 * u + 2]), __uint_as_float(v2[j][4 * u + 3]));
-                        } else {
-                            for (int i = 0; i < 16; ++i)
-                                if (col0 + i < n) dst[i] = __uint_as_float(v2[j][i]);
-                        }
-                    }
-                }
-                tc_fence_before();  // D reads done before the next matrix's MMAs
-            } else {
-                const bool next_mult = plan_is_mult(plan, s + 1);
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) split_tf32(__uint_as_float(v2[j][i]), h[j][i], l[j][i]);
-                // left operand of the next step: the new power, or the base
-                // (streamed from global one sub-chunk at a time)
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    if (next_mult) {
-                        uint32_t bh[16], bl[16];
-                        k3_global_row(src, n, row, colg + 16 * j, bh, bl);
-                        tmem_st16(t_lo + colg + 16 * j, bl);
-                    } else {
-                        tmem_st16(t_lo + colg + 16 * j, l[j]);
-                    }
-                    k3_put_half(s_hi, row, colg + 16 * j, h[j]);
-                }
-                publish(1, -1);
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    if (next_mult) {
-                        uint32_t bh[16], bl[16];
-                        k3_global_row(src, n, row, colg + 16 * j, bh, bl);
-                        tmem_st16(t_hi + colg + 16 * j, bh);
-                    } else {
-                        tmem_st16(t_hi + colg + 16 * j, h[j]);
-                    }
-                    k3_put_half(s_lo, row, colg + 16 * j, l[j]);
-                }
-                publish(2, -1);
-            }
-            if (kProf) { long long t = clock64(); p_epi += t - p_t; p_t = t; }
-        }
-    }
-    if (kProf && blockIdx.x == 0 && tid == 0) {
-        prof[0] = p_load; prof[1] = p_mma; prof[2] = p_epi;
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) tmem_dealloc<512>(tmem);
-}
-
-// Debug hook: when set (tools/), CTA 0 records per-phase cycle totals here.
-long long* g_k3_prof = nullptr;
-void k3_set_profile(long long* dev_buf) { g_k3_prof = dev_buf; }
-
-// MXP_K3 selects the small-n kernel for A/B measurements: "tf32" (this
-// single-chain 3xTF32 kernel), "bf16x3" (K3B); default: K3H (scaled fp16x2).
-static int k3_variant() {
-    static const int v = [] {
-        const char* e = std::getenv("MXP_K3");
-        if (e != nullptr && std::strcmp(e, "tf32") == 0) return 1;
-        if (e != nullptr && std::strcmp(e, "bf16x3") == 0) return 2;
-        return 0;
-    }();
-    return v;
+// Accuracy router.  The tensor core truncates its fp32 accumulator on every
+// MMA, a relative bias per multiply that a chain amplifies ~(k-1)-fold
+// (tools/bias_check.py: K3H b(n) ~ 2.5e-8 + 1.05e-9 n, K3B ~ 3.4e-8 + 3.6e-10 n).
+// When K3H's predicted (k-1) b(n) would use more than 60% of the
+// relative-Frobenius tolerance 16 m sqrt(n) 2^-24, the chain
+// runs on K3B instead.  Returns 0 (K3H) or 2 (K3B).
+int k3_route(int n, const PlanBits& plan) {
+    double k = 1.0;
+    for (int i = 0; i < plan.len; ++i) k = plan_is_mult(plan, i) ? k + 1.0 : 2.0 * k;
+    const double pred = (k - 1.0) * (2.5e-8 + 1.05e-9 * n);
+    const double tol = 16.0 * plan.len * std::sqrt(static_cast<double>(n)) * std::ldexp(1.0, -24);
+    return pred > 0.6 * tol ? 2 : 0;
 }
 
 cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
-                              const PlanBits& plan, int grid, cudaStream_t s) {
-    int variant = k3_variant();
-    if (variant == 0) {
-        // Accuracy guard.  The tensor core truncates its fp32 accumulator on
-        // every MMA, a relative bias per multiply that a chain amplifies
-        // ~(k-1)-fold (tools/bias_check.py: K3H b(n) ~ 2.5e-8 + 1.05e-9 n,
-        // K3B ~ 3.4e-8 + 3.6e-10 n).  When K3H's predicted (k-1) b(n) would
-        // use more than 60% of the relative-Frobenius tolerance
-        // 16 m sqrt(n) 2^-24, run the bf16x3 kernel instead.
-        double k = 1.0;
-        for (int i = 0; i < plan.len; ++i) k = plan_is_mult(plan, i) ? k + 1.0 : 2.0 * k;
-        const double pred = (k - 1.0) * (2.5e-8 + 1.05e-9 * n);
-        const double tol = 16.0 * plan.len * std::sqrt(static_cast<double>(n)) * std::ldexp(1.0, -24);
-        if (pred > 0.6 * tol) variant = 2;
-    }
-    if (variant == 0) return launch_k3h_batched(in, out, n, batch, plan, grid, s);
-    if (variant == 2) return launch_k3b_batched(in, out, n, batch, plan, grid, s);
-    if (grid > batch) grid = static_cast<int>(batch);
-    CUtensorMap map;
-    std::memset(&map, 0, sizeof map);
-    int use_tma = 0;
-    if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0)
-        use_tma = encode_batch_map(&map, in, n, batch) ? 1 : 0;
-    if (g_k3_prof != nullptr)
-        k3_batched_power<true><<<grid, kK3AllThreads, k3_smem_bytes(), s>>>(
-            map, use_tma, in, out, n, batch, plan, g_k3_prof);
-    else
-        k3_batched_power<false><<<grid, kK3AllThreads, k3_smem_bytes(), s>>>(
-            map, use_tma, in, out, n, batch, plan, nullptr);
-    return cudaGetLastError();
+                              const PlanBits& plan, int grid, unsigned long long* stamps,
+                              int* variant, cudaStream_t s) {
+    const int v = k3_route(n, plan);
+    if (variant) *variant = v;
+    if (v == 0) return launch_k3h_batched(in, out, n, batch, plan, grid, stamps, s);
+    return launch_k3b_batched(in, out, n, batch, plan, grid, s);
 }
 
 // ======================================================================
@@ -469,8 +146,7 @@ struct K1Cfg {
 // Split-K partial sums of one 128 x 128 tile held in the SMEM of the S CTAs
 // of a cluster (row r at r * 512 B, 16-byte unit u at (u ^ (r & 7)) << 4):
 // CTA `rank` reduces rows [rank R, (rank + 1) R), R = 128 / S, in split order
-// with round-to-nearest adds (splitk_reduce_kernel's order and arithmetic),
-// and hands each 4-column group to emit(row, unit, sum).  Up to 8 loads per
+// with round-to-nearest adds, and hands each 4-column group to emit(row, unit, sum).  Up to 8 loads per
 // group are in flight before the adds.
 template <uint32_t kUnits = 32, typename Emit>
 __device__ __forceinline__ void cluster_reduce_tile(uint32_t s0, uint32_t S_, uint32_t rank,
@@ -503,7 +179,7 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
                    const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
                    int n_pad, int m_pad, float* __restrict__ out_f32, int n_out, int m_out,
                    int ld_out, uint32_t* __restrict__ out_hi, uint32_t* __restrict__ out_lo,
-                   float* __restrict__ part, int dsmem_reduce) {
+                   int dsmem_reduce) {
     using Cfg = K1Cfg;
     constexpr int S = Cfg::kStages;
     constexpr int BN = Cfg::kBN;
@@ -642,14 +318,6 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
                 }
                 continue;
             }
-            if (part != nullptr) {  // split-K partial, reduced by splitk_reduce_kernel
-                float4* d = reinterpret_cast<float4*>(
-                    part + (static_cast<size_t>(blockIdx.y) * m_pad + row) * n_pad + col);
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    d[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
-                continue;
-            }
             if (out_hi != nullptr) {
                 uint4* dh = reinterpret_cast<uint4*>(out_hi + static_cast<size_t>(row) * n_pad + col);
                 uint4* dl = reinterpret_cast<uint4*>(out_lo + static_cast<size_t>(row) * n_pad + col);
@@ -683,9 +351,8 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
     if (dsmem_reduce) {
         // Split-K reduction over the cluster (the gridDim.y CTAs of this tile):
         // CTA r sums rows [r R, (r + 1) R) of the S partials, read from every
-        // CTA's SMEM in split order with round-to-nearest adds — the order
-        // and arithmetic of splitk_reduce_kernel, so results are bitwise the
-        // same — and writes the next step's planes / the fp32 result.
+        // CTA's SMEM in split order with round-to-nearest adds (deterministic),
+        // and writes the next step's planes / the fp32 result.
         cluster_sync_all();  // every partial is in SMEM (release / acquire)
         cluster_reduce_tile(smem_u32(smem), gridDim.y, cluster_ctarank(),
                             [&](uint32_t rr, uint32_t u, float4 a) {
@@ -968,22 +635,6 @@ bool encode_plane_map(CUtensorMap* map, const void* plane, int n_pad, int box_co
 
 // 3-D map over a batch of row-major n x n fp32 matrices: box {32, 128, 1},
 // SWIZZLE_128B, rows/columns beyond n zero-filled by TMA.
-bool encode_batch_map(CUtensorMap* map, const void* base, int n, int64_t batch) {
-    EncodeTiledFn fn = get_encode_fn();
-    if (fn == nullptr) return false;
-    cuuint64_t dims[3] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(n),
-                          static_cast<cuuint64_t>(batch)};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(n) * 4, static_cast<cuuint64_t>(n) * n * 4};
-    cuuint32_t box[3] = {32, 128, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides,
-                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-// 2-D map over `rows` rows of 128 fp32 (a batch of 128 x 128 matrices stacked
-// by rows): box {32, 32}, SWIZZLE_128B — the K3B warp-tile layout.
 bool encode_tile_map(CUtensorMap* map, const void* base, int64_t rows) {
     EncodeTiledFn fn = get_encode_fn();
     if (fn == nullptr) return false;
@@ -1007,15 +658,8 @@ int k1_block_n(int n_pad, int num_sms) {
 static cudaError_t prepare_k1c();  // (after the K1C kernel)
 
 cudaError_t prepare_tf32_kernels() {
-    cudaError_t e = cudaFuncSetAttribute(k3_batched_power<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(k3_smem_bytes()));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k3_batched_power<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(k3_smem_bytes()));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k1_gemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(K1Cfg::kSmem));
+    cudaError_t e = cudaFuncSetAttribute(k1_gemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(K1Cfg::kSmem));
     if (e == cudaSuccess) e = prepare_k1c();
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k1p_gemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1027,66 +671,7 @@ cudaError_t launch_k1_gemm(const GemmPlanes& m, int n_pad, int block_n, float* o
                            int n_out, int ld_out, uint32_t* out_hi, uint32_t* out_lo,
                            cudaStream_t s) {
     return launch_k1_gemm_rows(m, n_pad, n_pad, block_n, out_f32, n_out, n_out, ld_out, out_hi,
-                               out_lo, s, nullptr, 1);
-}
-
-// Deterministic split-K reduction: the S partial products are summed in a
-// fixed order with round-to-nearest fp32 adds, then split into the next
-// step's hi/lo planes (or written as fp32).
-__global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, int n_pad,
-                                     int m_pad, uint32_t* __restrict__ out_hi,
-                                     uint32_t* __restrict__ out_lo, float* __restrict__ out_f32,
-                                     int n_out, int m_out, int ld_out) {
-    const size_t quads = static_cast<size_t>(m_pad) * n_pad / 4;
-    const size_t plane = static_cast<size_t>(m_pad) * n_pad;
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < quads;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        float4 a = reinterpret_cast<const float4*>(part)[i];
-        for (int sp = 1; sp < splits; ++sp) {
-            const float4 b = reinterpret_cast<const float4*>(part + sp * plane)[i];
-            a.x = __fadd_rn(a.x, b.x);
-            a.y = __fadd_rn(a.y, b.y);
-            a.z = __fadd_rn(a.z, b.z);
-            a.w = __fadd_rn(a.w, b.w);
-        }
-        if (out_hi != nullptr) {
-            uint4 h, l;
-            split_tf32(a.x, h.x, l.x);
-            split_tf32(a.y, h.y, l.y);
-            split_tf32(a.z, h.z, l.z);
-            split_tf32(a.w, h.w, l.w);
-            reinterpret_cast<uint4*>(out_hi)[i] = h;
-            reinterpret_cast<uint4*>(out_lo)[i] = l;
-        }
-        if (out_f32 != nullptr) {
-            const size_t e = i * 4;
-            const int r = static_cast<int>(e / n_pad), c = static_cast<int>(e % n_pad);
-            if (r < m_out) {
-                const float v[4] = {a.x, a.y, a.z, a.w};
-                for (int k = 0; k < 4; ++k)
-                    if (c + k < n_out) out_f32[static_cast<size_t>(r) * ld_out + c + k] = v[k];
-            }
-        }
-    }
-}
-
-// MXP_SPLITK=global: the two-launch split-K (partials through HBM/L2 and
-// splitk_reduce_kernel) instead of the cluster/DSMEM reduction (A/B runs).
-bool k1_split_legacy() {
-    static const int v = [] {
-        const char* e = std::getenv("MXP_SPLITK");
-        return (e != nullptr && std::strcmp(e, "global") == 0) ? 1 : 0;
-    }();
-    return v != 0;
-}
-int k1_split_launches(int splits) { return (splits > 1 && k1_split_legacy()) ? 2 : 1; }
-// MXP_K1C_NARROW=0: K1C keeps K1's 128-column tiles (A/B runs).
-static bool k1c_narrow_enabled() {
-    static const int v = [] {
-        const char* e = std::getenv("MXP_K1C_NARROW");
-        return (e != nullptr && std::strcmp(e, "0") == 0) ? 0 : 1;
-    }();
-    return v != 0;
+                               out_lo, s, 1);
 }
 
 // Clusters of cs K1 CTAs that can be resident at once (one CTA per SM; a
@@ -1129,7 +714,7 @@ int k1_split_k(int n_pad, int m_pad, int num_sms) {
     for (;;) {
         const int nx = 2 * sk;
         if (nx > 8 || tiles * nx > num_sms || kb % nx != 0 || kb / nx < 2) break;
-        if (!k1_split_legacy() && tiles > k1_max_clusters(nx)) break;
+        if (tiles > k1_max_clusters(nx)) break;
         sk = nx;
     }
     return sk;
@@ -1425,14 +1010,14 @@ cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
                              uint32_t* const* planes, const PlanBits& plan, int n_pad, int splits,
                              float* out_f32, int n_out, unsigned int* bar_ctr, uint32_t* progress,
                              int fault_step, cudaStream_t s) {
-    if (splits < 1 || splits > 8 || n_pad % 128 != 0 || k1_split_legacy()) return cudaErrorNotSupported;
+    if (splits < 1 || splits > 8 || n_pad % 128 != 0) return cudaErrorNotSupported;
     const int tiles = (n_pad / 128) * (n_pad / 128);
     if (tiles > k1_max_clusters(splits)) return cudaErrorNotSupported;
     // 64-column tiles when twice the clusters still fit one wave
     int dev = 0, num_sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    const bool narrow = k1c_narrow_enabled() && 2 * tiles <= k1_max_clusters(splits) &&
+    const bool narrow = 2 * tiles <= k1_max_clusters(splits) &&
                         2 * tiles * splits <= num_sms;
     K1CMaps maps;
     K1CPlanes pl;
@@ -1523,8 +1108,8 @@ cudaError_t launch_peer_barrier(uint32_t* const* flags, int npeers, int rank, ui
 
 cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int block_n,
                                 float* out_f32, int n_out, int m_out, int ld_out, uint32_t* out_hi,
-                                uint32_t* out_lo, cudaStream_t s, float* part, int splits) {
-    if (block_n == 128 && splits > 1 && !k1_split_legacy()) {
+                                uint32_t* out_lo, cudaStream_t s, int splits) {
+    if (block_n == 128 && splits > 1) {
         // split-K in one launch: the splits of a tile form a cluster and
         // reduce through distributed shared memory
         cudaLaunchConfig_t cfg{};
@@ -1540,22 +1125,7 @@ cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int b
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         return cudaLaunchKernelEx(&cfg, k1_gemm_3xtf32, m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad,
-                                  out_f32, n_out, m_out, ld_out, out_hi, out_lo,
-                                  static_cast<float*>(nullptr), 1);
-    }
-    if (block_n == 128 && splits > 1 && part != nullptr) {
-        dim3 grid((n_pad / K1Cfg::kBN) * (m_pad / 128), splits);
-        k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(
-            m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, nullptr, n_out, m_out, ld_out, nullptr,
-            nullptr, part, 0);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-        const size_t quads = static_cast<size_t>(m_pad) * n_pad / 4;
-        int blocks = static_cast<int>((quads + 255) / 256);
-        if (blocks > 148 * 8) blocks = 148 * 8;
-        splitk_reduce_kernel<<<blocks, 256, 0, s>>>(part, splits, n_pad, m_pad, out_hi, out_lo,
-                                                    out_f32, n_out, m_out, ld_out);
-        return cudaGetLastError();
+                                  out_f32, n_out, m_out, ld_out, out_hi, out_lo, 1);
     }
     if (block_n == 256) {  // CTA-pair kernel: n_pad, m_pad multiples of 256
         dim3 grid(2 * (n_pad / 256) * (m_pad / 256));
@@ -1567,7 +1137,7 @@ cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int b
     dim3 grid((n_pad / K1Cfg::kBN) * (m_pad / 128), 1);
     k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(
         m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo,
-        nullptr, 0);
+        0);
     return cudaGetLastError();
 }
 

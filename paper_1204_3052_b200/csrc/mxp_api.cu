@@ -6,12 +6,16 @@
 // (expo.py:60-75) is baked into one captured CUDA graph of m GEMM launches
 // over ping-pong buffers in HBM; the graph is cached per (mode, n, k, in, out)
 // and replayed.
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -92,6 +96,93 @@ struct GraphKey {
     }
 };
 
+// A small pool of host threads for copies between pageable caller memory
+// and pinned staging buffers (mxp_power_batched with ordinary numpy arrays:
+// the DMA engines only stream from pinned pages, and the driver's own
+// pageable path is single-threaded).  run(f) calls f(i, n) on every worker
+// i in [0, n) and returns when all have finished.
+class HostPool {
+  public:
+    explicit HostPool(int n) : n_(n) {
+        for (int i = 0; i < n_; ++i) threads_.emplace_back([this, i] { loop(i); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : threads_) t.join();
+    }
+    int size() const { return n_; }
+    void run(const std::function<void(int, int)>& f) {
+        std::unique_lock<std::mutex> g(m_);
+        job_ = &f;
+        pending_ = n_;
+        ++gen_;
+        cv_.notify_all();
+        done_cv_.wait(g, [this] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+  private:
+    void loop(int i) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(int, int)>* job;
+            {
+                std::unique_lock<std::mutex> g(m_);
+                cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                job = job_;
+            }
+            (*job)(i, n_);
+            {
+                std::lock_guard<std::mutex> g(m_);
+                if (--pending_ == 0) done_cv_.notify_one();
+            }
+        }
+    }
+    int n_;
+    std::vector<std::thread> threads_;
+    std::mutex m_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int, int)>* job_ = nullptr;
+    int pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+// Copy up to two independent ranges with every pool thread (each thread takes
+// its slice of both, 4 KB-aligned).
+struct CopyJob {
+    void* dst;
+    const void* src;
+    size_t bytes;
+};
+void pool_copy(HostPool& pool, const CopyJob* jobs, int njobs) {
+    pool.run([&](int i, int n) {
+        for (int j = 0; j < njobs; ++j) {
+            const size_t per = ((jobs[j].bytes + n - 1) / n + 4095) & ~size_t(4095);
+            const size_t lo = per * i;
+            if (lo >= jobs[j].bytes) continue;
+            const size_t len = (lo + per <= jobs[j].bytes) ? per : jobs[j].bytes - lo;
+            std::memcpy(static_cast<char*>(jobs[j].dst) + lo,
+                        static_cast<const char*>(jobs[j].src) + lo, len);
+        }
+    });
+}
+
+bool is_pageable(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
 }  // namespace
 
 struct mxp_handle_s {
@@ -104,10 +195,8 @@ struct mxp_handle_s {
     // fp32 single-matrix workspace: 6 tf32 planes (base, ping, pong) x (hi, lo)
     int64_t ws32_pad = 0;  // padded order the planes are currently laid out for
     int64_t ws32_cap = 0;  // padded order they are allocated for (>= ws32_pad)
-    size_t part_bytes = 0;
     uint32_t* planes[6] = {};
-    float* part = nullptr;  // split-K workspace (splits x n_pad^2 fp32) for small n
-    int splits = 1;
+    int splits = 1;  // split-K factor of the 1-CTA K1 tiles at ws32_pad
     unsigned int* bar_ctr = nullptr;  // grid-barrier counter of the one-launch chain (K1C)
     CUtensorMap map_a[6], map_b[6];
     // right-hand side prepared by mxp_gemm_prepare_rhs (planes[2..3] / f64buf[1]);
@@ -126,11 +215,21 @@ struct mxp_handle_s {
     uint32_t* progress_host = nullptr;
     uint32_t* progress_dev = nullptr;
     int fault_step = -1;  // test hook (mxp_debug_inject_fault): trap at this step
+    // in-kernel clock of the last batched K3H launch: {clock64, globaltimer}
+    // at the start and the end of CTA 0 (mxp_last_kernel_clock)
+    unsigned long long* stamps = nullptr;
+    bool stamps_valid = false;
     // host-API staging device buffers
     size_t io_bytes = 0;
     void* d_in = nullptr;
     void* d_in2 = nullptr;
     void* d_out = nullptr;
+    // pinned staging for pageable host buffers (mxp_power_batched): two in and
+    // two out slots of stage_bytes each, and the copy threads
+    size_t stage_bytes = 0;
+    char* stage_in = nullptr;
+    char* stage_out = nullptr;
+    HostPool* pool = nullptr;
 
     // captured chains, keyed by (mode, n, k, in, out); bounded LRU (callers that
     // pass fresh buffers every call would otherwise grow it without limit)
@@ -211,15 +310,6 @@ int ensure_ws32(mxp_handle h, int64_t n_pad) {
         h->splits = (k1_block_n((int)n_pad, h->num_sms) == 128)
                         ? k1_split_k((int)n_pad, (int)n_pad, h->num_sms)
                         : 1;
-        const size_t need = h->splits > 1 ? static_cast<size_t>(n_pad) * n_pad * 4 * h->splits : 0;
-        if (need > h->part_bytes) {
-            h->drop_graphs();
-            if (h->part) cudaFree(h->part);
-            h->part = nullptr;
-            h->part_bytes = 0;
-            MXP_CUDA(cudaMalloc(&h->part, need));
-            h->part_bytes = need;
-        }
         h->ws32_pad = n_pad;
     }
     return MXP_OK;
@@ -269,15 +359,6 @@ int ensure_io(mxp_handle h, size_t bytes) {
 
 // ---- enqueue helpers (no validation; stream = h->stream) -----------------
 
-// MXP_K1C=0: run the K1 chain as one launch per step (A/B runs).
-bool k1c_enabled() {
-    static const bool on = [] {
-        const char* v = std::getenv("MXP_K1C");
-        return !(v != nullptr && std::strcmp(v, "0") == 0);
-    }();
-    return on;
-}
-
 // 3xTF32 chain for n > kSmallMax through K1, planes padded to 128.
 int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float* dA,
                       float* dOut, int64_t* launches, int64_t* failed) {
@@ -291,7 +372,7 @@ int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float
     if (e != cudaSuccess) return cuda_fail(e, "split");
     ++*launches;
     const int bn = k1_block_n(np, h->num_sms);
-    if (bn == 128 && k1c_enabled()) {
+    if (bn == 128) {
         // the whole chain in one launch when every split-K cluster fits at once
         e = launch_k1c_chain(h->map_a, h->map_b, h->planes, plan, np, h->splits, dOut, (int)n,
                              h->bar_ctr, h->progress_dev, h->fault_step, h->stream);
@@ -321,13 +402,12 @@ int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float
         m.b_lo = h->map_b[2 * rhs + 1];
         e = launch_k1_gemm_rows(m, np, np, bn, last ? dOut : nullptr, (int)n, (int)n, (int)n,
                                 last ? nullptr : h->planes[2 * dst],
-                                last ? nullptr : h->planes[2 * dst + 1], h->stream, h->part,
-                                h->splits);
+                                last ? nullptr : h->planes[2 * dst + 1], h->stream, h->splits);
         if (e != cudaSuccess) {
             *failed = s;
             return cuda_fail(e, "k1_gemm_3xtf32");
         }
-        *launches += (bn == 128) ? k1_split_launches(h->splits) : 1;
+        ++*launches;
         acc = dst;
     }
     return MXP_OK;
@@ -371,7 +451,7 @@ int enqueue_power(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA, 
         if (n <= kSmallMax) {
             cudaError_t e = launch_k3_batched(static_cast<const float*>(dA),
                                               static_cast<float*>(dOut), (int)n, 1, plan, 1,
-                                              h->stream);
+                                              nullptr, nullptr, h->stream);
             if (e != cudaSuccess) {
                 *failed = 0;
                 return cuda_fail(e, "k3_batched_power");
@@ -545,6 +625,7 @@ int mxp_create(int device, mxp_handle* out) {
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
     if (e == cudaSuccess) e = cudaMalloc(&h->bar_ctr, 256);
+    if (e == cudaSuccess) e = cudaMalloc(&h->stamps, 64);
     if (e == cudaSuccess)
         e = cudaHostAlloc(reinterpret_cast<void**>(&h->progress_host), 64, cudaHostAllocMapped);
     if (e == cudaSuccess)
@@ -564,8 +645,8 @@ int mxp_destroy(mxp_handle h) {
     h->drop_graphs();
     for (auto p : h->planes)
         if (p) cudaFree(p);
-    if (h->part) cudaFree(h->part);
     if (h->bar_ctr) cudaFree(h->bar_ctr);
+    if (h->stamps) cudaFree(h->stamps);
     if (h->progress_host) cudaFreeHost(h->progress_host);
     for (auto p : h->f64buf)
         if (p) cudaFree(p);
@@ -574,6 +655,9 @@ int mxp_destroy(mxp_handle h) {
     if (h->d_in) cudaFree(h->d_in);
     if (h->d_in2) cudaFree(h->d_in2);
     if (h->d_out) cudaFree(h->d_out);
+    if (h->stage_in) cudaFreeHost(h->stage_in);
+    if (h->stage_out) cudaFreeHost(h->stage_out);
+    delete h->pool;
     cudaEventDestroy(h->ev0);
     cudaEventDestroy(h->ev1);
     cudaStreamDestroy(h->stream);
@@ -670,8 +754,7 @@ int mxp_gemm(mxp_handle h, int mode, int64_t n, const void* dA, const void* dB, 
         if (e != cudaSuccess) return cuda_fail(e, "split");
         GemmPlanes m{h->map_a[0], h->map_a[1], h->map_b[2], h->map_b[3]};
         e = launch_k1_gemm_rows(m, np, np, k1_block_n(np, h->num_sms), static_cast<float*>(dC),
-                                (int)n, (int)n, (int)n, nullptr, nullptr, h->stream, h->part,
-                                h->splits);
+                                (int)n, (int)n, (int)n, nullptr, nullptr, h->stream, h->splits);
         if (e != cudaSuccess) return cuda_fail(e, "k1_gemm_3xtf32");
         return MXP_OK;
     }
@@ -747,7 +830,7 @@ int mxp_gemm_rows_prepared(mxp_handle h, int mode, int64_t n, int64_t rows, cons
         GemmPlanes m{a_hi, a_lo, b_hi, b_lo};
         // same k-split as the full multiply / chain: bitwise-identical rows
         e = launch_k1_gemm_rows(m, np, (int)r_pad, bn, static_cast<float*>(dC), (int)n, (int)rows,
-                                (int)n, nullptr, nullptr, h->stream, h->part, h->splits);
+                                (int)n, nullptr, nullptr, h->stream, h->splits);
         if (e != cudaSuccess) return cuda_fail(e, "k1_gemm_3xtf32");
         return MXP_OK;
     }
@@ -1012,12 +1095,15 @@ int mxp_power_batched_device(mxp_handle h, int mode, int64_t n, int64_t batch, i
         return rc;
     }
     if (mode == MXP_F32 && n <= kSmallMax) {
+        int variant = -1;
         cudaError_t e = launch_k3_batched(static_cast<const float*>(dA), static_cast<float*>(dOut),
-                                          (int)n, batch, make_plan(k), h->num_sms, h->stream);
+                                          (int)n, batch, make_plan(k), h->num_sms, h->stamps,
+                                          &variant, h->stream);
         if (e != cudaSuccess) {
             if (st) st->failed_step = 0;
             return cuda_fail(e, "k3_batched_power");
         }
+        h->stamps_valid = (variant == 0);
         if (st) st->launches = 1;
         return MXP_OK;
     }
@@ -1055,51 +1141,117 @@ int mxp_power_batched(mxp_handle h, int mode, int64_t n, int64_t batch, int64_t 
     const size_t chunk_bytes = static_cast<size_t>(chunk) * mat;
     rc = ensure_io(h, 2 * chunk_bytes);  // d_in/d_out hold two chunk slots each
     if (rc) return rc;
+    // Pageable caller memory goes through pinned staging slots, filled and
+    // drained by the host thread pool while the GPU works on the neighbouring
+    // chunk (chunk i is filled while chunk i-1 computes; it is drained two
+    // chunks later, when its slot comes round again).
+    const bool stage_in = is_pageable(hA), stage_out = is_pageable(hOut);
+    if (stage_in || stage_out) {
+        if (h->stage_bytes < chunk_bytes) {
+            MXP_CUDA(cudaStreamSynchronize(h->copy_in));
+            MXP_CUDA(cudaStreamSynchronize(h->copy_out));
+            if (h->stage_in) cudaFreeHost(h->stage_in);
+            if (h->stage_out) cudaFreeHost(h->stage_out);
+            h->stage_in = h->stage_out = nullptr;
+            h->stage_bytes = 0;
+            MXP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h->stage_in), 2 * chunk_bytes,
+                                   cudaHostAllocPortable));
+            MXP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h->stage_out), 2 * chunk_bytes,
+                                   cudaHostAllocPortable));
+            h->stage_bytes = chunk_bytes;
+        }
+        if (h->pool == nullptr) {
+            unsigned hw = std::thread::hardware_concurrency();
+            h->pool = new HostPool(static_cast<int>(hw < 2 ? 2 : (hw > 16 ? 16 : hw)));
+        }
+    }
+    const size_t sb = h->stage_bytes;
     cudaEvent_t in_ready[2], comp_done[2], out_done[2];
     for (int i = 0; i < 2; ++i) {
         MXP_CUDA(cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming));
         MXP_CUDA(cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming));
         MXP_CUDA(cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming));
     }
+    auto destroy_events = [&] {
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(in_ready[i]);
+            cudaEventDestroy(comp_done[i]);
+            cudaEventDestroy(out_done[i]);
+        }
+    };
+    const int64_t nchunks = (batch + chunk - 1) / chunk;
+    auto chunk_len = [&](int64_t c) -> size_t {
+        const int64_t b0 = c * chunk;
+        return static_cast<size_t>((b0 + chunk <= batch) ? chunk : batch - b0) * mat;
+    };
     MXP_CUDA(cudaEventRecord(h->ev0, h->stream));
     int64_t launches = 0;
-    int slot = 0;
-    bool used[2] = {false, false};
-    for (int64_t b0 = 0; b0 < batch; b0 += chunk, slot ^= 1) {
-        const int64_t nb = (b0 + chunk <= batch) ? chunk : batch - b0;
-        const size_t nbytes = static_cast<size_t>(nb) * mat;
+    cudaError_t err = cudaSuccess;
+    for (int64_t c = 0; c < nchunks && err == cudaSuccess; ++c) {
+        const int slot = static_cast<int>(c & 1);
+        const int64_t b0 = c * chunk;
+        const int64_t nb = static_cast<int64_t>(chunk_len(c) / mat);
+        const size_t nbytes = chunk_len(c);
         char* din = static_cast<char*>(h->d_in) + slot * chunk_bytes;
         char* dout = static_cast<char*>(h->d_out) + slot * chunk_bytes;
-        if (used[slot]) MXP_CUDA(cudaStreamWaitEvent(h->copy_in, comp_done[slot], 0));
-        MXP_CUDA(cudaMemcpyAsync(din, static_cast<const char*>(hA) + b0 * mat, nbytes,
-                                 cudaMemcpyHostToDevice, h->copy_in));
+        const char* src = static_cast<const char*>(hA) + b0 * mat;
+        if (stage_in || stage_out) {
+            // the slot's previous chunk (c - 2) has left the staging buffers
+            CopyJob jobs[2];
+            int nj = 0;
+            if (c >= 2) {
+                if ((err = cudaEventSynchronize(in_ready[slot])) != cudaSuccess) break;
+                if ((err = cudaEventSynchronize(out_done[slot])) != cudaSuccess) break;
+                if (stage_out)
+                    jobs[nj++] = {static_cast<char*>(hOut) + (c - 2) * chunk * mat,
+                                  h->stage_out + slot * sb, chunk_len(c - 2)};
+            }
+            if (stage_in) {
+                jobs[nj++] = {h->stage_in + slot * sb, src, nbytes};
+                src = h->stage_in + slot * sb;
+            }
+            if (nj) pool_copy(*h->pool, jobs, nj);
+        }
+        if (c >= 2) MXP_CUDA(cudaStreamWaitEvent(h->copy_in, comp_done[slot], 0));
+        MXP_CUDA(cudaMemcpyAsync(din, src, nbytes, cudaMemcpyHostToDevice, h->copy_in));
         MXP_CUDA(cudaEventRecord(in_ready[slot], h->copy_in));
         MXP_CUDA(cudaStreamWaitEvent(h->stream, in_ready[slot], 0));
-        if (used[slot]) MXP_CUDA(cudaStreamWaitEvent(h->stream, out_done[slot], 0));
+        if (c >= 2) MXP_CUDA(cudaStreamWaitEvent(h->stream, out_done[slot], 0));
         mxp_stats inner;
         rc = mxp_power_batched_device(h, mode, n, nb, k, din, dout, &inner);
         if (rc) {
+            cudaStreamSynchronize(h->copy_in);
+            cudaStreamSynchronize(h->copy_out);
+            destroy_events();
             if (st) st->failed_step = inner.failed_step;
             return rc;
         }
         launches += inner.launches;
         MXP_CUDA(cudaEventRecord(comp_done[slot], h->stream));
         MXP_CUDA(cudaStreamWaitEvent(h->copy_out, comp_done[slot], 0));
-        MXP_CUDA(cudaMemcpyAsync(static_cast<char*>(hOut) + b0 * mat, dout, nbytes,
-                                 cudaMemcpyDeviceToHost, h->copy_out));
+        void* dst = stage_out ? static_cast<void*>(h->stage_out + slot * sb)
+                              : static_cast<void*>(static_cast<char*>(hOut) + b0 * mat);
+        MXP_CUDA(cudaMemcpyAsync(dst, dout, nbytes, cudaMemcpyDeviceToHost, h->copy_out));
         MXP_CUDA(cudaEventRecord(out_done[slot], h->copy_out));
-        used[slot] = true;
     }
-    MXP_CUDA(cudaStreamWaitEvent(h->stream, out_done[0], 0));
-    if (used[1]) MXP_CUDA(cudaStreamWaitEvent(h->stream, out_done[1], 0));
-    MXP_CUDA(cudaEventRecord(h->ev1, h->stream));
-    cudaError_t e = cudaStreamSynchronize(h->stream);
-    for (int i = 0; i < 2; ++i) {
-        cudaEventDestroy(in_ready[i]);
-        cudaEventDestroy(comp_done[i]);
-        cudaEventDestroy(out_done[i]);
+    // drain the last (up to two) staged results
+    if (stage_out && err == cudaSuccess) {
+        for (int64_t c = (nchunks >= 2 ? nchunks - 2 : 0); c < nchunks && err == cudaSuccess; ++c) {
+            const int slot = static_cast<int>(c & 1);
+            if ((err = cudaEventSynchronize(out_done[slot])) != cudaSuccess) break;
+            CopyJob job{static_cast<char*>(hOut) + c * chunk * mat, h->stage_out + slot * sb,
+                        chunk_len(c)};
+            pool_copy(*h->pool, &job, 1);
+        }
     }
-    if (e != cudaSuccess) return cuda_fail(e, "batched power");
+    if (err == cudaSuccess) {
+        MXP_CUDA(cudaStreamWaitEvent(h->stream, out_done[0], 0));
+        if (nchunks > 1) MXP_CUDA(cudaStreamWaitEvent(h->stream, out_done[1], 0));
+        MXP_CUDA(cudaEventRecord(h->ev1, h->stream));
+        err = cudaStreamSynchronize(h->stream);
+    }
+    destroy_events();
+    if (err != cudaSuccess) return cuda_fail(err, "batched power");
     if (st) {
         fill_plan_stats(st, k, batch);
         float ms = 0.f;
@@ -1126,6 +1278,22 @@ int mxp_random_device(mxp_handle h, int mode, int64_t n, int64_t batch, uint64_t
     if (batch == 0) return MXP_OK;
     cudaError_t e = launch_random(mode, n, batch, seed0, lo, hi, scale, dOut, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "random_kernel");
+    return MXP_OK;
+}
+
+int mxp_last_kernel_clock(mxp_handle h, double* sm_mhz, double* kernel_ms) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (!h->stamps_valid)
+        return fail(MXP_E_UNSUPPORTED, "no batched K3H launch on this handle yet");
+    unsigned long long t[4];
+    MXP_CUDA(cudaStreamSynchronize(h->stream));
+    MXP_CUDA(cudaMemcpy(t, h->stamps, sizeof t, cudaMemcpyDeviceToHost));
+    const double cycles = static_cast<double>(t[2] - t[0]);
+    const double ns = static_cast<double>(t[3] - t[1]);
+    if (ns <= 0) return fail(MXP_E_CUDA, "globaltimer did not advance");
+    if (sm_mhz) *sm_mhz = cycles / ns * 1e3;
+    if (kernel_ms) *kernel_ms = ns * 1e-6;
     return MXP_OK;
 }
 

@@ -26,25 +26,27 @@ __host__ __device__ inline bool plan_is_mult(const PlanBits& p, int s) {
 // per device, before any launch or graph capture).
 cudaError_t prepare_kernels();
 
-// ---- 3xTF32 kernels (kernels_tf32.cu) ------------------------------------
-// K3: persistent batched chain for n <= 128, each CTA owns one matrix at a
-// time with the running power resident in shared memory.
+// ---- n <= 128: persistent batched chains --------------------------------
+// launch_k3_batched (kernels_tf32.cu) routes a chain to K3H or K3B by its
+// predicted accumulated truncation bias (k3_route: 0 = K3H, 2 = K3B).
+// stamps (device, may be null): K3H's CTA 0 writes {clock64, globaltimer} at
+// its start and end into stamps[0..3] (the in-kernel SM clock of the launch).
 constexpr int kSmallMax = 128;
-size_t k3_smem_bytes();
-void k3_set_profile(long long* dev_buf);  // debug: per-phase cycle totals of CTA 0
+int k3_route(int n, const PlanBits& plan);
 cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
-                              const PlanBits& plan, int grid, cudaStream_t s);
-// K3B (kernels_k3b.cu): the same contract, two chains per SM, bf16x3 split.
-// launch_k3_batched routes here unless MXP_K3=tf32 is set in the environment.
+                              const PlanBits& plan, int grid, unsigned long long* stamps,
+                              int* variant, cudaStream_t s);
+// K3B (kernels_k3b.cu): two chains per SM, bf16x3 split.
 size_t k3b_smem_bytes();
 cudaError_t prepare_k3b_kernel();
 cudaError_t launch_k3b_batched(const float* in, float* out, int n, int64_t batch,
                                const PlanBits& plan, int grid, cudaStream_t s);
-// K3H (kernels_k3h.cu): the same contract, two chains per SM, scaled fp16x2 split.
+// K3H (kernels_k3h.cu): two chains per SM, scaled fp16x2 split.
 size_t k3h_smem_bytes();
 cudaError_t prepare_k3h_kernel();
 cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch,
-                               const PlanBits& plan, int grid, cudaStream_t s);
+                               const PlanBits& plan, int grid, unsigned long long* stamps,
+                               cudaStream_t s);
 
 // fp32 (n x n, leading dim ld) -> tf32 hi/lo planes (n_pad x n_pad, zero pad).
 cudaError_t launch_split(const float* in, int n, int ld, uint32_t* hi, uint32_t* lo, int n_pad,
@@ -60,7 +62,6 @@ struct GemmPlanes {
     CUtensorMap a_hi, a_lo;  // box {32, 128}, SWIZZLE_128B (K-major left operand)
     CUtensorMap b_hi, b_lo;  // box {32, 32}, SWIZZLE_128B_ATOM_32B (MN-major right operand)
 };
-bool encode_batch_map(CUtensorMap* map, const void* base, int n, int64_t batch);
 bool encode_tile_map(CUtensorMap* map, const void* base, int64_t rows);
 bool encode_plane_map(CUtensorMap* map, const void* plane, int n_pad, int box_cols, int box_rows,
                       bool right_operand, int rows = 0);
@@ -87,15 +88,13 @@ cudaError_t launch_k1_gemm(const GemmPlanes& maps, int n_pad, int block_n, float
                            int n_out, int ld_out, uint32_t* out_hi, uint32_t* out_lo,
                            cudaStream_t s);
 // Row block: C[m_pad x n_pad] = A[m_pad x n_pad] * B[n_pad x n_pad].
-// part != nullptr and splits > 1: split-K over `splits` k-ranges into the fp32
-// workspace `part` (splits x m_pad x n_pad), then a deterministic reduction.
+// splits > 1 (1-CTA tiles): split-K over `splits` k-ranges, the splits of a
+// tile launched as one cluster and reduced deterministically through DSMEM.
 cudaError_t launch_k1_gemm_rows(const GemmPlanes& maps, int n_pad, int m_pad, int block_n,
                                 float* out_f32, int n_out, int m_out, int ld_out, uint32_t* out_hi,
-                                uint32_t* out_lo, cudaStream_t s, float* part = nullptr,
-                                int splits = 1);
+                                uint32_t* out_lo, cudaStream_t s, int splits = 1);
 int k1_split_k(int n_pad, int m_pad, int num_sms);
-int k1_split_launches(int splits);
-// K1C: the whole 3xTF32 chain in one cooperative launch (kernels_tf32.cu);
+// K1C: the whole 3xTF32 chain in one launch (kernels_tf32.cu);
 // cudaErrorNotSupported / a launch error => run the per-step chain
 // progress (host-mapped, may be null): every CTA stores step+1 at the start of
 // each plan step; fault_step >= 0 makes CTA (0,0) trap there (test hook).

@@ -278,6 +278,14 @@ class Engine:
                                              ctypes.c_uint64(seed0 & (2**64 - 1)), lo, hi, scale,
                                              ctypes.c_void_p(d_out)), "mxp_random_device")
 
+    def last_kernel_clock(self):
+        """(sm_mhz, kernel_ms) of the last batched K3H launch, measured in the
+        kernel (clock64 / globaltimer of CTA 0)."""
+        mhz, ms = ctypes.c_double(), ctypes.c_double()
+        _lib.check(self._L.mxp_last_kernel_clock(self._h, ctypes.byref(mhz), ctypes.byref(ms)),
+                   "mxp_last_kernel_clock")
+        return mhz.value, ms.value
+
     def splitmix64_device(self, d_out: int, seed: int, count: int) -> None:
         _lib.check(self._L.mxp_splitmix64_device(self._h, ctypes.c_uint64(seed & (2**64 - 1)),
                                                  int(count), ctypes.c_void_p(d_out)),

@@ -55,3 +55,7 @@ class ExtensionNotBuiltError(MatexpoError, RuntimeError):
 
 class ConfigError(MatexpoError, ValueError):
     """Benchmark configuration failed validation."""
+
+
+class TableError(MatexpoError, ValueError):
+    """The comparison table lacks a cell (errors.py:56 of the reference)."""

@@ -20,7 +20,7 @@ from typing import Optional, Sequence, TextIO, Union
 import numpy as np
 
 from .dtypes import DType
-from .errors import ConfigError
+from .errors import ConfigError, TableError
 from .expo import (
     Backend,
     CountingBackend,
@@ -38,6 +38,14 @@ BACKEND_NAMES = ("b200",)
 CSV_HEADER = ("size,power,strategy,backend,seconds,multiply_count,transfer_count,max_rel_err,"
               "nonfinite")
 CSV_EXTRA = "gpus,dtype_mode,device_ms,tflops"
+# the paper's comparison table (bench.py:44-50 of the reference)
+TABLE_ROW_LABELS = (
+    "Naïve GPU (In Sec)",
+    "Sequential CPU (In Sec)",
+    "Naïve Speed UP",
+    "Our Approach (In Sec)",
+    "Our Approach vs Naïve GPU",
+)
 
 
 def make_backend(name: str, tile=None) -> Backend:
@@ -205,3 +213,61 @@ def _read_csv(fh: TextIO) -> list:
                        tflops=None if p[12] == "" else float(p[12]))
         out.append(BenchmarkRecord(**rec))
     return out
+
+
+# --------------------------------------------------------------------------- table
+def emit_table(records) -> str:
+    """The paper's five-row comparison table for one matrix size, in the
+    reference's text format (bench.py:330-395): the sequential CPU row is
+    REPEATED on the ``naive`` backend, "Naïve GPU" is REPEATED on the
+    accelerated backend (here b200: k-1 device GEMMs) and "Our Approach" is
+    SQUARED on it (the CUDA-graph chain); the two speed-up rows are time ratios
+    with two decimals.  The naive rows are the reference's own measurements:
+    read them from a CSV written by the reference CLI (``matexpo bench
+    --backends naive --strategies repeated --csv ref.csv``) and pass the
+    records of both files; a missing cell raises TableError."""
+    from .expo import Strategy
+
+    if not records:
+        raise TableError("no records to tabulate")
+    sizes = sorted({r.size for r in records})
+    if len(sizes) != 1:
+        raise TableError(f"records span sizes {sizes}; tabulate one size at a time")
+    accel = sorted({r.backend for r in records if r.backend != "naive"})
+    if not accel:
+        raise TableError("need a non-naive backend for the accelerated rows")
+    if len(accel) > 1:
+        raise TableError(f"ambiguous accelerated backend: {accel}; filter records first")
+    roles = {"seq": (Strategy.REPEATED, "naive"), "gpu": (Strategy.REPEATED, accel[0]),
+             "ours": (Strategy.SQUARED, accel[0])}
+    powers = sorted({r.power for r in records})
+    cells = {role: {} for role in roles}
+    for r in records:
+        for role, (strategy, backend) in roles.items():
+            if r.strategy is strategy and r.backend == backend:
+                cells[role][r.power] = r.seconds
+    missing = [f"{strategy.value}/{backend} @ power={p}" for role, (strategy, backend)
+               in roles.items() for p in powers if p not in cells[role]]
+    if missing:
+        raise TableError("missing cells: " + ", ".join(missing))
+
+    def secs(v):
+        return f"{v:.6g}"
+
+    def ratio(v):
+        text = f"{v:.2f}"
+        return text.rstrip("0").rstrip(".") if "." in text else text
+
+    seq, gpu, ours = cells["seq"], cells["gpu"], cells["ours"]
+    rows = [(TABLE_ROW_LABELS[0], [secs(gpu[p]) for p in powers]),
+            (TABLE_ROW_LABELS[1], [secs(seq[p]) for p in powers]),
+            (TABLE_ROW_LABELS[2], [ratio(seq[p] / gpu[p]) for p in powers]),
+            (TABLE_ROW_LABELS[3], [secs(ours[p]) for p in powers]),
+            (TABLE_ROW_LABELS[4], [ratio(gpu[p] / ours[p]) for p in powers])]
+    lw = max(len(label) for label, _ in rows)
+    widths = [max(len(str(p)), *(len(vals[i]) for _, vals in rows)) for i, p in enumerate(powers)]
+    out = [f"Matrix size {sizes[0]} x {sizes[0]}",
+           " " * lw + "  " + "  ".join(str(p).rjust(w) for p, w in zip(powers, widths))]
+    out += [label.ljust(lw) + "  " + "  ".join(v.rjust(w) for v, w in zip(vals, widths))
+            for label, vals in rows]
+    return "\n".join(out) + "\n"

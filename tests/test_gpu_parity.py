@@ -492,57 +492,26 @@ def test_batched_mixed_magnitudes_and_schedule_edges():
         assert np.array_equal(mx.exponentiate_batched(stack, k), out)
 
 
-# ------------------------------------------------- one-launch chain (K1C) A/B
-_AB_SCRIPT = r"""
-import hashlib, math, sys
-import numpy as np
-sys.path.insert(0, ".")
-import oracle, paper_1204_3052_b200 as mx
-eng = mx.Engine(0)
-out = []
-for n, k in ((130, 7), (256, 64), (384, 33), (512, 1000), (896, 9)):
-    r = eng.power(oracle.scaled_input(n, np.float32, 42), k)
-    out.append(hashlib.sha256(np.ascontiguousarray(r).tobytes()).hexdigest())
-    out.append(str(eng.last_stats.launches))
-r = eng.multiply(oracle.scaled_input(512, np.float32, 1), oracle.scaled_input(512, np.float32, 2))
-out.append(hashlib.sha256(np.ascontiguousarray(r).tobytes()).hexdigest())
-print(" ".join(out))
-"""
+# ------------------------------------------------- one-launch chain (K1C)
+@pytest.mark.parametrize("n,k", [(130, 7), (256, 64), (384, 33), (512, 1000), (896, 9), (1300, 13)])
+def test_one_launch_chain_bitwise_equals_single_multiplies(eng, n, k):
+    """K1C runs the whole chain in one launch; it must be bitwise the same as
+    the plan executed one public multiply at a time (mxp_gemm: split, one K1
+    GEMM with the same split-K and reduction order, fp32 out), following
+    expo.py:131-138 with the accumulator on the left."""
+    import torch
 
-
-def _run_ab(env_extra):
-    import os
-    import subprocess
-    import sys
-
-    env = dict(os.environ)
-    env.update(env_extra)
-    res = subprocess.run([sys.executable, "-c", _AB_SCRIPT], env=env, capture_output=True, text=True,
-                         timeout=600, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    assert res.returncode == 0, res.stderr[-2000:]
-    return res.stdout.split()
-
-
-def test_one_launch_chain_bitwise_equals_per_step_chain():
-    """K1C (whole chain in one cooperative launch) against the same chain run
-    one K1 launch per step (MXP_K1C=0): bitwise equal, fewer launches."""
-    k1c = _run_ab({})
-    per_step = _run_ab({"MXP_K1C": "0"})
-    for i in range(0, 10, 2):
-        assert k1c[i] == per_step[i], f"chain {i // 2}"
-        assert int(k1c[i + 1]) == 2 and int(per_step[i + 1]) > 2
-    assert k1c[10] == per_step[10]
-
-
-def test_cluster_split_k_bitwise_equals_two_launch_split_k():
-    """K1 split-K with the cluster/DSMEM reduction against the two-launch form
-    (partials through a workspace + splitk_reduce_kernel) at the same split:
-    bitwise equal for chains and single multiplies (n where both pick the
-    same split: the cluster cap does not bind below 512)."""
-    a = _run_ab({"MXP_K1C": "0"})
-    b = _run_ab({"MXP_K1C": "0", "MXP_SPLITK": "global"})
-    for i in (0, 2, 4, 8):  # n = 130, 256, 384, 896
-        assert a[i] == b[i], f"chain {i // 2}"
+    a = torch.from_numpy(oracle.scaled_input(n, np.float32, 42)).cuda()
+    chain = torch.empty_like(a)
+    eng.power_device(a.data_ptr(), chain.data_ptr(), n, k)
+    assert eng.last_stats.launches == 2  # split + one chain launch
+    acc, tmp = a.clone(), torch.empty_like(a)
+    for step in mx.plan_exponentiation(k).steps:
+        rhs = acc if step is mx.Step.SQUARE else a
+        eng.gemm_device(acc.data_ptr(), rhs.data_ptr(), tmp.data_ptr(), n)
+        acc, tmp = tmp, acc
+    eng.synchronize()
+    assert torch.equal(chain, acc), (n, k)
 
 
 @pytest.mark.parametrize("n", [129, 200, 255, 257, 384, 511, 640, 768, 896, 1100, 1300])
@@ -664,3 +633,55 @@ def test_host_api_argument_validation(eng):
                 np.zeros((3, 8, 16), np.float32)[:, :, ::2]):
         with pytest.raises(ValueError):
             eng.power_batched(stack, 3, out=bad)
+
+
+def test_batched_host_api_pageable_equals_pinned(eng):
+    """mxp_power_batched with ordinary (pageable) numpy arrays goes through the
+    pinned staging ring; every combination of pageable / pinned input and
+    output gives bitwise the same stack as the device path (several chunks,
+    a ragged last chunk)."""
+    n, batch, k = 128, 2 * 1024 + 333, 13
+    stack = mx.scaled_batch(n, batch, mx.DType.F32, 17)
+    want = eng.power_batched(stack, k)  # pageable in and out
+    d_in, d_out = eng.alloc(stack.nbytes), eng.alloc(stack.nbytes)
+    try:
+        eng.upload(d_in, stack)
+        eng.power_batched_device(d_in, d_out, n, batch, k)
+        dev = np.empty_like(stack)
+        eng.download(dev, d_out)
+    finally:
+        eng.free(d_in)
+        eng.free(d_out)
+    assert want.tobytes() == dev.tobytes()
+    pin_in = eng.pinned_array(stack.shape, np.float32)
+    pin_out = eng.pinned_array(stack.shape, np.float32)
+    try:
+        pin_in[...] = stack
+        for src, dst in ((pin_in, pin_out), (pin_in, np.empty_like(stack)), (stack, pin_out)):
+            dst[...] = 0
+            eng.power_batched(src, k, out=dst)
+            assert dst.tobytes() == want.tobytes()
+            assert eng.last_stats.h2d_bytes == stack.nbytes == eng.last_stats.d2h_bytes
+    finally:
+        eng.host_free(pin_in.ctypes.data)
+        eng.host_free(pin_out.ctypes.data)
+
+
+def test_paper_table_with_b200_rows(capsys):
+    """The paper's comparison table regenerated with B200 rows: repeated and
+    squared on the b200 backend, merged with the reference CLI's own
+    sequential-CPU rows (tests/golden/ref_naive_64.csv)."""
+    import os
+
+    from paper_1204_3052_b200 import cli
+
+    ref_csv = os.path.join(os.path.dirname(__file__), "golden", "ref_naive_64.csv")
+    assert cli.main(["bench", "--sizes", "64", "--powers", "2,16,64", "--reps", "2",
+                     "--table", "-", "--baseline-csv", ref_csv]) == 0
+    out = capsys.readouterr().out.splitlines()
+    assert out[0] == "Matrix size 64 x 64"
+    labels = ["Naïve GPU (In Sec)", "Sequential CPU (In Sec)", "Naïve Speed UP",
+              "Our Approach (In Sec)", "Our Approach vs Naïve GPU"]
+    assert [ln[:len(lab)] for ln, lab in zip(out[2:], labels)] == labels
+    assert out[1].split() == ["2", "16", "64"]
+

@@ -3,6 +3,7 @@ exponentiate driving a generic backend, errors, Matrix, compare, tolerances.
 Mirrors pkg/tests/test_expo.py / test_linalg.py for the names this package keeps."""
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -245,3 +246,19 @@ def test_cli_validation_exit_code():
 
     assert cli.main(["verify", "--size", "4"]) == 1  # missing --power: usage error -> 1
     assert cli.main(["bench", "--sizes", "4", "--powers", "2", "--backend", "naive"]) == 1
+
+
+# ------------------------------------------------------------------ the paper's table (bench.py:330-395)
+def test_emit_table_matches_the_reference_rendering():
+    """tests/golden/table_expected.txt is the reference's own emit_table output
+    for the records in table_records.csv (tests/golden/make_golden_table.py)."""
+    from paper_1204_3052_b200 import harness
+
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    recs = harness.read_csv(os.path.join(here, "table_records.csv"))
+    with open(os.path.join(here, "table_expected.txt"), encoding="utf-8") as fh:
+        assert harness.emit_table(recs) == fh.read()
+    with pytest.raises(mx.TableError):
+        harness.emit_table([r for r in recs if not (r.backend == "naive" and r.power == 16)])
+    with pytest.raises(mx.TableError):
+        harness.emit_table([])
