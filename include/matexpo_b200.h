@@ -175,6 +175,14 @@ MXP_API int mxp_random_device(mxp_handle h, int mode, int64_t n, int64_t batch, 
  * count uint64 draws of `seed` into dOut.  Async on the handle stream. */
 MXP_API int mxp_splitmix64_device(mxp_handle h, uint64_t seed, int64_t count, void* dOut);
 
+/* Which persistent kernel an n <= 128 fp32 chain of power k runs on: the
+ * scaled fp16x2 K3H, or the bf16x3 K3B when K3H's accumulated tensor-core
+ * truncation bias, predicted as (k-1)(2.5e-8 + 1.05e-9 n), would exceed 60%
+ * of the chain tolerance 16 m(k) sqrt(n) 2^-24.  Host-only (no device). */
+#define MXP_KERNEL_K3H 0
+#define MXP_KERNEL_K3B 1
+MXP_API int mxp_small_kernel_for(int64_t n, int64_t k, int* kernel);
+
 /* The SM clock the last batched n <= 128 launch (K3H) actually ran at:
  * clock64 and globaltimer stamped by CTA 0 at its start and end, so
  * *sm_mhz = cycles / ns (NVML samples miss short kernels).  Synchronizes

@@ -27,6 +27,9 @@ MXP_F32 = 0
 MXP_F64 = 1
 MXP_U32_MOD = 2
 
+MXP_KERNEL_K3H = 0
+MXP_KERNEL_K3B = 1
+
 # Every symbol the header declares (tests/test_abi.py checks the .so exports them).
 EXPORTS = (
     "mxp_version", "mxp_device_count", "mxp_create", "mxp_destroy", "mxp_get_stream",
@@ -38,6 +41,7 @@ EXPORTS = (
     "mxp_ipc_get_handle", "mxp_ipc_open_handle", "mxp_ipc_close_handle", "mxp_split_planes",
     "mxp_gemm_rows_planes_peers", "mxp_peer_barrier", "mxp_debug_inject_fault",
     "mxp_splitmix64_device", "mxp_last_kernel_clock",
+    "mxp_small_kernel_for",
 )
 MXP_IPC_HANDLE_BYTES = 72
 
@@ -121,6 +125,7 @@ def load() -> ctypes.CDLL:
             "mxp_debug_inject_fault": [vp, i64],
             "mxp_splitmix64_device": [vp, ctypes.c_uint64, i64, vp],
             "mxp_last_kernel_clock": [vp, P(ctypes.c_double), P(ctypes.c_double)],
+            "mxp_small_kernel_for": [i64, i64, P(c_int)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -153,3 +158,11 @@ def check(status: int, what: str = "") -> None:
     exc = _STATUS_EXC.get(status, E.DeviceError)
     msg = last_error()
     raise exc(f"{what}: {msg}" if what else msg)
+
+
+def small_kernel_for(n: int, k: int) -> str:
+    """'k3h' or 'k3b': the persistent kernel an n <= 128 fp32 chain of power k
+    runs on (the accuracy router, mxp_small_kernel_for)."""
+    v = ctypes.c_int()
+    check(load().mxp_small_kernel_for(int(n), int(k), ctypes.byref(v)), "mxp_small_kernel_for")
+    return "k3h" if v.value == MXP_KERNEL_K3H else "k3b"

@@ -491,6 +491,16 @@ int64_t progress_step(mxp_handle h) {
     return static_cast<int64_t>(*reinterpret_cast<volatile uint32_t*>(h->progress_host)) - 1;
 }
 
+// errors an earlier kernel's fault leaves behind (sticky): they surface at
+// whatever runtime call comes next, not at the launch that caused them
+bool is_async_fault(cudaError_t e) {
+    return e == cudaErrorLaunchFailure || e == cudaErrorIllegalAddress ||
+           e == cudaErrorIllegalInstruction || e == cudaErrorMisalignedAddress ||
+           e == cudaErrorHardwareStackError || e == cudaErrorAssert ||
+           e == cudaErrorInvalidAddressSpace || e == cudaErrorInvalidPc ||
+           e == cudaErrorLaunchTimeout;
+}
+
 void fill_plan_stats(mxp_stats* st, int64_t k, int64_t batch) {
     if (!st) return;
     const PlanBits p = make_plan(k);
@@ -1055,13 +1065,16 @@ int mxp_power(mxp_handle h, int mode, int64_t n, int64_t k, const void* hA, void
         if (st) st->failed_step = inner.failed_step;
         return rc;
     }
-    MXP_CUDA(cudaEventRecord(h->ev1, h->stream));
-    MXP_CUDA(cudaMemcpyAsync(hOut, h->d_out, bytes, cudaMemcpyDeviceToHost, h->stream));
-    cudaError_t e = cudaStreamSynchronize(h->stream);
+    // An asynchronous fault inside the chain surfaces at the first runtime
+    // call after it: name the last plan step a kernel of this chain started
+    // (-1: before the first step; the n <= 128 kernels run a whole chain per
+    // CTA and leave no marks).
+    cudaError_t e = cudaEventRecord(h->ev1, h->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(hOut, h->d_out, bytes, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) {
-        // the last step a kernel of this chain started (0: before the first step;
-        // the n <= 128 kernels run a whole chain per CTA and leave no marks)
-        if (st) st->failed_step = static_cast<int64_t>(progress_step(h));
+        if (st) st->failed_step = progress_step(h);
         return cuda_fail(e, "power chain");
     }
     if (st) {
@@ -1281,6 +1294,14 @@ int mxp_random_device(mxp_handle h, int mode, int64_t n, int64_t batch, uint64_t
     return MXP_OK;
 }
 
+int mxp_small_kernel_for(int64_t n, int64_t k, int* kernel) {
+    if (!kernel) return fail(MXP_E_VALIDATION, "null output pointer");
+    if (n < 1 || n > kSmallMax || k < 2)
+        return fail(MXP_E_VALIDATION, "needs 1 <= n <= %d and k >= 2", kSmallMax);
+    *kernel = k3_route(static_cast<int>(n), make_plan(k)) == 0 ? MXP_KERNEL_K3H : MXP_KERNEL_K3B;
+    return MXP_OK;
+}
+
 int mxp_last_kernel_clock(mxp_handle h, double* sm_mhz, double* kernel_ms) {
     int rc = check_handle(h);
     if (rc) return rc;
@@ -1361,7 +1382,7 @@ int mxp_power_mod_device(mxp_handle h, int64_t n, int64_t k, uint32_t p, const v
             e = launch_mod_combine(B[6], B[7], B[8], p, np, B[3], B[4], B[5],
                                    last ? out : nullptr, (int)n, h->stream);
         if (e != cudaSuccess) {
-            if (st) st->failed_step = s;
+            if (st) st->failed_step = is_async_fault(e) ? progress_step(h) : s;
             return cuda_fail(e, "modular multiply");
         }
         launches += 5;
@@ -1391,9 +1412,10 @@ int mxp_power_mod(mxp_handle h, int64_t n, int64_t k, uint32_t p, const void* hA
         if (st) st->failed_step = inner.failed_step;
         return rc;
     }
-    MXP_CUDA(cudaEventRecord(h->ev1, h->stream));
-    MXP_CUDA(cudaMemcpyAsync(hOut, h->d_out, bytes, cudaMemcpyDeviceToHost, h->stream));
-    cudaError_t e = cudaStreamSynchronize(h->stream);
+    cudaError_t e = cudaEventRecord(h->ev1, h->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(hOut, h->d_out, bytes, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) {
         if (st) st->failed_step = progress_step(h);
         return cuda_fail(e, "modular power");

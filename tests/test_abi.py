@@ -92,3 +92,27 @@ def test_sass_uses_tcgen05_and_dmma(lib):
     assert "UTMALDG" in sass
     assert "LDTM" in sass
     assert "DMMA" in sass
+
+
+def test_small_kernel_router_both_sides_of_threshold():
+    """The K3H -> K3B accuracy router (kernels_tf32.cu k3_route): K3B exactly
+    when the predicted accumulated truncation bias (k-1)(2.5e-8 + 1.05e-9 n)
+    exceeds 60% of the tolerance 16 m(k) sqrt(n) 2^-24.  Host-only."""
+    import math
+
+    def predicted(n, k):
+        m = k.bit_length() - 1 + bin(k).count("1") - 1
+        bias = (k - 1) * (2.5e-8 + 1.05e-9 * n)
+        return "k3b" if bias > 0.6 * 16 * m * math.sqrt(n) * 2.0 ** -24 else "k3h"
+
+    seen = set()
+    for n in (1, 2, 7, 64, 100, 127, 128):
+        for k in list(range(2, 70)) + [255, 256, 257, 383, 384, 385, 511, 512, 1000, 1024, 4096]:
+            got = _lib.small_kernel_for(n, k)
+            assert got == predicted(n, k), (n, k)
+            seen.add(got)
+    assert seen == {"k3h", "k3b"}
+    # the configs: C1 (64^2 A^16) and C3 (128^2 A^64) run on K3H
+    assert _lib.small_kernel_for(64, 16) == "k3h" and _lib.small_kernel_for(128, 64) == "k3h"
+    # at n = 128 the switch sits between k = 383 and 384
+    assert _lib.small_kernel_for(128, 383) == "k3h" and _lib.small_kernel_for(128, 384) == "k3b"

@@ -685,3 +685,32 @@ def test_paper_table_with_b200_rows(capsys):
     assert [ln[:len(lab)] for ln, lab in zip(out[2:], labels)] == labels
     assert out[1].split() == ["2", "16", "64"]
 
+
+
+@pytest.mark.parametrize("k,kernel", [(383, "k3h"), (384, "k3b")])
+def test_router_threshold_both_kernels_meet_tolerance(eng, k, kernel):
+    """Chains just below (K3H) and just above (K3B) the router's switch at
+    n = 128: every matrix within the chain tolerance; the in-kernel clock
+    stamps exist only after a K3H launch (which kernel really ran)."""
+    n, batch = 128, 600
+    assert _lib.small_kernel_for(n, k) == kernel
+    stack = mx.scaled_batch(n, batch, mx.DType.F32, 31)
+    d_in, d_out = eng.alloc(stack.nbytes), eng.alloc(stack.nbytes)
+    try:
+        eng.upload(d_in, stack)
+        eng.power_batched_device(d_in, d_out, n, batch, k)
+        out = np.empty_like(stack)
+        eng.download(out, d_out)
+        if kernel == "k3h":
+            mhz, ms = eng.last_kernel_clock()
+            assert 100 < mhz < 2500 and ms > 0
+        else:
+            with pytest.raises(mx.UnsupportedError):
+                eng.last_kernel_clock()
+    finally:
+        eng.free(d_in)
+        eng.free(d_out)
+    ref = oracle.exponentiate_batched(stack, k, oracle.max_threads())
+    tol = mx.fro_tol(n, k, "f32")
+    for i in range(batch):
+        assert fro(out[i], ref[i]) <= tol, (k, i, fro(out[i], ref[i]), tol)
