@@ -166,6 +166,58 @@ def library_gemm_peak_tflops(device, dtype_name: str) -> float:
     return 2.0 * n ** 3 / (best / 1e3) / 1e12
 
 
+def int8_peak_tops(device) -> float:
+    """cuBLASLt int8 GEMM (torch._int_mm) 8192^3, best of 10: the denominator for
+    the exact modular mode's INT8 limb datapath (library used as a reference)."""
+    import torch
+
+    n = 8192
+    a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=device)
+    b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=device)
+    for _ in range(3):
+        torch._int_mm(a, b)
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(10):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch._int_mm(a, b)
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    return 2.0 * n ** 3 / (best / 1e3) / 1e12
+
+
+def run_mod(eng, n: int = 4096, k: int = 257, p: int = 2**31 - 1, steps: int = 5) -> dict:
+    """The exact modular mode: A^k mod p for an n x n uint32 matrix on the
+    INT8 limb datapath (K5I), device-resident, CUDA-event timed."""
+    import numpy as np
+    import torch
+
+    a = np.random.default_rng(42).integers(0, p, size=(n, n), dtype=np.int64).astype(np.uint32)
+    d_in, d_out = eng.alloc(a.nbytes), eng.alloc(a.nbytes)
+    eng.upload(d_in, a)
+    for _ in range(2):
+        eng.power_mod_device(d_in, d_out, n, k, p)
+    eng.synchronize()
+    launches = eng.last_stats.launches
+    stream = torch.cuda.ExternalStream(eng.stream)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(steps):
+        eng.power_mod_device(d_in, d_out, n, k, p)
+    end.record(stream)
+    end.synchronize()
+    ms = start.elapsed_time(end) / steps
+    eng.free(d_in)
+    eng.free(d_out)
+    return {"workload": f"{n}x{n} uint32 residues mod {p} A^{k} (exact, INT8 limb GEMMs)",
+            "ms": ms, "launches": launches,
+            "TOP/s": 2.0 * n ** 3 * mults(k) / (ms / 1e3) / 1e12,
+            "note": "effective 2 n^3 m integer multiply-adds (mod p); the datapath runs 16 "
+                    "byte-limb GEMMs per product"}
+
+
 def ncu_traffic(kernel: str):
     """dram bytes per launch from the committed ncu summary, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -701,6 +753,18 @@ def main() -> None:
                     extras[key] = ex
                 except Exception as exc:  # noqa: BLE001
                     extras[key] = {"error": str(exc)}
+            try:
+                mod = run_mod(eng)
+                try:
+                    i8 = int8_peak_tops(torch.device("cuda", local))
+                    mod["frac"] = mod["TOP/s"] / (i8 / 16.0)
+                    mod["peak"] = (f"cuBLASLt int8 8192^3 measured in this run ({i8:.0f} TOP/s) / 16 "
+                                   "limb GEMMs")
+                except Exception as exc:  # noqa: BLE001
+                    mod["peak_error"] = str(exc)
+                extras["mod"] = mod
+            except Exception as exc:  # noqa: BLE001
+                extras["mod"] = {"error": str(exc)}
             out["other_configs"] = extras
     print(json.dumps(out))
     if dist is not None:

@@ -37,6 +37,7 @@ cudaError_t prepare_kernels() {
     if (e == cudaSuccess) e = prepare_f64_kernels();
     if (e == cudaSuccess) e = prepare_k3b_kernel();
     if (e == cudaSuccess) e = prepare_k3h_kernel();
+    if (e == cudaSuccess) e = prepare_mod_i8_kernel();
     return e;
 }
 
@@ -209,6 +210,9 @@ struct mxp_handle_s {
     // modular workspace: base limbs (3), acc limbs (3), T0..T2 (3), n_pad^2 doubles each
     int64_t wsmod_pad = 0;
     double* modbuf[9] = {};
+    // INT8 modular workspace: byte limb planes (4 each) of base, ping, pong
+    int64_t wsi8_pad = 0;
+    uint8_t* i8buf[12] = {};
     // plan-step progress of the running chain (pinned, mapped): kernels store
     // step+1 at the start of each step, so after an asynchronous device fault
     // the host still reads which step failed (BackendStepError, errors.py:43-49)
@@ -661,6 +665,8 @@ int mxp_destroy(mxp_handle h) {
     for (auto p : h->f64buf)
         if (p) cudaFree(p);
     for (auto p : h->modbuf)
+        if (p) cudaFree(p);
+    for (auto p : h->i8buf)
         if (p) cudaFree(p);
     if (h->d_in) cudaFree(h->d_in);
     if (h->d_in2) cudaFree(h->d_in2);
@@ -1349,6 +1355,45 @@ int mxp_power_mod_device(mxp_handle h, int64_t n, int64_t k, uint32_t p, const v
         cudaError_t e = launch_mod_trivial(out, a, (int)n, p, k == 1, h->stream);
         if (e != cudaSuccess) return cuda_fail(e, "mod_trivial");
         if (st) st->launches = 1;
+        return MXP_OK;
+    }
+    if (round_up(n, 128) <= kModI8MaxN) {
+        // INT8 tensor cores: 16 limb-pair GEMMs accumulated per diagonal (K5I)
+        const int64_t np8 = round_up(n, 128);
+        if (h->wsi8_pad < np8) {
+            for (auto& q : h->i8buf) {
+                if (q) cudaFree(q);
+                q = nullptr;
+            }
+            h->wsi8_pad = 0;
+            for (auto& q : h->i8buf) MXP_CUDA(cudaMalloc(&q, static_cast<size_t>(np8) * np8));
+            h->wsi8_pad = np8;
+        }
+        uint8_t* const* L = h->i8buf;  // base 0..3, ping 4..7, pong 8..11
+        // planes are laid out at np8 (a larger workspace is reused at this stride)
+        cudaError_t e = launch_mod_split_u8(a, (int)n, p, L, (int)np8, h->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "mod_split_u8");
+        ++launches;
+        const PlanBits plan = make_plan(k);
+        int acc = 0;  // limb set: 0 base, 1 ping, 2 pong
+        for (int s = 0; s < plan.len; ++s) {
+            const int rhs = plan_is_mult(plan, s) ? 0 : acc;
+            const int dst = (acc == 1) ? 2 : 1;
+            const bool last = (s == plan.len - 1);
+            e = launch_progress_mark(h->progress_dev, static_cast<uint32_t>(s + 1), s == h->fault_step,
+                                     h->stream);
+            if (e == cudaSuccess)
+                e = launch_mod_i8_gemm(L + 4 * acc, L + 4 * rhs, (int)np8, p,
+                                       last ? nullptr : L + 4 * dst, last ? out : nullptr, (int)n,
+                                       h->stream);
+            if (e != cudaSuccess) {
+                if (st) st->failed_step = is_async_fault(e) ? progress_step(h) : s;
+                return cuda_fail(e, "modular multiply (int8)");
+            }
+            launches += 2;
+            acc = dst;
+        }
+        if (st) st->launches = launches;
         return MXP_OK;
     }
     const int64_t n_pad = f64_pad((int)n);

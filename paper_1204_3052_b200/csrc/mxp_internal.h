@@ -131,6 +131,16 @@ cudaError_t launch_f64_unpad(const double* in, int n_pad, double* out, int n, cu
 int f64_pad(int n);
 
 // ---- exact modular mode (kernels_mod.cu): 16-bit limbs, Karatsuba, DMMA ---
+// K5I (kernels_mod_i8.cu): one exact modular product on the INT8 tensor cores
+// over byte limb planes (n_pad % 128 == 0, n_pad <= kModI8MaxN so that every
+// s32 accumulator stays < 2^31).  Writes the next step's limb planes, or the
+// final n x n uint32 residues when out != nullptr.
+constexpr int kModI8MaxN = 8192;
+cudaError_t prepare_mod_i8_kernel();
+cudaError_t launch_mod_split_u8(const uint32_t* in, int n, uint32_t p, uint8_t* const* limb,
+                                int n_pad, cudaStream_t s);
+cudaError_t launch_mod_i8_gemm(uint8_t* const* a_limb, uint8_t* const* b_limb, int n_pad, uint32_t p,
+                               uint8_t* const* out_limb, uint32_t* out, int n, cudaStream_t s);
 cudaError_t launch_mod_split(const uint32_t* in, int n, uint32_t p, double* l0, double* l1,
                              double* ls, int n_pad, cudaStream_t s);
 cudaError_t launch_mod_combine(const double* t0, const double* t1, const double* t2, uint32_t p,

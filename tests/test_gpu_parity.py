@@ -324,6 +324,52 @@ def test_modular_bitexact_vs_oracle(eng, n, k, p):
     assert eng.last_stats.multiply_count == mx.multiply_count(k)
 
 
+@pytest.mark.parametrize("n,k,p", [(128, 13, 2**31 - 1), (384, 33, 2147483629), (1000, 9, 65537),
+                                   (1024, 257, 2**31 - 1), (129, 64, 3), (256, 5, 2)])
+def test_modular_int8_datapath_bitexact(eng, n, k, p):
+    """The INT8 tensor-core path (K5I: byte limbs, s32 diagonal accumulators,
+    Barrett folding) against the exact oracle: ragged n, moduli near 2^31
+    (every limb byte populated), tiny moduli, and long plans."""
+    rng = np.random.default_rng(n + k)
+    a = rng.integers(0, 2**32 - 1, size=(n, n), dtype=np.uint64).astype(np.uint32)
+    got = eng.power_mod(a, k, p)
+    ref = oracle.exponentiate_mod(a, k, p, oracle.max_threads())
+    assert np.array_equal(got, ref), (n, k, p, int((got != ref).sum()))
+
+
+def test_modular_worst_case_accumulators_8192(eng):
+    """n = 8192 (the largest order on the INT8 path) with every residue = p - 1
+    for p = 2^31 - 1: every limb byte is 0xFF except the top one (0x7F), so the
+    diagonal accumulators reach 4 n 255^2 - ... close to 2^31 without wrapping.
+    (p-1) J squared is n (p-1)^2 J = n J (mod p): checked against exact ints."""
+    n, p = 8192, 2**31 - 1
+    a = np.full((n, n), p - 1, dtype=np.uint32)
+    got = eng.power_mod(a, 2, p)
+    assert np.all(got == n % p)
+    got = eng.power_mod(a, 3, p)  # n^2 (p-1)^3 J = -n^2 J
+    assert np.all(got == (-(n * n)) % p)
+
+
+def test_modular_dmma_path_beyond_int8_range(eng):
+    """n > 8192 runs the FP64 DMMA Karatsuba path: a permutation of order 12
+    at n = 8200 (and its powers) exactly."""
+    n = 8200
+    perm = np.arange(n)
+    for base in range(0, n - 7, 7):
+        perm[base:base + 3] = np.roll(perm[base:base + 3], 1)
+        perm[base + 3:base + 7] = np.roll(perm[base + 3:base + 7], 1)
+    pm = np.zeros((n, n), dtype=np.uint32)
+    pm[np.arange(n), perm] = 1
+    assert np.array_equal(eng.power_mod(pm, 12, 1000003), np.eye(n, dtype=np.uint32))
+    p5 = np.arange(n)
+    for _ in range(5):
+        p5 = perm[p5]
+    want = np.zeros((n, n), dtype=np.uint32)
+    want[np.arange(n), p5] = 7
+    assert np.array_equal(eng.power_mod(pm * np.uint32(7), 5, 2**31 - 1) % np.uint32(2**31 - 1),
+                          (want.astype(np.uint64) * 7**4 % (2**31 - 1)).astype(np.uint32))
+
+
 def test_modular_kats(eng):
     q = np.array([[1, 1], [1, 0]], dtype=np.uint32)
     assert np.array_equal(eng.power_mod(q, 60, 10), np.eye(2))      # Pisano period pi(10) = 60
