@@ -9,16 +9,18 @@
 // and every D_s entry is an exact integer < 4 n 255^2 < 2^31 for n <= 8192, so
 // the s32 accumulators never wrap.  A 128 x 64 output tile keeps its seven
 // D_s accumulators in TMEM (7 x 64 = 448 columns) for the whole K loop; per
-// 128-deep k-block the issue thread runs the 16 limb pairs x 4 K=32 MMAs into
-// them.  The epilogue folds the diagonals exactly in uint64,
+// 64-deep k-block (four pipeline stages of 48 KB) the issue thread runs the
+// 16 limb pairs x 2 K=32 MMAs into them.  The epilogue folds the diagonals
+// exactly in uint64,
 //   lo = D0 + D1 2^8 + D2 2^16 + D3 2^24 < 2^56,  hi = D4 + D5 2^8 + D6 2^16,
 //   C = (lo mod p + (hi mod p) (2^32 mod p)) mod p      (Barrett reductions)
 // and writes the next step's byte planes (or the final uint32 matrix).
 //
 // Operands straight from the row-major byte planes: A K-major (TMA
-// SWIZZLE_128B, 128 k per row), B MN-major (TMA SWIZZLE_64B, 64 n per
-// k-row) — layouts and the 49-cycle M128 N64 K32 rate measured with
-// tools/i8_probe.cu (profiles/r02_i8_probe.txt).
+// SWIZZLE_64B, 64 k per row), B MN-major (TMA SWIZZLE_64B, 64 n per k-row);
+// operand layouts and the 49-cycle M128 N64 K32 rate (SMEM-operand-bound:
+// 6 KB of operands per MMA at 128 B/cycle) measured with tools/i8_probe.cu
+// (profiles/r02_i8_probe.txt).
 #include <cstring>
 
 #include "mxp_internal.h"
@@ -27,10 +29,11 @@
 namespace mxp {
 namespace {
 
-constexpr int kStages = 2;
-constexpr uint32_t kAPlane = 128u * 128u;  // 128 rows x 128 k (bytes)
-constexpr uint32_t kBPlane = 128u * 64u;   // 128 k-rows x 64 n
-constexpr uint32_t kStageBytes = 4u * kAPlane + 4u * kBPlane;  // 96 KB
+constexpr int kStages = 4;
+constexpr int kKB = 64;                     // k per pipeline stage
+constexpr uint32_t kAPlane = 128u * kKB;    // 128 rows x 64 k (bytes), K-major SW64
+constexpr uint32_t kBPlane = kKB * 64u;     // 64 k-rows x 64 n, MN-major SW64
+constexpr uint32_t kStageBytes = 4u * kAPlane + 4u * kBPlane;  // 48 KB
 constexpr size_t kSmem = kStages * kStageBytes + 1024 + 256;
 constexpr int kThreads = 384;
 constexpr int kBN = 64;
@@ -42,11 +45,43 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023u) & ~uintptr_t(1023));
 }
 
-__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+// One K=32 step of all 16 limb pairs (a, b) into the diagonal accumulators
+// D_{a+b} (TMEM columns tmem + 64 (a+b)), in ONE asm block issued by an
+// elected lane of the whole warp: descriptors and TMEM addresses are formed
+// with immediate offsets on the uniform datapath, so the 49-cycle MMAs are
+// issued back to back (per-MMA calls spent more cycles issuing than the
+// tensor pipe spent executing).  kFirst: the first MMA into each diagonal
+// overwrites it (the first K step of the tile).
+template <bool kFirst>
+__device__ __forceinline__ void mma_i8_x16(uint32_t tmem, uint64_t da, uint64_t db) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %4, p;\n}" ::"r"(d),
-        "l"(a), "l"(b), "r"(acc), "n"(kIdesc)
+        "{\n\t.reg .pred p, f, e;\n\t"
+        ".reg .b32 d0, d1, d2, d3, d4, d5, d6;\n\t"
+        ".reg .b64 a0, a1, a2, a3, b0, b1, b2, b3;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.eq.u32 p, 1, 1;\n\t"
+        "setp.eq.u32 f, %3, 0;\n\t"
+        "mov.b32 d0, %0;\n\tadd.u32 d1, d0, 64;\n\tadd.u32 d2, d0, 128;\n\tadd.u32 d3, d0, 192;\n\t"
+        "add.u32 d4, d0, 256;\n\tadd.u32 d5, d0, 320;\n\tadd.u32 d6, d0, 384;\n\t"
+        "mov.b64 a0, %1;\n\tadd.s64 a1, a0, %4;\n\tadd.s64 a2, a1, %4;\n\tadd.s64 a3, a2, %4;\n\t"
+        "mov.b64 b0, %2;\n\tadd.s64 b1, b0, %5;\n\tadd.s64 b2, b1, %5;\n\tadd.s64 b3, b2, %5;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d0], a0, b0, %6, f;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d1], a0, b1, %6, f;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d2], a0, b2, %6, f;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a0, b3, %6, f;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d1], a1, b0, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d2], a1, b1, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a1, b2, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d4], a1, b3, %6, f;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d2], a2, b0, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a2, b1, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d4], a2, b2, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a2, b3, %6, f;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a3, b0, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d4], a3, b1, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a3, b2, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a3, b3, %6, f;\n}" ::"r"(tmem),
+        "l"(da), "l"(db), "n"(kFirst ? 1 : 0), "n"(kAPlane >> 4), "n"(kBPlane >> 4), "n"(kIdesc)
         : "memory");
 }
 
@@ -63,8 +98,8 @@ __device__ __forceinline__ uint32_t barrett(uint64_t x, uint32_t p, uint64_t m) 
 }  // namespace
 
 struct I8Maps {
-    CUtensorMap a[4];  // left-operand limb planes, box {128 k, 128 rows}, SWIZZLE_128B
-    CUtensorMap b[4];  // right-operand limb planes, box {64 n, 128 k}, SWIZZLE_64B
+    CUtensorMap a[4];  // left-operand limb planes, box {64 k, 128 rows}, SWIZZLE_64B
+    CUtensorMap b[4];  // right-operand limb planes, box {64 n, 64 k}, SWIZZLE_64B
 };
 struct I8Out {
     uint8_t* limb[4];  // next step's limb planes (n_pad x n_pad), or
@@ -94,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int gm = min(num_m - first_m, kGroupM);
     const int m0 = (first_m + (pid % per_group) % gm) * 128;
     const int n0 = ((pid % per_group) / gm) * kBN;
-    const int num_kb = o.n_pad / 128;
+    const int num_kb = o.n_pad / kKB;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kStages; ++i) {
@@ -122,38 +157,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint8_t* base = smem + st * kStageBytes;
             mbar_expect_tx(&full[st], kStageBytes);
             for (int j = 0; j < 4; ++j) {
-                tma_load_2d(base + j * kAPlane, &maps.a[j], &full[st], kb * 128, m0);
-                tma_load_2d(base + 4 * kAPlane + j * kBPlane, &maps.b[j], &full[st], n0, kb * 128);
+                tma_load_2d(base + j * kAPlane, &maps.a[j], &full[st], kb * kKB, m0);
+                tma_load_2d(base + 4 * kAPlane + j * kBPlane, &maps.b[j], &full[st], n0, kb * kKB);
             }
         }
-    } else if (warp == 1 && lane == 0) {
-        // ---------------------------------------------------------- MMA issue
+    } else if (warp == 1) {
+        // ---------------------------------------------------------- MMA issue (whole warp)
         const uint32_t s0 = smem_u32(smem);
-        const uint64_t da = smem_desc(s0, 16, 1024, 2);                // K-major SW128
+        const uint64_t da = smem_desc(s0, 16, 512, 4);                 // K-major SW64
         const uint64_t db = smem_desc(s0 + 4 * kAPlane, 8192, 512, 4);  // MN-major SW64
         for (int kb = 0; kb < num_kb; ++kb) {
             const int st = kb % kStages;
             mbar_wait(&full[st], (kb / kStages) & 1);
             tc_fence_after();
             const uint64_t so = static_cast<uint64_t>((st * kStageBytes) >> 4);
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-#pragma unroll
-                for (int a = 0; a < 4; ++a) {
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const int s = a + b;
-                        // the first pair of diagonal s in this order has the smallest a
-                        const bool first = kb == 0 && ks == 0 && a == (s <= 3 ? 0 : s - 3);
-                        mma_i8(tmem + static_cast<uint32_t>(s * kBN),
-                               da + so + ((a * kAPlane + 32 * ks) >> 4),
-                               db + so + ((b * kBPlane + 2048 * ks) >> 4), first ? 0u : 1u);
-                    }
-                }
-            }
-            mma_commit(&empty[st]);
+            // K step 0 (+32 B of A, +2048 B of B per further step)
+            if (kb == 0) mma_i8_x16<true>(tmem, da + so, db + so);
+            else mma_i8_x16<false>(tmem, da + so, db + so);
+            mma_i8_x16<false>(tmem, da + so + (32 >> 4), db + so + (2048 >> 4));
+            __syncwarp();
+            if (lane == 0) mma_commit(&empty[st]);
+            __syncwarp();
         }
-        mma_commit(done);
+        if (lane == 0) mma_commit(done);
+        __syncwarp();
     } else if (warp >= 4) {
         // ---------------------------------------------------------- epilogue
         mbar_wait(done, 0);
@@ -258,11 +285,10 @@ bool encode_u8(CUtensorMap* m, const void* plane, int n_pad, bool right) {
     if (fn == nullptr) return false;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(n_pad), static_cast<cuuint64_t>(n_pad)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(n_pad)};
-    cuuint32_t box[2] = {right ? 64u : 128u, 128u};
+    cuuint32_t box[2] = {64u, right ? static_cast<cuuint32_t>(kKB) : 128u};
     cuuint32_t es[2] = {1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(plane), dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE,
-              right ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 }  // namespace
