@@ -8,7 +8,7 @@ sys.path.insert(0, ".")
 import oracle  # checker only
 import paper_1204_3052_b200 as mx
 
-tag = os.environ.get("MXP_K3", "k3h")
+tag = "k3h/k3b (as routed)"
 eng = mx.Engine(0)
 for n in (8, 16, 32, 48, 64, 96, 128):
     biases, errs = [], []

@@ -20,7 +20,7 @@ int main() {
     cudaMalloc(&ev, 4096 * 8 * 8); cudaMemset(ev, 0, 4096 * 8 * 8);
     cudaMemcpyToSymbol(g_k3h_evt, &ev, sizeof(ev));
     prepare_k3h_kernel();
-    for (int r = 0; r < 3; ++r) launch_k3h_batched(din, dout, n, B, plan, 148, 0);
+    for (int r = 0; r < 3; ++r) launch_k3h_batched(din, dout, n, B, plan, 148, nullptr, 0);
     cudaDeviceSynchronize();
     std::vector<long long> h(4096 * 8);
     cudaMemcpy(h.data(), ev, h.size() * 8, cudaMemcpyDeviceToHost);

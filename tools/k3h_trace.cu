@@ -22,10 +22,10 @@ int main(int argc, char** argv) {
     cudaMemcpyToSymbol(g_k3h_trace, &tr, sizeof(tr));
     prepare_k3h_kernel();
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    for (int r = 0; r < 2; ++r) launch_k3h_batched(din, dout, n, B, plan, sms, 0);
+    for (int r = 0; r < 2; ++r) launch_k3h_batched(din, dout, n, B, plan, sms, nullptr, 0);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    launch_k3h_batched(din, dout, n, B, plan, sms, 0);
+    launch_k3h_batched(din, dout, n, B, plan, sms, nullptr, 0);
     cudaEventRecord(e1);
     cudaError_t e = cudaDeviceSynchronize();
     float ms; cudaEventElapsedTime(&ms, e0, e1);
