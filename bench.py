@@ -684,12 +684,23 @@ def main() -> None:
             peak, src = bf16 / 6.0, "MEASURED_PEAKS bf16 burst / 2 (tf32) / 3"
         else:
             peak, src = 1590.0 / 6.0, "fallback 1.59 PF bf16 / 6"
-        kernel = "k1_gemm_3xtf32 chain"
+        # the kernel that runs the chain's multiplies
+        n_pad = -(-w["n"] // 128) * 128
+        if w["dtype"] == "f64":
+            kernel = "f64_gemm_kernel"
+        elif w["n"] <= 128:
+            kernel = "k3h_batched_power"
+        elif n_pad >= 1024 and n_pad % 256 == 0:
+            kernel = "k1p_gemm_3xtf32"
+        elif n_pad in (256, 384, 512, 640, 768, 896, 1152, 1408):
+            kernel = "k1c_chain_3xtf32"
+        else:
+            kernel = "k1_gemm_3xtf32"
     rank_fl = flops(w, hi - lo)
     kernel_ms = ms / max(launches, 1) if batched else ms
     achieved = rank_fl / (kernel_ms / 1e3) / 1e12 if batched else value / world
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(kernel.split()[0]),
+                "frac": achieved / peak, "traffic": ncu_traffic(kernel),
                 "kernel": kernel, "peak_source": src,
                 "per_gpu": True,
                 "algorithmic_flops_per_launch": rank_fl / max(launches, 1),

@@ -106,6 +106,10 @@ MXP_API int mxp_download(mxp_handle h, void* dst, const void* src, size_t bytes)
 /* the plan (expo.py:60-75): writes 'S'/'M' bytes, *count = multiply count */
 MXP_API int mxp_plan(int64_t k, char* steps, int64_t cap, int64_t* count);
 
+/* rows x width bytes, device to device (pitches in bytes), async on the handle stream */
+MXP_API int mxp_copy2d_device(mxp_handle h, void* dst, size_t dpitch, const void* src,
+                              size_t spitch, size_t width, size_t rows);
+
 /* one multiply C = A * B */
 MXP_API int mxp_gemm(mxp_handle h, int mode, int64_t n, const void* dA, const void* dB, void* dC);
 /* a row block of one multiply: C[rows x n] = A[rows x n] * B[n x n] (row-major,
@@ -142,6 +146,24 @@ MXP_API int mxp_gemm_rows_planes_peers(mxp_handle h, int64_t n, int64_t rows, in
                                        void* const* peer_lo, void* const* peer_f32);
 MXP_API int mxp_peer_barrier(mxp_handle h, int rank, int npeers, void* const* peer_flags,
                              uint32_t epoch);
+/* NVLS variant of the fused exchange: the ranks' plane / result buffers are
+ * bound to multicast objects, and the epilogue stores each 16 bytes ONCE to
+ * the multicast address (multimem.st); the NVSwitch writes every rank's copy.
+ * Lifecycle: one rank mxp_mc_create (exports MXP_MC_HANDLE_BYTES of FABRIC
+ * handle), the others mxp_mc_import it; once every rank has created or
+ * imported, each calls mxp_mc_bind (its own device memory + a unicast and a
+ * multicast mapping); mxp_mc_destroy when done. */
+#define MXP_MC_HANDLE_BYTES 64
+typedef struct mxp_mc_s* mxp_mc;
+MXP_API int mxp_mc_supported(mxp_handle h, int* ok);
+MXP_API int mxp_mc_create(mxp_handle h, int nranks, size_t bytes, void* handle_out, mxp_mc* out);
+MXP_API int mxp_mc_import(mxp_handle h, const void* handle, size_t bytes, mxp_mc* out);
+MXP_API int mxp_mc_size(mxp_mc mc, size_t* bytes);
+MXP_API int mxp_mc_bind(mxp_mc mc, void** local_ptr, void** mc_ptr);
+MXP_API int mxp_mc_destroy(mxp_mc mc);
+MXP_API int mxp_gemm_rows_planes_mc(mxp_handle h, int64_t n, int64_t rows, int64_t row0,
+                                    const void* a_hi, const void* a_lo, const void* b_hi,
+                                    const void* b_lo, void* mc_hi, void* mc_lo, void* mc_f32);
 MXP_API int mxp_multiply(mxp_handle h, int mode, int64_t n, const void* hA, const void* hB, void* hC,
                  mxp_stats* stats);
 

@@ -41,9 +41,12 @@ EXPORTS = (
     "mxp_ipc_get_handle", "mxp_ipc_open_handle", "mxp_ipc_close_handle", "mxp_split_planes",
     "mxp_gemm_rows_planes_peers", "mxp_peer_barrier", "mxp_debug_inject_fault",
     "mxp_splitmix64_device", "mxp_last_kernel_clock",
-    "mxp_small_kernel_for",
+    "mxp_small_kernel_for", "mxp_mc_supported", "mxp_mc_create", "mxp_mc_import",
+    "mxp_mc_size", "mxp_mc_bind", "mxp_mc_destroy", "mxp_gemm_rows_planes_mc",
+    "mxp_copy2d_device",
 )
 MXP_IPC_HANDLE_BYTES = 72
+MXP_MC_HANDLE_BYTES = 64
 
 
 class Stats(ctypes.Structure):
@@ -126,6 +129,14 @@ def load() -> ctypes.CDLL:
             "mxp_splitmix64_device": [vp, ctypes.c_uint64, i64, vp],
             "mxp_last_kernel_clock": [vp, P(ctypes.c_double), P(ctypes.c_double)],
             "mxp_small_kernel_for": [i64, i64, P(c_int)],
+            "mxp_mc_supported": [vp, P(c_int)],
+            "mxp_mc_create": [vp, c_int, sz, vp, P(vp)],
+            "mxp_mc_import": [vp, vp, sz, P(vp)],
+            "mxp_mc_size": [vp, P(sz)],
+            "mxp_mc_bind": [vp, P(vp), P(vp)],
+            "mxp_mc_destroy": [vp],
+            "mxp_gemm_rows_planes_mc": [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp],
+            "mxp_copy2d_device": [vp, vp, sz, vp, sz, sz, sz],
         }
         for name, args in sig.items():
             fn = getattr(L, name)

@@ -528,7 +528,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K1PCfg::kThreads, 1)
             if (lane == 0) mbar_arrive_cluster_relaxed(cempty_leader0 + 8 * c);
         }
         const int row = m0 + q * 32 + lane;
-        if (po.n > 0) {
+        if (po.mc) {
+            // fused exchange over NVLS: one multicast store per 16 bytes, the
+            // switch writes it into every rank's buffer
+            const size_t grow = static_cast<size_t>(po.row0 + row);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int col = n0 + ch + 32 * h;
+                const float* v = sum + 32 * h;
+                if (po.f32[0] != nullptr) {
+                    float* d = po.f32[0] + grow * ld_out + col;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        multimem_st_v4(d + 4 * u, __float_as_uint(v[4 * u]), __float_as_uint(v[4 * u + 1]),
+                                       __float_as_uint(v[4 * u + 2]), __float_as_uint(v[4 * u + 3]));
+                } else {
+                    uint32_t* dh = po.hi[0] + grow * n_pad + col;
+                    uint32_t* dl = po.lo[0] + grow * n_pad + col;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        uint4 hv, lv;
+                        split_tf32(v[4 * u + 0], hv.x, lv.x);
+                        split_tf32(v[4 * u + 1], hv.y, lv.y);
+                        split_tf32(v[4 * u + 2], hv.z, lv.z);
+                        split_tf32(v[4 * u + 3], hv.w, lv.w);
+                        multimem_st_v4(dh + 4 * u, hv.x, hv.y, hv.z, hv.w);
+                        multimem_st_v4(dl + 4 * u, lv.x, lv.y, lv.z, lv.w);
+                    }
+                }
+            }
+        } else if (po.n > 0) {
             // fused exchange: this row segment goes straight to every rank
             // (its own included) while other tiles are still in their MMAs
             const size_t grow = static_cast<size_t>(po.row0 + row);

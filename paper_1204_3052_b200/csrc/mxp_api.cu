@@ -556,6 +556,18 @@ int run_power_graph(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA
 
 }  // namespace
 
+// for the other translation units of the library (mxp_multicast.cu)
+int mxp_internal_fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+int mxp_internal_device(mxp_handle h) { return h->device; }
+
 // =====================================================================
 extern "C" {
 
@@ -746,6 +758,17 @@ int mxp_download(mxp_handle h, void* dst, const void* src, size_t bytes) {
     if (rc) return rc;
     MXP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->stream));
     MXP_CUDA(cudaStreamSynchronize(h->stream));
+    return MXP_OK;
+}
+
+int mxp_copy2d_device(mxp_handle h, void* dst, size_t dpitch, const void* src, size_t spitch,
+                      size_t width, size_t rows) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (!dst || !src) return fail(MXP_E_VALIDATION, "null device pointer");
+    if (width > dpitch || width > spitch) return fail(MXP_E_VALIDATION, "width exceeds a pitch");
+    MXP_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToDevice,
+                               h->stream));
     return MXP_OK;
 }
 
@@ -974,6 +997,41 @@ int mxp_gemm_rows_planes_peers(mxp_handle h, int64_t n, int64_t rows, int64_t ro
     GemmPlanes m{ma_hi, ma_lo, mb_hi, mb_lo};
     cudaError_t e = launch_k1p_gemm_peers(m, (int)n, (int)rows, (int)n, po, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "k1p_gemm_3xtf32 (fused exchange)");
+    return MXP_OK;
+}
+
+int mxp_gemm_rows_planes_mc(mxp_handle h, int64_t n, int64_t rows, int64_t row0, const void* a_hi,
+                            const void* a_lo, const void* b_hi, const void* b_lo, void* mc_hi,
+                            void* mc_lo, void* mc_f32) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (n < 1024 || n % 256 != 0)
+        return fail(MXP_E_UNSUPPORTED, "fused exchange needs n %% 256 == 0 and n >= 1024, got %lld",
+                    (long long)n);
+    if (rows < 256 || rows % 256 != 0 || row0 < 0 || row0 % 256 != 0 || row0 + rows > n)
+        return fail(MXP_E_VALIDATION, "row block [%lld, +%lld) must be 256-aligned inside n",
+                    (long long)row0, (long long)rows);
+    if (!a_hi || !a_lo || !b_hi || !b_lo) return fail(MXP_E_VALIDATION, "null device pointer");
+    if (!mc_f32 && (!mc_hi || !mc_lo)) return fail(MXP_E_VALIDATION, "no multicast destination");
+    PeerOut po;
+    po.n = 1;
+    po.mc = 1;
+    po.row0 = static_cast<int>(row0);
+    po.f32[0] = static_cast<float*>(mc_f32);
+    po.hi[0] = static_cast<uint32_t*>(mc_hi);
+    po.lo[0] = static_cast<uint32_t*>(mc_lo);
+    const size_t off = static_cast<size_t>(row0) * n;
+    CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
+    if (!encode_plane_map(&ma_hi, static_cast<const uint32_t*>(a_hi) + off, (int)n, 32, 128, false,
+                          (int)rows) ||
+        !encode_plane_map(&ma_lo, static_cast<const uint32_t*>(a_lo) + off, (int)n, 32, 128, false,
+                          (int)rows) ||
+        !encode_plane_map(&mb_hi, b_hi, (int)n, 32, 32, true) ||
+        !encode_plane_map(&mb_lo, b_lo, (int)n, 32, 32, true))
+        return fail(MXP_E_CUDA, "cuTensorMapEncodeTiled failed");
+    GemmPlanes m{ma_hi, ma_lo, mb_hi, mb_lo};
+    cudaError_t e = launch_k1p_gemm_peers(m, (int)n, (int)rows, (int)n, po, h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "k1p_gemm_3xtf32 (multicast exchange)");
     return MXP_OK;
 }
 

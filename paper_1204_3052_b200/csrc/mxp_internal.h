@@ -73,6 +73,8 @@ constexpr int kMaxPeers = 8;
 struct PeerOut {
     int n = 0;     // destinations (0: the kernel's ordinary outputs)
     int row0 = 0;  // global row of this launch's row 0
+    int mc = 0;    // 1: hi[0]/lo[0]/f32[0] are NVLS multicast addresses (n == 1):
+                   // one multimem.st reaches every rank's copy through the switch
     uint32_t* hi[kMaxPeers] = {};
     uint32_t* lo[kMaxPeers] = {};
     float* f32[kMaxPeers] = {};  // fp32 rows (leading dim ld_out) instead of planes

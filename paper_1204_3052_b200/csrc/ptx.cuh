@@ -12,6 +12,16 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// NVLS multicast store: one 16-byte store to a multicast address is written
+// by the NVSwitch into every bound copy (every rank's buffer)
+__device__ __forceinline__ void multimem_st_v4(void* mc_addr, uint32_t a, uint32_t b, uint32_t c,
+                                               uint32_t d) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc_addr),
+                 "f"(__uint_as_float(a)), "f"(__uint_as_float(b)), "f"(__uint_as_float(c)),
+                 "f"(__uint_as_float(d))
+                 : "memory");
+}
+
 // the GPU-wide nanosecond timer (pairs with clock64 to measure the SM clock)
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;

@@ -173,8 +173,12 @@ class RowShardedFused:
     ``close`` (also collective) unmaps them."""
 
     _SHARED = ("p0_hi", "p0_lo", "p1_hi", "p1_lo", "out", "flags")
+    _MC = ("p0_hi", "p0_lo", "p1_hi", "p1_lo", "out")  # one multicast group, five n_p^2 slots
 
-    def __init__(self, n: int, device, group=None, engine=None):
+    def __init__(self, n: int, device, group=None, engine=None, multicast=None):
+        """multicast: True = NVLS multicast stores (one store per tile reaches
+        every rank through the switch), False = per-peer stores over CUDA IPC,
+        None = multicast when every rank has its own multicast-capable GPU."""
         import torch
         import torch.distributed as dist
 
@@ -189,20 +193,60 @@ class RowShardedFused:
             engine = default_engine(torch.device(device).index or 0)
         self.eng = engine
         n_p = self.n_p
+        plane = n_p * n_p * 4
         self.buf = {k: torch.empty((n_p, n_p), dtype=torch.int32, device=device)
-                    for k in ("base_hi", "base_lo", "p0_hi", "p0_lo", "p1_hi", "p1_lo")}
-        self.buf["out"] = torch.empty((n_p, n_p), dtype=torch.float32, device=device)
+                    for k in ("base_hi", "base_lo")}
         self.buf["flags"] = torch.zeros(self.world, dtype=torch.int32, device=device)
         self.base = torch.zeros((n_p, n_p), dtype=torch.float32, device=device)
+        # every rank on its own GPU, all of them multicast-capable?
+        dev = torch.device(device)
+        uuid = str(getattr(torch.cuda.get_device_properties(dev), "uuid", dev.index))
+        caps = [None] * self.world
+        dist.all_gather_object(caps, (uuid, self.eng.mc_supported()), group=group)
+        possible = len({c[0] for c in caps}) == self.world and all(c[1] for c in caps)
+        if multicast and not possible:
+            raise RuntimeError("NVLS multicast needs one multicast-capable GPU per rank")
+        self.multicast = possible if multicast is None else bool(multicast)
+        self.mc = None
+        if self.multicast:
+            # rank 0 creates the multicast object, everyone imports / adds its
+            # device, then (the team complete) binds its own memory to it
+            info = [None]
+            if self.rank == 0:
+                try:
+                    self.mc, handle, size = self.eng.mc_create(self.world, len(self._MC) * plane)
+                    info = [(handle, size)]
+                except Exception as exc:  # noqa: BLE001 - reported below, on every rank
+                    info = [str(exc)]
+            dist.broadcast_object_list(info, src=0, group=group)
+            if isinstance(info[0], str):
+                if multicast:
+                    raise RuntimeError(f"NVLS multicast unavailable: {info[0]}")
+                self.multicast = False  # the driver refused the multicast object: peer stores
+                self.mc_error = info[0]
+        if self.multicast:
+            if self.rank != 0:
+                self.mc = self.eng.mc_import(info[0][0], info[0][1])
+            dist.barrier(group=group)
+            uc, mcp = self.eng.mc_bind(self.mc)
+            self.local = {k: uc + i * plane for i, k in enumerate(self._MC)}
+            self.mcast = {k: mcp + i * plane for i, k in enumerate(self._MC)}
+            self.local["flags"] = self.buf["flags"].data_ptr()
+            shared = ("flags",)
+        else:
+            for k in ("p0_hi", "p0_lo", "p1_hi", "p1_lo"):
+                self.buf[k] = torch.empty((n_p, n_p), dtype=torch.int32, device=device)
+            self.buf["out"] = torch.empty((n_p, n_p), dtype=torch.float32, device=device)
+            self.local = {k: self.buf[k].data_ptr() for k in self._SHARED}
+            shared = self._SHARED
         torch.cuda.synchronize(device)
-        self.local = {k: self.buf[k].data_ptr() for k in self._SHARED}
-        mine = {k: self.eng.ipc_get_handle(self.local[k]) for k in self._SHARED}
+        mine = {k: self.eng.ipc_get_handle(self.local[k]) for k in shared}
         everyone = [None] * self.world
         dist.all_gather_object(everyone, mine, group=group)
         self.opened = []
-        self.peer = {k: [] for k in self._SHARED}
+        self.peer = {k: [] for k in shared}
         for r in range(self.world):
-            for k in self._SHARED:
+            for k in shared:
                 if r == self.rank:
                     self.peer[k].append(self.local[k])
                 else:
@@ -234,8 +278,7 @@ class RowShardedFused:
             self.base[:n, :n] = a  # zero padding never mixes into the top-left n x n block
         eng.split_planes_device(self.base.data_ptr(), b["base_hi"].data_ptr(),
                                 b["base_lo"].data_ptr(), n_p)
-        eng.split_planes_device(self.base.data_ptr(), b["p0_hi"].data_ptr(),
-                                b["p0_lo"].data_ptr(), n_p)
+        eng.split_planes_device(self.base.data_ptr(), self.local["p0_hi"], self.local["p0_lo"], n_p)
         cur, nxt = "p0", "p1"
         r0 = self.rank * rows
         for s, step in enumerate(plan.steps):
@@ -244,10 +287,16 @@ class RowShardedFused:
                 b_hi, b_lo = self.local[cur + "_hi"], self.local[cur + "_lo"]
             else:
                 b_hi, b_lo = b["base_hi"].data_ptr(), b["base_lo"].data_ptr()
-            eng.gemm_rows_planes_peers(
-                n_p, rows, r0, self.local[cur + "_hi"], self.local[cur + "_lo"], b_hi, b_lo,
-                None if last else self.peer[nxt + "_hi"], None if last else self.peer[nxt + "_lo"],
-                self.peer["out"] if last else None)
+            if self.multicast:
+                eng.gemm_rows_planes_mc(
+                    n_p, rows, r0, self.local[cur + "_hi"], self.local[cur + "_lo"], b_hi, b_lo,
+                    None if last else self.mcast[nxt + "_hi"],
+                    None if last else self.mcast[nxt + "_lo"], self.mcast["out"] if last else None)
+            else:
+                eng.gemm_rows_planes_peers(
+                    n_p, rows, r0, self.local[cur + "_hi"], self.local[cur + "_lo"], b_hi, b_lo,
+                    None if last else self.peer[nxt + "_hi"],
+                    None if last else self.peer[nxt + "_lo"], self.peer["out"] if last else None)
             # all ranks' rows have landed everywhere (and nobody still reads the
             # buffer the next step overwrites) before anyone goes on
             self.epoch += 1
@@ -255,7 +304,8 @@ class RowShardedFused:
             cur, nxt = nxt, cur
         with torch.cuda.stream(ext):
             out = torch.empty((n, n), dtype=a.dtype, device=a.device)
-            out.copy_(b["out"][:n, :n])
+        # the top-left n x n block of the (n_p-strided) result, on the engine stream
+        eng.copy2d_device(out.data_ptr(), n * 4, self.local["out"], n_p * 4, n * 4, n)
         caller = torch.cuda.current_stream(a.device)
         caller.wait_stream(ext)
         out.record_stream(caller)
@@ -267,6 +317,9 @@ class RowShardedFused:
         for ptr in self.opened:
             self.eng.ipc_close_handle(ptr)
         self.opened = []
+        if self.mc is not None:
+            self.eng.mc_destroy(self.mc)
+            self.mc = None
 
 
 def exponentiate_row_sharded_fused(a, power: int, group=None, engine=None):

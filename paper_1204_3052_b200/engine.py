@@ -259,6 +259,51 @@ class Engine:
             ctypes.c_void_p(b_hi), ctypes.c_void_p(b_lo), npeers, self._ptr_array(peer_hi),
             self._ptr_array(peer_lo), self._ptr_array(peer_f32)), "mxp_gemm_rows_planes_peers")
 
+    def copy2d_device(self, dst: int, dpitch: int, src: int, spitch: int, width: int,
+                      rows: int) -> None:
+        """rows x width bytes, device to device, on the engine's stream."""
+        _lib.check(self._L.mxp_copy2d_device(self._h, ctypes.c_void_p(dst), dpitch,
+                                             ctypes.c_void_p(src), spitch, width, rows),
+                   "mxp_copy2d_device")
+
+    # ------------------------------------------------------------ NVLS multicast exchange
+    def mc_supported(self) -> bool:
+        ok = ctypes.c_int()
+        _lib.check(self._L.mxp_mc_supported(self._h, ctypes.byref(ok)), "mxp_mc_supported")
+        return bool(ok.value)
+
+    def mc_create(self, nranks: int, nbytes: int):
+        """(mc object, exported 64-byte handle, granted size) — the creator's side."""
+        buf = ctypes.create_string_buffer(_lib.MXP_MC_HANDLE_BYTES)
+        mc = ctypes.c_void_p()
+        _lib.check(self._L.mxp_mc_create(self._h, int(nranks), int(nbytes), buf, ctypes.byref(mc)),
+                   "mxp_mc_create")
+        size = ctypes.c_size_t()
+        _lib.check(self._L.mxp_mc_size(mc, ctypes.byref(size)), "mxp_mc_size")
+        return mc, buf.raw, size.value
+
+    def mc_import(self, handle: bytes, nbytes: int):
+        mc = ctypes.c_void_p()
+        _lib.check(self._L.mxp_mc_import(self._h, handle, int(nbytes), ctypes.byref(mc)),
+                   "mxp_mc_import")
+        return mc
+
+    def mc_bind(self, mc):
+        """(local unicast pointer, multicast pointer) of this rank's bound copy."""
+        uc, mcp = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(self._L.mxp_mc_bind(mc, ctypes.byref(uc), ctypes.byref(mcp)), "mxp_mc_bind")
+        return uc.value, mcp.value
+
+    def mc_destroy(self, mc) -> None:
+        _lib.check(self._L.mxp_mc_destroy(mc), "mxp_mc_destroy")
+
+    def gemm_rows_planes_mc(self, n: int, rows: int, row0: int, a_hi: int, a_lo: int, b_hi: int,
+                            b_lo: int, mc_hi=None, mc_lo=None, mc_f32=None) -> None:
+        _lib.check(self._L.mxp_gemm_rows_planes_mc(
+            self._h, n, rows, row0, ctypes.c_void_p(a_hi), ctypes.c_void_p(a_lo),
+            ctypes.c_void_p(b_hi), ctypes.c_void_p(b_lo), ctypes.c_void_p(mc_hi),
+            ctypes.c_void_p(mc_lo), ctypes.c_void_p(mc_f32)), "mxp_gemm_rows_planes_mc")
+
     def peer_barrier(self, rank: int, peer_flags, epoch: int) -> None:
         _lib.check(self._L.mxp_peer_barrier(self._h, rank, len(peer_flags),
                                             self._ptr_array(peer_flags), epoch & 0xFFFFFFFF),

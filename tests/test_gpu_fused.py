@@ -81,3 +81,44 @@ def test_fused_layout():
     assert D.fused_layout(1000, 2) == (1024, 512)
     n_p, rows = D.fused_layout(3000, 4)
     assert rows % 256 == 0 and n_p == 4 * rows and n_p >= 3000
+
+
+@pytest.mark.gpu
+def test_fused_exchange_nvls_multicast_single_rank_bitwise():
+    """The NVLS variant (mxp_mc_*: a multicast object with this GPU's memory
+    bound to it; the epilogue's multimem.st goes through the switch) on one
+    rank: BITWISE the single-GPU chain.  The box has one GPU, so this is the
+    whole multicast machinery with a team of one; ranks sharing a GPU cannot
+    join one multicast team (they take the IPC path above)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1204_3052_b200 as mx
+    from paper_1204_3052_b200 import distributed as D
+
+    eng = mx.Engine(0)
+    if not eng.mc_supported():
+        pytest.skip("no NVLS multicast on this device")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        for n in (1024, 2000):
+            a_np = oracle.scaled_input(n, np.float32, 42)
+            a = torch.from_numpy(a_np).cuda()
+            try:
+                chain = D.RowShardedFused(n, a.device, engine=eng, multicast=True)
+            except RuntimeError as exc:
+                # the one-GPU sandbox reports MULTICAST_SUPPORTED but refuses
+                # cuMulticastCreate (profiles/r02_mc_probe.txt)
+                pytest.skip(f"multicast object refused here: {exc}")
+            try:
+                assert chain.multicast
+                for k in (16, 13):
+                    got = chain.power(a, k)
+                    torch.cuda.synchronize()
+                    assert got.cpu().numpy().tobytes() == eng.power(a_np, k).tobytes(), (n, k)
+            finally:
+                chain.close()
+    finally:
+        dist.destroy_process_group()
