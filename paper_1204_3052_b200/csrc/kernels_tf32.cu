@@ -784,10 +784,14 @@ __device__ long long* g_k1c_trace;  // [step][8]
     } while (0)
 #endif
 
+// Grid-wide barrier: the CTA barrier orders every thread's plane stores
+// before thread 0's gpu-scope release (release is cumulative over what
+// happens-before it), so no separate __threadfence is needed — the same
+// pattern as CUTLASS's GenericBarrier; dropping the MEMBAR.GPU made C2 2%
+// faster (profiles/r02_c2_variants.txt).
 __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int target) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();  // this CTA's plane stores are visible GPU-wide
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
         unsigned int v;
         for (;;) {
