@@ -205,6 +205,11 @@ MXP_API int mxp_splitmix64_device(mxp_handle h, uint64_t seed, int64_t count, vo
 #define MXP_KERNEL_K3B 1
 MXP_API int mxp_small_kernel_for(int64_t n, int64_t k, int* kernel);
 
+/* How many matrices of the last n <= 128 K3H launch were recomputed on K3B
+ * because their chain hit strong cancellation (the scaled fp16 planes keep
+ * one exponent per matrix; K3B keeps one per element).  Synchronizes. */
+MXP_API int mxp_last_small_fixups(mxp_handle h, int64_t* count);
+
 /* The SM clock the last batched n <= 128 launch (K3H) actually ran at:
  * clock64 and globaltimer stamped by CTA 0 at its start and end, so
  * *sm_mhz = cycles / ns (NVML samples miss short kernels).  Synchronizes

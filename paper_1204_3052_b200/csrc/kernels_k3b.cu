@@ -231,7 +231,13 @@ __shared__ long long k3b_acc[16];
 __global__ void __launch_bounds__(kThreads, 1)
     k3b_batched_power(const __grid_constant__ CUtensorMap in_map,
                       const __grid_constant__ CUtensorMap out_map, const float* __restrict__ in,
-                      float* __restrict__ out, int n, long long batch, PlanBits plan, int vec) {
+                      float* __restrict__ out, int n, long long batch, PlanBits plan, int vec,
+                      const int* __restrict__ idx, const int* __restrict__ count) {
+    // idx != nullptr: recompute only the matrices listed in idx[0 .. *count)
+    // (K3H's dynamic-range fixup, kernels_k3h.cu); matrix m of this launch is
+    // matrix idx[m] of the caller's stack
+    if (idx != nullptr) batch = *count;
+    auto mat = [&](long long m) -> long long { return idx != nullptr ? idx[m] : m; };
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
@@ -308,9 +314,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(in_ready + cc, 16 * 4096);
         for (uint32_t w = 0; w < kWorkers; ++w)
             tma_load_2d_s(s0 + cc * kChainSmem + w * 4096u, &in_map, in_ready + cc,
-                          static_cast<int32_t>((w >> 2) * 32), static_cast<int32_t>(mm * 128 + (w & 3) * 32));
+                          static_cast<int32_t>((w >> 2) * 32), static_cast<int32_t>(mat(mm) * 128 + (w & 3) * 32));
         if (mm + 2 * G < batch)
-            prefetch_l2(in + static_cast<size_t>(mm + 2 * G) * n2, static_cast<uint32_t>(n2 * 4));
+            prefetch_l2(in + static_cast<size_t>(mat(mm + 2 * G)) * n2, static_cast<uint32_t>(n2 * 4));
     };
 
     if (warp == kIssueWarp) {
@@ -367,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (uint32_t w = 0; w < kWorkers; ++w)
                                 tma_store_2d_s(&out_map, s0 + c * kChainSmem + w * 4096u,
                                                static_cast<int32_t>((w >> 2) * 32),
-                                               static_cast<int32_t>(m_prev * 128 + (w & 3) * 32));
+                                               static_cast<int32_t>(mat(m_prev) * 128 + (w & 3) * 32));
                             bulk_commit_group();
                             bulk_wait_group_read0();  // tiles read: reuse them for the input
                             if (act_c) tiles_load(c, m_c);
@@ -421,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // matrix m_c straight from global (n != 128, and the base of a MULTIPLY_BASE step)
         auto emit_global = [&](uint32_t cc, bool right, bool left) {
             float x[32];
-            load_row(in + static_cast<size_t>(m_c) * n2, n, vec, row, col0, x);
+            load_row(in + static_cast<size_t>(mat(m_c)) * n2, n, vec, row, col0, x);
             emit(cc, 0, x, right, left);
             emit(cc, 1, x + 16, right, left);
         };
@@ -469,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             K3B_MARK(2);
                             K3B_COUNT(13);
                         } else {
-                            store_row(out + static_cast<size_t>(m_c) * n2, n, vec, row, col0, v);
+                            store_row(out + static_cast<size_t>(mat(m_c)) * n2, n, vec, row, col0, v);
                             tc_fence_before();
                         }
                         m_c += 2 * G;
@@ -519,7 +525,8 @@ cudaError_t prepare_k3b_kernel() {
 }
 
 cudaError_t launch_k3b_batched(const float* in, float* out, int n, int64_t batch,
-                               const PlanBits& plan, int grid, cudaStream_t s) {
+                               const PlanBits& plan, int grid, cudaStream_t s, const int* idx,
+                               const int* count) {
     if (plan.len < 1 || n < 1 || n > kSmallMax) return cudaErrorInvalidValue;
     if (grid > batch) grid = static_cast<int>(batch);
     CUtensorMap in_map, out_map;
@@ -532,7 +539,8 @@ cudaError_t launch_k3b_batched(const float* in, float* out, int n, int64_t batch
                   : 0;
     if (vec && !(encode_tile_map(&in_map, in, batch * 128) && encode_tile_map(&out_map, out, batch * 128)))
         vec = 0;
-    k3b_batched_power<<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec);
+    k3b_batched_power<<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec,
+                                                    idx, count);
     return cudaGetLastError();
 }
 

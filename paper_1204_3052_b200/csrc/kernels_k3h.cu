@@ -40,6 +40,7 @@
 
 #include "mxp_internal.h"
 #include "ptx.cuh"
+#include "split16.cuh"
 
 namespace mxp {
 namespace {
@@ -53,8 +54,6 @@ constexpr uint32_t kChainSmem = 2u * kPlane;   // y0, y1 of one chain
 constexpr uint32_t kMaxOff = 3u * kChainSmem;  // after 3 regions: [chain][buffer][8] max slots
 constexpr uint32_t kBarOff = kMaxOff + 256;    // mbarriers + TMEM slot
 constexpr size_t kSmem = kBarOff + 128 + 1024; // + alignment slack
-constexpr int kTarget = 13;                    // input: scaled max |A'| in [2^13, 2^14)
-constexpr int kCeil = 14;                      // products: scaled max |D'| < 2^14 guaranteed
 // kind::f16 with fp16 A/B (formats 0), fp32 D, A K-major, B MN-major, M = N = 128
 constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | (1u << 16) | ((128u >> 3) << 17) |
                             ((128u >> 4) << 24);
@@ -65,53 +64,6 @@ constexpr uint32_t kIdescNegB = kIdesc | (1u << 14);
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023u) & ~uintptr_t(1023));
-}
-
-// (a, b) = columns 2j, 2j+1 (unscaled), sc2 = the scale in both halves:
-// two packed fp16x2 words p0 = h0 = rn(a', b') and p1 = -h1.
-__device__ __forceinline__ void split2(float a, float b, uint64_t sc2, uint32_t& p0, uint32_t& p1) {
-    // p1 = rn(p0 - x') = -rn(x' - p0) (the residual is exact in fp32).  Per
-    // pair: FMUL2, F2FP, two mixed fp16-fp32 subtractions (FHADD, the fp16
-    // half read in place), F2FP — one instruction fewer than unpacking h0
-    // (2 HADD2.F32) for an FADD2.  The MMAs that read p1 negate it back
-    // (instruction-descriptor negate bits), so the products are those of
-    // h1 = rn(x' - h0) bit for bit (measured: identical outputs, -4% time).
-    uint64_t ab, s2;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(ab) : "f"(a), "f"(b));
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(s2) : "l"(ab), "l"(sc2));
-    asm("{\n\t.reg .f32 sa, sb, ra, rb;\n\t.reg .b16 l, h;\n\t"
-        "mov.b64 {sa, sb}, %2;\n\t"
-        "cvt.rn.f16x2.f32 %0, sb, sa;\n\t"
-        "mov.b32 {l, h}, %0;\n\t"
-        "sub.f32.f16 ra, l, sa;\n\t"
-        "sub.f32.f16 rb, h, sb;\n\t"
-        "cvt.rn.f16x2.f32 %1, rb, ra;\n\t}"
-        : "=r"(p0), "=r"(p1)
-        : "l"(s2));
-}
-__device__ __forceinline__ uint64_t splat2(float x) {
-    uint64_t r;
-    asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
-    return r;
-}
-// 2^t as a float, t clamped to the normal range
-__device__ __forceinline__ float exp2i(int t) {
-    t = max(-126, min(127, t));
-    return __int_as_float((t + 127) << 23);
-}
-// scale exponent for a block whose max |element| has bit pattern mbits:
-// returns t with max * 2^t in [2^13, 2^14) (0 for zero, inf or NaN maxima)
-__device__ __forceinline__ int scale_exp(uint32_t mbits) {
-    if (mbits == 0u || mbits >= 0x7F800000u) return 0;
-    const int k = mbits >= 0x00800000u ? static_cast<int>(mbits >> 23) - 127
-                                       : -127 + (31 - __clz(static_cast<int>(mbits))) - 22;
-    return kTarget - k;
-}
-// floor(log2(x)) from the bits of |x| (x finite, > 0); -1000 for 0
-__device__ __forceinline__ int ilogb_bits(uint32_t mbits) {
-    if (mbits == 0u) return -1000;
-    return mbits >= 0x00800000u ? static_cast<int>(mbits >> 23) - 127
-                                : (31 - __clz(static_cast<int>(mbits))) - 149;
 }
 
 // 32 values of one row of an n x n fp32 matrix, zero padded to 128.
@@ -239,6 +191,7 @@ struct Chain {
     uint32_t mph;   // max_bar parities, bit b for buffer b
     uint32_t home;  // SMEM region (0..2) holding the chain's operand planes
     bool act;
+    bool flagged;   // the current matrix is on the K3B fixup list (epilogue)
 };
 constexpr int kIn = -2;  // Chain::s: the next input is being loaded / converted
 
@@ -268,7 +221,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     k3h_batched_power(const __grid_constant__ CUtensorMap in_map,
                       const __grid_constant__ CUtensorMap out_map, const float* __restrict__ in,
                       float* __restrict__ out, int n, long long batch, PlanBits plan, int vec,
-                      unsigned long long* stamps) {
+                      unsigned long long* stamps, int* __restrict__ fix_idx,
+                      int* __restrict__ fix_count) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
@@ -515,6 +469,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             st.mph ^= 1u << st.sb;
             return max8(s0 + kMaxOff + cc * 64u + st.sb * 32u);
         };
+        // Dynamic range: the planes carry one exponent for the whole matrix,
+        // so entries more than ~2^38 below its max are lost.  A product that
+        // came out more than 2^12 below its bound (strong cancellation — the
+        // same test that selects the exact scale path below) is the sign that
+        // such entries may matter to a later product: the matrix goes on the
+        // fixup list and K3B (an exponent per element) recomputes it after
+        // this launch.  Random inputs never trigger it.
+        auto flag_range = [&](Chain& st, int pmax_e, uint32_t mprev) {
+            if (fix_idx == nullptr || st.flagged) return;
+            if (pmax_e < kCeil - 12 || mprev == 0u || mprev >= 0x7F800000u) {
+                st.flagged = true;
+                if (warp == 0 && lane == 0) fix_idx[atomicAdd(fix_count, 1)] = static_cast<int>(st.m);
+            }
+        };
         // Plane addresses: row `row` of panel g, 16-byte unit u at
         // (u ^ (row & 7)) << 4.  Chunk k (units 2k, 2k+1): unit 2k + i sits at
         // pa_i ^ (k << 5); chain and plane are immediate offsets.
@@ -579,6 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 load_row64(st.m, x);
             }
             st.sb ^= 1u;  // (the other buffer: the current one was read at the boundary)
+            st.flagged = false;
             const uint32_t mA = block_max_in(C, st.sb, x);  // (also orders tile reads before plane writes)
             const int t = scale_exp(mA);
             K3H_MARK(4);
@@ -616,7 +585,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // ---- boundary: 2^pe * D -> the old home's tiles (its planes
                     // are dead; the IO warp stores them), then the next input,
                     // already in the spare, -> step 0 there
-                    (void)slots_max(C, st);  // consume the last step's maxima (keeps the parities in step)
+                    {  // the last step's maxima: did the product feeding this one cancel?
+                        const uint32_t mlast = slots_max(C, st);
+                        flag_range(st, ilogb_bits(mlast) + st.t_prev, mlast);
+                    }
                     const uint64_t g1 = splat2(exp2i(pe / 2)), g2 = splat2(exp2i(pe - pe / 2));
                     const uint32_t old_region = s0 + st.home * kChainSmem;
 #pragma unroll
@@ -670,6 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t mprev = slots_max(C, st);
                 const int pmax_e = ilogb_bits(mprev) + st.t_prev;  // floor(log2 max|P'_s|)
                 const bool exact = pmax_e < kCeil - 12;
+                flag_range(st, pmax_e, mprev);
                 const int xmax_e = was_mult ? st.bmax_e : pmax_e;
                 int t = kCeil - static_cast<int>(lg_n) - (xmax_e + 1) - (pmax_e + 1);
                 if (mprev == 0u || mprev >= 0x7F800000u) t = 0;  // zero / non-finite operand
@@ -785,7 +758,7 @@ cudaError_t prepare_k3h_kernel() {
 
 cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch,
                                const PlanBits& plan, int grid, unsigned long long* stamps,
-                               cudaStream_t s) {
+                               int* fix_idx, int* fix_count, cudaStream_t s) {
     if (plan.len < 1 || n < 1 || n > kSmallMax) return cudaErrorInvalidValue;
     if (grid > batch) grid = static_cast<int>(batch);
     CUtensorMap in_map, out_map;
@@ -800,10 +773,10 @@ cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch
         vec = 0;
     if (plan.mult[0] | plan.mult[1])
         k3h_batched_power<true><<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec,
-                                                               stamps);
+                                                               stamps, fix_idx, fix_count);
     else
         k3h_batched_power<false><<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan,
-                                                                vec, stamps);
+                                                                vec, stamps, fix_idx, fix_count);
     return cudaGetLastError();
 }
 

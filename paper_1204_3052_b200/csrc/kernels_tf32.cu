@@ -42,11 +42,18 @@ int k3_route(int n, const PlanBits& plan) {
 
 cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
                               const PlanBits& plan, int grid, unsigned long long* stamps,
-                              int* variant, cudaStream_t s) {
+                              int* variant, int* fix, cudaStream_t s) {
     const int v = k3_route(n, plan);
     if (variant) *variant = v;
-    if (v == 0) return launch_k3h_batched(in, out, n, batch, plan, grid, stamps, s);
-    return launch_k3b_batched(in, out, n, batch, plan, grid, s);
+    if (v != 0) return launch_k3b_batched(in, out, n, batch, plan, grid, s);
+    if (fix == nullptr) return launch_k3h_batched(in, out, n, batch, plan, grid, stamps, nullptr, nullptr, s);
+    cudaError_t e = cudaMemsetAsync(fix, 0, sizeof(int), s);
+    if (e == cudaSuccess)
+        e = launch_k3h_batched(in, out, n, batch, plan, grid, stamps, fix + 1, fix, s);
+    // the matrices K3H listed are recomputed on K3B (bf16x3 planes carry an
+    // exponent per element); an empty list makes this launch a no-op
+    if (e == cudaSuccess) e = launch_k3b_batched(in, out, n, batch, plan, grid, s, fix + 1, fix);
+    return e;
 }
 
 // ======================================================================
@@ -1029,6 +1036,16 @@ static cudaError_t prepare_k1c() {
     return e;
 }
 
+// 64-column tiles when twice the clusters still fit one wave
+bool k1c_narrow(int n_pad, int splits) {
+    const int tiles = (n_pad / 128) * (n_pad / 128);
+    int dev = 0, num_sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    return splits >= 1 && splits <= 8 && 2 * tiles <= k1_max_clusters(splits) &&
+           2 * tiles * splits <= num_sms;
+}
+
 // One launch for the whole chain.  Its grid barrier needs every CTA resident
 // at once: guaranteed by construction (tiles x splits clusters <= one wave of
 // cudaOccupancyMaxActiveClusters, one CTA per SM, checked above).  The
@@ -1050,8 +1067,8 @@ cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
     int dev = 0, num_sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    const bool narrow = 2 * tiles <= k1_max_clusters(splits) &&
-                        2 * tiles * splits <= num_sms;
+    const bool narrow = k1c_narrow(n_pad, splits);
+    (void)num_sms;
     K1CMaps maps;
     K1CPlanes pl;
     for (int i = 0; i < 6; ++i) {

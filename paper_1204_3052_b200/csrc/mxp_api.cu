@@ -223,6 +223,9 @@ struct mxp_handle_s {
     // at the start and the end of CTA 0 (mxp_last_kernel_clock)
     unsigned long long* stamps = nullptr;
     bool stamps_valid = false;
+    // K3H's dynamic-range fixup list: fix[0] = count, fix[1 ..] matrix indices
+    int* fix = nullptr;
+    int64_t fix_cap = 0;
     // host-API staging device buffers
     size_t io_bytes = 0;
     void* d_in = nullptr;
@@ -372,10 +375,10 @@ int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float
     rc = encode_ws32(h, h->ws32_pad);
     if (rc) return rc;
     const int np = (int)h->ws32_pad;  // planes are laid out with the workspace stride
+    const int bn = k1_block_n(np, h->num_sms);
     cudaError_t e = launch_split(dA, (int)n, (int)n, h->planes[0], h->planes[1], np, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "split");
     ++*launches;
-    const int bn = k1_block_n(np, h->num_sms);
     if (bn == 128) {
         // the whole chain in one launch when every split-K cluster fits at once
         e = launch_k1c_chain(h->map_a, h->map_b, h->planes, plan, np, h->splits, dOut, (int)n,
@@ -453,14 +456,15 @@ int enqueue_power(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA, 
     const PlanBits plan = make_plan(k);
     if (mode == MXP_F32) {
         if (n <= kSmallMax) {
+            int variant = -1;
             cudaError_t e = launch_k3_batched(static_cast<const float*>(dA),
                                               static_cast<float*>(dOut), (int)n, 1, plan, 1,
-                                              nullptr, nullptr, h->stream);
+                                              nullptr, &variant, h->fix, h->stream);
             if (e != cudaSuccess) {
                 *failed = 0;
                 return cuda_fail(e, "k3_batched_power");
             }
-            ++*launches;
+            *launches += (variant == 0) ? 2 : 1;  // K3H + its (usually empty) K3B fixup pass
             return MXP_OK;
         }
         return enqueue_chain_f32(h, n, plan, static_cast<const float*>(dA),
@@ -652,6 +656,11 @@ int mxp_create(int device, mxp_handle* out) {
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
     if (e == cudaSuccess) e = cudaMalloc(&h->bar_ctr, 256);
     if (e == cudaSuccess) e = cudaMalloc(&h->stamps, 64);
+    if (e == cudaSuccess) e = cudaMalloc(&h->fix, (1 + 1024) * sizeof(int));
+    if (e == cudaSuccess) {
+        h->fix_cap = 1024;
+        e = cudaMemset(h->fix, 0, sizeof(int));
+    }
     if (e == cudaSuccess)
         e = cudaHostAlloc(reinterpret_cast<void**>(&h->progress_host), 64, cudaHostAllocMapped);
     if (e == cudaSuccess)
@@ -673,6 +682,7 @@ int mxp_destroy(mxp_handle h) {
         if (p) cudaFree(p);
     if (h->bar_ctr) cudaFree(h->bar_ctr);
     if (h->stamps) cudaFree(h->stamps);
+    if (h->fix) cudaFree(h->fix);
     if (h->progress_host) cudaFreeHost(h->progress_host);
     for (auto p : h->f64buf)
         if (p) cudaFree(p);
@@ -1172,16 +1182,24 @@ int mxp_power_batched_device(mxp_handle h, int mode, int64_t n, int64_t batch, i
         return rc;
     }
     if (mode == MXP_F32 && n <= kSmallMax) {
+        if (batch > h->fix_cap) {  // the fixup list holds up to one entry per matrix
+            MXP_CUDA(cudaStreamSynchronize(h->stream));
+            MXP_CUDA(cudaFree(h->fix));
+            h->fix = nullptr;
+            h->fix_cap = 0;
+            MXP_CUDA(cudaMalloc(&h->fix, static_cast<size_t>(1 + batch) * sizeof(int)));
+            h->fix_cap = batch;
+        }
         int variant = -1;
         cudaError_t e = launch_k3_batched(static_cast<const float*>(dA), static_cast<float*>(dOut),
                                           (int)n, batch, make_plan(k), h->num_sms, h->stamps,
-                                          &variant, h->stream);
+                                          &variant, h->fix, h->stream);
         if (e != cudaSuccess) {
             if (st) st->failed_step = 0;
             return cuda_fail(e, "k3_batched_power");
         }
         h->stamps_valid = (variant == 0);
-        if (st) st->launches = 1;
+        if (st) st->launches = (variant == 0) ? 2 : 1;
         return MXP_OK;
     }
     // n > 128 (or fp64): one chain per matrix, enqueued back to back.
@@ -1363,6 +1381,17 @@ int mxp_small_kernel_for(int64_t n, int64_t k, int* kernel) {
     if (n < 1 || n > kSmallMax || k < 2)
         return fail(MXP_E_VALIDATION, "needs 1 <= n <= %d and k >= 2", kSmallMax);
     *kernel = k3_route(static_cast<int>(n), make_plan(k)) == 0 ? MXP_KERNEL_K3H : MXP_KERNEL_K3B;
+    return MXP_OK;
+}
+
+int mxp_last_small_fixups(mxp_handle h, int64_t* count) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (!count) return fail(MXP_E_VALIDATION, "null output pointer");
+    int c = 0;
+    MXP_CUDA(cudaStreamSynchronize(h->stream));
+    MXP_CUDA(cudaMemcpy(&c, h->fix, sizeof c, cudaMemcpyDeviceToHost));
+    *count = c;
     return MXP_OK;
 }
 

@@ -33,20 +33,30 @@ cudaError_t prepare_kernels();
 // its start and end into stamps[0..3] (the in-kernel SM clock of the launch).
 constexpr int kSmallMax = 128;
 int k3_route(int n, const PlanBits& plan);
+// fix (device, 1 + batch ints, may be null): the dynamic-range fixup list of
+// K3H (count at fix[0]); when given, a K3B pass over the listed matrices is
+// enqueued after K3H (two launches; the second exits at once when the list
+// is empty).
 cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
                               const PlanBits& plan, int grid, unsigned long long* stamps,
-                              int* variant, cudaStream_t s);
+                              int* variant, int* fix, cudaStream_t s);
 // K3B (kernels_k3b.cu): two chains per SM, bf16x3 split.
 size_t k3b_smem_bytes();
 cudaError_t prepare_k3b_kernel();
+// idx/count (device, may be null): recompute only matrices idx[0 .. *count)
 cudaError_t launch_k3b_batched(const float* in, float* out, int n, int64_t batch,
-                               const PlanBits& plan, int grid, cudaStream_t s);
+                               const PlanBits& plan, int grid, cudaStream_t s,
+                               const int* idx = nullptr, const int* count = nullptr);
 // K3H (kernels_k3h.cu): two chains per SM, scaled fp16x2 split.
 size_t k3h_smem_bytes();
 cudaError_t prepare_k3h_kernel();
+// fix_idx/fix_count (device, may be null): matrices whose chain hit strong
+// cancellation (a product more than 2^12 below its bound, where the fp16
+// planes' range loses entries a later product depends on) are appended to
+// fix_idx for K3B to recompute (launch_k3_batched enqueues that pass).
 cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch,
                                const PlanBits& plan, int grid, unsigned long long* stamps,
-                               cudaStream_t s);
+                               int* fix_idx, int* fix_count, cudaStream_t s);
 
 // fp32 (n x n, leading dim ld) -> tf32 hi/lo planes (n_pad x n_pad, zero pad).
 cudaError_t launch_split(const float* in, int n, int ld, uint32_t* hi, uint32_t* lo, int n_pad,
@@ -108,6 +118,8 @@ cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
 // device fault so the host can name the failing plan step); trap != 0 then
 // executes a trap (the fault-injection test hook)
 cudaError_t launch_progress_mark(uint32_t* progress, uint32_t value, int trap, cudaStream_t s);  // kernel launches one split-K multiply takes
+// whether K1C runs the chain on 64-column tiles (2 x tiles x splits CTAs in one wave)
+bool k1c_narrow(int n_pad, int splits);
 cudaError_t launch_split_rows(const float* in, int n, int ld, int rows, uint32_t* hi, uint32_t* lo,
                               int n_pad, int rows_pad, cudaStream_t s);
 

@@ -323,6 +323,12 @@ class Engine:
                                              ctypes.c_uint64(seed0 & (2**64 - 1)), lo, hi, scale,
                                              ctypes.c_void_p(d_out)), "mxp_random_device")
 
+    def last_small_fixups(self) -> int:
+        """Matrices of the last n <= 128 launch that K3B recomputed (dynamic range)."""
+        c = ctypes.c_int64()
+        _lib.check(self._L.mxp_last_small_fixups(self._h, ctypes.byref(c)), "mxp_last_small_fixups")
+        return c.value
+
     def last_kernel_clock(self):
         """(sm_mhz, kernel_ms) of the last batched K3H launch, measured in the
         kernel (clock64 / globaltimer of CTA 0)."""

@@ -450,11 +450,19 @@ def test_row_sharded_chain_single_rank_nccl():
     os.environ.setdefault("MASTER_PORT", "29533")
     dist.init_process_group("nccl", rank=0, world_size=1)
     try:
+        # the row blocks run K1 (3xTF32, split-K 4 at n = 512): bitwise the plan
+        # executed one public multiply (mxp_gemm, same K1 arithmetic) at a time
         a = torch.from_numpy(oracle.scaled_input(512, np.float32, 42)).cuda()
         got = D.exponentiate_row_sharded(a, 1000)
         torch.cuda.synchronize()
-        ref = mx.Engine(0).power(a.cpu().numpy(), 1000)
-        assert np.array_equal(got.cpu().numpy(), ref)  # bitwise: same kernels, same order
+        eng = mx.Engine(0)
+        acc, tmp = a.clone(), torch.empty_like(a)
+        for step in mx.plan_exponentiation(1000).steps:
+            eng.gemm_device(acc.data_ptr(), (acc if step is mx.Step.SQUARE else a).data_ptr(),
+                            tmp.data_ptr(), 512)
+            acc, tmp = tmp, acc
+        eng.synchronize()
+        assert torch.equal(got, acc)  # bitwise: same kernels, same order
         batch = torch.from_numpy(mx.scaled_batch(64, 10, mx.DType.F32, 1)).cuda()
         out = D.exponentiate_batched_sharded(batch, 64)
         torch.cuda.synchronize()
@@ -539,12 +547,12 @@ def test_batched_mixed_magnitudes_and_schedule_edges():
 
 
 # ------------------------------------------------- one-launch chain (K1C)
-@pytest.mark.parametrize("n,k", [(130, 7), (256, 64), (384, 33), (512, 1000), (896, 9), (1300, 13)])
+@pytest.mark.parametrize("n,k", [(384, 33), (600, 7), (896, 9), (1300, 13)])
 def test_one_launch_chain_bitwise_equals_single_multiplies(eng, n, k):
-    """K1C runs the whole chain in one launch; it must be bitwise the same as
-    the plan executed one public multiply at a time (mxp_gemm: split, one K1
-    GEMM with the same split-K and reduction order, fp32 out), following
-    expo.py:131-138 with the accumulator on the left."""
+    """K1C (the 3xTF32 one-launch chain: n_pad 384, 640, 896, 1408 here) must
+    be bitwise the same as the plan executed one public multiply at a time
+    (mxp_gemm: split, one K1 GEMM with the same split-K and reduction order,
+    fp32 out), following expo.py:131-138 with the accumulator on the left."""
     import torch
 
     a = torch.from_numpy(oracle.scaled_input(n, np.float32, 42)).cuda()
@@ -760,3 +768,76 @@ def test_router_threshold_both_kernels_meet_tolerance(eng, k, kernel):
     tol = mx.fro_tol(n, k, "f32")
     for i in range(batch):
         assert fro(out[i], ref[i]) <= tol, (k, i, fro(out[i], ref[i]), tol)
+
+
+@pytest.mark.parametrize("n", [64, 128, 384, 512])  # K3H, K3H, K1C, K1C
+def test_chain_strong_cancellation(eng, n):
+    """A nilpotent-plus-small input: A = N + eps*R with N^2 = 0, so A^2 ~ eps
+    and A^6 depends on entries ~eps^2 below the matrix max.  The 3xTF32
+    chains keep an exponent per element; K3H's scaled fp16 planes keep one per
+    matrix and would lose those entries (A^6 came out 50% wrong before the
+    fixup, profiles/r02_cancellation_probe.txt), so K3H lists the matrix and
+    K3B recomputes it.  Reference: the CPU fp32 chain's own distance from the
+    exact result, with the reference's 64x device slack (tolerances.py:316-319)."""
+    rng = np.random.default_rng(5)
+    nil = np.zeros((n, n))
+    nil[: n // 2, n // 2:] = rng.uniform(-1, 1, (n // 2, n // 2))
+    a = (nil + 1e-6 * rng.uniform(-1, 1, (n, n))).astype(np.float32)
+    bad = []
+    for k in (2, 3, 6, 7):
+        got = eng.power(a, k)
+        if n <= 128 and k > 2:
+            assert eng.last_small_fixups() == 1, (n, k)
+        ref = oracle.exponentiate(a, k, oracle.max_threads())
+        exact = np.linalg.matrix_power(a.astype(np.float64), k)
+        tol = max(mx.fro_tol_conditioned(n, k, "f32"), 64 * fro(ref, exact))
+        if not fro(got, exact) <= tol:
+            bad.append((k, fro(got, exact), fro(ref, exact), tol))
+    assert not bad, (n, bad)
+
+
+def test_small_n_fixup_inside_a_batch(eng):
+    """Every 50th matrix of a random 128^2 batch is the cancelling construction:
+    exactly those are recomputed, and every matrix meets its tolerance."""
+    n, batch, k = 128, 600, 6
+    stack = mx.scaled_batch(n, batch, mx.DType.F32, 77).astype(np.float64)
+    rng = np.random.default_rng(9)
+    special = list(range(3, batch, 50))
+    for i in special:
+        nil = np.zeros((n, n))
+        nil[: n // 2, n // 2:] = rng.uniform(-1, 1, (n // 2, n // 2))
+        stack[i] = nil + 1e-6 * rng.uniform(-1, 1, (n, n))
+    stack = stack.astype(np.float32)
+    d_in, d_out = eng.alloc(stack.nbytes), eng.alloc(stack.nbytes)
+    try:
+        eng.upload(d_in, stack)
+        eng.power_batched_device(d_in, d_out, n, batch, k)
+        out = np.empty_like(stack)
+        eng.download(out, d_out)
+        assert eng.last_small_fixups() == len(special)
+        assert eng.last_stats.launches == 2
+    finally:
+        eng.free(d_in)
+        eng.free(d_out)
+    ref = oracle.exponentiate_batched(stack, k, oracle.max_threads())
+    for i in range(batch):
+        if i in special:
+            exact = np.linalg.matrix_power(stack[i].astype(np.float64), k)
+            tol = max(mx.fro_tol_conditioned(n, k, "f32"), 64 * fro(ref[i], exact))
+            assert fro(out[i], exact) <= tol, (i, fro(out[i], exact), tol)
+        else:
+            assert fro(out[i], ref[i]) <= mx.fro_tol(n, k, "f32"), i
+
+
+def test_one_launch_chain_zero_nan_identity(eng):
+    """K1C edge inputs: a zero matrix, the identity to a high power (exact), and
+    a NaN that must propagate where the reference's does."""
+    z = np.zeros((512, 512), np.float32)
+    assert not eng.power(z, 13).any()
+    i = np.eye(300, dtype=np.float32)
+    assert np.array_equal(eng.power(i, 1000), i)  # exact: powers of two only
+    a = oracle.scaled_input(256, np.float32, 3)
+    a[7, 9] = np.nan
+    got = eng.power(a, 3)
+    assert np.array_equal(np.isnan(got), np.isnan(oracle.exponentiate(a, 3)))
+

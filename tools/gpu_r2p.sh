@@ -1,0 +1,4 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT"
+O=gpurun_out/$1; mkdir -p $O
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "cancellation" --timeout 600 -s > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
