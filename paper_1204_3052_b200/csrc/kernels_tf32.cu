@@ -45,6 +45,9 @@ cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
                               int* variant, int* fix, cudaStream_t s) {
     const int v = k3_route(n, plan);
     if (variant) *variant = v;
+#ifdef MXP_K3_NO_FIXUP  // A/B builds only (tools/c3_variants.sh)
+    fix = nullptr;
+#endif
     if (v != 0) return launch_k3b_batched(in, out, n, batch, plan, grid, s);
     if (fix == nullptr) return launch_k3h_batched(in, out, n, batch, plan, grid, stamps, nullptr, nullptr, s);
     cudaError_t e = cudaMemsetAsync(fix, 0, sizeof(int), s);

@@ -583,10 +583,15 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 // rna (round to nearest, ties away from zero) on the bit pattern: add half an
 // ulp of the 10-bit mantissa (0x1000) and clear the 13 dropped bits.  Exact
 // for finite values (carry into the exponent is the correct rounding, and
-// overflow rounds to inf); inf stays inf.  Two integer ops instead of the
-// ~5-instruction cvt.rna.tf32.f32 lowering.
+// overflow rounds to inf); inf stays inf.  NaNs are clamped to the quiet NaN
+// 0x7FC00000 first: the GPU's arithmetic NaN is 0x7FFFFFFF, whose +0x1000
+// would carry into the sign bit and turn it into -0 (a NaN in a chain's
+// product vanished that way — test_one_launch_chain_zero_nan_identity).
+// Four integer ops instead of the ~5-instruction cvt.rna.tf32.f32 lowering.
 __device__ __forceinline__ uint32_t cvt_tf32(float x) {
-    return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+    const uint32_t b = __float_as_uint(x);
+    const uint32_t r = min(b & 0x7FFFFFFFu, 0x7FC00000u) + 0x1000u;
+    return (r & 0xFFFFE000u) | (b & 0x80000000u);
 }
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
     hi = cvt_tf32(x);
