@@ -841,3 +841,53 @@ def test_one_launch_chain_zero_nan_identity(eng):
     got = eng.power(a, 3)
     assert np.array_equal(np.isnan(got), np.isnan(oracle.exponentiate(a, 3)))
 
+
+
+# ------------------------------------------------------------------ structured inputs, every kernel
+def _structured(kind, n, rng):
+    if kind == "upper_triangular":          # nilpotent strictly-upper part + a small diagonal
+        a = np.triu(rng.uniform(-1, 1, (n, n)), 1) + np.diag(rng.uniform(-0.1, 0.1, n))
+    elif kind == "two_scales":              # blocks 2^30 apart, coupled weakly
+        a = rng.uniform(-1, 1, (n, n)) / np.sqrt(n)
+        a[n // 2:, n // 2:] *= 2.0 ** -30
+        a[: n // 2, n // 2:] *= 2.0 ** -15
+    elif kind == "rank_one":                # u v^T: A^k = (v.u)^(k-1) A
+        u, v = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+        a = np.outer(u, v) / abs(v @ u)
+    elif kind == "integer":                 # small integers: exact products while < 2^24
+        a = rng.integers(-1, 2, (n, n)).astype(np.float64) * (rng.uniform(0, 1, (n, n)) < 2.0 / n)
+    elif kind == "signed_permutation":
+        p = rng.permutation(n)
+        a = np.zeros((n, n))
+        a[np.arange(n), p] = rng.choice([-1.5, 0.75], n)
+    else:
+        raise ValueError(kind)
+    return a
+
+
+@pytest.mark.parametrize("n,dt", [(64, "f32"), (128, "f32"), (300, "f32"), (1024, "f32"), (256, "f64")])
+@pytest.mark.parametrize("kind", ["upper_triangular", "two_scales", "rank_one", "integer",
+                                  "signed_permutation"])
+def test_structured_inputs_every_kernel(eng, n, dt, kind):
+    """K3H/K3B (64, 128), K1C (300), K1P (1024) and K2 (f64): structured
+    matrices with cancellation, wide dynamic range, low rank, exact integer
+    products and permutations.  Criterion: no further from the exact result
+    than the reference's own CPU chain by more than the reference's 64x
+    device slack (tolerances.py:316-319), or inside the conditioned chain
+    tolerance."""
+    import zlib
+
+    rng = np.random.default_rng(zlib.crc32(f"{kind}-{n}".encode()))
+    npd = np.float32 if dt == "f32" else np.float64
+    a = _structured(kind, n, rng).astype(npd)
+    for k in (3, 8, 13):
+        got = eng.power(a, k)
+        ref = oracle.exponentiate(a, k, oracle.max_threads())
+        exact = np.linalg.matrix_power(a.astype(np.float64), k)
+        if not np.isfinite(exact).all():
+            continue
+        tol = max(mx.fro_tol_conditioned(n, k, dt), 64 * fro(ref, exact))
+        assert np.array_equal(np.isfinite(got), np.isfinite(ref)), (kind, k)
+        assert fro(got, exact) <= tol, (kind, n, k, fro(got, exact), fro(ref, exact), tol)
+        if kind in ("integer", "signed_permutation") and np.abs(exact).max() < 2 ** 20:
+            assert np.array_equal(got, exact.astype(npd)), (kind, k)  # exact arithmetic

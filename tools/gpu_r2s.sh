@@ -1,5 +1,5 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT"
 O=gpurun_out/$1; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "nan or cancellation or fixup or zero" --timeout 600 > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
-bash tools/c3_variants.sh $1
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "structured" --timeout 600 > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
+
