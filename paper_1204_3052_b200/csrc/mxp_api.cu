@@ -1261,19 +1261,25 @@ int mxp_power_batched(mxp_handle h, int mode, int64_t n, int64_t batch, int64_t 
         }
     }
     const size_t sb = h->stage_bytes;
-    cudaEvent_t in_ready[2], comp_done[2], out_done[2];
+    // the pipeline's events, destroyed on every exit path
+    struct Events {
+        cudaEvent_t in_ready[2] = {}, comp_done[2] = {}, out_done[2] = {};
+        ~Events() {
+            for (int i = 0; i < 2; ++i) {
+                if (in_ready[i]) cudaEventDestroy(in_ready[i]);
+                if (comp_done[i]) cudaEventDestroy(comp_done[i]);
+                if (out_done[i]) cudaEventDestroy(out_done[i]);
+            }
+        }
+    } ev;
+    cudaEvent_t* in_ready = ev.in_ready;
+    cudaEvent_t* comp_done = ev.comp_done;
+    cudaEvent_t* out_done = ev.out_done;
     for (int i = 0; i < 2; ++i) {
         MXP_CUDA(cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming));
         MXP_CUDA(cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming));
         MXP_CUDA(cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming));
     }
-    auto destroy_events = [&] {
-        for (int i = 0; i < 2; ++i) {
-            cudaEventDestroy(in_ready[i]);
-            cudaEventDestroy(comp_done[i]);
-            cudaEventDestroy(out_done[i]);
-        }
-    };
     const int64_t nchunks = (batch + chunk - 1) / chunk;
     auto chunk_len = [&](int64_t c) -> size_t {
         const int64_t b0 = c * chunk;
@@ -1317,7 +1323,6 @@ int mxp_power_batched(mxp_handle h, int mode, int64_t n, int64_t batch, int64_t 
         if (rc) {
             cudaStreamSynchronize(h->copy_in);
             cudaStreamSynchronize(h->copy_out);
-            destroy_events();
             if (st) st->failed_step = inner.failed_step;
             return rc;
         }
@@ -1345,7 +1350,6 @@ int mxp_power_batched(mxp_handle h, int mode, int64_t n, int64_t batch, int64_t 
         MXP_CUDA(cudaEventRecord(h->ev1, h->stream));
         err = cudaStreamSynchronize(h->stream);
     }
-    destroy_events();
     if (err != cudaSuccess) return cuda_fail(err, "batched power");
     if (st) {
         fill_plan_stats(st, k, batch);
