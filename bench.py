@@ -590,6 +590,7 @@ def main() -> None:
             # driver's evidence that N ranks ran
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout keeps the one JSON line
             tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = tdist
         one = torch.ones(1, device="cuda") if not share else torch.ones(1)
