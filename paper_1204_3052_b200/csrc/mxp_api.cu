@@ -1184,6 +1184,7 @@ int mxp_power_batched_device(mxp_handle h, int mode, int64_t n, int64_t batch, i
     if (mode == MXP_F32 && n <= kSmallMax) {
         if (batch > h->fix_cap) {  // the fixup list holds up to one entry per matrix
             MXP_CUDA(cudaStreamSynchronize(h->stream));
+            h->drop_graphs();  // captured n <= 128 chains point at the old list
             MXP_CUDA(cudaFree(h->fix));
             h->fix = nullptr;
             h->fix_cap = 0;

@@ -891,3 +891,18 @@ def test_structured_inputs_every_kernel(eng, n, dt, kind):
         assert fro(got, exact) <= tol, (kind, n, k, fro(got, exact), fro(ref, exact), tol)
         if kind in ("integer", "signed_permutation") and np.abs(exact).max() < 2 ** 20:
             assert np.array_equal(got, exact.astype(npd)), (kind, k)  # exact arithmetic
+
+
+def test_small_n_graph_survives_fixup_list_growth():
+    """A cached n <= 128 chain graph holds the handle's fixup list; a batched
+    launch larger than the list reallocates it, which must drop the graphs
+    (a replay would otherwise write through a freed pointer)."""
+    eng = mx.Engine(0)
+    a = oracle.scaled_input(64, np.float32, 4)
+    want = eng.power(a, 13)
+    assert eng.power(a, 13).tobytes() == want.tobytes()  # cached graph
+    big = mx.scaled_batch(64, 3000, mx.DType.F32, 1)  # > the initial 1024-entry list
+    eng.power_batched(big, 13)
+    for _ in range(3):
+        assert eng.power(a, 13).tobytes() == want.tobytes()
+    eng.synchronize()
