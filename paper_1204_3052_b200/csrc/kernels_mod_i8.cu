@@ -18,9 +18,9 @@
 //
 // Operands straight from the row-major byte planes: A K-major (TMA
 // SWIZZLE_64B, 64 k per row), B MN-major (TMA SWIZZLE_64B, 64 n per k-row);
-// operand layouts and the 49-cycle M128 N64 K32 rate (SMEM-operand-bound:
-// 6 KB of operands per MMA at 128 B/cycle) measured with tools/i8_probe.cu
-// (profiles/r02_i8_probe.txt).
+// operand layouts and the 49-cycle M128 N64 K32 rate measured with
+// tools/i8_probe.cu (profiles/r02_i8_probe.txt; reading A from TMEM instead
+// only gets it to 44.5 cycles).
 #include <cstring>
 
 #include "mxp_internal.h"

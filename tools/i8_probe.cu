@@ -3,6 +3,7 @@
 //   V1: A K-major SWIZZLE_128B, B MN-major SWIZZLE_64B (N = 64)
 //   V2: A K-major SWIZZLE_128B, B K-major SWIZZLE_128B (B^T rows, N = 64)
 //   V3: A K-major SWIZZLE_128B, B MN-major SWIZZLE_128B (N = 128)
+//   V4: as V1 with A copied into TMEM (tcgen05.cp 128x256b) and read from there (TS)
 // Each: D = A[128 x 128] * B[128 x N] (4 MMAs of K = 32) vs a host int matmul.
 // Then the issue rate of 256 back-to-back MMAs (N = 64 and N = 128).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 -I include \
@@ -26,6 +27,18 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint3
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
+}
+
+__device__ __forceinline__ void mma_i8_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                          uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
 }
 
 template <int N, bool kBMN>
@@ -55,7 +68,7 @@ __global__ void probe_kernel(const __grid_constant__ Maps m, int* out, long long
         mbar_init(bar + 1, 1);
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc<128>(slot);
+    if (warp == 0) tmem_alloc<512>(slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -64,7 +77,7 @@ __global__ void probe_kernel(const __grid_constant__ Maps m, int* out, long long
         const uint32_t bbytes = (V == 2) ? N * 128 : 128 * N;
         mbar_expect_tx(bar, 16384 + bbytes);
         tma_load_2d(sa, &m.a, bar, 0, 0);
-        if (V == 1) {
+        if (V == 1 || V == 4) {
             tma_load_2d(sb, &m.b, bar, 0, 0);           // box {64 N, 128 K}
         } else if (V == 2) {
             tma_load_2d(sb, &m.b, bar, 0, 0);           // box {128 K, 64 N}
@@ -75,6 +88,21 @@ __global__ void probe_kernel(const __grid_constant__ Maps m, int* out, long long
         tc_fence_after();
         const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
         constexpr uint32_t idesc = idesc_i8<N, V != 2>();
+        if (V == 4) {
+            // A -> TMEM columns 256 + 8 ks (128 lanes x 32 bytes per K=32 step)
+            for (int k = 0; k < 4; ++k) tmem_cp_128x256b(tmem + 256 + 8 * k, smem_desc(a0 + 32 * k, 16, 1024, 2));
+            for (int k = 0; k < 4; ++k)
+                mma_i8_ts(tmem, tmem + 256 + 8 * k, smem_desc(b0 + 2048 * k, 8192, 512, 4), idesc, k > 0);
+            mma_commit(bar + 1);
+            mbar_wait(bar + 1, 0);
+            const long long t0 = clock64();
+            for (int r = 0; r < 64; ++r)
+                for (int k = 0; k < 4; ++k)
+                    mma_i8_ts(tmem, tmem + 256 + 8 * k, smem_desc(b0 + 2048 * k, 8192, 512, 4), idesc, 1);
+            mma_commit(bar + 1);
+            mbar_wait(bar + 1, 1);
+            cycles[0] = clock64() - t0;
+        } else {
         for (int k = 0; k < 4; ++k) {
             const uint64_t ad = smem_desc(a0 + 32 * k, 16, 1024, 2);
             uint64_t bd;
@@ -98,6 +126,7 @@ __global__ void probe_kernel(const __grid_constant__ Maps m, int* out, long long
         mma_commit(bar + 1);
         mbar_wait(bar + 1, 1);
         cycles[0] = clock64() - t0;
+        }
     }
     __syncthreads();
     tc_fence_after();
@@ -112,7 +141,7 @@ __global__ void probe_kernel(const __grid_constant__ Maps m, int* out, long long
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc<128>(tmem);
+    if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -153,7 +182,7 @@ static void run(const std::vector<uint8_t>& A, const std::vector<uint8_t>& B) {
     cudaMemcpy(dB, V == 2 ? Bt.data() : B.data(), 128 * N, cudaMemcpyHostToDevice);
     Maps m;
     map2d(&m.a, dA, 128, 128, 128, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-    if (V == 1) map2d(&m.b, dB, N, 128, N, 128, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (V == 1 || V == 4) map2d(&m.b, dB, N, 128, N, 128, CU_TENSOR_MAP_SWIZZLE_64B);
     else if (V == 2) map2d(&m.b, dB, 128, N, 128, N, CU_TENSOR_MAP_SWIZZLE_128B);
     else map2d(&m.b, dB, N, 128, N, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     cudaFuncSetAttribute(probe_kernel<N, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000);
@@ -199,5 +228,6 @@ int main() {
     run<64, 1>(A, B64);
     run<64, 2>(A, B64);
     run<128, 3>(A, B128);
+    run<64, 4>(A, B64);
     return 0;
 }
