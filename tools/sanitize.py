@@ -26,6 +26,17 @@ eng.power(oracle.scaled_input(384, np.float32, 42), 13)                 # K1C on
 eng.multiply(oracle.scaled_input(256, np.float32, 1), oracle.scaled_input(256, np.float32, 2))  # K1 cluster split-K
 eng.power(oracle.scaled_input(1024, np.float32, 42), 5)                 # K1P CTA pairs
 eng.power(oracle.scaled_input(256, np.float64, 42), 9)                  # FP64 DMMA
-eng.power_mod(np.arange(100 * 100, dtype=np.uint32).reshape(100, 100), 11, 65521)
+eng.power_mod(np.arange(100 * 100, dtype=np.uint32).reshape(100, 100), 11, 65521)  # K5I (INT8)
+eng.power_mod(np.arange(300 * 300, dtype=np.uint32).reshape(300, 300) * 7919, 6, 2**31 - 1)
 mx.random_matrix(33, mx.DType.F32, 5)
+mx.splitmix64(42, 1000)
+# K3H dynamic-range fixup: cancelling matrices inside a batch -> list-driven K3B pass
+rng = np.random.default_rng(5)
+stack = mx.scaled_batch(128, 300, mx.DType.F32, 3).astype(np.float64)
+for i in (0, 150, 299):
+    nil = np.zeros((128, 128))
+    nil[:64, 64:] = rng.uniform(-1, 1, (64, 64))
+    stack[i] = nil + 1e-6 * rng.uniform(-1, 1, (128, 128))
+mx.exponentiate_batched(stack.astype(np.float32), 6)
+print("fixups", mx.engine.default_engine(0).last_small_fixups())  # the engine exponentiate_batched used
 print("sanitize workload done")
