@@ -236,7 +236,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // idx != nullptr: recompute only the matrices listed in idx[0 .. *count)
     // (K3H's dynamic-range fixup, kernels_k3h.cu); matrix m of this launch is
     // matrix idx[m] of the caller's stack
-    if (idx != nullptr) batch = *count;
+    if (idx != nullptr) {
+        // launched as K3H's programmatic dependent: wait for K3H's list
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        batch = *count;
+        if (batch == 0) return;  // nothing listed: leave before any setup
+    }
     auto mat = [&](long long m) -> long long { return idx != nullptr ? idx[m] : m; };
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
@@ -539,9 +544,25 @@ cudaError_t launch_k3b_batched(const float* in, float* out, int n, int64_t batch
                   : 0;
     if (vec && !(encode_tile_map(&in_map, in, batch * 128) && encode_tile_map(&out_map, out, batch * 128)))
         vec = 0;
-    k3b_batched_power<<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec,
-                                                    idx, count);
-    return cudaGetLastError();
+    if (idx == nullptr) {
+        k3b_batched_power<<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec,
+                                                        idx, count);
+        return cudaGetLastError();
+    }
+    // the fixup pass: a programmatic dependent launch, so its launch latency
+    // overlaps K3H's tail (it waits for K3H with griddepcontrol.wait)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k3b_batched_power, in_map, out_map, in, out, n,
+                              static_cast<long long>(batch), plan, vec, idx, count);
 }
 
 }  // namespace mxp
