@@ -397,11 +397,17 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
 }
 
 // ======================================================================
-// K1P — the same GEMM step on CTA pairs (cta_group::2): a cluster of two
-// CTAs on one TPC computes a 256 x 256 tile with M = 256, N = 256 MMAs issued
-// by the leader.  Each CTA stages its own 128 rows of A and its own 128
-// columns of B (so per-SM shared-memory operand traffic is halved vs K1) and
-// holds its 128 x 256 share of the accumulator in its own TMEM.
+// K1P — the same GEMM step on CTA pairs (cta_group::2): two CTAs on one TPC
+// compute a 256 x 256 tile with M = 256, N = 256 MMAs issued by the pair's
+// leader.  Each CTA stages its own 128 rows of A and its own 128 columns of B
+// (so per-SM shared-memory operand traffic is halved vs K1) and holds its
+// 128 x 256 share of the accumulator in its own TMEM.
+// kPairs = 2: a cluster of two pairs on horizontally adjacent tiles (same A
+// rows).  The A planes are fed by TMA multicast: CTA (pair p, half h) loads
+// plane p of its 128 A rows once and the copy lands in both pairs' h-CTAs
+// (and completes on both pair leaders' barriers), so every SM pulls 48 of the
+// 64 KB per k-block from L2; each stage is released only after BOTH pairs'
+// MMAs have read it (the empty barrier counts one commit per pair).
 //   warp 0 : TMA producer (both CTAs; bytes complete on the leader's barrier)
 //   warp 1 : MMA issuer (leader only)     warp 2 : TMEM allocator (both)
 //   warps 4-11 : epilogue (both CTAs; lane quarter = warp % 4, 128-column half)
@@ -419,7 +425,8 @@ struct K1PCfg {
 };
 }  // namespace
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K1PCfg::kThreads, 1)
+template <int kPairs>
+__global__ void __launch_bounds__(K1PCfg::kThreads, 1)
     k1p_gemm_3xtf32(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                     const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
                     int n_pad, int m_pad, float* __restrict__ out_f32, int n_out, int m_out,
@@ -437,24 +444,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K1PCfg::kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_ctarank();
+    const uint32_t crank = cluster_ctarank();
+    const uint32_t rank = crank & 1;          // half of the pair (A rows, B columns)
+    const uint32_t pp = crank >> 1;           // pair within the cluster
+    const uint32_t pair_leader = crank & ~1u; // cluster rank of this pair's leader
     const bool leader = (rank == 0);
 
-    // pair tile raster (grouped along M, as K1)
+    // cluster tile raster (grouped along M, as K1); a cluster's pairs take
+    // kPairs adjacent N tiles of the same M tile
     constexpr int kGroupM = 8;
-    const int num_m = m_pad / 256, num_n = n_pad / 256;
-    const int pid = blockIdx.x >> 1;
-    const int per_group = kGroupM * num_n;
+    const int num_m = m_pad / 256, num_nc = n_pad / (256 * kPairs);
+    const int pid = blockIdx.x / (2 * kPairs);
+    const int per_group = kGroupM * num_nc;
     const int first_m = (pid / per_group) * kGroupM;
     const int gm = min(num_m - first_m, kGroupM);
     const int m0 = (first_m + (pid % per_group) % gm) * 256 + static_cast<int>(rank) * 128;
-    const int n0 = ((pid % per_group) / gm) * 256;
+    const int n0 = (((pid % per_group) / gm) * kPairs + static_cast<int>(pp)) * 256;
     const int num_kb = n_pad / 32;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
+            mbar_init(&empty[i], kPairs);  // one MMA commit per pair reading the stage
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&cfull[i], 1);
@@ -480,8 +491,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K1PCfg::kThreads, 1)
             mbar_wait(&empty[st], ph ^ 1);
             uint8_t* base = smem + st * Cfg::kStageBytes;
             if (leader) mbar_expect_tx(&full[st], 2 * Cfg::kStageBytes);
-            tma_load_2d_pair(base, &ma_hi, &full[st], kb * 32, m0);
-            tma_load_2d_pair(base + Cfg::kABytes, &ma_lo, &full[st], kb * 32, m0);
+#ifdef MXP_K1P_NO_MC
+            if constexpr (true) {
+#else
+            if constexpr (kPairs == 1) {
+#endif
+                tma_load_2d_pair(base, &ma_hi, &full[st], kb * 32, m0);
+                tma_load_2d_pair(base + Cfg::kABytes, &ma_lo, &full[st], kb * 32, m0);
+            } else {
+                // plane pp of these A rows, multicast to this half of both pairs
+                const uint16_t amask = static_cast<uint16_t>(0x5u << rank);
+                tma_load_2d_pair_mc(base + pp * Cfg::kABytes, pp ? &ma_lo : &ma_hi, &full[st],
+                                    kb * 32, m0, amask);
+            }
             uint8_t* bh = base + 2 * Cfg::kABytes;
             uint8_t* bl = bh + Cfg::kBBytes;
             const int nb = n0 + static_cast<int>(rank) * 128;
@@ -517,14 +539,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K1PCfg::kThreads, 1)
                 const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((1024 * k) >> 4);
                 mma_tf32_pair(d, da_hi + ao, db_hi + bo, kIdesc, 1u);
             }
-            mma_commit_pair(&empty[st]);
-            mma_commit_pair(&cfull[c]);
+            // the stage's A planes were multicast by both pairs' producers:
+            // release it in every CTA of the cluster
+            mma_commit_pair(&empty[st], static_cast<uint16_t>((1u << (2 * kPairs)) - 1));
+            mma_commit_pair(&cfull[c], static_cast<uint16_t>(0x3u << pair_leader));
         }
     } else if (warp >= 4) {
         const int q = warp & 3;
         const int ch = ((warp - 4) >> 2) * 128;  // column half of the 256
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
-        const uint32_t cempty_leader0 = mapa_shared(smem_u32(&cempty[0]), 0);
+        const uint32_t cempty_leader0 = mapa_shared(smem_u32(&cempty[0]), pair_leader);
         float sum[128];
 #pragma unroll
         for (int i = 0; i < 128; ++i) sum[i] = 0.f;
@@ -707,8 +731,13 @@ cudaError_t prepare_tf32_kernels() {
                                          static_cast<int>(K1Cfg::kSmem));
     if (e == cudaSuccess) e = prepare_k1c();
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k1p_gemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(k1p_gemm_3xtf32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(K1PCfg::kSmem));
+#if MXP_K1P_MAX_PAIRS >= 2
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k1p_gemm_3xtf32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(K1PCfg::kSmem));
+#endif
     return e;
 }
 
@@ -1121,15 +1150,45 @@ cudaError_t launch_progress_mark(uint32_t* progress, uint32_t value, int trap, c
     return cudaGetLastError();
 }
 
+// K1P launch.  n_pad, m_pad multiples of 256.  The product launches single
+// pairs: a 4-CTA cluster geometry fits only 33 clusters (132 SMs) on the B200
+// against 74 pairs (148 SMs), and the A multicast does not buy back the 16 SMs
+// (profiles/r02_k1p_multicast.txt: 48.0 ms C5 vs 45.0 ms).  The two-pair
+// multicast build is the A/B variant: -DMXP_K1P_MAX_PAIRS=2
+// (tools/build_variant.py; -DMXP_K1P_NO_MC for the same clusters unicast).
+#ifndef MXP_K1P_MAX_PAIRS
+#define MXP_K1P_MAX_PAIRS 1
+#endif
+static cudaError_t launch_k1p(const GemmPlanes& m, int n_pad, int m_pad, float* out_f32, int n_out,
+                              int m_out, int ld_out, uint32_t* out_hi, uint32_t* out_lo,
+                              const PeerOut& po, cudaStream_t s) {
+    const int pairs = (MXP_K1P_MAX_PAIRS >= 2 && (n_pad / 256) % 2 == 0) ? 2 : 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * (n_pad / 256) * (m_pad / 256));
+    cfg.blockDim = dim3(K1PCfg::kThreads);
+    cfg.dynamicSmemBytes = K1PCfg::kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(2 * pairs);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+#if MXP_K1P_MAX_PAIRS >= 2
+    if (pairs == 2)
+        return cudaLaunchKernelEx(&cfg, k1p_gemm_3xtf32<2>, m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad,
+                                  m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo, po);
+#endif
+    return cudaLaunchKernelEx(&cfg, k1p_gemm_3xtf32<1>, m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad,
+                              m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo, po);
+}
+
 cudaError_t launch_k1p_gemm_peers(const GemmPlanes& m, int n_pad, int m_pad, int ld_out,
                                   const PeerOut& po, cudaStream_t s) {
     if (n_pad % 256 != 0 || m_pad % 256 != 0 || po.n < 1 || po.n > kMaxPeers)
         return cudaErrorInvalidValue;
-    dim3 grid(2 * (n_pad / 256) * (m_pad / 256));
-    k1p_gemm_3xtf32<<<grid, K1PCfg::kThreads, K1PCfg::kSmem, s>>>(
-        m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, nullptr, n_pad, m_pad, ld_out, nullptr,
-        nullptr, po);
-    return cudaGetLastError();
+    return launch_k1p(m, n_pad, m_pad, nullptr, n_pad, m_pad, ld_out, nullptr, nullptr, po, s);
 }
 
 namespace {
@@ -1187,11 +1246,8 @@ cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int b
                                   out_f32, n_out, m_out, ld_out, out_hi, out_lo, 1);
     }
     if (block_n == 256) {  // CTA-pair kernel: n_pad, m_pad multiples of 256
-        dim3 grid(2 * (n_pad / 256) * (m_pad / 256));
-        k1p_gemm_3xtf32<<<grid, K1PCfg::kThreads, K1PCfg::kSmem, s>>>(
-            m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, out_f32, n_out, m_out, ld_out, out_hi,
-            out_lo, PeerOut{});
-        return cudaGetLastError();
+        return launch_k1p(m, n_pad, m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo,
+                          PeerOut{}, s);
     }
     dim3 grid((n_pad / K1Cfg::kBN) * (m_pad / 128), 1);
     k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(

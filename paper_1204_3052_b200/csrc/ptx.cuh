@@ -486,6 +486,17 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
         "r"(smem_u32(bar) & kPeerBitMask)
         : "memory");
 }
+// the same box written into every CTA of `mask` (same SMEM offset); each
+// destination's bytes complete on its pair leader's barrier at `bar`'s offset
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                    int32_t c0, int32_t c1, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1),
+        "r"(smem_u32(bar) & kPeerBitMask), "h"(mask)
+        : "memory");
+}
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* slot) {  // one warp in EACH CTA
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -509,11 +520,13 @@ __device__ __forceinline__ void mma_tf32_pair(uint32_t d_tmem, uint64_t a_desc, 
         : "memory");
 }
 // commit the pair's MMAs to the barrier at this offset in both CTAs
-__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+// arrive on `bar` (same offset) in every CTA of `mask` once the issued MMAs
+// complete (0x3: both CTAs of the pair at cluster ranks 0/1)
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask = 0x3) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
         " [%0], %1;" ::"r"(smem_u32(bar)),
-        "h"(static_cast<uint16_t>(0x3))
+        "h"(mask)
         : "memory");
 }
 
