@@ -1,0 +1,8 @@
+#!/bin/bash
+# full GPU check: build artefacts travel; run gpu tests, smoke, bench
+cd "$GRAFT_REPO_ROOT"
+O=gpurun_out/$1; mkdir -p $O
+nvidia-smi > $O/smi.txt 2>&1
+timeout 2400 python -m pytest tests -m gpu -q -x --timeout 1200 > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
+timeout 600 python bench.py > $O/bench.json 2> $O/bench.err; echo "rc=$?" >> $O/bench.err
