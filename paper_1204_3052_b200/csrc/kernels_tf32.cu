@@ -814,13 +814,13 @@ struct K1CPlanes {
 };
 
 #ifdef K1C_TRACE  // tools/k1c_trace.cu: per-step phase stamps of CTA (0, 0)
-__device__ long long* g_k1c_trace;  // [step][8]
+__device__ long long* g_k1c_trace;  // [step][16]
 #define K1C_STAMP(k)                                                                       \
     do {                                                                                   \
         if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && step < 64) {  \
             long long t_;                                                                  \
             asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_) : : "memory");              \
-            g_k1c_trace[step * 8 + (k)] = t_;                                              \
+            g_k1c_trace[step * 16 + (k)] = t_;                                             \
         }                                                                                  \
     } while (0)
 #else
@@ -933,6 +933,7 @@ __global__ void __launch_bounds__(384, 1)
             // the planes this step reads were written by other CTAs' generic
             // stores before the grid barrier: order them before TMA (async proxy)
             asm volatile("fence.proxy.async.global;" ::: "memory");
+            K1C_STAMP(8);
             const CUtensorMap* ah = &maps.a[2 * acc];
             const CUtensorMap* al = &maps.a[2 * acc + 1];
             const CUtensorMap* bh_m = &maps.b[2 * rhs];
@@ -968,6 +969,7 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_wait(&cempty[c], ((g >> 1) & 1) ^ 1);
                 mbar_wait(&full[st], ph);
                 tc_fence_after();
+                K1C_STAMP(9 + kb);  // 9..12: k-block kb's operands landed
                 const uint64_t so = static_cast<uint64_t>((st * Cfg::kStageBytes) >> 4);
                 const uint32_t d = tmem + c * BN;
 #pragma unroll

@@ -2,7 +2,7 @@
 # C2 (512^2 A^1000, K1C) time with each library variant in tools/_variants/ and the product build
 cd "$GRAFT_REPO_ROOT"
 O=gpurun_out/$1; mkdir -p $O
-for rep in 1 2; do
+for rep in 1; do
 for lib in product tools/_variants/*.so; do
   if [ $lib = product ]; then unset MXP_LIB_PATH; else export MXP_LIB_PATH=$PWD/$lib; fi
   timeout 300 python -c "

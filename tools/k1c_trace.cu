@@ -19,7 +19,7 @@ int main(int argc, char** argv) {
     prepare_tf32_kernels();
     float *a, *out; uint32_t* planes[6]; unsigned int* ctr; long long* tr;
     cudaMalloc(&a, n * n * 4); cudaMalloc(&out, n * n * 4); cudaMalloc(&ctr, 256);
-    cudaMalloc(&tr, 64 * 8 * 8); cudaMemset(tr, 0, 64 * 8 * 8);
+    cudaMalloc(&tr, 64 * 16 * 8); cudaMemset(tr, 0, 64 * 16 * 8);
     cudaMemcpyToSymbol(g_k1c_trace, &tr, sizeof(tr));
     std::vector<float> h(n * n);
     uint32_t x = 1;
@@ -45,14 +45,14 @@ int main(int argc, char** argv) {
     cudaError_t e = cudaDeviceSynchronize();
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     printf("n=%d splits=%d err=%s chain %.1f us (%.2f us/step)\n", n, splits, cudaGetErrorString(e), ms * 1e3, ms * 1e3 / 14);
-    std::vector<long long> t(64 * 8);
+    std::vector<long long> t(64 * 16);
     cudaMemcpy(t.data(), tr, t.size() * 8, cudaMemcpyDeviceToHost);
-    printf("step: mainloop | partial->smem | csync1 | reduce | csync2 | grid barrier | (6->7) (7->next 0) | total (cycles)\n");
+    printf("step: mainloop | partial | csync1 | reduce | csync2 | grid bar | (6->7) (7->next 0) | total || tma issue, kb0..3 landed (from step start)\n");
     for (int s = 0; s < 14; ++s) {
-        const long long* r = &t[s * 8];
-        printf("%2d %c: %6lld %6lld %6lld %6lld %6lld %6lld | %6lld %6lld | %6lld\n", s, pat[s], r[1] - r[0], r[2] - r[1], r[3] - r[2],
-               r[4] - r[3], r[5] - r[4], s < 13 ? r[6] - r[5] : 0, r[7] - r[6], s < 13 ? t[(s + 1) * 8] - r[7] : 0,
-               s < 13 ? t[(s + 1) * 8] - r[0] : r[5] - r[0]);
+        const long long* r = &t[s * 16];
+        printf("%2d %c: %6lld %6lld %6lld %6lld %6lld %6lld | %6lld %6lld | %6lld || %6lld %6lld %6lld %6lld %6lld\n", s, pat[s], r[1] - r[0], r[2] - r[1], r[3] - r[2],
+               r[4] - r[3], r[5] - r[4], s < 13 ? r[6] - r[5] : 0, r[7] - r[6], s < 13 ? t[(s + 1) * 16] - r[7] : 0,
+               s < 13 ? t[(s + 1) * 16] - r[0] : r[5] - r[0], r[8] - r[0], r[9] - r[0], r[10] - r[0], r[11] - r[0], r[12] - r[0]);
     }
     return 0;
 }
