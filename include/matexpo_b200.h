@@ -179,6 +179,25 @@ MXP_API int mxp_power_batched_device(mxp_handle h, int mode, int64_t n, int64_t 
 MXP_API int mxp_power_batched(mxp_handle h, int mode, int64_t n, int64_t batch, int64_t k,
                       const void* hA, void* hOut, mxp_stats* stats);
 
+/* A^k on several GPUs from ONE process (SURVEY §8(b) mxp_power_multi; the
+ * reference has no multi-device path: SPEC.md:447, device.ts:6-8).  devices:
+ * ngpus device ordinals (NULL: 0 .. ngpus-1; a device may repeat, each
+ * occurrence gets its own internal handle and stream), 1 <= ngpus <= 8.
+ *   batch >= 2: contiguous batch shards, one host thread per device running
+ *     mxp_power_batched — no communication, bitwise equal to one device;
+ *   batch == 1, MXP_F32, n > 128, k >= 2: row-sharded chain, each step's
+ *     new rows stored by the CTA-pair GEMM epilogue straight into every
+ *     device's next planes over NVLink (peer access), CUDA events between
+ *     steps; bitwise equal to mxp_power where that also runs the CTA-pair
+ *     kernel (n % 256 == 0, n >= 1024);
+ *   otherwise: devices[0] alone (replicas only).
+ * Host buffers as mxp_power / mxp_power_batched.  stats: launches summed,
+ * h2d = one per device used, device_ms = max over devices.
+ * mxp_multi_release destroys the internal handles. */
+MXP_API int mxp_power_multi(int ngpus, const int* devices, int mode, int64_t n, int64_t batch,
+                            int64_t k, const void* hA, void* hOut, mxp_stats* stats);
+MXP_API int mxp_multi_release(void);
+
 /* exact modular mode: uint32 residues, result (A^k) mod p, 2 <= p < 2^31 */
 MXP_API int mxp_power_mod_device(mxp_handle h, int64_t n, int64_t k, uint32_t p, const void* dA,
                          void* dOut, mxp_stats* stats);

@@ -44,6 +44,7 @@ from .expo import (
     count_transfers,
     exponentiate,
     exponentiate_batched,
+    exponentiate_multi,
     multiply_count_for,
     plan_exponentiation,
     repeated_exponentiate,
@@ -61,7 +62,8 @@ __all__ = [
     "scaled_batch", "scaled_input", "vectorized_tol", "associativity_tol", "oracle_tol",
     "device_tol", "fro_tol", "fro_tol_conditioned", "multiply_count", "Step", "Strategy",
     "ExponentPlan", "plan_exponentiation", "Backend", "CountingBackend", "B200Backend",
-    "b200_backend", "exponentiate", "exponentiate_batched", "repeated_exponentiate",
+    "b200_backend", "exponentiate", "exponentiate_batched", "exponentiate_multi",
+    "repeated_exponentiate",
     "count_transfers", "multiply_count_for", "Engine", "__version__",
 ]
 

@@ -157,7 +157,8 @@ def exponentiate_row_sharded(a, power: int, group=None, ops=None, chunks: Option
 def fused_layout(n: int, world: int) -> tuple[int, int]:
     """(padded n, rows per rank) for the fused exchange: 256-row CTA-pair row
     blocks per rank and n_p >= 1024 (the CTA-pair kernel's range)."""
-    n_p = max(1024, math.ceil(n / (256 * world)) * 256 * world)
+    blk = 256 * world
+    n_p = max(math.ceil(1024 / blk), math.ceil(n / blk)) * blk  # every rank: 256-row blocks
     return n_p, n_p // world
 
 

@@ -86,7 +86,8 @@ class Engine:
         _lib.check(self._L.mxp_debug_inject_fault(self._h, int(step)), "mxp_debug_inject_fault")
 
     # ------------------------------------------------------------ errors
-    def _raise_chain(self, status: int, stats: _lib.Stats, plan: str, what: str) -> None:
+    @staticmethod
+    def _raise_chain(status: int, stats: _lib.Stats, plan: str, what: str) -> None:
         """Map a failed chain to BackendStepError (errors.py:43-49) when the
         failing plan step is known, else to the status' exception."""
         if status == _lib.MXP_OK:
@@ -403,6 +404,45 @@ def default_engine(device: Optional[int] = None) -> Engine:
             eng = Engine(device)
             _engines[key] = eng
         return eng
+
+
+def power_multi(a: np.ndarray, k: int, devices=None, out: Optional[np.ndarray] = None) -> np.ndarray:
+    """A^k on several GPUs of this process (``mxp_power_multi``): a (batch, n, n)
+    stack is split into contiguous batch shards (no communication); a single
+    n x n FP32 matrix (n > 128) is row-sharded with each step's rows stored by
+    the GEMM epilogue into every device's planes over NVLink.  ``devices``: a
+    list of device ordinals (may repeat), an int N (devices 0..N-1), or None
+    (every visible device)."""
+    a = np.ascontiguousarray(a)
+    if a.ndim not in (2, 3) or a.shape[-1] != a.shape[-2]:
+        raise E.ShapeError(f"expected an (n, n) or (batch, n, n) array, got shape {a.shape}")
+    if isinstance(devices, int):
+        devices = list(range(devices))
+    devs = [int(d) for d in devices] if devices is not None else list(range(device_count()))
+    if not devs:
+        raise E.DeviceUnavailableError("no CUDA device available")
+    mode = _mode_of(a)
+    if out is None:
+        out = np.empty_like(a)
+    elif (not isinstance(out, np.ndarray) or out.shape != a.shape or out.dtype != a.dtype
+          or not out.flags.c_contiguous or not out.flags.writeable):
+        raise E.ShapeError(f"out must be a writeable C-contiguous {a.dtype} array of shape {a.shape}")
+    batch = a.shape[0] if a.ndim == 3 else 1
+    if batch == 0:
+        return out
+    L = _lib.load()
+    arr = (ctypes.c_int * len(devs))(*devs)
+    st = _lib.Stats()
+    rc = L.mxp_power_multi(len(devs), arr, mode, a.shape[-1], batch, int(k), _ptr(a), _ptr(out),
+                           ctypes.byref(st))
+    power_multi.last_stats = st
+    Engine._raise_chain(rc, st, plan_string(k) if k >= 0 else "", "mxp_power_multi")
+    return out
+
+
+def release_multi() -> None:
+    """Destroy the internal per-device handles of ``power_multi``."""
+    _lib.check(_lib.load().mxp_multi_release(), "mxp_multi_release")
 
 
 def device_count() -> int:

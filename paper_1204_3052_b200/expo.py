@@ -195,6 +195,21 @@ def exponentiate_batched(a: np.ndarray, power: int, device: int = 0) -> np.ndarr
     return default_engine(device).power_batched(np.ascontiguousarray(a), power)
 
 
+def exponentiate_multi(a, power: int, devices=None) -> np.ndarray:
+    """A**power on several GPUs of this process (the C ABI's mxp_power_multi):
+    a (batch, n, n) stack is sharded by matrices, one n x n FP32 matrix by
+    rows with the exchange fused into the GEMM epilogue.  ``a`` may be a
+    Matrix or an ndarray; the result is an ndarray.  The reference has no
+    multi-device path; the plan, k = 0 / 1 and error semantics
+    are exponentiate's."""
+    if power < 0:
+        raise ValueError(f"power must be >= 0, got {power}")
+    from .engine import power_multi
+
+    arr = a.array if hasattr(a, "array") else a
+    return power_multi(np.ascontiguousarray(arr), power, devices)
+
+
 def repeated_exponentiate(a, power: int, backend):
     """A**power by power-1 successive multiplies (expo.py:142-156)."""
     if power < 1:

@@ -116,3 +116,31 @@ def test_small_kernel_router_both_sides_of_threshold():
     assert _lib.small_kernel_for(64, 16) == "k3h" and _lib.small_kernel_for(128, 64) == "k3h"
     # at n = 128 the switch sits between k = 383 and 384
     assert _lib.small_kernel_for(128, 383) == "k3h" and _lib.small_kernel_for(128, 384) == "k3b"
+
+
+def test_power_multi_validation_without_device(lib):
+    """mxp_power_multi validates before touching a device and, with no GPU,
+    reports the device as unavailable (no CPU fallback)."""
+    import numpy as np
+    import torch
+
+    st = _lib.Stats()
+    a = np.zeros((4, 4), np.float32)
+    out = np.empty_like(a)
+    p = ctypes.c_void_p(a.ctypes.data)
+    q = ctypes.c_void_p(out.ctypes.data)
+    assert lib.mxp_power_multi(0, None, 0, 4, 1, 3, p, q, ctypes.byref(st)) == _lib.MXP_E_VALIDATION
+    assert lib.mxp_power_multi(9, None, 0, 4, 1, 3, p, q, ctypes.byref(st)) == _lib.MXP_E_VALIDATION
+    assert lib.mxp_power_multi(1, None, 0, 4, 1, -1, p, q, ctypes.byref(st)) == _lib.MXP_E_VALIDATION
+    assert lib.mxp_power_multi(1, None, 7, 4, 1, 3, p, q, ctypes.byref(st)) == _lib.MXP_E_VALIDATION
+    assert lib.mxp_power_multi(1, None, 0, 4, 1, 3, None, q, ctypes.byref(st)) == _lib.MXP_E_VALIDATION
+    with pytest.raises(ValueError):
+        mx.exponentiate_multi(a, -1, [0])
+    with pytest.raises(mx.ShapeError):
+        mx.exponentiate_multi(np.zeros((4, 5), np.float32), 3, [0])
+    if not torch.cuda.is_available():
+        devs = (ctypes.c_int * 2)(0, 0)
+        rc = lib.mxp_power_multi(2, devs, 0, 4, 1, 3, p, q, ctypes.byref(st))
+        assert rc == _lib.MXP_E_DEVICE_UNAVAILABLE
+        with pytest.raises(mx.DeviceUnavailableError):
+            mx.exponentiate_multi(a, 3, [0, 0])
