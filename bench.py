@@ -506,6 +506,66 @@ def plan_only(args, w, world, rank) -> None:
         tdist.destroy_process_group()
 
 
+def roofline_of(w: dict, batched: bool, rank_fl: float, ms: float, launches: int, value: float,
+                world: int, peaks: dict, tf32) -> dict:
+    """The bench line's roofline object for the kernel that runs workload w:
+    rank_fl algorithmic flops of this rank's step, ms its device time,
+    launches the engine's kernel launches per step (value: whole-job rate)."""
+    # Roofline denominator = the datapath the kernel runs on.  C3 (K3H) forms
+    # each fp32 product from three fp16 tensor-core products (scaled fp16x2
+    # split), so its effective peak is the dense 16-bit tensor peak / 3
+    # (MEASURED_PEAKS bf16; fp16 runs at the same rate).  The K1/K1P chains
+    # (C2, C5) run 3xTF32: cuBLAS TF32 measured here / 3.
+    bf16 = peaks.get("bf16_tflops")
+    if batched and w["dtype"] == "f32":
+        if bf16:
+            peak, src = bf16 / 3.0, "MEASURED_PEAKS bf16 dense burst (fp16 same rate) / 3 products"
+        else:
+            peak, src = 2250.0 / 3.0, "fallback: nominal 2.25 PF dense fp16 / 3 products"
+        kernel = "k3h_batched_power"
+    else:
+        if tf32:
+            peak, src = tf32 / 3.0, f"cuBLAS TF32 8192^3 measured in this run ({tf32:.0f} TFLOP/s) / 3"
+        elif bf16:
+            peak, src = bf16 / 6.0, "MEASURED_PEAKS bf16 burst / 2 (tf32) / 3"
+        else:
+            peak, src = 1590.0 / 6.0, "fallback 1.59 PF bf16 / 6"
+        # the kernel that runs the chain's multiplies (INTEGRATION.md §6)
+        n_pad = -(-w["n"] // 128) * 128
+        if w["dtype"] == "f64":
+            kernel = "f64_gemm_kernel"
+        elif w["n"] <= 128:
+            kernel = "k3h_batched_power"
+        elif n_pad >= 1024 and n_pad % 256 == 0:
+            kernel = "k1p_gemm_3xtf32"
+        elif n_pad in (256, 384, 512, 640, 768, 896, 1152, 1408):
+            kernel = "k1c_chain_3xtf32"
+        else:
+            kernel = "k1_gemm_3xtf32"
+    # A batched step is ONE K3H launch doing all the work plus the K3B fixup
+    # pass, which returns at once on an empty list (0 matrices on this input;
+    # ~4 us, overlapped with K3H's tail by programmatic dependent launch).  The
+    # K3H launch time is therefore taken as the whole step time: a lower bound
+    # on the kernel's rate, never an inflated one.
+    kernel_ms = ms
+    achieved = rank_fl / (kernel_ms / 1e3) / 1e12 if batched else value / world
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(kernel),
+                "kernel": kernel, "peak_source": src,
+                "per_gpu": True,
+                "algorithmic_flops_per_launch": rank_fl if batched else rank_fl / max(launches, 1),
+                "kernel_time": ("step time: the K3H launch + the empty K3B fixup pass"
+                                if batched else "chain time / launches"),
+                "bf16_measured_peak": bf16,
+                "bf16_measured_peak_sustained": peaks.get("bf16_tflops_sustained"),
+                "frac_vs_sustained": (achieved / (peaks["bf16_tflops_sustained"] / 3.0)
+                                      if peaks.get("bf16_tflops_sustained") and batched
+                                      else None),
+                "tf32_cublas_measured": tf32,
+                "vs_3xtf32_effective_peak": achieved / (tf32 / 3.0) if tf32 else None}
+    return roofline
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -666,59 +726,7 @@ def main() -> None:
             tf32 = library_gemm_peak_tflops(torch.device("cuda", local), "tf32")
         except Exception:  # noqa: BLE001
             tf32 = None
-    # Roofline denominator = the datapath the kernel runs on.  C3 (K3H) forms
-    # each fp32 product from three fp16 tensor-core products (scaled fp16x2
-    # split), so its effective peak is the dense 16-bit tensor peak / 3
-    # (MEASURED_PEAKS bf16; fp16 runs at the same rate).  The K1/K1P chains
-    # (C2, C5) run 3xTF32: cuBLAS TF32 measured here / 3.
-    bf16 = peaks.get("bf16_tflops")
-    if batched and w["dtype"] == "f32":
-        if bf16:
-            peak, src = bf16 / 3.0, "MEASURED_PEAKS bf16 dense burst (fp16 same rate) / 3 products"
-        else:
-            peak, src = 2250.0 / 3.0, "fallback: nominal 2.25 PF dense fp16 / 3 products"
-        kernel = "k3h_batched_power"
-    else:
-        if tf32:
-            peak, src = tf32 / 3.0, f"cuBLAS TF32 8192^3 measured in this run ({tf32:.0f} TFLOP/s) / 3"
-        elif bf16:
-            peak, src = bf16 / 6.0, "MEASURED_PEAKS bf16 burst / 2 (tf32) / 3"
-        else:
-            peak, src = 1590.0 / 6.0, "fallback 1.59 PF bf16 / 6"
-        # the kernel that runs the chain's multiplies
-        n_pad = -(-w["n"] // 128) * 128
-        if w["dtype"] == "f64":
-            kernel = "f64_gemm_kernel"
-        elif w["n"] <= 128:
-            kernel = "k3h_batched_power"
-        elif n_pad >= 1024 and n_pad % 256 == 0:
-            kernel = "k1p_gemm_3xtf32"
-        elif n_pad in (256, 384, 512, 640, 768, 896, 1152, 1408):
-            kernel = "k1c_chain_3xtf32"
-        else:
-            kernel = "k1_gemm_3xtf32"
-    rank_fl = flops(w, hi - lo)
-    # A batched step is ONE K3H launch doing all the work plus the K3B fixup
-    # pass, which returns at once on an empty list (0 matrices on this input;
-    # ~4 us, overlapped with K3H's tail by programmatic dependent launch).  The
-    # K3H launch time is therefore taken as the whole step time: a lower bound
-    # on the kernel's rate, never an inflated one.
-    kernel_ms = ms
-    achieved = rank_fl / (kernel_ms / 1e3) / 1e12 if batched else value / world
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(kernel),
-                "kernel": kernel, "peak_source": src,
-                "per_gpu": True,
-                "algorithmic_flops_per_launch": rank_fl if batched else rank_fl / max(launches, 1),
-                "kernel_time": ("step time: the K3H launch + the empty K3B fixup pass"
-                                if batched else "chain time / launches"),
-                "bf16_measured_peak": bf16,
-                "bf16_measured_peak_sustained": peaks.get("bf16_tflops_sustained"),
-                "frac_vs_sustained": (achieved / (peaks["bf16_tflops_sustained"] / 3.0)
-                                      if peaks.get("bf16_tflops_sustained") and batched
-                                      else None),
-                "tf32_cublas_measured": tf32,
-                "vs_3xtf32_effective_peak": achieved / (tf32 / 3.0) if tf32 else None}
+    roofline = roofline_of(w, batched, flops(w, hi - lo), ms, launches, value, world, peaks, tf32)
     out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
            "higher_is_better": True, "scaling": "strong",

@@ -55,3 +55,23 @@ def test_shard_rule_matches_the_package():
         for world in (1, 2, 3, 8):
             for r in range(world):
                 assert bench.shard_range(total, r, world) == D.shard_range(total, r, world)
+
+
+def test_roofline_counts_the_k3h_launch_over_the_step():
+    """A C3 step is one K3H launch (all the flops) + the K3B fixup pass (no
+    work on an empty list): the roofline's rate is the step's flops over the
+    step time, so a step at the measured 3.7 ms stays below the datapath peak
+    (round 2 divided by 2 launches and reported frac 1.59)."""
+    import bench
+
+    w = bench.WORKLOADS["c3"]
+    fl = bench.flops(w)
+    peaks = {"bf16_tflops": 1641.9, "bf16_tflops_sustained": 1383.8}
+    r = bench.roofline_of(w, True, fl, 3.7, 2, fl / 3.7e-3 / 1e12, 1, peaks, 759.0)
+    assert abs(r["achieved"] - fl / 3.7e-3 / 1e12) < 1e-6
+    assert r["algorithmic_flops_per_launch"] == fl
+    assert 0.5 < r["frac"] < 1.0
+    assert r["kernel"] == "k3h_batched_power"
+    r5 = bench.roofline_of(bench.WORKLOADS["c5"], False, bench.flops(bench.WORKLOADS["c5"]), 44.0,
+                           21, bench.flops(bench.WORKLOADS["c5"]) / 44e-3 / 1e12, 1, peaks, 759.0)
+    assert r5["kernel"] == "k1p_gemm_3xtf32" and 0.5 < r5["frac"] < 1.05
