@@ -814,13 +814,23 @@ struct K1CPlanes {
 };
 
 #ifdef K1C_TRACE  // tools/k1c_trace.cu: per-step phase stamps of CTA (0, 0)
-__device__ long long* g_k1c_trace;  // [step][16]
+__device__ long long* g_k1c_trace;   // [step][16]: clock64 of CTA (0, 0)
+__device__ long long* g_k1c_gtrace;  // [step][cta][4]: globaltimer of every CTA at 0, 1, 4, 7
 #define K1C_STAMP(k)                                                                       \
     do {                                                                                   \
-        if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && step < 64) {  \
-            long long t_;                                                                  \
-            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_) : : "memory");              \
-            g_k1c_trace[step * 16 + (k)] = t_;                                             \
+        if ((threadIdx.x & 31) == 0 && step < 64) {                                        \
+            if (blockIdx.x == 0 && blockIdx.y == 0) {                                      \
+                long long t_;                                                              \
+                asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_) : : "memory");          \
+                g_k1c_trace[step * 16 + (k)] = t_;                                         \
+            }                                                                              \
+            if ((k) == 0 || (k) == 1 || (k) == 4 || (k) == 7) {                            \
+                long long g_;                                                              \
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_) : : "memory");       \
+                const int slot_ = (k) == 0 ? 0 : (k) == 1 ? 1 : (k) == 4 ? 2 : 3;         \
+                const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                      \
+                g_k1c_gtrace[(step * gridDim.x * gridDim.y + cta_) * 4 + slot_] = g_;      \
+            }                                                                              \
         }                                                                                  \
     } while (0)
 #else

@@ -66,6 +66,45 @@ __global__ void __launch_bounds__(384, 1) bar_kernel(unsigned* ctr, unsigned* fl
                 }
             }
             __syncthreads();
+        } else if (V == 6 || V == 7 || V == 9) {
+            // arrival counter + a separate release flag written by the last arriver
+            // (6: pollers ld.acquire; 7: ld.relaxed + fence after; 9: as 6 with
+            // 16 KB of plane stores per CTA before the barrier, like K1C's reduce)
+            if (V == 9) {
+                float4* dst = reinterpret_cast<float4*>(flags + 65536) + cta * 1024;
+                for (int i = threadIdx.x; i < 1024; i += blockDim.x) dst[i] = make_float4(it, 0, 0, 0);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned old;
+                asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+                if (old == nctas * it - 1) {
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags), "r"((unsigned)it) : "memory");
+                } else if (V == 7) {
+                    unsigned v;
+                    do {
+                        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flags) : "memory");
+                    } while (v < (unsigned)it);
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                } else {
+                    while (ld_acq(flags) < (unsigned)it) {
+                    }
+                }
+            }
+            __syncthreads();
+        } else if (V == 8) {
+            // 0 with 16 KB of plane stores per CTA before the barrier
+            float4* dst = reinterpret_cast<float4*>(flags + 65536) + cta * 1024;
+            for (int i = threadIdx.x; i < 1024; i += blockDim.x) dst[i] = make_float4(it, 0, 0, 0);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+                for (;;) {
+                    if (ld_acq(ctr) >= nctas * it) break;
+                    __nanosleep(64);
+                }
+            }
+            __syncthreads();
         } else if (V == 4) {
             cluster_sync_all();
             if (cluster_ctarank() == 0 && threadIdx.x < 32) {
@@ -91,12 +130,12 @@ void run(int nx, int iters) {
     unsigned *ctr, *flags;
     unsigned long long* out;
     cudaMalloc(&ctr, 4);
-    cudaMalloc(&flags, 4096 * 32 * 4);
+    cudaMalloc(&flags, 65536 * 4 + 256 * 1024 * 16);
     cudaMalloc(&out, 8);
     float best = 1e30f;
     for (int rep = 0; rep < 5; ++rep) {
         cudaMemset(ctr, 0, 4);
-        cudaMemset(flags, 0, 4096 * 32 * 4);
+        cudaMemset(flags, 0, 65536 * 4);
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(nx, 4);
         cfg.blockDim = dim3(384);
@@ -131,6 +170,10 @@ int main() {
     cudaFuncSetAttribute(bar_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(bar_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(bar_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (int v = 6; v <= 9; ++v) {
+        void* f = v == 6 ? (void*)bar_kernel<6> : v == 7 ? (void*)bar_kernel<7> : v == 8 ? (void*)bar_kernel<8> : (void*)bar_kernel<9>;
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    }
     for (int nx : {8, 32}) {
         run<0>(nx, 2000);
         run<1>(nx, 2000);
@@ -138,6 +181,10 @@ int main() {
         run<3>(nx, 2000);
         run<4>(nx, 2000);
         run<5>(nx, 2000);
+        run<6>(nx, 2000);
+        run<7>(nx, 2000);
+        run<8>(nx, 2000);
+        run<9>(nx, 2000);
     }
     return 0;
 }

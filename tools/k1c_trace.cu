@@ -8,6 +8,8 @@
 //   paper_1204_3052_b200/csrc/kernels_k3h.cu -o k1c_trace -lcuda
 #include <cstdio>
 #include <vector>
+#include <algorithm>
+#include <climits>
 #include "../paper_1204_3052_b200/csrc/kernels_tf32.cu"
 using namespace mxp;
 int main(int argc, char** argv) {
@@ -21,6 +23,10 @@ int main(int argc, char** argv) {
     cudaMalloc(&a, n * n * 4); cudaMalloc(&out, n * n * 4); cudaMalloc(&ctr, 256);
     cudaMalloc(&tr, 64 * 16 * 8); cudaMemset(tr, 0, 64 * 16 * 8);
     cudaMemcpyToSymbol(g_k1c_trace, &tr, sizeof(tr));
+    long long* gtr;
+    cudaMalloc(&gtr, 64 * 256 * 4 * 8);
+    cudaMemset(gtr, 0, 64 * 256 * 4 * 8);
+    cudaMemcpyToSymbol(g_k1c_gtrace, &gtr, sizeof(gtr));
     std::vector<float> h(n * n);
     uint32_t x = 1;
     for (auto& v : h) { x = x * 1664525u + 1013904223u; v = ((x >> 8) / 16777216.0f - 0.5f) * 0.153f; }
@@ -53,6 +59,25 @@ int main(int argc, char** argv) {
         printf("%2d %c: %6lld %6lld %6lld %6lld %6lld %6lld | %6lld %6lld | %6lld || %6lld %6lld %6lld %6lld %6lld\n", s, pat[s], r[1] - r[0], r[2] - r[1], r[3] - r[2],
                r[4] - r[3], r[5] - r[4], s < 13 ? r[6] - r[5] : 0, r[7] - r[6], s < 13 ? t[(s + 1) * 16] - r[7] : 0,
                s < 13 ? t[(s + 1) * 16] - r[0] : r[5] - r[0], r[8] - r[0], r[9] - r[0], r[10] - r[0], r[11] - r[0], r[12] - r[0]);
+    }
+    // every CTA (globaltimer, ns): spread of the step phases across the grid
+    const int nctas = 2 * (np / 128) * (np / 128) * splits;  // 64-column K1C tiles
+    std::vector<long long> g(64 * 256 * 4);
+    cudaMemcpy(g.data(), gtr, g.size() * 8, cudaMemcpyDeviceToHost);
+    printf("\nall %d CTAs (ns from the earliest step start): start min/max | mainloop done min/med/max | reduce done min/max | after barrier min/max   [slowest mainloop CTA]\n", nctas);
+    for (int s = 0; s < 14; ++s) {
+        std::vector<long long> v[4];
+        long long t0 = LLONG_MAX;
+        int slow = 0; long long slowv = 0;
+        for (int c = 0; c < nctas; ++c) {
+            for (int k = 0; k < 4; ++k) v[k].push_back(g[(s * nctas + c) * 4 + k]);
+            t0 = std::min(t0, g[(s * nctas + c) * 4 + 0]);
+            if (g[(s * nctas + c) * 4 + 1] > slowv) { slowv = g[(s * nctas + c) * 4 + 1]; slow = c; }
+        }
+        for (auto& x : v) std::sort(x.begin(), x.end());
+        auto r = [&](int k, int i) { return v[k][i] - t0; };
+        printf("%2d: %5lld %5lld | %5lld %5lld %5lld | %5lld %5lld | %5lld %5lld   [cta %d]\n", s, r(0, 0), r(0, nctas - 1),
+               r(1, 0), r(1, nctas / 2), r(1, nctas - 1), r(2, 0), r(2, nctas - 1), r(3, 0), r(3, nctas - 1), slow);
     }
     return 0;
 }
