@@ -71,6 +71,9 @@ cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
 __global__ void split_pad_kernel(const float* __restrict__ in, int n, int ld,
                                  uint32_t* __restrict__ hi, uint32_t* __restrict__ lo,
                                  int n_pad, int rows, int rows_pad) {
+    // a programmatically dependent K1C may start its prologue now; it waits
+    // (griddepcontrol.wait) for this grid to complete before reading the planes
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const size_t quads = static_cast<size_t>(rows_pad) * n_pad / 4;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < quads;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -921,6 +924,9 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t s0 = smem_u32(smem);
+    // launched as a programmatic dependent of the split kernel: everything
+    // above overlapped it; its planes are complete and visible after this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     int acc = 0;  // plane pair holding the running power: 0 base, 1 ping, 2 pong
     for (int step = 0; step < plan.len; ++step) {
@@ -1074,6 +1080,18 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 2) tmem_dealloc<2 * BN>(tmem);
+    if (threadIdx.x == 0) {
+        // The last CTA out resets the barrier counters for the next launch
+        // (no memset node in the chain's graph).  Every CTA's last read of
+        // bar_ctr[0] precedes its exit increment, so no one can see the reset.
+        unsigned int old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                     : "=r"(old) : "l"(bar_ctr + 1) : "memory");
+        if (old == nctas - 1) {
+            bar_ctr[0] = 0;
+            bar_ctr[1] = 0;
+        }
+    }
 }
 
 static cudaError_t prepare_k1c() {
@@ -1126,20 +1144,22 @@ cudaError_t launch_k1c_chain(const CUtensorMap* map_a, const CUtensorMap* map_b,
         maps.b[i] = map_b[i];
         pl.p[i] = planes[i];
     }
-    cudaError_t e = cudaMemsetAsync(bar_ctr, 0, sizeof(unsigned int), s);
-    if (e != cudaSuccess) return e;
+    // bar_ctr[0..1] are zero on entry: zeroed when the handle is created and
+    // reset by the last CTA of every launch
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(narrow ? 2 * tiles : tiles, splits);
     cfg.blockDim = dim3(384);
     cfg.dynamicSmemBytes = narrow ? K1CCfg<64>::kSmem : K1CCfg<128>::kSmem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = static_cast<unsigned>(splits);
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     if (narrow)
         return cudaLaunchKernelEx(&cfg, k1c_chain_3xtf32<64>, maps, pl, plan, n_pad, out_f32, n_out,
                                   bar_ctr, progress, fault_step);

@@ -655,6 +655,7 @@ int mxp_create(int device, mxp_handle* out) {
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
     if (e == cudaSuccess) e = cudaMalloc(&h->bar_ctr, 256);
+    if (e == cudaSuccess) e = cudaMemset(h->bar_ctr, 0, 256);  // K1C keeps it zero between launches
     if (e == cudaSuccess) e = cudaMalloc(&h->stamps, 64);
     if (e == cudaSuccess) e = cudaMalloc(&h->fix, (1 + 1024) * sizeof(int));
     if (e == cudaSuccess) {

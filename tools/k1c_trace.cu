@@ -20,7 +20,7 @@ int main(int argc, char** argv) {
     for (int i = 0; i < 14; ++i) if (pat[i] == 'M') plan.mult[0] |= 1ull << i;
     prepare_tf32_kernels();
     float *a, *out; uint32_t* planes[6]; unsigned int* ctr; long long* tr;
-    cudaMalloc(&a, n * n * 4); cudaMalloc(&out, n * n * 4); cudaMalloc(&ctr, 256);
+    cudaMalloc(&a, n * n * 4); cudaMalloc(&out, n * n * 4); cudaMalloc(&ctr, 256); cudaMemset(ctr, 0, 256);
     cudaMalloc(&tr, 64 * 16 * 8); cudaMemset(tr, 0, 64 * 16 * 8);
     cudaMemcpyToSymbol(g_k1c_trace, &tr, sizeof(tr));
     long long* gtr;
