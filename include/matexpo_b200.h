@@ -190,6 +190,9 @@ MXP_API int mxp_power_batched(mxp_handle h, int mode, int64_t n, int64_t batch, 
  *     device's next planes over NVLink (peer access), CUDA events between
  *     steps; bitwise equal to mxp_power where that also runs the CTA-pair
  *     kernel (n % 256 == 0, n >= 1024);
+ *   batch == 1, MXP_F64, n >= 256, k >= 2: row-sharded with the DMMA
+ *     row-block GEMM and peer copies of each device's rows, bitwise equal to
+ *     mxp_power;
  *   otherwise: devices[0] alone (replicas only).
  * Host buffers as mxp_power / mxp_power_batched.  stats: launches summed,
  * h2d = one per device used, device_ms = max over devices.

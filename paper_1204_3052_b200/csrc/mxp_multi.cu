@@ -18,11 +18,14 @@
 //     the single-GPU kernel and k-order, so the result is bitwise equal to
 //     mxp_power when the single-GPU chain runs the same CTA-pair kernel
 //     (n % 256 == 0, n >= 1024);
-//   * anything else (n <= 128, FP64, k <= 1) is too small or has no sharded
-//     form here: it runs on devices[0] (replicas only).
+//   * batch == 1, FP64, n >= 256, k >= 2: row-sharded with the DMMA row-block
+//     GEMM and peer copies of each device's rows (power_multi_rows_f64);
+//   * anything else (n <= 128 FP32, small FP64, k <= 1) is too small to
+//     shard: it runs on devices[0] (replicas only).
 // The reference has no multi-device path (its
 // device is one queue, gpu-backend/src/device.ts:6-8); this entry keeps the
 // reference call's semantics (plan, k = 0 / 1, errors) on top.
+#include <array>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -140,6 +143,179 @@ int power_multi_batched(const std::vector<mxp_handle>& hs, int mode, int64_t n, 
     return MXP_OK;
 }
 
+// peer access between distinct devices (UVA pointers then work across them)
+int enable_peers(const std::vector<int>& dev) {
+    const int G = static_cast<int>(dev.size());
+    for (int g = 0; g < G; ++g)
+        for (int q = 0; q < G; ++q) {
+            if (dev[g] == dev[q]) continue;
+            int ok = 0;
+            if (cudaDeviceCanAccessPeer(&ok, dev[g], dev[q]) != cudaSuccess || !ok)
+                return mxp_internal_fail(MXP_E_UNSUPPORTED,
+                                         "device %d cannot access device %d (no P2P / NVLink)",
+                                         dev[g], dev[q]);
+            cudaSetDevice(dev[g]);
+            cudaError_t e = cudaDeviceEnablePeerAccess(dev[q], 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) {
+                cudaGetLastError();
+            } else if (e != cudaSuccess) {
+                return mxp_internal_fail(MXP_E_CUDA, "cudaDeviceEnablePeerAccess(%d -> %d): %s",
+                                         dev[g], dev[q], cudaGetErrorString(e));
+            }
+        }
+    return MXP_OK;
+}
+
+// every device's stream waits for every other device's work so far
+int cross_fence(const std::vector<int>& dev, const std::vector<cudaStream_t>& stream,
+                const std::vector<cudaEvent_t>& ev) {
+    const int G = static_cast<int>(dev.size());
+    for (int g = 0; g < G; ++g) {
+        cudaSetDevice(dev[g]);
+        if (cudaEventRecord(ev[g], stream[g]) != cudaSuccess)
+            return mxp_internal_fail(MXP_E_CUDA, "event record on device %d", dev[g]);
+    }
+    for (int g = 0; g < G; ++g) {
+        cudaSetDevice(dev[g]);
+        for (int q = 0; q < G; ++q)
+            if (q != g && cudaStreamWaitEvent(stream[g], ev[q], 0) != cudaSuccess)
+                return mxp_internal_fail(MXP_E_CUDA, "stream wait on device %d", dev[g]);
+    }
+    return MXP_OK;
+}
+
+// ---- one FP64 matrix, row shards -----------------------------------------
+// tcgen05 has no f64 kind and the DMMA kernel has no fused peer epilogue:
+// each device computes its contiguous row block with the public row-block
+// GEMM (mxp_gemm_prepare_rhs + mxp_gemm_rows_prepared: the single-GPU kernel
+// and k-order, so every row is bitwise the single-device chain's), then
+// copies the block into every other device's next buffer over NVLink
+// (cudaMemcpyAsync between peers on its own stream); CUDA events order the
+// steps.  SURVEY §8(e) C4: "same scheme, optional".
+int power_multi_rows_f64(const std::vector<mxp_handle>& hs, const int* devices, int64_t n,
+                         int64_t k, const void* hA, void* hOut, mxp_stats* st) {
+    const int G = static_cast<int>(hs.size());
+    const size_t mat = static_cast<size_t>(n) * n * 8;
+    std::vector<int> dev(G);
+    for (int g = 0; g < G; ++g) dev[g] = devices ? devices[g] : g;
+    int rc = enable_peers(dev);
+    if (rc) return rc;
+    struct Guard {
+        const std::vector<mxp_handle>& hs;
+        std::vector<std::array<void*, 3>> buf;  // base, ping, pong
+        std::vector<cudaEvent_t> ev;
+        explicit Guard(const std::vector<mxp_handle>& h) : hs(h), buf(h.size()), ev(h.size()) {
+            for (auto& b : buf) b = {nullptr, nullptr, nullptr};
+        }
+        ~Guard() {
+            for (size_t g = 0; g < buf.size(); ++g) {
+                mxp_synchronize(hs[g]);
+                for (void* p : buf[g])
+                    if (p) mxp_free(hs[g], p);
+                if (ev[g]) cudaEventDestroy(ev[g]);
+            }
+        }
+    } guard(hs);
+    std::vector<cudaStream_t> stream(G);
+    for (int g = 0; g < G && rc == MXP_OK; ++g) {
+        void* s = nullptr;
+        rc = mxp_get_stream(hs[g], &s);
+        stream[g] = static_cast<cudaStream_t>(s);
+        for (int i = 0; i < 3 && rc == MXP_OK; ++i) rc = mxp_alloc(hs[g], mat, &guard.buf[g][i]);
+        if (rc == MXP_OK) {
+            cudaSetDevice(dev[g]);
+            if (cudaEventCreateWithFlags(&guard.ev[g], cudaEventDisableTiming) != cudaSuccess)
+                rc = mxp_internal_fail(MXP_E_CUDA, "event creation on device %d", dev[g]);
+        }
+    }
+    if (rc) return rc;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    cudaSetDevice(dev[0]);
+    if (cudaEventCreate(&t0) != cudaSuccess || cudaEventCreate(&t1) != cudaSuccess)
+        return mxp_internal_fail(MXP_E_CUDA, "event creation");
+    struct EvGuard {
+        cudaEvent_t a, b;
+        ~EvGuard() {
+            if (a) cudaEventDestroy(a);
+            if (b) cudaEventDestroy(b);
+        }
+    } evg{t0, t1};
+    cudaEventRecord(t0, stream[0]);
+    for (int g = 0; g < G; ++g) {
+        cudaSetDevice(dev[g]);
+        cudaError_t e = cudaMemcpyAsync(guard.buf[g][0], hA, mat, cudaMemcpyHostToDevice, stream[g]);
+        if (e != cudaSuccess)
+            return mxp_internal_fail(MXP_E_CUDA, "upload to device %d: %s", dev[g],
+                                     cudaGetErrorString(e));
+    }
+    if ((rc = cross_fence(dev, stream, guard.ev))) return rc;
+    int64_t sq = 0;
+    const int64_t m = plan_len(k, &sq);
+    int cur = 0, launches = 0;
+    int64_t bit = 62;
+    while (!((k >> bit) & 1)) --bit;
+    int64_t step = 0;
+    for (int64_t s = bit - 1; s >= 0; --s) {
+        for (int mult = 0; mult < 2; ++mult) {
+            if (mult && !((k >> s) & 1)) break;
+            const int nxt = cur == 1 ? 2 : 1;
+            for (int g = 0; g < G; ++g) {
+                int64_t lo, hi;
+                shard_range(n, g, G, &lo, &hi);
+                if (hi == lo) continue;
+                const size_t off = static_cast<size_t>(lo) * n * 8;
+                char* c_cur = static_cast<char*>(guard.buf[g][cur]);
+                char* c_nxt = static_cast<char*>(guard.buf[g][nxt]);
+                rc = mxp_gemm_prepare_rhs(hs[g], MXP_F64, n, guard.buf[g][mult ? 0 : cur]);
+                if (rc == MXP_OK)
+                    rc = mxp_gemm_rows_prepared(hs[g], MXP_F64, n, hi - lo, c_cur + off, c_nxt + off);
+                if (rc) {
+                    if (st) st->failed_step = step;
+                    return rc;
+                }
+                launches += 4;  // rhs pad, rows pad, GEMM, unpad
+                cudaSetDevice(dev[g]);
+                for (int q = 0; q < G; ++q) {
+                    if (q == g) continue;
+                    cudaError_t e = cudaMemcpyAsync(static_cast<char*>(guard.buf[q][nxt]) + off,
+                                                    c_nxt + off, static_cast<size_t>(hi - lo) * n * 8,
+                                                    cudaMemcpyDefault, stream[g]);
+                    if (e != cudaSuccess) {
+                        if (st) st->failed_step = step;
+                        return mxp_internal_fail(MXP_E_CUDA, "row exchange %d -> %d: %s", dev[g],
+                                                 dev[q], cudaGetErrorString(e));
+                    }
+                }
+            }
+            if ((rc = cross_fence(dev, stream, guard.ev))) return rc;
+            cur = nxt;
+            ++step;
+        }
+    }
+    cudaSetDevice(dev[0]);
+    cudaEventRecord(t1, stream[0]);
+    cudaError_t e = cudaMemcpyAsync(hOut, guard.buf[0][cur], mat, cudaMemcpyDeviceToHost, stream[0]);
+    for (int g = 0; g < G && e == cudaSuccess; ++g) {
+        cudaSetDevice(dev[g]);
+        e = cudaStreamSynchronize(stream[g]);
+    }
+    if (e != cudaSuccess)
+        return mxp_internal_fail(MXP_E_CUDA, "row-sharded FP64 chain: %s", cudaGetErrorString(e));
+    if (st) {
+        st->multiply_count = m;
+        st->square_count = sq;
+        st->launches = launches;
+        st->h2d = G;
+        st->d2h = 1;
+        st->h2d_bytes = static_cast<int64_t>(G * mat);
+        st->d2h_bytes = static_cast<int64_t>(mat);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t0, t1);
+        st->device_ms = ms;
+    }
+    return MXP_OK;
+}
+
 // ---- one matrix, row shards, exchange fused into the GEMM epilogue ------
 struct RowBufs {
     void* base = nullptr;               // n_p x n_p fp32 (zero padded input)
@@ -159,24 +335,8 @@ int power_multi_rows(const std::vector<mxp_handle>& hs, const int* devices, int6
     const size_t plane = static_cast<size_t>(n_p) * n_p * 4;
     std::vector<int> dev(G);
     for (int g = 0; g < G; ++g) dev[g] = devices ? devices[g] : g;
-    // peer access between distinct devices (UVA pointers work across them)
-    for (int g = 0; g < G; ++g)
-        for (int q = 0; q < G; ++q) {
-            if (dev[g] == dev[q]) continue;
-            int ok = 0;
-            if (cudaDeviceCanAccessPeer(&ok, dev[g], dev[q]) != cudaSuccess || !ok)
-                return mxp_internal_fail(MXP_E_UNSUPPORTED,
-                                         "device %d cannot access device %d (no P2P / NVLink)",
-                                         dev[g], dev[q]);
-            cudaSetDevice(dev[g]);
-            cudaError_t e = cudaDeviceEnablePeerAccess(dev[q], 0);
-            if (e == cudaErrorPeerAccessAlreadyEnabled) {
-                cudaGetLastError();
-            } else if (e != cudaSuccess) {
-                return mxp_internal_fail(MXP_E_CUDA, "cudaDeviceEnablePeerAccess(%d -> %d): %s",
-                                         dev[g], dev[q], cudaGetErrorString(e));
-            }
-        }
+    int rc = enable_peers(dev);
+    if (rc) return rc;
     // buffers, freed on every exit path
     struct Guard {
         const std::vector<mxp_handle>& hs;
@@ -195,7 +355,6 @@ int power_multi_rows(const std::vector<mxp_handle>& hs, const int* devices, int6
     } guard(hs);
     auto& B = guard.b;
     std::vector<cudaStream_t> stream(G);
-    int rc = MXP_OK;
     for (int g = 0; g < G && rc == MXP_OK; ++g) {
         void* s = nullptr;
         rc = mxp_get_stream(hs[g], &s);
@@ -340,6 +499,8 @@ extern "C" int mxp_power_multi(int ngpus, const int* devices, int mode, int64_t 
     }
     if (ngpus >= 2 && mode == MXP_F32 && n > 128 && k >= 2)
         return power_multi_rows(hs, devices, n, k, hA, hOut, st);
+    if (ngpus >= 2 && mode == MXP_F64 && n >= 256 && k >= 2)
+        return power_multi_rows_f64(hs, devices, n, k, hA, hOut, st);
     return mxp_power(hs[0], mode, n, k, hA, hOut, st);  // replicas only
 }
 

@@ -79,9 +79,20 @@ def test_row_shards_small_order_vs_oracle(eng):
     assert err <= mx.fro_tol(300, 100, "f32"), err
 
 
+@pytest.mark.parametrize("devices,n,k", [([0, 0], 256, 9), ([0, 0, 0], 1000, 13),
+                                         ([0, 0, 0, 0], 600, 257)])
+def test_row_shards_f64_bitwise_single_device(eng, devices, n, k):
+    """FP64: DMMA row-block GEMMs + peer copies of each device's rows."""
+    a = oracle.scaled_input(n, np.float64, 42)
+    got = mx.exponentiate_multi(a, k, devices)
+    assert got.tobytes() == eng.power(a, k).tobytes()
+    st = E.power_multi.last_stats
+    assert st.multiply_count == mx.multiply_count(k) and st.h2d == len(devices) and st.d2h == 1
+
+
 def test_replica_cases_equal_mxp_power(eng):
-    """n <= 128, FP64 and k <= 1 run on devices[0] alone."""
-    for n, dt, k in ((64, np.float32, 16), (256, np.float64, 9), (300, np.float32, 1),
+    """n <= 128 FP32, small FP64 and k <= 1 run on devices[0] alone."""
+    for n, dt, k in ((64, np.float32, 16), (200, np.float64, 9), (300, np.float32, 1),
                      (300, np.float32, 0)):
         a = oracle.scaled_input(n, dt, 3)
         got = mx.exponentiate_multi(a, k, [0, 0])
