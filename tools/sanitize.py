@@ -39,4 +39,14 @@ for i in (0, 150, 299):
     stack[i] = nil + 1e-6 * rng.uniform(-1, 1, (128, 128))
 mx.exponentiate_batched(stack.astype(np.float32), 6)
 print("fixups", mx.engine.default_engine(0).last_small_fixups())  # the engine exponentiate_batched used
+# C2's shape: the one-launch K1C chain as a programmatic dependent of the split,
+# grid-barrier counters reset by its last CTA (run twice: the second launch
+# relies on the first one's reset)
+eng.power(oracle.scaled_input(512, np.float32, 42), 1000)
+eng.power(oracle.scaled_input(512, np.float32, 42), 1000)
+# mxp_power_multi: batch shards, FP32 fused row shards, FP64 row shards (one GPU listed twice)
+mx.exponentiate_multi(mx.scaled_batch(128, 300, mx.DType.F32, 3), 13, [0, 0])
+mx.exponentiate_multi(oracle.scaled_input(1024, np.float32, 42), 5, [0, 0])
+mx.exponentiate_multi(oracle.scaled_input(300, np.float64, 42), 5, [0, 0])
+mx.engine.release_multi()
 print("sanitize workload done")
