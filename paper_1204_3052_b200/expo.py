@@ -186,13 +186,16 @@ def exponentiate(a, power: int, backend=None):
     return acc
 
 
-def exponentiate_batched(a: np.ndarray, power: int, device: int = 0) -> np.ndarray:
-    """A_i**power for a (batch, n, n) float32/float64 stack (BASELINE config 3)."""
+def exponentiate_batched(a: np.ndarray, power: int, device: int = 0,
+                         out: np.ndarray | None = None) -> np.ndarray:
+    """A_i**power for a (batch, n, n) float32/float64 stack (BASELINE config 3).
+    ``out`` (optional): a C-contiguous array of a's shape and dtype to write
+    into — reusing it spares the first-touch page faults of a fresh result."""
     if power < 0:
         raise ValueError(f"power must be >= 0, got {power}")
     from .engine import default_engine
 
-    return default_engine(device).power_batched(np.ascontiguousarray(a), power)
+    return default_engine(device).power_batched(np.ascontiguousarray(a), power, out=out)
 
 
 def exponentiate_multi(a, power: int, devices=None) -> np.ndarray:

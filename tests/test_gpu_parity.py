@@ -255,6 +255,20 @@ def test_batched_small_n_with_multiplies():
             assert fro(out[i], ref) <= mx.fro_tol_conditioned(n, k, "f32"), (n, k, i)
 
 
+def test_batched_into_caller_out():
+    """exponentiate_batched(..., out=) writes into the caller's array, bitwise
+    the fresh-result call; a wrong out is rejected before any device work."""
+    stack = mx.scaled_batch(128, 200, mx.DType.F32, 11)
+    ref = mx.exponentiate_batched(stack, 64)
+    out = np.full_like(stack, np.nan)
+    got = mx.exponentiate_batched(stack, 64, out=out)
+    assert got is out and out.tobytes() == ref.tobytes()
+    with pytest.raises(mx.ShapeError):
+        mx.exponentiate_batched(stack, 64, out=np.empty((200, 128, 127), np.float32))
+    with pytest.raises(mx.ShapeError):
+        mx.exponentiate_batched(stack, 64, out=np.empty_like(stack, dtype=np.float64))
+
+
 def test_large_chain_with_multiplies_f32():
     for n, k in ((200, 13), (256, 257), (384, 100)):
         a = oracle.scaled_input(n, np.float32, 42)
