@@ -137,6 +137,8 @@ class Engine:
         """C = A * B (one product; 2 uploads + 1 readback like gpuMatmul, host.ts:67-95)."""
         a = np.ascontiguousarray(a)
         b = np.ascontiguousarray(b)
+        if a.ndim != 2 or a.shape[0] != a.shape[1]:
+            raise E.ShapeError(f"expected a square 2-D array, got shape {a.shape}")
         if a.shape != b.shape:
             raise E.ShapeError(f"matrix orders differ: {a.shape[0]} vs {b.shape[0]}")
         if a.dtype != b.dtype:

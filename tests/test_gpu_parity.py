@@ -920,3 +920,18 @@ def test_small_n_graph_survives_fixup_list_growth():
     for _ in range(3):
         assert eng.power(a, 13).tobytes() == want.tobytes()
     eng.synchronize()
+
+
+def test_host_api_rejects_non_square_before_device_work():
+    """Engine.multiply / power / power_mod validate shapes before the C call
+    (a (5, 4) array would otherwise be read as 5 x 5)."""
+    eng = mx.Engine(0)
+    a = np.zeros((5, 4), np.float32)
+    with pytest.raises(mx.ShapeError):
+        eng.multiply(a, a)
+    with pytest.raises(mx.ShapeError):
+        eng.power(a, 3)
+    with pytest.raises(mx.ShapeError):
+        eng.power_mod(np.zeros((5, 4), np.uint32), 3, 97)
+    with pytest.raises(mx.ShapeError):
+        eng.multiply(np.zeros(16, np.float32), np.zeros(16, np.float32))
