@@ -82,6 +82,8 @@ class ClockSampler:
 
     def __init__(self, index: int, period: float = 0.002):
         self.samples = []
+        self.power_mw = []
+        self.power_limit_w = None
         self.reasons = 0
         self.max_mhz = None
         self._stop = threading.Event()
@@ -93,6 +95,10 @@ class ClockSampler:
             self._nv = pynvml
             self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            try:
+                self.power_limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self._h) / 1e3
+            except Exception:  # noqa: BLE001
+                pass
         except Exception:  # noqa: BLE001 - clocks are reported as unavailable
             self._nv = None
         self.period = period
@@ -102,6 +108,10 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                try:
+                    self.power_mw.append(nv.nvmlDeviceGetPowerUsage(self._h))
+                except Exception:  # noqa: BLE001
+                    pass
                 self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
             except Exception:  # noqa: BLE001
                 try:
@@ -125,8 +135,12 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
         reasons = [name for bit, name in self.BITS.items() if self.reasons & bit]
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(self.samples)}
+        out = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+               "reasons": reasons, "samples": len(self.samples)}
+        if self.power_mw:
+            out["power_w"] = statistics.median(self.power_mw) / 1e3
+            out["power_limit_w"] = self.power_limit_w
+        return out
 
 
 # ----------------------------------------------------------------------------- peaks
@@ -402,6 +416,24 @@ def run_device(eng, w: dict, steps: int, warmup: int, seed0: int, dist=None, sam
             clocks["sm_mhz_source"] = "NVML median over the timed region; sm_mhz_in_kernel from the kernel"
         except Exception:  # noqa: BLE001 - K3B launches carry no stamps
             pass
+        # board power under a sustained run of the same step (untimed, ~1.5 s:
+        # NVML's power counter averages over far longer than the timed region)
+        sus = ClockSampler(torch.cuda.current_device(), period=0.01)
+        sus.__enter__()
+        t_end = time.perf_counter() + 1.5
+        while time.perf_counter() < t_end:
+            for _ in range(10):
+                step()
+            eng.synchronize()
+        sus.__exit__()
+        ss = sus.summary()
+        try:
+            mhz, _kms = eng.last_kernel_clock()
+        except Exception:  # noqa: BLE001
+            mhz = None
+        clocks["sustained"] = {"seconds": 1.5, "power_w": ss.get("power_w"),
+                               "power_limit_w": ss.get("power_limit_w"),
+                               "sm_mhz_in_kernel": mhz, "reasons": ss.get("reasons")}
     eng.free(d_in)
     eng.free(d_out)
     return ms, launches, clocks
