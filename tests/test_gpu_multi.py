@@ -113,3 +113,16 @@ def test_exact_inputs_row_sharded(eng):
         ref = (ref.astype(np.float64) @ p.astype(np.float64)).astype(np.float32)
     got = mx.exponentiate_multi(p, k, [0, 0, 0, 0])
     assert np.array_equal(got, ref)
+
+
+def test_more_devices_than_matrices_and_bad_ordinals(eng):
+    """batch < ngpus uses one device per matrix; an ordinal the machine does
+    not have is a validation error before any work (no silent fallback)."""
+    a = _batch(64, 2)
+    got = mx.exponentiate_multi(a, 16, [0, 0, 0])
+    assert got.tobytes() == eng.power_batched(a, 16).tobytes()
+    assert E.power_multi.last_stats.h2d == 2
+    with pytest.raises(mx.ValidationError):
+        mx.exponentiate_multi(a, 16, [0, E.device_count()])
+    with pytest.raises(mx.ValidationError):
+        mx.exponentiate_multi(oracle.scaled_input(512, np.float32, 1), 4, [0] * 9)
