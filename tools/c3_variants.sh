@@ -10,7 +10,8 @@ import sys; sys.path.insert(0,'.')
 import bench, paper_1204_3052_b200 as mx
 eng = mx.Engine(0)
 ms, l, c = bench.run_device(eng, bench.WORKLOADS['c3'], 20, 3, 42)
-print('$lib', f'{ms:.3f} ms', l, 'launches', f\"{c.get('sm_mhz_in_kernel', 0):.0f} MHz\")
+su = c.get('sustained', {})
+print('$lib', f'{ms:.3f} ms', l, 'launches', f\"{c.get('sm_mhz_in_kernel', 0):.0f} MHz\", 'sustained', f\"{su.get('power_w') or 0:.0f} W\", f\"{su.get('sm_mhz_in_kernel') or 0:.0f} MHz\", su.get('reasons'))
 " >> $O/c3_variants.txt 2>&1
 done
 done
