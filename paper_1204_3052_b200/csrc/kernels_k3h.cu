@@ -124,14 +124,9 @@ __device__ __forceinline__ void k3h_issue(uint32_t tbase, uint32_t region, uint6
     const uint64_t y0 = smem_desc(region, 16384, 1024, 2);
     constexpr uint32_t D = C * 256u, X0 = D + 128u, X1 = D + 192u;
     constexpr uint32_t Y1 = kPlane >> 4;
-#ifdef K3H_PROBE_TWO_PRODUCTS  // power-sensitivity probe only (wrong results)
-    mma_f16_ts_x8<D, X0, Y1, kBStep, true>(tbase, y0, kIdescNegB);
-    mma_f16_ts_x8<D, X0, 0, kBStep>(tbase, y0, kIdesc);
-#else
     mma_f16_ts_x8<D, X1, 0, kBStep, true>(tbase, y0, kIdescNegA);  // x1*y0 (first: D =)
     mma_f16_ts_x8<D, X0, Y1, kBStep>(tbase, y0, kIdescNegB);                // x0*y1
     mma_f16_ts_x8<D, X0, 0, kBStep>(tbase, y0, kIdesc);                 // x0*y0
-#endif
     mma_commit_warp(mma_bar + C);
 }
 

@@ -23,15 +23,6 @@ __device__ __forceinline__ void split2(float a, float b, uint64_t sc2, uint32_t&
     uint64_t ab, s2;
     asm("mov.b64 %0, {%1, %2};" : "=l"(ab) : "f"(a), "f"(b));
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(s2) : "l"(ab), "l"(sc2));
-#ifdef K3H_PROBE_CHEAP_SPLIT  // power-sensitivity probe only (drops the residual)
-    asm("{\n\t.reg .f32 sa, sb;\n\t"
-        "mov.b64 {sa, sb}, %2;\n\t"
-        "cvt.rn.f16x2.f32 %0, sb, sa;\n\t"
-        "mov.b32 %1, 0;\n\t}"
-        : "=r"(p0), "=r"(p1)
-        : "l"(s2));
-    return;
-#endif
     asm("{\n\t.reg .f32 sa, sb, ra, rb;\n\t.reg .b16 l, h;\n\t"
         "mov.b64 {sa, sb}, %2;\n\t"
         "cvt.rn.f16x2.f32 %0, sb, sa;\n\t"
