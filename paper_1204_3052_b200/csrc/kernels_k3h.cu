@@ -188,11 +188,12 @@ struct Chain {
     int t_prev;     // scale exponent applied at this chain's previous epilogue
     int bmax_e;     // floor(log2 max |base'|)
     uint32_t sb;    // max-slot buffer the next epilogue reads (0/1)
-    uint32_t mph;   // max_bar parities, bit b for buffer b
+    uint32_t mph;   // max_bar parities, bit b for buffer b; bit 31: a step of the
+                    // current matrix lost range (listed for K3B at its boundary)
     uint32_t home;  // SMEM region (0..2) holding the chain's operand planes
     bool act;
-    bool flagged;   // the current matrix is on the K3B fixup list (epilogue)
 };
+constexpr uint32_t kLost = 1u << 31;  // Chain::mph: range lost in this matrix
 constexpr int kIn = -2;  // Chain::s: the next input is being loaded / converted
 
 // Matrices of CTA b are b, b + G, b + 2G, ... (G = gridDim.x); chain c takes
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap out_map, const float* __restrict__ in,
                       float* __restrict__ out, int n, long long batch, PlanBits plan, int vec,
                       unsigned long long* stamps, int* __restrict__ fix_idx,
-                      int* __restrict__ fix_count, cudaGraphConditionalHandle fix_cond) {
+                      int* __restrict__ fix_count) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
@@ -255,7 +256,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // let the K3B fixup pass (a programmatic dependent) launch now: it only
     // waits for this grid's completion (griddepcontrol.wait), so its launch
     // latency hides under this kernel instead of adding to a short chain
+#ifndef K3H_PROBE_NO_PDL
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
     if (stamps != nullptr && blockIdx.x == 0 && tid == 0) {
         stamps[0] = clock64();
         stamps[1] = globaltimer_ns();
@@ -480,18 +483,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // same test that selects the exact scale path below) is the sign that
         // such entries may matter to a later product: the matrix goes on the
         // fixup list and K3B (an exponent per element) recomputes it after
-        // this launch.  Random inputs never trigger it.
-        auto flag_range = [&](Chain& st, int pmax_e, uint32_t mprev) {
-            if (fix_idx == nullptr || st.flagged) return;
-            if (pmax_e < kCeil - 12 || mprev == 0u || mprev >= 0x7F800000u) {
-                st.flagged = true;
-                if (warp == 0 && lane == 0) {
-                    fix_idx[atomicAdd(fix_count, 1)] = static_cast<int>(st.m);
-                    // inside a CUDA graph: switch on the conditional node
-                    // that holds the K3B pass (it is skipped otherwise)
-                    if (fix_cond != 0) cudaGraphSetConditional(fix_cond, 1u);
-                }
-            }
+        // this launch.  Random inputs never trigger it.  The steps only OR
+        // the test into st.mph's kLost bit; the list append happens once, at the
+        // matrix boundary (an atomic inside the per-step epilogue cost 4%).
+        auto range_lost = [](int pmax_e, uint32_t mprev) {
+            return pmax_e < kCeil - 12 || mprev == 0u || mprev >= 0x7F800000u;
         };
         // Plane addresses: row `row` of panel g, 16-byte unit u at
         // (u ^ (row & 7)) << 4.  Chunk k (units 2k, 2k+1): unit 2k + i sits at
@@ -557,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 load_row64(st.m, x);
             }
             st.sb ^= 1u;  // (the other buffer: the current one was read at the boundary)
-            st.flagged = false;
+            st.mph &= ~kLost;
             const uint32_t mA = block_max_in(C, st.sb, x);  // (also orders tile reads before plane writes)
             const int t = scale_exp(mA);
             K3H_MARK(4);
@@ -597,7 +593,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // already in the spare, -> step 0 there
                     {  // the last step's maxima: did the product feeding this one cancel?
                         const uint32_t mlast = slots_max(C, st);
-                        flag_range(st, ilogb_bits(mlast) + st.t_prev, mlast);
+                        const bool lost = (st.mph & kLost) || range_lost(ilogb_bits(mlast) + st.t_prev, mlast);
+#ifndef K3H_PROBE_NO_FLAG
+                        if (lost && fix_idx != nullptr && warp == 0 && lane == 0)
+                            fix_idx[atomicAdd(fix_count, 1)] = static_cast<int>(st.m);
+#endif
                     }
                     const uint64_t g1 = splat2(exp2i(pe / 2)), g2 = splat2(exp2i(pe - pe / 2));
                     const uint32_t old_region = s0 + st.home * kChainSmem;
@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t mprev = slots_max(C, st);
                 const int pmax_e = ilogb_bits(mprev) + st.t_prev;  // floor(log2 max|P'_s|)
                 const bool exact = pmax_e < kCeil - 12;
-                flag_range(st, pmax_e, mprev);
+                if (range_lost(pmax_e, mprev)) st.mph |= kLost;
                 const int xmax_e = was_mult ? st.bmax_e : pmax_e;
                 int t = kCeil - static_cast<int>(lg_n) - (xmax_e + 1) - (pmax_e + 1);
                 if (mprev == 0u || mprev >= 0x7F800000u) t = 0;  // zero / non-finite operand
@@ -768,7 +768,7 @@ cudaError_t prepare_k3h_kernel() {
 
 cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch,
                                const PlanBits& plan, int grid, unsigned long long* stamps,
-                               int* fix_idx, int* fix_count, unsigned long long fix_cond,
+                               int* fix_idx, int* fix_count,
                                cudaStream_t s) {
     if (plan.len < 1 || n < 1 || n > kSmallMax) return cudaErrorInvalidValue;
     if (grid > batch) grid = static_cast<int>(batch);
@@ -784,10 +784,10 @@ cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch
         vec = 0;
     if (plan.mult[0] | plan.mult[1])
         k3h_batched_power<true><<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan, vec,
-                                                               stamps, fix_idx, fix_count, fix_cond);
+                                                               stamps, fix_idx, fix_count);
     else
         k3h_batched_power<false><<<grid, kThreads, kSmem, s>>>(in_map, out_map, in, out, n, batch, plan,
-                                                                vec, stamps, fix_idx, fix_count, fix_cond);
+                                                                vec, stamps, fix_idx, fix_count);
     return cudaGetLastError();
 }
 

@@ -50,7 +50,7 @@ cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
 #endif
     if (v != 0) return launch_k3b_batched(in, out, n, batch, plan, grid, s);
     if (fix == nullptr)
-        return launch_k3h_batched(in, out, n, batch, plan, grid, stamps, nullptr, nullptr, 0, s);
+        return launch_k3h_batched(in, out, n, batch, plan, grid, stamps, nullptr, nullptr, s);
     // the list count starts at 0: a memset node, or K3H's only CTA clears it
     // itself (single chains: a graph node less on the C1 latency path)
     cudaError_t e = (grid > 1 && batch > 1) ? cudaMemsetAsync(fix, 0, sizeof(int), s) : cudaSuccess;
@@ -60,7 +60,7 @@ cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
     // (A conditional graph node that K3H switches on was measured instead:
     // the node cost C1 24.3 us against 18.5 for this plain launch.)
     (void)side;
-    e = launch_k3h_batched(in, out, n, batch, plan, grid, stamps, fix + 1, fix, 0, s);
+    e = launch_k3h_batched(in, out, n, batch, plan, grid, stamps, fix + 1, fix, s);
     if (e == cudaSuccess) e = launch_k3b_batched(in, out, n, batch, plan, grid, s, fix + 1, fix);
     return e;
 }

@@ -54,12 +54,9 @@ cudaError_t prepare_k3h_kernel();
 // cancellation (a product more than 2^12 below its bound, where the fp16
 // planes' range loses entries a later product depends on) are appended to
 // fix_idx for K3B to recompute (launch_k3_batched enqueues that pass).
-// fix_cond: a CUDA-graph conditional handle (0: none) K3H sets to 1 when it
-// lists a matrix, so a graph runs its K3B pass only when needed.
 cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch,
                                const PlanBits& plan, int grid, unsigned long long* stamps,
-                               int* fix_idx, int* fix_count, unsigned long long fix_cond,
-                               cudaStream_t s);
+                               int* fix_idx, int* fix_count, cudaStream_t s);
 
 // fp32 (n x n, leading dim ld) -> tf32 hi/lo planes (n_pad x n_pad, zero pad).
 cudaError_t launch_split(const float* in, int n, int ld, uint32_t* hi, uint32_t* lo, int n_pad,
