@@ -67,8 +67,9 @@ extern "C" {
 #define MXP_E_NCCL 5               /* collective failure (multi-GPU paths) */
 
 /* element modes */
-#define MXP_F32 0     /* float32 in/out; split-fp32 on tcgen05 tensor cores (3xTF32
-                         for n > 128, scaled fp16x2 / bf16x3 for n <= 128) */
+#define MXP_F32 0     /* float32 in/out; split-fp32 on tcgen05 tensor cores (scaled
+                         fp16x2 / bf16x3 for n <= 128; 3xTF32 for n > 128, scaled
+                         fp16x2 for the CTA-pair sizes, see mxp_set_f32_datapath) */
 #define MXP_F64 1     /* float64 in/out; DMMA tensor pipe */
 #define MXP_U32_MOD 2 /* uint32 residues mod p; exact (see mxp_power_mod) */
 
@@ -218,6 +219,24 @@ MXP_API int mxp_random_device(mxp_handle h, int mode, int64_t n, int64_t batch, 
 /* the raw SplitMix64 stream (linalg.py:117-124 splitmix64(seed, count)):
  * count uint64 draws of `seed` into dOut.  Async on the handle stream. */
 MXP_API int mxp_splitmix64_device(mxp_handle h, uint64_t seed, int64_t count, void* dOut);
+
+/* Datapath of single-matrix FP32 chains at the CTA-pair sizes (padded order
+ * n_pad = roundup(n, 128) with n_pad % 256 == 0 and n_pad >= 1024, e.g. C5):
+ *   MXP_DATAPATH_AUTO (default): K1PH — scaled fp16x2 planes, one exponent
+ *     per matrix, half the tensor work of 3xTF32 at the same 22-bit operand
+ *     precision; a chain whose product loses dynamic range (strong
+ *     cancellation, zero or non-finite) is recomputed on 3xTF32 inside the
+ *     same call (a gated chain enqueued behind it);
+ *   MXP_DATAPATH_3XTF32: always 3xTF32 (an exponent per element) — the
+ *     datapath of the row-sharded multi-GPU chains, so their results are
+ *     bitwise this single-device chain's.
+ * Other sizes and n <= 128 are unaffected.  Per handle; drops cached graphs. */
+#define MXP_DATAPATH_AUTO 0
+#define MXP_DATAPATH_3XTF32 1
+MXP_API int mxp_set_f32_datapath(mxp_handle h, int datapath);
+/* Whether the last K1PH chain of this handle raised its dynamic-range flag
+ * (its result then came from the 3xTF32 recomputation).  Synchronizes. */
+MXP_API int mxp_last_f32_fallback(mxp_handle h, int* raised);
 
 /* Which persistent kernel an n <= 128 fp32 chain of power k runs on: the
  * scaled fp16x2 K3H, or the bf16x3 K3B when K3H's accumulated tensor-core

@@ -44,6 +44,7 @@ EXPORTS = (
     "mxp_small_kernel_for", "mxp_mc_supported", "mxp_mc_create", "mxp_mc_import",
     "mxp_mc_size", "mxp_mc_bind", "mxp_mc_destroy", "mxp_gemm_rows_planes_mc",
     "mxp_copy2d_device", "mxp_last_small_fixups", "mxp_power_multi", "mxp_multi_release",
+    "mxp_set_f32_datapath", "mxp_last_f32_fallback",
 )
 MXP_IPC_HANDLE_BYTES = 72
 MXP_MC_HANDLE_BYTES = 64
@@ -138,6 +139,8 @@ def load() -> ctypes.CDLL:
             "mxp_gemm_rows_planes_mc": [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp],
             "mxp_copy2d_device": [vp, vp, sz, vp, sz, sz, sz],
             "mxp_last_small_fixups": [vp, P(i64)],
+            "mxp_set_f32_datapath": [vp, c_int],
+            "mxp_last_f32_fallback": [vp, P(c_int)],
             "mxp_power_multi": [c_int, P(c_int), c_int, i64, i64, i64, vp, vp, P(Stats)],
             "mxp_multi_release": [],
         }

@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 OUT = os.path.join(HERE, "libmatexpo_b200.so")
-SOURCES = ["mxp_api.cu", "mxp_multicast.cu", "mxp_multi.cu", "kernels_tf32.cu", "kernels_f64.cu", "kernels_gen.cu", "kernels_mod.cu", "kernels_mod_i8.cu", "kernels_k3b.cu", "kernels_k3h.cu"]
+SOURCES = ["mxp_api.cu", "mxp_multicast.cu", "mxp_multi.cu", "kernels_tf32.cu", "kernels_f64.cu", "kernels_gen.cu", "kernels_mod.cu", "kernels_mod_i8.cu", "kernels_k3b.cu", "kernels_k3h.cu", "kernels_f16x2.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]

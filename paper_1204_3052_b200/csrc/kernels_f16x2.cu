@@ -1,0 +1,389 @@
+// K1PH — the large-n FP32 chain on the 16-bit tensor datapath (sm_100a).
+//
+// The same split-FP32 idea K3H uses for n <= 128, at CTA-pair GEMM scale
+// (C5: 8192^2 A^1024).  Every power P of the chain is held as two fp16
+// planes with ONE power-of-two exponent for the whole matrix:
+//   P = 2^-t P',  max|P'| in [2^13, 2^14),  h0 = rn_fp16(P'),  h1 = rn_fp16(P' - h0)
+// (P' - h0 is exact in fp32; |P' - h0 - h1| <= 2^-22 |P'| while h1 is a
+// normal fp16, the operand precision of tf32 hi/lo), and a product is
+//   X Y = 2^-(tx + ty) (x1 y0 + x0 y1 + x0 y0)       (x1 y1 ~ 2^-22 dropped)
+// — three kind::f16 MMAs per K=16 where 3xTF32 needs three kind::tf32 MMAs
+// per K=8: half the tensor work, half the operand bytes.  The reference's
+// product is the ascending-k fp32 loop (linalg.py:151-164); parity is by the
+// relative-Frobenius tolerance.
+//
+// One exponent per matrix loses entries more than ~2^38 below the matrix max
+// (h1 underflows first, below ~2^-17 of the max).  As in K3H, the tell-tale is
+// a product that came out more than 2^12 below its bound n max|X| max|Y|
+// (strong cancellation), or a zero / non-finite product: the split of that
+// product raises the chain's flag, and the 3xTF32 chain (an exponent per
+// element), enqueued behind this one with every launch gated on the flag,
+// recomputes the whole power.  Random inputs never raise it.
+//
+// Per step: k1ph_gemm_f16x2 (CTA pairs, M = N = 256, K = 64 per stage, the
+// accumulator drained per stage into fp32 register sums as in K1P) writes
+// the unscaled fp32 product and its max |.| (atomicMax on the bit patterns);
+// split16_kernel turns it into the next step's planes with the exact scale.
+#include <cuda_fp16.h>
+
+#include <cmath>
+
+#include "mxp_internal.h"
+#include "ptx.cuh"
+#include "split16.cuh"
+
+namespace mxp {
+namespace {
+
+__device__ __forceinline__ uint8_t* align1024h(uint8_t* p) {
+    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023u) & ~uintptr_t(1023));
+}
+
+struct K1HCfg {
+    static constexpr int kStages = 3;
+    static constexpr int kBK = 64;                               // fp16 K per stage (128 B rows)
+    static constexpr uint32_t kABytes = 128u * 128u;             // one plane: 128 rows x 64 fp16
+    static constexpr uint32_t kBBytes = 64u * 128u * 2u;         // one plane: 2 panels x 64 k-rows x 128 B
+    static constexpr uint32_t kStageBytes = 2 * kABytes + 2 * kBBytes;  // 64 KB per CTA
+    static constexpr size_t kSmem = kStages * kStageBytes + 1024 + 256;
+    static constexpr int kThreads = 384;
+};
+
+// kind::f16, fp16 A/B (formats 0), fp32 D, A K-major, B MN-major, M = N = 256 (pair)
+constexpr uint32_t kIdescPair = (1u << 4) | (1u << 16) | ((256u >> 3) << 17) | ((256u >> 4) << 24);
+
+__device__ __forceinline__ void mma_f16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// 2^-(tx + ty) as two factors (each in the normal range)
+__device__ __forceinline__ void product_scale(uint32_t xmax, uint32_t ymax, float& g1, float& g2) {
+    const int pe = -(scale_exp(xmax) + scale_exp(ymax));
+    g1 = exp2i(pe / 2);
+    g2 = exp2i(pe - pe / 2);
+}
+
+}  // namespace
+
+// C = X Y over scaled fp16 planes.  Grid: 2 CTAs per 256 x 256 tile, one
+// cluster per pair (M = n_pad rows, N = n_pad columns).
+//   warp 0 : TMA producer (both CTAs; bytes complete on the leader's barrier)
+//   warp 1 : MMA issuer (leader only)     warp 2 : TMEM allocator (both)
+//   warps 4-11 : epilogue (both CTAs; lane quarter = warp % 4, 128-column half)
+// out (fp32, n_out x n_out, leading dim ld_out) = 2^-(tx+ty) * sums; omax
+// (may be null) receives max |out| over the tile as an atomicMax of bits.
+__global__ void __launch_bounds__(K1HCfg::kThreads, 1)
+    k1ph_gemm_f16x2(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUtensorMap ma1,
+                    const __grid_constant__ CUtensorMap mb0, const __grid_constant__ CUtensorMap mb1,
+                    int n_pad, float* __restrict__ out, int n_out, int ld_out,
+                    const uint32_t* __restrict__ xmax, const uint32_t* __restrict__ ymax,
+                    uint32_t* __restrict__ omax) {
+    using Cfg = K1HCfg;
+    constexpr int S = Cfg::kStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024h(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+    uint64_t* empty = full + S;
+    uint64_t* cfull = empty + S;   // [2] chunk accumulator ready (multicast by the leader)
+    uint64_t* cempty = cfull + 2;  // [2] chunk drained (leader's copy counts both CTAs)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank() & 1;  // half of the pair (A rows, B columns)
+    const bool leader = (rank == 0);
+
+    // tile raster grouped along M (as K1P)
+    constexpr int kGroupM = 8;
+    const int num_m = n_pad / 256, num_n = n_pad / 256;
+    const int pid = blockIdx.x / 2;
+    const int per_group = kGroupM * num_n;
+    const int first_m = (pid / per_group) * kGroupM;
+    const int gm = min(num_m - first_m, kGroupM);
+    const int m0 = (first_m + (pid % per_group) % gm) * 256 + static_cast<int>(rank) * 128;
+    const int n0 = ((pid % per_group) / gm) * 256;
+    const int num_kb = n_pad / Cfg::kBK;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&cfull[i], 1);
+            mbar_init(&cempty[i], 16);  // 8 epilogue warps x 2 CTAs
+        }
+        fence_mbar_init();
+        tma_prefetch(&ma0);
+        tma_prefetch(&ma1);
+        tma_prefetch(&mb0);
+        tma_prefetch(&mb1);
+    }
+    if (warp == 2) tmem_alloc_pair<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA traffic
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        for (int kb = 0; kb < num_kb; ++kb) {
+            const int st = kb % S;
+            const uint32_t ph = (kb / S) & 1;
+            mbar_wait(&empty[st], ph ^ 1);
+            uint8_t* base = smem + st * Cfg::kStageBytes;
+            if (leader) mbar_expect_tx(&full[st], 2 * Cfg::kStageBytes);
+            const int kk = kb * Cfg::kBK;
+            tma_load_2d_pair(base, &ma0, &full[st], kk, m0);
+            tma_load_2d_pair(base + Cfg::kABytes, &ma1, &full[st], kk, m0);
+            uint8_t* b0 = base + 2 * Cfg::kABytes;
+            uint8_t* b1 = b0 + Cfg::kBBytes;
+            const int nb = n0 + static_cast<int>(rank) * 128;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {  // two 64-column panels of this CTA's 128 columns
+                tma_load_2d_pair(b0 + j * 8192, &mb0, &full[st], nb + 64 * j, kk);
+                tma_load_2d_pair(b1 + j * 8192, &mb1, &full[st], nb + 64 * j, kk);
+            }
+        }
+    } else if (warp == 1 && lane == 0 && leader) {
+        const uint32_t s0 = smem_u32(smem);
+        const uint64_t da0 = kmajor_desc(s0), da1 = kmajor_desc(s0 + Cfg::kABytes);
+        // MN-major SW128: 64-column panels 8 KB apart (LBO), 8 k-rows per 1 KB atom (SBO)
+        const uint64_t db0 = smem_desc(s0 + 2 * Cfg::kABytes, 8192, 1024, 2);
+        const uint64_t db1 = smem_desc(s0 + 2 * Cfg::kABytes + Cfg::kBBytes, 8192, 1024, 2);
+        for (int kb = 0; kb < num_kb; ++kb) {
+            const int st = kb % S;
+            const uint32_t ph = (kb / S) & 1;
+            const int c = kb & 1;
+            mbar_wait(&cempty[c], ((kb >> 1) & 1) ^ 1);
+            mbar_wait(&full[st], ph);
+            tc_fence_after();
+            const uint64_t so = static_cast<uint64_t>((st * Cfg::kStageBytes) >> 4);
+            const uint32_t d = tmem + c * 256;
+            // small cross terms first (the accumulator truncates), then x0 y0
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((2048 * k) >> 4);
+                mma_f16_pair(d, da1 + ao, db0 + bo, kIdescPair, k > 0 ? 1u : 0u);
+                mma_f16_pair(d, da0 + ao, db1 + bo, kIdescPair, 1u);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((2048 * k) >> 4);
+                mma_f16_pair(d, da0 + ao, db0 + bo, kIdescPair, 1u);
+            }
+            mma_commit_pair(&empty[st], 0x3);
+            mma_commit_pair(&cfull[c], 0x3);
+        }
+    } else if (warp >= 4) {
+        const int q = warp & 3;
+        const int ch = ((warp - 4) >> 2) * 128;  // column half of the 256
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        const uint32_t cempty_leader0 = mapa_shared(smem_u32(&cempty[0]), 0);
+        float sum[128];
+#pragma unroll
+        for (int i = 0; i < 128; ++i) sum[i] = 0.f;
+        for (int kb = 0; kb < num_kb; ++kb) {
+            const int c = kb & 1;
+            mbar_wait(&cfull[c], (kb >> 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                uint32_t v[16];
+                tmem_ld16(lane_base + c * 256 + ch + 16 * g, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) sum[16 * g + i] = __fadd_rn(sum[16 * g + i], __uint_as_float(v[i]));
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster_relaxed(cempty_leader0 + 8 * c);
+        }
+        float g1, g2;
+        product_scale(__ldg(xmax), __ldg(ymax), g1, g2);
+        const int row = m0 + q * 32 + lane;
+        uint32_t mbits = 0;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int col = n0 + ch + 32 * h;
+            float* v = sum + 32 * h;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                v[i] = __fmul_rn(__fmul_rn(v[i], g1), g2);
+                mbits = max(mbits, __float_as_uint(v[i]) & 0x7FFFFFFFu);
+            }
+            if (row < n_out && col < n_out) {
+                float* d = out + static_cast<size_t>(row) * ld_out + col;
+                if ((ld_out & 3) == 0 && col + 32 <= n_out) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        reinterpret_cast<float4*>(d)[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+                } else {
+                    for (int i = 0; i < 32; ++i)
+                        if (col + i < n_out) d[i] = v[i];
+                }
+            }
+        }
+        if (omax != nullptr) {
+            mbits = __reduce_max_sync(0xFFFFFFFFu, mbits);
+            if (lane == 0) atomicMax(omax, mbits);
+        }
+    }
+    // both CTAs done with the pair's TMEM before the paired dealloc
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 2) tmem_dealloc_pair<512>(tmem);
+}
+
+namespace {
+
+// max |x| over an n x n fp32 matrix (leading dim ld) -> atomicMax of the bits
+__global__ void absmax_kernel(const float* __restrict__ in, int n, int ld, uint32_t* __restrict__ omax) {
+    uint32_t m = 0;
+    const size_t total = static_cast<size_t>(n) * n;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t r = i / n, c = i - r * n;
+        m = max(m, __float_as_uint(__ldg(in + r * ld + c)) & 0x7FFFFFFFu);
+    }
+    m = __reduce_max_sync(0xFFFFFFFFu, m);
+    if ((threadIdx.x & 31) == 0) atomicMax(omax, m);
+}
+
+// fp32 (n x n, leading dim ld) -> scaled fp16 planes h0, h1 (n_pad x n_pad,
+// zero padded) with the exact scale of *maxw.  check != 0 (block 0): the
+// dynamic-range test of the product *maxw = X Y against its bound
+// n max|X| max|Y| (xmax, ymax) — raises *flag on strong cancellation or a
+// zero / non-finite product.
+__global__ void split16_kernel(const float* __restrict__ in, int n, int ld,
+                               __half* __restrict__ h0, __half* __restrict__ h1, int n_pad,
+                               const uint32_t* __restrict__ maxw, const uint32_t* __restrict__ xmax,
+                               const uint32_t* __restrict__ ymax, int lg_n, int* __restrict__ flag) {
+    const uint32_t mb = *maxw;
+    if (flag != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint32_t xb = *xmax, yb = *ymax;
+        bool lost = mb == 0u || mb >= 0x7F800000u || xb >= 0x7F800000u || yb >= 0x7F800000u;
+        if (!lost && xb != 0u && yb != 0u) {
+            const int bound_e = (ilogb_bits(xb) + 1) + (ilogb_bits(yb) + 1) + lg_n;
+            lost = ilogb_bits(mb) < bound_e - 12;
+        }
+        if (lost) *flag = 1;
+    }
+    const int t = max(-126, min(126, scale_exp(mb)));
+    const float sc = exp2i(t);
+    const size_t groups = static_cast<size_t>(n_pad) * n_pad / 8;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < groups;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t e = i * 8;
+        const int r = static_cast<int>(e / n_pad);
+        const int c = static_cast<int>(e - static_cast<size_t>(r) * n_pad);
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = 0.f;
+        if (r < n) {
+            const float* p = in + static_cast<size_t>(r) * ld + c;
+            if ((ld & 3) == 0 && c + 7 < n) {
+                const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+                const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+                v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+                v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (c + k < n) v[k] = __ldg(p + k);
+            }
+        }
+        __align__(16) __half a0[8], a1[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float x = __fmul_rn(v[k], sc);
+            a0[k] = __float2half_rn(x);
+            a1[k] = __float2half_rn(__fsub_rn(x, __half2float(a0[k])));
+        }
+        reinterpret_cast<uint4*>(h0)[i] = *reinterpret_cast<const uint4*>(a0);
+        reinterpret_cast<uint4*>(h1)[i] = *reinterpret_cast<const uint4*>(a1);
+    }
+}
+
+}  // namespace
+
+cudaError_t prepare_f16x2_kernels() {
+    return cudaFuncSetAttribute(k1ph_gemm_f16x2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(K1HCfg::kSmem));
+}
+
+bool k1ph_eligible(int64_t n_pad) { return n_pad % 256 == 0 && n_pad >= 1024; }
+
+// fp16 plane map: box {64 columns (128 B), box_rows}, SWIZZLE_128B — the
+// K-major left-operand box (128 rows) and the MN-major right-operand panel
+// (64 k-rows) over the same row-major plane.
+bool encode_plane16_map(CUtensorMap* map, const void* plane, int n_pad, int box_rows) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn fn = nullptr;
+    if (fn == nullptr) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+        fn = reinterpret_cast<EncodeFn>(p);
+    }
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(n_pad), static_cast<cuuint64_t>(n_pad)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(n_pad) * 2};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(plane), dims, strides, box,
+              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, float* out, int n_out,
+                             int ld_out, const uint32_t* xmax, const uint32_t* ymax, uint32_t* omax,
+                             cudaStream_t s) {
+    if (!k1ph_eligible(n_pad)) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * (n_pad / 256) * (n_pad / 256));
+    cfg.blockDim = dim3(K1HCfg::kThreads);
+    cfg.dynamicSmemBytes = K1HCfg::kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k1ph_gemm_f16x2, x.a0, x.a1, y.b0, y.b1, n_pad, out, n_out, ld_out,
+                              xmax, ymax, omax);
+}
+
+cudaError_t launch_absmax(const float* in, int n, int ld, uint32_t* omax, cudaStream_t s) {
+    const size_t total = static_cast<size_t>(n) * n;
+    int blocks = static_cast<int>((total + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    absmax_kernel<<<blocks, 256, 0, s>>>(in, n, ld, omax);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_split16(const float* in, int n, int ld, void* h0, void* h1, int n_pad,
+                           const uint32_t* maxw, const uint32_t* xmax, const uint32_t* ymax,
+                           int* flag, cudaStream_t s) {
+    int lg_n = 0;
+    while ((1ll << lg_n) < n) ++lg_n;
+    const size_t groups = static_cast<size_t>(n_pad) * n_pad / 8;
+    int blocks = static_cast<int>((groups + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    split16_kernel<<<blocks, 256, 0, s>>>(in, n, ld, static_cast<__half*>(h0), static_cast<__half*>(h1),
+                                          n_pad, maxw, xmax, ymax, lg_n, flag);
+    return cudaGetLastError();
+}
+
+}  // namespace mxp

@@ -70,10 +70,11 @@ cudaError_t launch_k3_batched(const float* in, float* out, int n, int64_t batch,
 // ======================================================================
 __global__ void split_pad_kernel(const float* __restrict__ in, int n, int ld,
                                  uint32_t* __restrict__ hi, uint32_t* __restrict__ lo,
-                                 int n_pad, int rows, int rows_pad) {
+                                 int n_pad, int rows, int rows_pad, const int* __restrict__ gate) {
     // a programmatically dependent K1C may start its prologue now; it waits
     // (griddepcontrol.wait) for this grid to complete before reading the planes
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (gate != nullptr && *gate == 0) return;  // gated fallback chain, not needed
     const size_t quads = static_cast<size_t>(rows_pad) * n_pad / 4;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < quads;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -103,16 +104,16 @@ __global__ void split_pad_kernel(const float* __restrict__ in, int n, int ld,
 }
 
 cudaError_t launch_split(const float* in, int n, int ld, uint32_t* hi, uint32_t* lo, int n_pad,
-                         cudaStream_t s) {
-    return launch_split_rows(in, n, ld, n, hi, lo, n_pad, n_pad, s);
+                         cudaStream_t s, const int* gate) {
+    return launch_split_rows(in, n, ld, n, hi, lo, n_pad, n_pad, s, gate);
 }
 
 cudaError_t launch_split_rows(const float* in, int n, int ld, int rows, uint32_t* hi, uint32_t* lo,
-                              int n_pad, int rows_pad, cudaStream_t s) {
+                              int n_pad, int rows_pad, cudaStream_t s, const int* gate) {
     const size_t quads = static_cast<size_t>(rows_pad) * n_pad / 4;
     int blocks = static_cast<int>((quads + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    split_pad_kernel<<<blocks, 256, 0, s>>>(in, n, ld, hi, lo, n_pad, rows, rows_pad);
+    split_pad_kernel<<<blocks, 256, 0, s>>>(in, n, ld, hi, lo, n_pad, rows, rows_pad, gate);
     return cudaGetLastError();
 }
 
@@ -434,7 +435,10 @@ __global__ void __launch_bounds__(K1PCfg::kThreads, 1)
                     const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
                     int n_pad, int m_pad, float* __restrict__ out_f32, int n_out, int m_out,
                     int ld_out, uint32_t* __restrict__ out_hi, uint32_t* __restrict__ out_lo,
-                    const __grid_constant__ PeerOut po) {
+                    const __grid_constant__ PeerOut po, const int* __restrict__ gate) {
+    // gated fallback chain (behind a K1PH chain): nothing to do unless raised;
+    // every CTA reads the same word, so whole clusters leave together
+    if (gate != nullptr && *gate == 0) return;
     using Cfg = K1PCfg;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -1193,7 +1197,7 @@ cudaError_t launch_progress_mark(uint32_t* progress, uint32_t value, int trap, c
 #endif
 static cudaError_t launch_k1p(const GemmPlanes& m, int n_pad, int m_pad, float* out_f32, int n_out,
                               int m_out, int ld_out, uint32_t* out_hi, uint32_t* out_lo,
-                              const PeerOut& po, cudaStream_t s) {
+                              const PeerOut& po, cudaStream_t s, const int* gate = nullptr) {
     const int pairs = (MXP_K1P_MAX_PAIRS >= 2 && (n_pad / 256) % 2 == 0) ? 2 : 1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * (n_pad / 256) * (m_pad / 256));
@@ -1210,10 +1214,10 @@ static cudaError_t launch_k1p(const GemmPlanes& m, int n_pad, int m_pad, float* 
 #if MXP_K1P_MAX_PAIRS >= 2
     if (pairs == 2)
         return cudaLaunchKernelEx(&cfg, k1p_gemm_3xtf32<2>, m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad,
-                                  m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo, po);
+                                  m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo, po, gate);
 #endif
     return cudaLaunchKernelEx(&cfg, k1p_gemm_3xtf32<1>, m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad,
-                              m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo, po);
+                              m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo, po, gate);
 }
 
 cudaError_t launch_k1p_gemm_peers(const GemmPlanes& m, int n_pad, int m_pad, int ld_out,
@@ -1258,7 +1262,7 @@ cudaError_t launch_peer_barrier(uint32_t* const* flags, int npeers, int rank, ui
 
 cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int block_n,
                                 float* out_f32, int n_out, int m_out, int ld_out, uint32_t* out_hi,
-                                uint32_t* out_lo, cudaStream_t s, int splits) {
+                                uint32_t* out_lo, cudaStream_t s, int splits, const int* gate) {
     if (block_n == 128 && splits > 1) {
         // split-K in one launch: the splits of a tile form a cluster and
         // reduce through distributed shared memory
@@ -1279,7 +1283,7 @@ cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int b
     }
     if (block_n == 256) {  // CTA-pair kernel: n_pad, m_pad multiples of 256
         return launch_k1p(m, n_pad, m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo,
-                          PeerOut{}, s);
+                          PeerOut{}, s, gate);
     }
     dim3 grid((n_pad / K1Cfg::kBN) * (m_pad / 128), 1);
     k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(

@@ -38,6 +38,7 @@ cudaError_t prepare_kernels() {
     if (e == cudaSuccess) e = prepare_k3b_kernel();
     if (e == cudaSuccess) e = prepare_k3h_kernel();
     if (e == cudaSuccess) e = prepare_mod_i8_kernel();
+    if (e == cudaSuccess) e = prepare_f16x2_kernels();
     return e;
 }
 
@@ -204,6 +205,18 @@ struct mxp_handle_s {
     // any other use of the workspace invalidates it
     int rhs_mode = -1;
     int64_t rhs_n = 0;
+    // K1PH workspace (scaled fp16x2 chain): h0/h1 planes of base, ping, pong,
+    // the fp32 product of the running step, and the chain state: maxw[0] =
+    // max|A| bits, maxw[s + 1] = max|product of step s| bits, then the
+    // dynamic-range flag that gates the 3xTF32 recomputation
+    int f32_datapath = MXP_DATAPATH_AUTO;
+    int64_t ws16_pad = 0;  // padded order the maps are encoded for
+    int64_t ws16_cap = 0;  // padded order the buffers are allocated for
+    void* planes16[6] = {};
+    float* fbuf = nullptr;
+    uint32_t* f16state = nullptr;  // [kF16Steps + 1] maxima, then the flag
+    F16Maps maps16[3];
+    bool f16_ran = false;  // the last chain ran K1PH (mxp_last_f32_fallback)
     // fp64 workspace: base, ping, pong (n_pad^2 doubles)
     int64_t ws64_pad = 0;
     double* f64buf[3] = {};
@@ -332,6 +345,45 @@ int encode_ws32(mxp_handle h, int64_t n_pad) {
     return MXP_OK;
 }
 
+constexpr int kF16Steps = 128;  // plan steps (k < 2^63: at most 126)
+constexpr size_t kF16StateBytes = (kF16Steps + 2) * sizeof(uint32_t);
+
+// K1PH workspace for n_pad (allocated for the largest order seen; the TMA
+// maps are re-encoded when the order changes — captured graphs keep their own
+// copies, and the buffers they point into stay allocated).
+int ensure_ws16(mxp_handle h, int64_t n_pad) {
+    if (h->ws16_pad == n_pad) return MXP_OK;
+    if (h->ws16_cap < n_pad) {
+        h->drop_graphs();
+        for (auto& p : h->planes16) {
+            if (p) cudaFree(p);
+            p = nullptr;
+        }
+        if (h->fbuf) cudaFree(h->fbuf);
+        h->fbuf = nullptr;
+        h->ws16_cap = h->ws16_pad = 0;
+        const size_t n2 = static_cast<size_t>(n_pad) * n_pad;
+        for (auto& p : h->planes16) MXP_CUDA(cudaMalloc(&p, n2 * 2));
+        MXP_CUDA(cudaMalloc(&h->fbuf, n2 * 4));
+        h->ws16_cap = n_pad;
+    }
+    if (!h->f16state) MXP_CUDA(cudaMalloc(&h->f16state, kF16StateBytes));
+    for (int i = 0; i < 3; ++i) {
+        F16Maps& m = h->maps16[i];
+        if (!encode_plane16_map(&m.a0, h->planes16[2 * i], (int)n_pad, 128) ||
+            !encode_plane16_map(&m.a1, h->planes16[2 * i + 1], (int)n_pad, 128) ||
+            !encode_plane16_map(&m.b0, h->planes16[2 * i], (int)n_pad, 64) ||
+            !encode_plane16_map(&m.b1, h->planes16[2 * i + 1], (int)n_pad, 64))
+            return fail(MXP_E_CUDA, "cuTensorMapEncodeTiled (fp16) failed (n_pad=%lld)", (long long)n_pad);
+    }
+    h->ws16_pad = n_pad;
+    return MXP_OK;
+}
+
+bool use_k1ph(mxp_handle h, int64_t n) {
+    return h->f32_datapath == MXP_DATAPATH_AUTO && n > kSmallMax && k1ph_eligible(round_up(n, 128));
+}
+
 int ensure_ws64(mxp_handle h, int64_t n_pad) {
     h->rhs_mode = -1;
     if (h->ws64_pad >= n_pad) return MXP_OK;
@@ -366,9 +418,70 @@ int ensure_io(mxp_handle h, size_t bytes) {
 
 // ---- enqueue helpers (no validation; stream = h->stream) -----------------
 
-// 3xTF32 chain for n > kSmallMax through K1, planes padded to 128.
+int enqueue_chain_tf32(mxp_handle h, int64_t n, const PlanBits& plan, const float* dA,
+                       float* dOut, int64_t* launches, int64_t* failed, const int* gate);
+
+// K1PH chain (scaled fp16x2 planes, one exponent per matrix), then the 3xTF32
+// chain gated on the dynamic-range flag the splits raise (no-op launches
+// unless a product lost range).  Planes: 0 base, 1 ping, 2 pong.
+int enqueue_chain_f16x2(mxp_handle h, int64_t n, const PlanBits& plan, const float* dA,
+                        float* dOut, int64_t* launches, int64_t* failed) {
+    const int64_t n_pad = round_up(n, 128);
+    int rc = ensure_ws16(h, n_pad);
+    if (rc) return rc;
+    const int np = (int)n_pad;
+    uint32_t* maxw = h->f16state;
+    int* flag = reinterpret_cast<int*>(h->f16state + kF16Steps + 1);
+    cudaError_t e = cudaMemsetAsync(h->f16state, 0, kF16StateBytes, h->stream);
+    if (e == cudaSuccess) e = launch_absmax(dA, (int)n, (int)n, maxw, h->stream);
+    if (e == cudaSuccess)
+        e = launch_split16(dA, (int)n, (int)n, h->planes16[0], h->planes16[1], np, maxw, nullptr,
+                           nullptr, nullptr, h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "k1ph split");
+    *launches += 2;
+    int acc = 0, acc_m = 0;  // plane pair of the running power, index of its max
+    for (int s = 0; s < plan.len; ++s) {
+        const bool mult = plan_is_mult(plan, s);
+        const bool last = (s == plan.len - 1);
+        const int dst = (acc == 1) ? 2 : 1;
+        const int rhs = mult ? 0 : acc, rhs_m = mult ? 0 : acc_m;
+        e = launch_progress_mark(h->progress_dev, static_cast<uint32_t>(s + 1), s == h->fault_step,
+                                 h->stream);
+        if (e == cudaSuccess)
+            e = launch_k1ph_gemm(h->maps16[acc], h->maps16[rhs], np, last ? dOut : h->fbuf,
+                                 last ? (int)n : np, last ? (int)n : np, maxw + acc_m, maxw + rhs_m,
+                                 last ? nullptr : maxw + s + 1, h->stream);
+        if (e == cudaSuccess && !last)
+            e = launch_split16(h->fbuf, np, np, h->planes16[2 * dst], h->planes16[2 * dst + 1], np,
+                               maxw + s + 1, maxw + acc_m, maxw + rhs_m, flag, h->stream);
+        if (e != cudaSuccess) {
+            *failed = s;
+            return cuda_fail(e, "k1ph_gemm_f16x2");
+        }
+        *launches += last ? 2 : 3;
+        acc = dst;
+        acc_m = s + 1;
+    }
+    // the 3xTF32 recomputation, every launch gated on the flag
+    int64_t gated = 0;
+    rc = enqueue_chain_tf32(h, n, plan, dA, dOut, &gated, failed, flag);
+    *launches += gated;
+    return rc;
+}
+
+// Single-matrix FP32 chain for n > kSmallMax: K1PH at the CTA-pair sizes
+// (MXP_DATAPATH_AUTO), else 3xTF32 through K1 / K1C / K1P.
 int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float* dA,
                       float* dOut, int64_t* launches, int64_t* failed) {
+    h->f16_ran = use_k1ph(h, n);
+    if (h->f16_ran) return enqueue_chain_f16x2(h, n, plan, dA, dOut, launches, failed);
+    return enqueue_chain_tf32(h, n, plan, dA, dOut, launches, failed, nullptr);
+}
+
+// 3xTF32 chain for n > kSmallMax through K1, planes padded to 128.  gate
+// (device, may be null): every launch is a no-op unless *gate != 0.
+int enqueue_chain_tf32(mxp_handle h, int64_t n, const PlanBits& plan, const float* dA,
+                       float* dOut, int64_t* launches, int64_t* failed, const int* gate) {
     const int64_t n_pad = round_up(n, 128);
     int rc = ensure_ws32(h, n_pad);
     if (rc) return rc;
@@ -376,10 +489,10 @@ int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float
     if (rc) return rc;
     const int np = (int)h->ws32_pad;  // planes are laid out with the workspace stride
     const int bn = k1_block_n(np, h->num_sms);
-    cudaError_t e = launch_split(dA, (int)n, (int)n, h->planes[0], h->planes[1], np, h->stream);
+    cudaError_t e = launch_split(dA, (int)n, (int)n, h->planes[0], h->planes[1], np, h->stream, gate);
     if (e != cudaSuccess) return cuda_fail(e, "split");
     ++*launches;
-    if (bn == 128) {
+    if (bn == 128 && gate == nullptr) {
         // the whole chain in one launch when every split-K cluster fits at once
         e = launch_k1c_chain(h->map_a, h->map_b, h->planes, plan, np, h->splits, dOut, (int)n,
                              h->bar_ctr, h->progress_dev, h->fault_step, h->stream);
@@ -395,13 +508,15 @@ int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float
         const bool last = (s == plan.len - 1);
         const int dst = (acc == 1) ? 2 : 1;
         const int rhs = mult ? 0 : acc;
-        e = launch_progress_mark(h->progress_dev, static_cast<uint32_t>(s + 1), s == h->fault_step,
-                                 h->stream);
-        if (e != cudaSuccess) {
-            *failed = s;
-            return cuda_fail(e, "progress mark");
+        if (gate == nullptr) {  // (a gated recomputation keeps the K1PH chain's marks)
+            e = launch_progress_mark(h->progress_dev, static_cast<uint32_t>(s + 1),
+                                     s == h->fault_step, h->stream);
+            if (e != cudaSuccess) {
+                *failed = s;
+                return cuda_fail(e, "progress mark");
+            }
+            ++*launches;
         }
-        ++*launches;
         GemmPlanes m;
         m.a_hi = h->map_a[2 * acc];
         m.a_lo = h->map_a[2 * acc + 1];
@@ -409,7 +524,7 @@ int enqueue_chain_f32(mxp_handle h, int64_t n, const PlanBits& plan, const float
         m.b_lo = h->map_b[2 * rhs + 1];
         e = launch_k1_gemm_rows(m, np, np, bn, last ? dOut : nullptr, (int)n, (int)n, (int)n,
                                 last ? nullptr : h->planes[2 * dst],
-                                last ? nullptr : h->planes[2 * dst + 1], h->stream, h->splits);
+                                last ? nullptr : h->planes[2 * dst + 1], h->stream, h->splits, gate);
         if (e != cudaSuccess) {
             *failed = s;
             return cuda_fail(e, "k1_gemm_3xtf32");
@@ -526,6 +641,7 @@ int run_power_graph(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA
         // workspace must exist before capture (no cudaMalloc inside capture)
         if (mode == MXP_F32 && n > kSmallMax) {
             int rc = ensure_ws32(h, round_up(n, 128));
+            if (rc == MXP_OK && use_k1ph(h, n)) rc = ensure_ws16(h, round_up(n, 128));
             if (rc) return rc;
         } else if (mode == MXP_F64) {
             int rc = ensure_ws64(h, f64_pad((int)n));
@@ -551,6 +667,7 @@ int run_power_graph(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA
     // the chain overwrites the workspace planes a prepared right-hand side
     // lives in (cache hit or miss alike)
     h->rhs_mode = -1;
+    h->f16_ran = mode == MXP_F32 && use_k1ph(h, n);
     it->second.last_use = ++h->graph_clock;
     cudaError_t e = cudaGraphLaunch(it->second.exec, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
@@ -681,6 +798,10 @@ int mxp_destroy(mxp_handle h) {
     h->drop_graphs();
     for (auto p : h->planes)
         if (p) cudaFree(p);
+    for (auto p : h->planes16)
+        if (p) cudaFree(p);
+    if (h->fbuf) cudaFree(h->fbuf);
+    if (h->f16state) cudaFree(h->f16state);
     if (h->bar_ctr) cudaFree(h->bar_ctr);
     if (h->stamps) cudaFree(h->stamps);
     if (h->fix) cudaFree(h->fix);
@@ -1387,6 +1508,32 @@ int mxp_small_kernel_for(int64_t n, int64_t k, int* kernel) {
     if (n < 1 || n > kSmallMax || k < 2)
         return fail(MXP_E_VALIDATION, "needs 1 <= n <= %d and k >= 2", kSmallMax);
     *kernel = k3_route(static_cast<int>(n), make_plan(k)) == 0 ? MXP_KERNEL_K3H : MXP_KERNEL_K3B;
+    return MXP_OK;
+}
+
+int mxp_set_f32_datapath(mxp_handle h, int datapath) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (datapath != MXP_DATAPATH_AUTO && datapath != MXP_DATAPATH_3XTF32)
+        return fail(MXP_E_VALIDATION, "unknown f32 datapath %d", datapath);
+    if (datapath != h->f32_datapath) {
+        MXP_CUDA(cudaStreamSynchronize(h->stream));
+        h->drop_graphs();  // cached chains were captured for the other datapath
+        h->f32_datapath = datapath;
+    }
+    return MXP_OK;
+}
+
+int mxp_last_f32_fallback(mxp_handle h, int* raised) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (!raised) return fail(MXP_E_VALIDATION, "null argument");
+    if (!h->f16_ran || !h->f16state) return fail(MXP_E_UNSUPPORTED, "no K1PH chain ran on this handle");
+    MXP_CUDA(cudaSetDevice(h->device));
+    MXP_CUDA(cudaStreamSynchronize(h->stream));
+    int flag = 0;
+    MXP_CUDA(cudaMemcpy(&flag, h->f16state + kF16Steps + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    *raised = flag != 0;
     return MXP_OK;
 }
 

@@ -60,7 +60,7 @@ cudaError_t launch_k3h_batched(const float* in, float* out, int n, int64_t batch
 
 // fp32 (n x n, leading dim ld) -> tf32 hi/lo planes (n_pad x n_pad, zero pad).
 cudaError_t launch_split(const float* in, int n, int ld, uint32_t* hi, uint32_t* lo, int n_pad,
-                         cudaStream_t s);
+                         cudaStream_t s, const int* gate = nullptr);
 // identity (k = 0) into an n x n fp32 / fp64 buffer
 cudaError_t launch_identity_f32(float* out, int n, cudaStream_t s);
 cudaError_t launch_identity_f64(double* out, int n, cudaStream_t s);
@@ -104,7 +104,8 @@ cudaError_t launch_k1_gemm(const GemmPlanes& maps, int n_pad, int block_n, float
 // tile launched as one cluster and reduced deterministically through DSMEM.
 cudaError_t launch_k1_gemm_rows(const GemmPlanes& maps, int n_pad, int m_pad, int block_n,
                                 float* out_f32, int n_out, int m_out, int ld_out, uint32_t* out_hi,
-                                uint32_t* out_lo, cudaStream_t s, int splits = 1);
+                                uint32_t* out_lo, cudaStream_t s, int splits = 1,
+                                const int* gate = nullptr);
 int k1_split_k(int n_pad, int m_pad, int num_sms);
 // K1C: the whole 3xTF32 chain in one launch (kernels_tf32.cu);
 // cudaErrorNotSupported / a launch error => run the per-step chain
@@ -121,7 +122,33 @@ cudaError_t launch_progress_mark(uint32_t* progress, uint32_t value, int trap, c
 // whether K1C runs the chain on 64-column tiles (2 x tiles x splits CTAs in one wave)
 bool k1c_narrow(int n_pad, int splits);
 cudaError_t launch_split_rows(const float* in, int n, int ld, int rows, uint32_t* hi, uint32_t* lo,
-                              int n_pad, int rows_pad, cudaStream_t s);
+                              int n_pad, int rows_pad, cudaStream_t s, const int* gate = nullptr);
+
+// ---- K1PH (kernels_f16x2.cu): the large-n chain on scaled fp16x2 planes ----
+// gate (device, may be null) on the 3xTF32 launches above: the kernel does
+// nothing unless *gate != 0 (the fallback chain enqueued behind a K1PH chain
+// runs only when that chain raised its dynamic-range flag).
+struct F16Maps {
+    CUtensorMap a0, a1;  // h0 / h1 as the K-major left operand: box {64, 128}, SWIZZLE_128B
+    CUtensorMap b0, b1;  // h0 / h1 as the MN-major right operand: box {64, 64}, SWIZZLE_128B
+};
+cudaError_t prepare_f16x2_kernels();
+bool k1ph_eligible(int64_t n_pad);  // n_pad % 256 == 0 && n_pad >= 1024 (K1P's sizes)
+bool encode_plane16_map(CUtensorMap* map, const void* plane, int n_pad, int box_rows);
+// out = X Y (fp32, n_out x n_out, leading dim ld_out) from the planes of X
+// (left) and Y (right) whose fp32 maxima are *xmax / *ymax (bit patterns);
+// *omax (may be null) <- max |out| (atomicMax of bits, zeroed beforehand)
+cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, float* out, int n_out,
+                             int ld_out, const uint32_t* xmax, const uint32_t* ymax, uint32_t* omax,
+                             cudaStream_t s);
+// *omax <- max(*omax, max |in|) over n x n (leading dim ld)
+cudaError_t launch_absmax(const float* in, int n, int ld, uint32_t* omax, cudaStream_t s);
+// fp32 n x n (leading dim ld) -> h0 / h1 planes (n_pad x n_pad, zero padded)
+// at the exact scale of *maxw; flag (may be null): raised when the product
+// *maxw = X Y lost dynamic range against its bound n max|X| max|Y|
+cudaError_t launch_split16(const float* in, int n, int ld, void* h0, void* h1, int n_pad,
+                           const uint32_t* maxw, const uint32_t* xmax, const uint32_t* ymax,
+                           int* flag, cudaStream_t s);
 
 // ---- generation (kernels_gen.cu) -------------------------------------------
 // Reference random_matrix (linalg.py:127-148) on device; scale != 0 selects

@@ -326,6 +326,22 @@ class Engine:
                                              ctypes.c_uint64(seed0 & (2**64 - 1)), lo, hi, scale,
                                              ctypes.c_void_p(d_out)), "mxp_random_device")
 
+    def set_f32_datapath(self, datapath: str) -> None:
+        """FP32 chains at the CTA-pair sizes (n_pad % 256 == 0, n_pad >= 1024):
+        "auto" = K1PH (scaled fp16x2, 3xTF32 recomputation when a product
+        loses dynamic range), "3xtf32" = always 3xTF32 (the row-sharded
+        multi-GPU chains' datapath)."""
+        codes = {"auto": 0, "3xtf32": 1}
+        if datapath not in codes:
+            raise ValueError(f"unknown f32 datapath {datapath!r} (auto | 3xtf32)")
+        _lib.check(self._L.mxp_set_f32_datapath(self._h, codes[datapath]), "mxp_set_f32_datapath")
+
+    def last_f32_fallback(self) -> bool:
+        """Whether the last K1PH chain was recomputed on 3xTF32 (dynamic range)."""
+        c = ctypes.c_int()
+        _lib.check(self._L.mxp_last_f32_fallback(self._h, ctypes.byref(c)), "mxp_last_f32_fallback")
+        return bool(c.value)
+
     def last_small_fixups(self) -> int:
         """Matrices of the last n <= 128 launch that K3B recomputed (dynamic range)."""
         c = ctypes.c_int64()

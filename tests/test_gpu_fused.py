@@ -35,6 +35,7 @@ def _worker(rank, world, port, n, ks, q):
     try:
         torch.cuda.set_device(0)
         eng = mx.Engine(0)
+        eng.set_f32_datapath("3xtf32")  # the row shards' datapath: bitwise comparable
         a_np = oracle.scaled_input(n, np.float32, 42)
         a = torch.from_numpy(a_np).cuda()
         res = {}
@@ -97,6 +98,7 @@ def test_fused_exchange_nvls_multicast_single_rank_bitwise():
     from paper_1204_3052_b200 import distributed as D
 
     eng = mx.Engine(0)
+    eng.set_f32_datapath("3xtf32")
     if not eng.mc_supported():
         pytest.skip("no NVLS multicast on this device")
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
