@@ -71,19 +71,40 @@ __device__ __forceinline__ void product_scale(uint32_t xmax, uint32_t ymax, floa
 
 }  // namespace
 
-// C = X Y over scaled fp16 planes.  Grid: 2 CTAs per 256 x 256 tile, one
-// cluster per pair (M = n_pad rows, N = n_pad columns).
+// Per-chain state (device memory, zeroed before the chain): index 0 is the
+// base A, index s + 1 the product of plan step s.
+//   maxw[i]  max |P_i| (fp32 bit pattern, atomicMax by the producing GEMM)
+//   texp[i]  the planes of P_i hold P_i * 2^texp[i]
+//   bexp[i]  floor(log2) bound of P_i's magnitude: max|P_i| < 2^bexp[i]
+//   flag     a product lost dynamic range (-> the gated 3xTF32 recomputation)
+struct F16Chain {
+    uint32_t maxw[kF16MaxSteps + 1];
+    int texp[kF16MaxSteps + 1];
+    int bexp[kF16MaxSteps + 1];
+    int flag;
+};
+
+// C = X Y over scaled fp16 planes, persistent: one CTA pair per two SMs
+// walks the 256 x 256 tiles (grouped raster), so a tile's epilogue (scale,
+// split, stores) overlaps the next tile's first MMAs (the two 256-column
+// chunk accumulators run ahead of the drain).
 //   warp 0 : TMA producer (both CTAs; bytes complete on the leader's barrier)
 //   warp 1 : MMA issuer (leader only)     warp 2 : TMEM allocator (both)
 //   warps 4-11 : epilogue (both CTAs; lane quarter = warp % 4, 128-column half)
-// out (fp32, n_out x n_out, leading dim ld_out) = 2^-(tx+ty) * sums; omax
-// (may be null) receives max |out| over the tile as an atomicMax of bits.
+// Output, with P = 2^-(texp[xi] + texp[yi]) * sums:
+//   out != nullptr: P as fp32 (n_out x n_out, leading dim ld_out) — the last step;
+//   else: the next step's planes at the bound scale t = 14 - bexp[oi],
+//     bexp[oi] = (ilogb max|X| + 1) + (ilogb max|Y| + 1) + lg_n, so
+//     |P * 2^t| < 2^14 (no fp16 overflow) without waiting for P's own max
+//     (K3H's bound-based scale); max|P| -> maxw[oi].
+// CTA 0 also runs the dynamic-range test on the LEFT operand P_xi (xi > 0):
+// zero, non-finite, or more than 2^12 below its bound raises st->flag.
 __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
     k1ph_gemm_f16x2(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUtensorMap ma1,
                     const __grid_constant__ CUtensorMap mb0, const __grid_constant__ CUtensorMap mb1,
-                    int n_pad, float* __restrict__ out, int n_out, int ld_out,
-                    const uint32_t* __restrict__ xmax, const uint32_t* __restrict__ ymax,
-                    uint32_t* __restrict__ omax) {
+                    int n_pad, int lg_n, float* __restrict__ out, int n_out, int ld_out,
+                    __half* __restrict__ o0, __half* __restrict__ o1, F16Chain* __restrict__ st,
+                    int xi, int yi, int oi) {
     using Cfg = K1HCfg;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -99,16 +120,19 @@ __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
     const uint32_t rank = cluster_ctarank() & 1;  // half of the pair (A rows, B columns)
     const bool leader = (rank == 0);
 
-    // tile raster grouped along M (as K1P)
+    // grouped tile raster (as K1P); pair p takes tiles p, p + P, p + 2P, ...
     constexpr int kGroupM = 8;
     const int num_m = n_pad / 256, num_n = n_pad / 256;
-    const int pid = blockIdx.x / 2;
+    const int num_tiles = num_m * num_n;
     const int per_group = kGroupM * num_n;
-    const int first_m = (pid / per_group) * kGroupM;
-    const int gm = min(num_m - first_m, kGroupM);
-    const int m0 = (first_m + (pid % per_group) % gm) * 256 + static_cast<int>(rank) * 128;
-    const int n0 = ((pid % per_group) / gm) * 256;
     const int num_kb = n_pad / Cfg::kBK;
+    const int pairs = gridDim.x / 2;
+    auto tile_origin = [&](int tile, int& m0, int& n0) {
+        const int first_m = (tile / per_group) * kGroupM;
+        const int gm = min(num_m - first_m, kGroupM);
+        m0 = (first_m + (tile % per_group) % gm) * 256 + static_cast<int>(rank) * 128;
+        n0 = ((tile % per_group) / gm) * 256;
+    };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
@@ -133,22 +157,27 @@ __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0 && lane == 0) {
-        for (int kb = 0; kb < num_kb; ++kb) {
-            const int st = kb % S;
-            const uint32_t ph = (kb / S) & 1;
-            mbar_wait(&empty[st], ph ^ 1);
-            uint8_t* base = smem + st * Cfg::kStageBytes;
-            if (leader) mbar_expect_tx(&full[st], 2 * Cfg::kStageBytes);
-            const int kk = kb * Cfg::kBK;
-            tma_load_2d_pair(base, &ma0, &full[st], kk, m0);
-            tma_load_2d_pair(base + Cfg::kABytes, &ma1, &full[st], kk, m0);
-            uint8_t* b0 = base + 2 * Cfg::kABytes;
-            uint8_t* b1 = b0 + Cfg::kBBytes;
+        uint32_t g = 0;  // k-blocks issued by this CTA over all its tiles
+        for (int tile = blockIdx.x / 2; tile < num_tiles; tile += pairs) {
+            int m0, n0;
+            tile_origin(tile, m0, n0);
             const int nb = n0 + static_cast<int>(rank) * 128;
+            for (int kb = 0; kb < num_kb; ++kb, ++g) {
+                const uint32_t stg = g % S;
+                const uint32_t ph = (g / S) & 1;
+                mbar_wait(&empty[stg], ph ^ 1);
+                uint8_t* base = smem + stg * Cfg::kStageBytes;
+                if (leader) mbar_expect_tx(&full[stg], 2 * Cfg::kStageBytes);
+                const int kk = kb * Cfg::kBK;
+                tma_load_2d_pair(base, &ma0, &full[stg], kk, m0);
+                tma_load_2d_pair(base + Cfg::kABytes, &ma1, &full[stg], kk, m0);
+                uint8_t* b0 = base + 2 * Cfg::kABytes;
+                uint8_t* b1 = b0 + Cfg::kBBytes;
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {  // two 64-column panels of this CTA's 128 columns
-                tma_load_2d_pair(b0 + j * 8192, &mb0, &full[st], nb + 64 * j, kk);
-                tma_load_2d_pair(b1 + j * 8192, &mb1, &full[st], nb + 64 * j, kk);
+                for (int j = 0; j < 2; ++j) {  // two 64-column panels of this CTA's 128 columns
+                    tma_load_2d_pair(b0 + j * 8192, &mb0, &full[stg], nb + 64 * j, kk);
+                    tma_load_2d_pair(b1 + j * 8192, &mb1, &full[stg], nb + 64 * j, kk);
+                }
             }
         }
     } else if (warp == 1 && lane == 0 && leader) {
@@ -157,81 +186,129 @@ __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
         // MN-major SW128: 64-column panels 8 KB apart (LBO), 8 k-rows per 1 KB atom (SBO)
         const uint64_t db0 = smem_desc(s0 + 2 * Cfg::kABytes, 8192, 1024, 2);
         const uint64_t db1 = smem_desc(s0 + 2 * Cfg::kABytes + Cfg::kBBytes, 8192, 1024, 2);
-        for (int kb = 0; kb < num_kb; ++kb) {
-            const int st = kb % S;
-            const uint32_t ph = (kb / S) & 1;
-            const int c = kb & 1;
-            mbar_wait(&cempty[c], ((kb >> 1) & 1) ^ 1);
-            mbar_wait(&full[st], ph);
-            tc_fence_after();
-            const uint64_t so = static_cast<uint64_t>((st * Cfg::kStageBytes) >> 4);
-            const uint32_t d = tmem + c * 256;
-            // small cross terms first (the accumulator truncates), then x0 y0
+        uint32_t g = 0;
+        for (int tile = blockIdx.x / 2; tile < num_tiles; tile += pairs) {
+            for (int kb = 0; kb < num_kb; ++kb, ++g) {
+                const uint32_t stg = g % S;
+                const uint32_t ph = (g / S) & 1;
+                const uint32_t c = g & 1;
+                mbar_wait(&cempty[c], ((g >> 1) & 1) ^ 1);
+                mbar_wait(&full[stg], ph);
+                tc_fence_after();
+                const uint64_t so = static_cast<uint64_t>((stg * Cfg::kStageBytes) >> 4);
+                const uint32_t d = tmem + c * 256;
+                // small cross terms first (the accumulator truncates), then x0 y0
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((2048 * k) >> 4);
-                mma_f16_pair(d, da1 + ao, db0 + bo, kIdescPair, k > 0 ? 1u : 0u);
-                mma_f16_pair(d, da0 + ao, db1 + bo, kIdescPair, 1u);
-            }
+                for (int k = 0; k < 4; ++k) {
+                    const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((2048 * k) >> 4);
+                    mma_f16_pair(d, da1 + ao, db0 + bo, kIdescPair, k > 0 ? 1u : 0u);
+                    mma_f16_pair(d, da0 + ao, db1 + bo, kIdescPair, 1u);
+                }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((2048 * k) >> 4);
-                mma_f16_pair(d, da0 + ao, db0 + bo, kIdescPair, 1u);
+                for (int k = 0; k < 4; ++k) {
+                    const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((2048 * k) >> 4);
+                    mma_f16_pair(d, da0 + ao, db0 + bo, kIdescPair, 1u);
+                }
+                mma_commit_pair(&empty[stg], 0x3);
+                mma_commit_pair(&cfull[c], 0x3);
             }
-            mma_commit_pair(&empty[st], 0x3);
-            mma_commit_pair(&cfull[c], 0x3);
         }
     } else if (warp >= 4) {
         const int q = warp & 3;
         const int ch = ((warp - 4) >> 2) * 128;  // column half of the 256
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
         const uint32_t cempty_leader0 = mapa_shared(smem_u32(&cempty[0]), 0);
-        float sum[128];
-#pragma unroll
-        for (int i = 0; i < 128; ++i) sum[i] = 0.f;
-        for (int kb = 0; kb < num_kb; ++kb) {
-            const int c = kb & 1;
-            mbar_wait(&cfull[c], (kb >> 1) & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                uint32_t v[16];
-                tmem_ld16(lane_base + c * 256 + ch + 16 * g, v);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) sum[16 * g + i] = __fadd_rn(sum[16 * g + i], __uint_as_float(v[i]));
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster_relaxed(cempty_leader0 + 8 * c);
+        // scales: P = 2^-(tx + ty) sums; next planes at 2^t_out
+        const uint32_t xb = st->maxw[xi], yb = st->maxw[yi];
+        const int pe = -(st->texp[xi] + st->texp[yi]);
+        int t_out = 0, bound_e = 0;
+        if (xb != 0u && yb != 0u && xb < 0x7F800000u && yb < 0x7F800000u) {
+            bound_e = (ilogb_bits(xb) + 1) + (ilogb_bits(yb) + 1) + lg_n;
+            t_out = max(-126, min(126, kCeil - bound_e));
         }
-        float g1, g2;
-        product_scale(__ldg(xmax), __ldg(ymax), g1, g2);
-        const int row = m0 + q * 32 + lane;
-        uint32_t mbits = 0;
+        if (out == nullptr && blockIdx.x == 0 && threadIdx.x == 128) {
+            st->texp[oi] = t_out;
+            st->bexp[oi] = bound_e;
+        }
+        if (xi > 0 && blockIdx.x == 0 && threadIdx.x == 128) {
+            // dynamic range of the left operand P_xi against its bound
+            const bool lost = xb == 0u || xb >= 0x7F800000u || ilogb_bits(xb) < st->bexp[xi] - 12;
+            if (lost) st->flag = 1;
+        }
+        const float g1 = exp2i(pe / 2), g2 = exp2i(pe - pe / 2), go = exp2i(t_out);
+        uint32_t g = 0;
+        for (int tile = blockIdx.x / 2; tile < num_tiles; tile += pairs) {
+            int m0, n0;
+            tile_origin(tile, m0, n0);
+            float sum[128];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const int col = n0 + ch + 32 * h;
-            float* v = sum + 32 * h;
+            for (int i = 0; i < 128; ++i) sum[i] = 0.f;
+            for (int kb = 0; kb < num_kb; ++kb, ++g) {
+                const uint32_t c = g & 1;
+                mbar_wait(&cfull[c], (g >> 1) & 1);
+                tc_fence_after();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                v[i] = __fmul_rn(__fmul_rn(v[i], g1), g2);
-                mbits = max(mbits, __float_as_uint(v[i]) & 0x7FFFFFFFu);
+                for (int gg = 0; gg < 8; ++gg) {
+                    uint32_t v[16];
+                    tmem_ld16(lane_base + c * 256 + ch + 16 * gg, v);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        sum[16 * gg + i] = __fadd_rn(sum[16 * gg + i], __uint_as_float(v[i]));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster_relaxed(cempty_leader0 + 8 * c);
             }
-            if (row < n_out && col < n_out) {
-                float* d = out + static_cast<size_t>(row) * ld_out + col;
-                if ((ld_out & 3) == 0 && col + 32 <= n_out) {
+            const int row = m0 + q * 32 + lane;
+            uint32_t mbits = 0;
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        reinterpret_cast<float4*>(d)[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+            for (int h = 0; h < 4; ++h) {
+                const int col = n0 + ch + 32 * h;
+                float* v = sum + 32 * h;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    v[i] = __fmul_rn(__fmul_rn(v[i], g1), g2);
+                    mbits = max(mbits, __float_as_uint(v[i]) & 0x7FFFFFFFu);
+                }
+                if (out != nullptr) {
+                    if (row < n_out && col < n_out) {
+                        float* d = out + static_cast<size_t>(row) * ld_out + col;
+                        if ((ld_out & 3) == 0 && col + 32 <= n_out) {
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                reinterpret_cast<float4*>(d)[u] =
+                                    make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+                        } else {
+                            for (int i = 0; i < 32; ++i)
+                                if (col + i < n_out) d[i] = v[i];
+                        }
+                    }
                 } else {
-                    for (int i = 0; i < 32; ++i)
-                        if (col + i < n_out) d[i] = v[i];
+                    // split at the bound scale: h0 = rn(x'), h1 = rn(x' - h0)
+                    uint4* d0 = reinterpret_cast<uint4*>(o0 + static_cast<size_t>(row) * n_pad + col);
+                    uint4* d1 = reinterpret_cast<uint4*>(o1 + static_cast<size_t>(row) * n_pad + col);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        uint32_t w0[4], w1[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float xa = __fmul_rn(v[8 * u + 2 * j], go);
+                            const float xb2 = __fmul_rn(v[8 * u + 2 * j + 1], go);
+                            const __half2 hh = __floats2half2_rn(xa, xb2);
+                            const float2 hf = __half22float2(hh);
+                            const __half2 hl = __floats2half2_rn(__fsub_rn(xa, hf.x), __fsub_rn(xb2, hf.y));
+                            w0[j] = *reinterpret_cast<const uint32_t*>(&hh);
+                            w1[j] = *reinterpret_cast<const uint32_t*>(&hl);
+                        }
+                        d0[u] = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+                        d1[u] = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+                    }
                 }
             }
-        }
-        if (omax != nullptr) {
-            mbits = __reduce_max_sync(0xFFFFFFFFu, mbits);
-            if (lane == 0) atomicMax(omax, mbits);
+            if (out == nullptr) {
+                mbits = __reduce_max_sync(0xFFFFFFFFu, mbits);
+                if (lane == 0) atomicMax(&st->maxw[oi], mbits);
+            }
         }
     }
     // both CTAs done with the pair's TMEM before the paired dealloc
@@ -245,36 +322,35 @@ namespace {
 // max |x| over an n x n fp32 matrix (leading dim ld) -> atomicMax of the bits
 __global__ void absmax_kernel(const float* __restrict__ in, int n, int ld, uint32_t* __restrict__ omax) {
     uint32_t m = 0;
-    const size_t total = static_cast<size_t>(n) * n;
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const size_t r = i / n, c = i - r * n;
-        m = max(m, __float_as_uint(__ldg(in + r * ld + c)) & 0x7FFFFFFFu);
+    if ((ld & 3) == 0 && (n & 3) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+        const size_t quads = static_cast<size_t>(n) * n / 4;
+        const int qpr = n / 4;  // quads per row
+        for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < quads;
+             i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+            const size_t r = i / qpr, c = (i - r * qpr) * 4;
+            const uint4 w = __ldg(reinterpret_cast<const uint4*>(in + r * ld + c));
+            m = max(max(m, w.x & 0x7FFFFFFFu), max(w.y & 0x7FFFFFFFu, max(w.z & 0x7FFFFFFFu, w.w & 0x7FFFFFFFu)));
+        }
+    } else {
+        const size_t total = static_cast<size_t>(n) * n;
+        for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+             i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+            const size_t r = i / n, c = i - r * n;
+            m = max(m, __float_as_uint(__ldg(in + r * ld + c)) & 0x7FFFFFFFu);
+        }
     }
     m = __reduce_max_sync(0xFFFFFFFFu, m);
     if ((threadIdx.x & 31) == 0) atomicMax(omax, m);
 }
 
-// fp32 (n x n, leading dim ld) -> scaled fp16 planes h0, h1 (n_pad x n_pad,
-// zero padded) with the exact scale of *maxw.  check != 0 (block 0): the
-// dynamic-range test of the product *maxw = X Y against its bound
-// n max|X| max|Y| (xmax, ymax) — raises *flag on strong cancellation or a
-// zero / non-finite product.
+// the base: fp32 (n x n, leading dim ld) -> scaled fp16 planes h0, h1
+// (n_pad x n_pad, zero padded) at the exact scale of st->maxw[0] (block 0
+// records it in st->texp[0])
 __global__ void split16_kernel(const float* __restrict__ in, int n, int ld,
                                __half* __restrict__ h0, __half* __restrict__ h1, int n_pad,
-                               const uint32_t* __restrict__ maxw, const uint32_t* __restrict__ xmax,
-                               const uint32_t* __restrict__ ymax, int lg_n, int* __restrict__ flag) {
-    const uint32_t mb = *maxw;
-    if (flag != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
-        const uint32_t xb = *xmax, yb = *ymax;
-        bool lost = mb == 0u || mb >= 0x7F800000u || xb >= 0x7F800000u || yb >= 0x7F800000u;
-        if (!lost && xb != 0u && yb != 0u) {
-            const int bound_e = (ilogb_bits(xb) + 1) + (ilogb_bits(yb) + 1) + lg_n;
-            lost = ilogb_bits(mb) < bound_e - 12;
-        }
-        if (lost) *flag = 1;
-    }
-    const int t = max(-126, min(126, scale_exp(mb)));
+                               F16Chain* __restrict__ st) {
+    const int t = max(-126, min(126, scale_exp(st->maxw[0])));
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->texp[0] = t;
     const float sc = exp2i(t);
     const size_t groups = static_cast<size_t>(n_pad) * n_pad / 8;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < groups;
@@ -287,7 +363,7 @@ __global__ void split16_kernel(const float* __restrict__ in, int n, int ld,
         for (int k = 0; k < 8; ++k) v[k] = 0.f;
         if (r < n) {
             const float* p = in + static_cast<size_t>(r) * ld + c;
-            if ((ld & 3) == 0 && c + 7 < n) {
+            if ((ld & 3) == 0 && c + 7 < n && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
                 const float4 a = __ldg(reinterpret_cast<const float4*>(p));
                 const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
                 v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
@@ -345,12 +421,21 @@ bool encode_plane16_map(CUtensorMap* map, const void* plane, int n_pad, int box_
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, float* out, int n_out,
-                             int ld_out, const uint32_t* xmax, const uint32_t* ymax, uint32_t* omax,
-                             cudaStream_t s) {
-    if (!k1ph_eligible(n_pad)) return cudaErrorInvalidValue;
+size_t f16_chain_state_bytes() { return sizeof(F16Chain); }
+int* f16_chain_flag(void* state) { return &static_cast<F16Chain*>(state)->flag; }
+
+cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, int n, float* out,
+                             int n_out, int ld_out, void* o0, void* o1, void* state, int xi, int yi,
+                             int oi, int num_sms, cudaStream_t s) {
+    if (!k1ph_eligible(n_pad) || xi < 0 || yi < 0 || oi < 0 || xi > kF16MaxSteps ||
+        yi > kF16MaxSteps || oi > kF16MaxSteps)
+        return cudaErrorInvalidValue;
+    int lg_n = 0;
+    while ((1ll << lg_n) < n) ++lg_n;
+    const int tiles = (n_pad / 256) * (n_pad / 256);
+    const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * (n_pad / 256) * (n_pad / 256));
+    cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(K1HCfg::kThreads);
     cfg.dynamicSmemBytes = K1HCfg::kSmem;
     cfg.stream = s;
@@ -361,28 +446,24 @@ cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, floa
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k1ph_gemm_f16x2, x.a0, x.a1, y.b0, y.b1, n_pad, out, n_out, ld_out,
-                              xmax, ymax, omax);
+    return cudaLaunchKernelEx(&cfg, k1ph_gemm_f16x2, x.a0, x.a1, y.b0, y.b1, n_pad, lg_n, out, n_out,
+                              ld_out, static_cast<__half*>(o0), static_cast<__half*>(o1),
+                              static_cast<F16Chain*>(state), xi, yi, oi);
 }
 
-cudaError_t launch_absmax(const float* in, int n, int ld, uint32_t* omax, cudaStream_t s) {
+cudaError_t launch_split16_base(const float* in, int n, int ld, void* h0, void* h1, int n_pad,
+                                void* state, cudaStream_t s) {
+    F16Chain* st = static_cast<F16Chain*>(state);
     const size_t total = static_cast<size_t>(n) * n;
-    int blocks = static_cast<int>((total + 255) / 256);
+    int blocks = static_cast<int>((total / 4 + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
-    absmax_kernel<<<blocks, 256, 0, s>>>(in, n, ld, omax);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_split16(const float* in, int n, int ld, void* h0, void* h1, int n_pad,
-                           const uint32_t* maxw, const uint32_t* xmax, const uint32_t* ymax,
-                           int* flag, cudaStream_t s) {
-    int lg_n = 0;
-    while ((1ll << lg_n) < n) ++lg_n;
+    if (blocks < 1) blocks = 1;
+    absmax_kernel<<<blocks, 256, 0, s>>>(in, n, ld, &st->maxw[0]);
     const size_t groups = static_cast<size_t>(n_pad) * n_pad / 8;
-    int blocks = static_cast<int>((groups + 255) / 256);
+    blocks = static_cast<int>((groups + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
     split16_kernel<<<blocks, 256, 0, s>>>(in, n, ld, static_cast<__half*>(h0), static_cast<__half*>(h1),
-                                          n_pad, maxw, xmax, ymax, lg_n, flag);
+                                          n_pad, st);
     return cudaGetLastError();
 }
 

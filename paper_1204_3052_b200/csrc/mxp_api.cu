@@ -205,16 +205,13 @@ struct mxp_handle_s {
     // any other use of the workspace invalidates it
     int rhs_mode = -1;
     int64_t rhs_n = 0;
-    // K1PH workspace (scaled fp16x2 chain): h0/h1 planes of base, ping, pong,
-    // the fp32 product of the running step, and the chain state: maxw[0] =
-    // max|A| bits, maxw[s + 1] = max|product of step s| bits, then the
-    // dynamic-range flag that gates the 3xTF32 recomputation
+    // K1PH workspace (scaled fp16x2 chain): h0/h1 planes of base, ping, pong
+    // and the chain state (kernels_f16x2.cu: F16Chain)
     int f32_datapath = MXP_DATAPATH_AUTO;
     int64_t ws16_pad = 0;  // padded order the maps are encoded for
     int64_t ws16_cap = 0;  // padded order the buffers are allocated for
     void* planes16[6] = {};
-    float* fbuf = nullptr;
-    uint32_t* f16state = nullptr;  // [kF16Steps + 1] maxima, then the flag
+    void* f16state = nullptr;  // the chain state (maxima, plane exponents, bounds, flag)
     F16Maps maps16[3];
     bool f16_ran = false;  // the last chain ran K1PH (mxp_last_f32_fallback)
     // fp64 workspace: base, ping, pong (n_pad^2 doubles)
@@ -345,9 +342,6 @@ int encode_ws32(mxp_handle h, int64_t n_pad) {
     return MXP_OK;
 }
 
-constexpr int kF16Steps = 128;  // plan steps (k < 2^63: at most 126)
-constexpr size_t kF16StateBytes = (kF16Steps + 2) * sizeof(uint32_t);
-
 // K1PH workspace for n_pad (allocated for the largest order seen; the TMA
 // maps are re-encoded when the order changes — captured graphs keep their own
 // copies, and the buffers they point into stay allocated).
@@ -359,15 +353,12 @@ int ensure_ws16(mxp_handle h, int64_t n_pad) {
             if (p) cudaFree(p);
             p = nullptr;
         }
-        if (h->fbuf) cudaFree(h->fbuf);
-        h->fbuf = nullptr;
         h->ws16_cap = h->ws16_pad = 0;
         const size_t n2 = static_cast<size_t>(n_pad) * n_pad;
         for (auto& p : h->planes16) MXP_CUDA(cudaMalloc(&p, n2 * 2));
-        MXP_CUDA(cudaMalloc(&h->fbuf, n2 * 4));
         h->ws16_cap = n_pad;
     }
-    if (!h->f16state) MXP_CUDA(cudaMalloc(&h->f16state, kF16StateBytes));
+    if (!h->f16state) MXP_CUDA(cudaMalloc(&h->f16state, f16_chain_state_bytes()));
     for (int i = 0; i < 3; ++i) {
         F16Maps& m = h->maps16[i];
         if (!encode_plane16_map(&m.a0, h->planes16[2 * i], (int)n_pad, 128) ||
@@ -422,49 +413,44 @@ int enqueue_chain_tf32(mxp_handle h, int64_t n, const PlanBits& plan, const floa
                        float* dOut, int64_t* launches, int64_t* failed, const int* gate);
 
 // K1PH chain (scaled fp16x2 planes, one exponent per matrix), then the 3xTF32
-// chain gated on the dynamic-range flag the splits raise (no-op launches
-// unless a product lost range).  Planes: 0 base, 1 ping, 2 pong.
+// chain gated on the dynamic-range flag the GEMMs raise (no-op launches
+// unless a product lost range).  Planes: 0 base, 1 ping, 2 pong; chain state
+// index 0 = the base, s + 1 = the product of step s.
 int enqueue_chain_f16x2(mxp_handle h, int64_t n, const PlanBits& plan, const float* dA,
                         float* dOut, int64_t* launches, int64_t* failed) {
     const int64_t n_pad = round_up(n, 128);
     int rc = ensure_ws16(h, n_pad);
     if (rc) return rc;
     const int np = (int)n_pad;
-    uint32_t* maxw = h->f16state;
-    int* flag = reinterpret_cast<int*>(h->f16state + kF16Steps + 1);
-    cudaError_t e = cudaMemsetAsync(h->f16state, 0, kF16StateBytes, h->stream);
-    if (e == cudaSuccess) e = launch_absmax(dA, (int)n, (int)n, maxw, h->stream);
+    void* st = h->f16state;
+    cudaError_t e = cudaMemsetAsync(st, 0, f16_chain_state_bytes(), h->stream);
     if (e == cudaSuccess)
-        e = launch_split16(dA, (int)n, (int)n, h->planes16[0], h->planes16[1], np, maxw, nullptr,
-                           nullptr, nullptr, h->stream);
+        e = launch_split16_base(dA, (int)n, (int)n, h->planes16[0], h->planes16[1], np, st, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "k1ph split");
     *launches += 2;
-    int acc = 0, acc_m = 0;  // plane pair of the running power, index of its max
+    int acc = 0, acc_i = 0;  // plane pair of the running power, its state index
     for (int s = 0; s < plan.len; ++s) {
         const bool mult = plan_is_mult(plan, s);
         const bool last = (s == plan.len - 1);
         const int dst = (acc == 1) ? 2 : 1;
-        const int rhs = mult ? 0 : acc, rhs_m = mult ? 0 : acc_m;
+        const int rhs = mult ? 0 : acc, rhs_i = mult ? 0 : acc_i;
         e = launch_progress_mark(h->progress_dev, static_cast<uint32_t>(s + 1), s == h->fault_step,
                                  h->stream);
         if (e == cudaSuccess)
-            e = launch_k1ph_gemm(h->maps16[acc], h->maps16[rhs], np, last ? dOut : h->fbuf,
-                                 last ? (int)n : np, last ? (int)n : np, maxw + acc_m, maxw + rhs_m,
-                                 last ? nullptr : maxw + s + 1, h->stream);
-        if (e == cudaSuccess && !last)
-            e = launch_split16(h->fbuf, np, np, h->planes16[2 * dst], h->planes16[2 * dst + 1], np,
-                               maxw + s + 1, maxw + acc_m, maxw + rhs_m, flag, h->stream);
+            e = launch_k1ph_gemm(h->maps16[acc], h->maps16[rhs], np, (int)n, last ? dOut : nullptr,
+                                 (int)n, (int)n, h->planes16[2 * dst], h->planes16[2 * dst + 1], st,
+                                 acc_i, rhs_i, s + 1, h->num_sms, h->stream);
         if (e != cudaSuccess) {
             *failed = s;
             return cuda_fail(e, "k1ph_gemm_f16x2");
         }
-        *launches += last ? 2 : 3;
+        *launches += 2;
         acc = dst;
-        acc_m = s + 1;
+        acc_i = s + 1;
     }
     // the 3xTF32 recomputation, every launch gated on the flag
     int64_t gated = 0;
-    rc = enqueue_chain_tf32(h, n, plan, dA, dOut, &gated, failed, flag);
+    rc = enqueue_chain_tf32(h, n, plan, dA, dOut, &gated, failed, f16_chain_flag(st));
     *launches += gated;
     return rc;
 }
@@ -800,7 +786,6 @@ int mxp_destroy(mxp_handle h) {
         if (p) cudaFree(p);
     for (auto p : h->planes16)
         if (p) cudaFree(p);
-    if (h->fbuf) cudaFree(h->fbuf);
     if (h->f16state) cudaFree(h->f16state);
     if (h->bar_ctr) cudaFree(h->bar_ctr);
     if (h->stamps) cudaFree(h->stamps);
@@ -1532,7 +1517,7 @@ int mxp_last_f32_fallback(mxp_handle h, int* raised) {
     MXP_CUDA(cudaSetDevice(h->device));
     MXP_CUDA(cudaStreamSynchronize(h->stream));
     int flag = 0;
-    MXP_CUDA(cudaMemcpy(&flag, h->f16state + kF16Steps + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    MXP_CUDA(cudaMemcpy(&flag, f16_chain_flag(h->f16state), sizeof(int), cudaMemcpyDeviceToHost));
     *raised = flag != 0;
     return MXP_OK;
 }

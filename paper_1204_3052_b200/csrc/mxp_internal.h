@@ -135,20 +135,21 @@ struct F16Maps {
 cudaError_t prepare_f16x2_kernels();
 bool k1ph_eligible(int64_t n_pad);  // n_pad % 256 == 0 && n_pad >= 1024 (K1P's sizes)
 bool encode_plane16_map(CUtensorMap* map, const void* plane, int n_pad, int box_rows);
-// out = X Y (fp32, n_out x n_out, leading dim ld_out) from the planes of X
-// (left) and Y (right) whose fp32 maxima are *xmax / *ymax (bit patterns);
-// *omax (may be null) <- max |out| (atomicMax of bits, zeroed beforehand)
-cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, float* out, int n_out,
-                             int ld_out, const uint32_t* xmax, const uint32_t* ymax, uint32_t* omax,
-                             cudaStream_t s);
-// *omax <- max(*omax, max |in|) over n x n (leading dim ld)
-cudaError_t launch_absmax(const float* in, int n, int ld, uint32_t* omax, cudaStream_t s);
-// fp32 n x n (leading dim ld) -> h0 / h1 planes (n_pad x n_pad, zero padded)
-// at the exact scale of *maxw; flag (may be null): raised when the product
-// *maxw = X Y lost dynamic range against its bound n max|X| max|Y|
-cudaError_t launch_split16(const float* in, int n, int ld, void* h0, void* h1, int n_pad,
-                           const uint32_t* maxw, const uint32_t* xmax, const uint32_t* ymax,
-                           int* flag, cudaStream_t s);
+// Chain state (device, f16_chain_state_bytes(), zeroed before a chain):
+// index 0 = the base A, s + 1 = the product of plan step s; the flag word
+// (f16_chain_flag) gates the 3xTF32 recomputation.
+constexpr int kF16MaxSteps = 128;  // plan steps (k < 2^63: at most 126)
+size_t f16_chain_state_bytes();
+int* f16_chain_flag(void* state);
+// the base planes (index 0): max |A| then the split at its exact scale
+cudaError_t launch_split16_base(const float* in, int n, int ld, void* h0, void* h1, int n_pad,
+                                void* state, cudaStream_t s);
+// P_oi = P_xi P_yi from the planes of P_xi (left) and P_yi (right): the next
+// planes o0 / o1 at the bound scale (out == nullptr), or the fp32 result
+// (out: n_out x n_out, leading dim ld_out).  n: the true order (bound).
+cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, int n, float* out,
+                             int n_out, int ld_out, void* o0, void* o1, void* state, int xi, int yi,
+                             int oi, int num_sms, cudaStream_t s);
 
 // ---- generation (kernels_gen.cu) -------------------------------------------
 // Reference random_matrix (linalg.py:127-148) on device; scale != 0 selects
