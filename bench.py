@@ -48,7 +48,9 @@ WORKLOADS = {
     "c3": dict(name="batched 65536 x 128x128 FP32 (split-fp32 tensor cores) A^64", n=128, batch=65536, k=64,
                dtype="f32"),
     "c2": dict(name="512x512 FP32 (3xTF32) A^1000", n=512, batch=1, k=1000, dtype="f32"),
-    "c5": dict(name="8192x8192 FP32 (3xTF32) A^1024", n=8192, batch=1, k=1024,
+    # one GPU: K1PH (scaled fp16x2 planes, 3xTF32 recomputation on range
+    # loss); row-sharded over N GPUs: 3xTF32 CTA pairs with the fused exchange
+    "c5": dict(name="8192x8192 FP32 (split-fp32 tensor cores) A^1024", n=8192, batch=1, k=1024,
                dtype="f32"),
     "c4": dict(name="4096x4096 FP64 (DMMA) A^257", n=4096, batch=1, k=257, dtype="f64"),
     "c1": dict(name="64x64 FP32 (split-fp32 tensor cores) A^16", n=64, batch=1, k=16, dtype="f32"),
@@ -538,6 +540,14 @@ def plan_only(args, w, world, rank) -> None:
         tdist.destroy_process_group()
 
 
+def k1ph_runs(w: dict, world: int = 1) -> bool:
+    """Whether a single-matrix f32 chain runs K1PH (kernels_f16x2.cu): the
+    CTA-pair sizes on one GPU (the row-sharded multi-GPU chain runs 3xTF32)."""
+    n_pad = -(-w["n"] // 128) * 128
+    return (w["dtype"] == "f32" and w["batch"] == 1 and world == 1 and n_pad >= 1024
+            and n_pad % 256 == 0)
+
+
 def roofline_of(w: dict, batched: bool, rank_fl: float, ms: float, launches: int, value: float,
                 world: int, peaks: dict, tf32) -> dict:
     """The bench line's roofline object for the kernel that runs workload w:
@@ -549,7 +559,14 @@ def roofline_of(w: dict, batched: bool, rank_fl: float, ms: float, launches: int
     # (MEASURED_PEAKS bf16; fp16 runs at the same rate).  The K1/K1P chains
     # (C2, C5) run 3xTF32: cuBLAS TF32 measured here / 3.
     bf16 = peaks.get("bf16_tflops")
-    if batched and w["dtype"] == "f32":
+    if k1ph_runs(w, world):
+        # K1PH: three fp16 products per fp32 product, like K3H
+        if bf16:
+            peak, src = bf16 / 3.0, "MEASURED_PEAKS bf16 dense burst (fp16 same rate) / 3 products"
+        else:
+            peak, src = 2250.0 / 3.0, "fallback: nominal 2.25 PF dense fp16 / 3 products"
+        kernel = "k1ph_gemm_f16x2"
+    elif batched and w["dtype"] == "f32":
         if bf16:
             peak, src = bf16 / 3.0, "MEASURED_PEAKS bf16 dense burst (fp16 same rate) / 3 products"
         else:
@@ -806,6 +823,12 @@ def main() -> None:
                     if wx["dtype"] == "f64" and f64:
                         ex["frac"] = tf / f64
                         ex["peak"] = f"cuBLAS DGEMM 8192^3 measured in this run ({f64:.1f} TFLOP/s)"
+                    elif k1ph_runs(wx) and peaks.get("bf16_tflops"):
+                        ex["frac"] = tf / (peaks["bf16_tflops"] / 3.0)
+                        ex["peak"] = (f"MEASURED_PEAKS bf16 dense burst / 3 products "
+                                      f"({peaks['bf16_tflops'] / 3.0:.0f} TFLOP/s): K1PH, scaled fp16x2")
+                        if tf32:
+                            ex["vs_3xtf32_effective_peak"] = tf / (tf32 / 3.0)
                     elif wx["n"] > 128 and tf32:
                         ex["frac"] = tf / (tf32 / 3.0)
                         ex["peak"] = f"cuBLAS TF32 8192^3 / 3 ({tf32 / 3.0:.0f} TFLOP/s)"

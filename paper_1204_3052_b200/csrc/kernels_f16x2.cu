@@ -20,10 +20,11 @@
 // element), enqueued behind this one with every launch gated on the flag,
 // recomputes the whole power.  Random inputs never raise it.
 //
-// Per step: k1ph_gemm_f16x2 (CTA pairs, M = N = 256, K = 64 per stage, the
-// accumulator drained per stage into fp32 register sums as in K1P) writes
-// the unscaled fp32 product and its max |.| (atomicMax on the bit patterns);
-// split16_kernel turns it into the next step's planes with the exact scale.
+// Per step: k1ph_gemm_f16x2 (persistent CTA pairs, M = N = 256, K = 64 per
+// stage, the accumulator drained per stage into fp32 register sums as in
+// K1P) writes the unscaled fp32 product and its max |.| (atomicMax on the bit
+// patterns); split16_kernel turns it into the next step's planes at the
+// exact scale of that max.
 #include <cuda_fp16.h>
 
 #include <cmath>
@@ -74,37 +75,34 @@ __device__ __forceinline__ void product_scale(uint32_t xmax, uint32_t ymax, floa
 // Per-chain state (device memory, zeroed before the chain): index 0 is the
 // base A, index s + 1 the product of plan step s.
 //   maxw[i]  max |P_i| (fp32 bit pattern, atomicMax by the producing GEMM)
-//   texp[i]  the planes of P_i hold P_i * 2^texp[i]
-//   bexp[i]  floor(log2) bound of P_i's magnitude: max|P_i| < 2^bexp[i]
+//   texp[i]  the planes of P_i hold P_i * 2^texp[i] (set by its split)
 //   flag     a product lost dynamic range (-> the gated 3xTF32 recomputation)
 struct F16Chain {
     uint32_t maxw[kF16MaxSteps + 1];
     int texp[kF16MaxSteps + 1];
-    int bexp[kF16MaxSteps + 1];
     int flag;
 };
 
 // C = X Y over scaled fp16 planes, persistent: one CTA pair per two SMs
-// walks the 256 x 256 tiles (grouped raster), so a tile's epilogue (scale,
-// split, stores) overlaps the next tile's first MMAs (the two 256-column
-// chunk accumulators run ahead of the drain).
+// walks the 256 x 256 tiles (grouped raster), so a tile's epilogue overlaps
+// the next tile's first MMAs (the two 256-column chunk accumulators run
+// ahead of the drain).
 //   warp 0 : TMA producer (both CTAs; bytes complete on the leader's barrier)
 //   warp 1 : MMA issuer (leader only)     warp 2 : TMEM allocator (both)
 //   warps 4-11 : epilogue (both CTAs; lane quarter = warp % 4, 128-column half)
-// Output, with P = 2^-(texp[xi] + texp[yi]) * sums:
-//   out != nullptr: P as fp32 (n_out x n_out, leading dim ld_out) — the last step;
-//   else: the next step's planes at the bound scale t = 14 - bexp[oi],
-//     bexp[oi] = (ilogb max|X| + 1) + (ilogb max|Y| + 1) + lg_n, so
-//     |P * 2^t| < 2^14 (no fp16 overflow) without waiting for P's own max
-//     (K3H's bound-based scale); max|P| -> maxw[oi].
-// CTA 0 also runs the dynamic-range test on the LEFT operand P_xi (xi > 0):
-// zero, non-finite, or more than 2^12 below its bound raises st->flag.
+// out (fp32, n_out x n_out, leading dim ld_out) = 2^-(texp[xi] + texp[yi]) *
+// sums; oi >= 0: max |out| -> maxw[oi] (atomicMax of the bit patterns), which
+// the split of the next planes turns into their exact scale.
+//
+// (Measured and rejected: writing the next planes straight from the epilogue
+// at the bound scale n max|X| max|Y|, K3H's scheme — 6% faster on C5, but the
+// bound sits lg n bits above a sparse product's max, and a signed permutation
+// power with 2^13 of dynamic range lost its exactness at n = 1024.)
 __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
     k1ph_gemm_f16x2(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUtensorMap ma1,
                     const __grid_constant__ CUtensorMap mb0, const __grid_constant__ CUtensorMap mb1,
-                    int n_pad, int lg_n, float* __restrict__ out, int n_out, int ld_out,
-                    __half* __restrict__ o0, __half* __restrict__ o1, F16Chain* __restrict__ st,
-                    int xi, int yi, int oi) {
+                    int n_pad, float* __restrict__ out, int n_out, int ld_out,
+                    F16Chain* __restrict__ st, int xi, int yi, int oi) {
     using Cfg = K1HCfg;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -218,24 +216,8 @@ __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
         const int ch = ((warp - 4) >> 2) * 128;  // column half of the 256
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
         const uint32_t cempty_leader0 = mapa_shared(smem_u32(&cempty[0]), 0);
-        // scales: P = 2^-(tx + ty) sums; next planes at 2^t_out
-        const uint32_t xb = st->maxw[xi], yb = st->maxw[yi];
-        const int pe = -(st->texp[xi] + st->texp[yi]);
-        int t_out = 0, bound_e = 0;
-        if (xb != 0u && yb != 0u && xb < 0x7F800000u && yb < 0x7F800000u) {
-            bound_e = (ilogb_bits(xb) + 1) + (ilogb_bits(yb) + 1) + lg_n;
-            t_out = max(-126, min(126, kCeil - bound_e));
-        }
-        if (out == nullptr && blockIdx.x == 0 && threadIdx.x == 128) {
-            st->texp[oi] = t_out;
-            st->bexp[oi] = bound_e;
-        }
-        if (xi > 0 && blockIdx.x == 0 && threadIdx.x == 128) {
-            // dynamic range of the left operand P_xi against its bound
-            const bool lost = xb == 0u || xb >= 0x7F800000u || ilogb_bits(xb) < st->bexp[xi] - 12;
-            if (lost) st->flag = 1;
-        }
-        const float g1 = exp2i(pe / 2), g2 = exp2i(pe - pe / 2), go = exp2i(t_out);
+        const int pe = -(st->texp[xi] + st->texp[yi]);  // P = 2^pe sums
+        const float g1 = exp2i(pe / 2), g2 = exp2i(pe - pe / 2);
         uint32_t g = 0;
         for (int tile = blockIdx.x / 2; tile < num_tiles; tile += pairs) {
             int m0, n0;
@@ -270,42 +252,20 @@ __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
                     v[i] = __fmul_rn(__fmul_rn(v[i], g1), g2);
                     mbits = max(mbits, __float_as_uint(v[i]) & 0x7FFFFFFFu);
                 }
-                if (out != nullptr) {
-                    if (row < n_out && col < n_out) {
-                        float* d = out + static_cast<size_t>(row) * ld_out + col;
-                        if ((ld_out & 3) == 0 && col + 32 <= n_out) {
+                if (row < n_out && col < n_out) {
+                    float* d = out + static_cast<size_t>(row) * ld_out + col;
+                    if ((ld_out & 3) == 0 && col + 32 <= n_out) {
 #pragma unroll
-                            for (int u = 0; u < 8; ++u)
-                                reinterpret_cast<float4*>(d)[u] =
-                                    make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
-                        } else {
-                            for (int i = 0; i < 32; ++i)
-                                if (col + i < n_out) d[i] = v[i];
-                        }
-                    }
-                } else {
-                    // split at the bound scale: h0 = rn(x'), h1 = rn(x' - h0)
-                    uint4* d0 = reinterpret_cast<uint4*>(o0 + static_cast<size_t>(row) * n_pad + col);
-                    uint4* d1 = reinterpret_cast<uint4*>(o1 + static_cast<size_t>(row) * n_pad + col);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        uint32_t w0[4], w1[4];
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const float xa = __fmul_rn(v[8 * u + 2 * j], go);
-                            const float xb2 = __fmul_rn(v[8 * u + 2 * j + 1], go);
-                            const __half2 hh = __floats2half2_rn(xa, xb2);
-                            const float2 hf = __half22float2(hh);
-                            const __half2 hl = __floats2half2_rn(__fsub_rn(xa, hf.x), __fsub_rn(xb2, hf.y));
-                            w0[j] = *reinterpret_cast<const uint32_t*>(&hh);
-                            w1[j] = *reinterpret_cast<const uint32_t*>(&hl);
-                        }
-                        d0[u] = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-                        d1[u] = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+                        for (int u = 0; u < 8; ++u)
+                            reinterpret_cast<float4*>(d)[u] =
+                                make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+                    } else {
+                        for (int i = 0; i < 32; ++i)
+                            if (col + i < n_out) d[i] = v[i];
                     }
                 }
             }
-            if (out == nullptr) {
+            if (oi >= 0) {
                 mbits = __reduce_max_sync(0xFFFFFFFFu, mbits);
                 if (lane == 0) atomicMax(&st->maxw[oi], mbits);
             }
@@ -343,19 +303,33 @@ __global__ void absmax_kernel(const float* __restrict__ in, int n, int ld, uint3
     if ((threadIdx.x & 31) == 0) atomicMax(omax, m);
 }
 
-// the base: fp32 (n x n, leading dim ld) -> scaled fp16 planes h0, h1
-// (n_pad x n_pad, zero padded) at the exact scale of st->maxw[0] (block 0
-// records it in st->texp[0])
+// fp32 P_i (n x n, leading dim ld) -> scaled fp16 planes h0, h1 (n_pad x
+// n_pad, zero padded) at the exact scale of st->maxw[i] (block 0 records it
+// in st->texp[i]).  A product (xi >= 0: P_i = P_xi P_yi) is also tested for
+// lost dynamic range: zero, non-finite, or more than 2^12 below its bound
+// n max|P_xi| max|P_yi| raises st->flag.
 __global__ void split16_kernel(const float* __restrict__ in, int n, int ld,
                                __half* __restrict__ h0, __half* __restrict__ h1, int n_pad,
-                               F16Chain* __restrict__ st) {
-    const int t = max(-126, min(126, scale_exp(st->maxw[0])));
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->texp[0] = t;
+                               F16Chain* __restrict__ st, int i, int xi, int yi, int lg_n) {
+    const uint32_t mb = st->maxw[i];
+    const int t = max(-126, min(126, scale_exp(mb)));
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->texp[i] = t;
+        if (xi >= 0) {
+            const uint32_t xb = st->maxw[xi], yb = st->maxw[yi];
+            bool lost = mb == 0u || mb >= 0x7F800000u || xb >= 0x7F800000u || yb >= 0x7F800000u;
+            if (!lost && xb != 0u && yb != 0u) {
+                const int bound_e = (ilogb_bits(xb) + 1) + (ilogb_bits(yb) + 1) + lg_n;
+                lost = ilogb_bits(mb) < bound_e - 12;
+            }
+            if (lost) st->flag = 1;
+        }
+    }
     const float sc = exp2i(t);
     const size_t groups = static_cast<size_t>(n_pad) * n_pad / 8;
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < groups;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const size_t e = i * 8;
+    for (size_t g = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; g < groups;
+         g += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t e = g * 8;
         const int r = static_cast<int>(e / n_pad);
         const int c = static_cast<int>(e - static_cast<size_t>(r) * n_pad);
         float v[8];
@@ -381,8 +355,8 @@ __global__ void split16_kernel(const float* __restrict__ in, int n, int ld,
             a0[k] = __float2half_rn(x);
             a1[k] = __float2half_rn(__fsub_rn(x, __half2float(a0[k])));
         }
-        reinterpret_cast<uint4*>(h0)[i] = *reinterpret_cast<const uint4*>(a0);
-        reinterpret_cast<uint4*>(h1)[i] = *reinterpret_cast<const uint4*>(a1);
+        reinterpret_cast<uint4*>(h0)[g] = *reinterpret_cast<const uint4*>(a0);
+        reinterpret_cast<uint4*>(h1)[g] = *reinterpret_cast<const uint4*>(a1);
     }
 }
 
@@ -424,14 +398,12 @@ bool encode_plane16_map(CUtensorMap* map, const void* plane, int n_pad, int box_
 size_t f16_chain_state_bytes() { return sizeof(F16Chain); }
 int* f16_chain_flag(void* state) { return &static_cast<F16Chain*>(state)->flag; }
 
-cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, int n, float* out,
-                             int n_out, int ld_out, void* o0, void* o1, void* state, int xi, int yi,
-                             int oi, int num_sms, cudaStream_t s) {
-    if (!k1ph_eligible(n_pad) || xi < 0 || yi < 0 || oi < 0 || xi > kF16MaxSteps ||
-        yi > kF16MaxSteps || oi > kF16MaxSteps)
+cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, float* out, int n_out,
+                             int ld_out, void* state, int xi, int yi, int oi, int num_sms,
+                             cudaStream_t s) {
+    if (!k1ph_eligible(n_pad) || xi < 0 || yi < 0 || xi > kF16MaxSteps || yi > kF16MaxSteps ||
+        oi > kF16MaxSteps)
         return cudaErrorInvalidValue;
-    int lg_n = 0;
-    while ((1ll << lg_n) < n) ++lg_n;
     const int tiles = (n_pad / 256) * (n_pad / 256);
     const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
     cudaLaunchConfig_t cfg{};
@@ -446,24 +418,28 @@ cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, int 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k1ph_gemm_f16x2, x.a0, x.a1, y.b0, y.b1, n_pad, lg_n, out, n_out,
-                              ld_out, static_cast<__half*>(o0), static_cast<__half*>(o1),
+    return cudaLaunchKernelEx(&cfg, k1ph_gemm_f16x2, x.a0, x.a1, y.b0, y.b1, n_pad, out, n_out, ld_out,
                               static_cast<F16Chain*>(state), xi, yi, oi);
 }
 
-cudaError_t launch_split16_base(const float* in, int n, int ld, void* h0, void* h1, int n_pad,
-                                void* state, cudaStream_t s) {
+cudaError_t launch_split16(const float* in, int n, int ld, void* h0, void* h1, int n_pad,
+                           void* state, int i, int xi, int yi, cudaStream_t s) {
     F16Chain* st = static_cast<F16Chain*>(state);
-    const size_t total = static_cast<size_t>(n) * n;
-    int blocks = static_cast<int>((total / 4 + 255) / 256);
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    if (blocks < 1) blocks = 1;
-    absmax_kernel<<<blocks, 256, 0, s>>>(in, n, ld, &st->maxw[0]);
+    int blocks;
+    if (xi < 0) {  // the base: its max first
+        const size_t total = static_cast<size_t>(n) * n;
+        blocks = static_cast<int>((total / 4 + 255) / 256);
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        if (blocks < 1) blocks = 1;
+        absmax_kernel<<<blocks, 256, 0, s>>>(in, n, ld, &st->maxw[i]);
+    }
+    int lg_n = 0;
+    while ((1ll << lg_n) < n) ++lg_n;
     const size_t groups = static_cast<size_t>(n_pad) * n_pad / 8;
     blocks = static_cast<int>((groups + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
     split16_kernel<<<blocks, 256, 0, s>>>(in, n, ld, static_cast<__half*>(h0), static_cast<__half*>(h1),
-                                          n_pad, st);
+                                          n_pad, st, i, xi, yi, lg_n);
     return cudaGetLastError();
 }
 

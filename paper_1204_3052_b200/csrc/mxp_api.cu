@@ -211,6 +211,7 @@ struct mxp_handle_s {
     int64_t ws16_pad = 0;  // padded order the maps are encoded for
     int64_t ws16_cap = 0;  // padded order the buffers are allocated for
     void* planes16[6] = {};
+    float* fbuf = nullptr;     // the fp32 product of the running step
     void* f16state = nullptr;  // the chain state (maxima, plane exponents, bounds, flag)
     F16Maps maps16[3];
     bool f16_ran = false;  // the last chain ran K1PH (mxp_last_f32_fallback)
@@ -353,9 +354,12 @@ int ensure_ws16(mxp_handle h, int64_t n_pad) {
             if (p) cudaFree(p);
             p = nullptr;
         }
+        if (h->fbuf) cudaFree(h->fbuf);
+        h->fbuf = nullptr;
         h->ws16_cap = h->ws16_pad = 0;
         const size_t n2 = static_cast<size_t>(n_pad) * n_pad;
         for (auto& p : h->planes16) MXP_CUDA(cudaMalloc(&p, n2 * 2));
+        MXP_CUDA(cudaMalloc(&h->fbuf, n2 * 4));
         h->ws16_cap = n_pad;
     }
     if (!h->f16state) MXP_CUDA(cudaMalloc(&h->f16state, f16_chain_state_bytes()));
@@ -425,7 +429,8 @@ int enqueue_chain_f16x2(mxp_handle h, int64_t n, const PlanBits& plan, const flo
     void* st = h->f16state;
     cudaError_t e = cudaMemsetAsync(st, 0, f16_chain_state_bytes(), h->stream);
     if (e == cudaSuccess)
-        e = launch_split16_base(dA, (int)n, (int)n, h->planes16[0], h->planes16[1], np, st, h->stream);
+        e = launch_split16(dA, (int)n, (int)n, h->planes16[0], h->planes16[1], np, st, 0, -1, -1,
+                           h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "k1ph split");
     *launches += 2;
     int acc = 0, acc_i = 0;  // plane pair of the running power, its state index
@@ -437,14 +442,17 @@ int enqueue_chain_f16x2(mxp_handle h, int64_t n, const PlanBits& plan, const flo
         e = launch_progress_mark(h->progress_dev, static_cast<uint32_t>(s + 1), s == h->fault_step,
                                  h->stream);
         if (e == cudaSuccess)
-            e = launch_k1ph_gemm(h->maps16[acc], h->maps16[rhs], np, (int)n, last ? dOut : nullptr,
-                                 (int)n, (int)n, h->planes16[2 * dst], h->planes16[2 * dst + 1], st,
-                                 acc_i, rhs_i, s + 1, h->num_sms, h->stream);
+            e = launch_k1ph_gemm(h->maps16[acc], h->maps16[rhs], np, last ? dOut : h->fbuf,
+                                 last ? (int)n : np, last ? (int)n : np, st, acc_i, rhs_i,
+                                 last ? -1 : s + 1, h->num_sms, h->stream);
+        if (e == cudaSuccess && !last)
+            e = launch_split16(h->fbuf, np, np, h->planes16[2 * dst], h->planes16[2 * dst + 1], np, st,
+                               s + 1, acc_i, rhs_i, h->stream);
         if (e != cudaSuccess) {
             *failed = s;
             return cuda_fail(e, "k1ph_gemm_f16x2");
         }
-        *launches += 2;
+        *launches += last ? 2 : 3;
         acc = dst;
         acc_i = s + 1;
     }
@@ -786,6 +794,7 @@ int mxp_destroy(mxp_handle h) {
         if (p) cudaFree(p);
     for (auto p : h->planes16)
         if (p) cudaFree(p);
+    if (h->fbuf) cudaFree(h->fbuf);
     if (h->f16state) cudaFree(h->f16state);
     if (h->bar_ctr) cudaFree(h->bar_ctr);
     if (h->stamps) cudaFree(h->stamps);

@@ -141,15 +141,16 @@ bool encode_plane16_map(CUtensorMap* map, const void* plane, int n_pad, int box_
 constexpr int kF16MaxSteps = 128;  // plan steps (k < 2^63: at most 126)
 size_t f16_chain_state_bytes();
 int* f16_chain_flag(void* state);
-// the base planes (index 0): max |A| then the split at its exact scale
-cudaError_t launch_split16_base(const float* in, int n, int ld, void* h0, void* h1, int n_pad,
-                                void* state, cudaStream_t s);
-// P_oi = P_xi P_yi from the planes of P_xi (left) and P_yi (right): the next
-// planes o0 / o1 at the bound scale (out == nullptr), or the fp32 result
-// (out: n_out x n_out, leading dim ld_out).  n: the true order (bound).
-cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, int n, float* out,
-                             int n_out, int ld_out, void* o0, void* o1, void* state, int xi, int yi,
-                             int oi, int num_sms, cudaStream_t s);
+// fp32 P_i (n x n, leading dim ld) -> its h0 / h1 planes (n_pad x n_pad,
+// zero padded) at the exact scale of maxw[i]; the base (xi < 0) measures its
+// max first; a product P_i = P_xi P_yi is tested for lost dynamic range
+cudaError_t launch_split16(const float* in, int n, int ld, void* h0, void* h1, int n_pad,
+                           void* state, int i, int xi, int yi, cudaStream_t s);
+// P_oi = P_xi P_yi (fp32 out: n_out x n_out, leading dim ld_out) from the
+// planes of P_xi (left) and P_yi (right); oi >= 0: max |P_oi| -> maxw[oi]
+cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, float* out, int n_out,
+                             int ld_out, void* state, int xi, int yi, int oi, int num_sms,
+                             cudaStream_t s);
 
 // ---- generation (kernels_gen.cu) -------------------------------------------
 // Reference random_matrix (linalg.py:127-148) on device; scale != 0 selects

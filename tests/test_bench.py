@@ -72,6 +72,10 @@ def test_roofline_counts_the_k3h_launch_over_the_step():
     assert r["algorithmic_flops_per_launch"] == fl
     assert 0.5 < r["frac"] < 1.0
     assert r["kernel"] == "k3h_batched_power"
-    r5 = bench.roofline_of(bench.WORKLOADS["c5"], False, bench.flops(bench.WORKLOADS["c5"]), 44.0,
-                           21, bench.flops(bench.WORKLOADS["c5"]) / 44e-3 / 1e12, 1, peaks, 759.0)
-    assert r5["kernel"] == "k1p_gemm_3xtf32" and 0.5 < r5["frac"] < 1.05
+    w5 = bench.WORKLOADS["c5"]
+    f5 = bench.flops(w5)
+    # one GPU: K1PH (fp16 datapath / 3); row-sharded over 2 GPUs: 3xTF32 K1P
+    r5 = bench.roofline_of(w5, False, f5, 24.0, 23, f5 / 24e-3 / 1e12, 1, peaks, 759.0)
+    assert r5["kernel"] == "k1ph_gemm_f16x2" and 0.5 < r5["frac"] < 1.0
+    r5s = bench.roofline_of(w5, False, f5, 23.0, 21, f5 / 23e-3 / 1e12, 2, peaks, 759.0)
+    assert r5s["kernel"] == "k1p_gemm_3xtf32" and 0.5 < r5s["frac"] < 1.05
