@@ -544,8 +544,8 @@ def k1ph_runs(w: dict, world: int = 1) -> bool:
     """Whether a single-matrix f32 chain runs K1PH (kernels_f16x2.cu): the
     CTA-pair sizes on one GPU (the row-sharded multi-GPU chain runs 3xTF32)."""
     n_pad = -(-w["n"] // 128) * 128
-    return (w["dtype"] == "f32" and w["batch"] == 1 and world == 1 and n_pad >= 1024
-            and n_pad % 256 == 0)
+    return (w["dtype"] == "f32" and w["batch"] == 1 and world == 1
+            and ((n_pad >= 1024 and n_pad % 256 == 0) or w["n"] > 1408))
 
 
 def roofline_of(w: dict, batched: bool, rank_fl: float, ms: float, launches: int, value: float,

@@ -220,8 +220,8 @@ MXP_API int mxp_random_device(mxp_handle h, int mode, int64_t n, int64_t batch, 
  * count uint64 draws of `seed` into dOut.  Async on the handle stream. */
 MXP_API int mxp_splitmix64_device(mxp_handle h, uint64_t seed, int64_t count, void* dOut);
 
-/* Datapath of single-matrix FP32 chains at the CTA-pair sizes (padded order
- * n_pad = roundup(n, 128) with n_pad % 256 == 0 and n_pad >= 1024, e.g. C5):
+/* Datapath of single-matrix FP32 chains at the CTA-pair sizes (roundup(n, 128)
+ * a multiple of 256 and >= 1024, e.g. C5; and every n > 1408, padded to 256):
  *   MXP_DATAPATH_AUTO (default): K1PH — scaled fp16x2 planes, one exponent
  *     per matrix, half the tensor work of 3xTF32 at the same 22-bit operand
  *     precision; a chain whose product loses dynamic range (strong

@@ -199,7 +199,10 @@ __global__ void __launch_bounds__(K1Cfg::kThreads, 1)
                    const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
                    int n_pad, int m_pad, float* __restrict__ out_f32, int n_out, int m_out,
                    int ld_out, uint32_t* __restrict__ out_hi, uint32_t* __restrict__ out_lo,
-                   int dsmem_reduce) {
+                   int dsmem_reduce, const int* __restrict__ gate) {
+    // gated recomputation chain (behind a K1PH chain): nothing to do unless
+    // raised; a split-K cluster's CTAs read the same word and leave together
+    if (gate != nullptr && *gate == 0) return;
     using Cfg = K1Cfg;
     constexpr int S = Cfg::kStages;
     constexpr int BN = Cfg::kBN;
@@ -1279,7 +1282,7 @@ cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int b
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         return cudaLaunchKernelEx(&cfg, k1_gemm_3xtf32, m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad,
-                                  out_f32, n_out, m_out, ld_out, out_hi, out_lo, 1);
+                                  out_f32, n_out, m_out, ld_out, out_hi, out_lo, 1, gate);
     }
     if (block_n == 256) {  // CTA-pair kernel: n_pad, m_pad multiples of 256
         return launch_k1p(m, n_pad, m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo,
@@ -1288,7 +1291,7 @@ cudaError_t launch_k1_gemm_rows(const GemmPlanes& m, int n_pad, int m_pad, int b
     dim3 grid((n_pad / K1Cfg::kBN) * (m_pad / 128), 1);
     k1_gemm_3xtf32<<<grid, K1Cfg::kThreads, K1Cfg::kSmem, s>>>(
         m.a_hi, m.a_lo, m.b_hi, m.b_lo, n_pad, m_pad, out_f32, n_out, m_out, ld_out, out_hi, out_lo,
-        0);
+        0, gate);
     return cudaGetLastError();
 }
 

@@ -375,9 +375,15 @@ int ensure_ws16(mxp_handle h, int64_t n_pad) {
     return MXP_OK;
 }
 
-bool use_k1ph(mxp_handle h, int64_t n) {
-    return h->f32_datapath == MXP_DATAPATH_AUTO && n > kSmallMax && k1ph_eligible(round_up(n, 128));
+// Padded order a K1PH chain runs at, 0 when the chain stays on 3xTF32: the
+// CTA-pair sizes (roundup(n, 128) a multiple of 256, >= 1024), and beyond
+// K1C's one-launch range (n > 1408) every other order, padded to 256.
+int64_t k1ph_pad(mxp_handle h, int64_t n) {
+    if (h->f32_datapath != MXP_DATAPATH_AUTO || n <= kSmallMax) return 0;
+    if (k1ph_eligible(round_up(n, 128))) return round_up(n, 128);
+    return n > 1408 ? round_up(n, 256) : 0;
 }
+bool use_k1ph(mxp_handle h, int64_t n) { return k1ph_pad(h, n) != 0; }
 
 int ensure_ws64(mxp_handle h, int64_t n_pad) {
     h->rhs_mode = -1;
@@ -422,7 +428,7 @@ int enqueue_chain_tf32(mxp_handle h, int64_t n, const PlanBits& plan, const floa
 // index 0 = the base, s + 1 = the product of step s.
 int enqueue_chain_f16x2(mxp_handle h, int64_t n, const PlanBits& plan, const float* dA,
                         float* dOut, int64_t* launches, int64_t* failed) {
-    const int64_t n_pad = round_up(n, 128);
+    const int64_t n_pad = k1ph_pad(h, n);
     int rc = ensure_ws16(h, n_pad);
     if (rc) return rc;
     const int np = (int)n_pad;
@@ -635,7 +641,7 @@ int run_power_graph(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA
         // workspace must exist before capture (no cudaMalloc inside capture)
         if (mode == MXP_F32 && n > kSmallMax) {
             int rc = ensure_ws32(h, round_up(n, 128));
-            if (rc == MXP_OK && use_k1ph(h, n)) rc = ensure_ws16(h, round_up(n, 128));
+            if (rc == MXP_OK && use_k1ph(h, n)) rc = ensure_ws16(h, k1ph_pad(h, n));
             if (rc) return rc;
         } else if (mode == MXP_F64) {
             int rc = ensure_ws64(h, f64_pad((int)n));

@@ -30,7 +30,8 @@ def _both(eng, a, k):
     return g16, fb, g32
 
 
-@pytest.mark.parametrize("n,k", [(1024, 13), (1280, 9), (1500, 16), (2048, 7), (1024, 1000)])
+@pytest.mark.parametrize("n,k", [(1024, 13), (1280, 9), (1500, 16), (2048, 7), (1024, 1000),
+                                 (1600, 13), (2000, 9)])  # (1664 / 2048 padded to 1792 / 2048)
 def test_k1ph_chain_vs_oracle_and_3xtf32(eng, n, k):
     a = oracle.scaled_input(n, np.float32, 42)
     g16, fb, g32 = _both(eng, a, k)
@@ -43,7 +44,8 @@ def test_k1ph_chain_vs_oracle_and_3xtf32(eng, n, k):
 
 
 def test_k1ph_not_used_off_pair_sizes(eng):
-    """n_pad % 256 != 0 (n = 1100 -> 1152) stays on 3xTF32 whatever the switch."""
+    """n = 1100 (n_pad 1152, inside K1C's one-launch range) stays on 3xTF32
+    whatever the switch."""
     a = oracle.scaled_input(1100, np.float32, 5)
     eng.set_f32_datapath("auto")
     g16 = eng.power(a, 9)
@@ -62,7 +64,7 @@ def _cancelling(n, seed=5):
     return (nil + 1e-6 * rng.uniform(-1, 1, (n, n))).astype(np.float32)
 
 
-@pytest.mark.parametrize("n", [1024, 1536])
+@pytest.mark.parametrize("n", [1024, 1536, 1600])  # 1600: K1PH at 1792, recomputation on K1 at 1664
 def test_k1ph_cancellation_recomputed_on_3xtf32(eng, n):
     """A = N + eps R, N^2 = 0: A^2 ~ eps, so the one-exponent planes would
     lose the eps^2 entries A^6 depends on.  The split of A^2 raises the flag

@@ -24,7 +24,15 @@ eng.gemm_rows_prepared_device(t[256:384].data_ptr(), o.data_ptr(), 512, 128)
 eng.synchronize()
 eng.power(oracle.scaled_input(384, np.float32, 42), 13)                 # K1C one-launch chain
 eng.multiply(oracle.scaled_input(256, np.float32, 1), oracle.scaled_input(256, np.float32, 2))  # K1 cluster split-K
-eng.power(oracle.scaled_input(1024, np.float32, 42), 5)                 # K1P CTA pairs
+eng.power(oracle.scaled_input(1024, np.float32, 42), 5)                 # K1PH persistent pairs + split16
+eng.power(oracle.scaled_input(1600, np.float32, 42), 3)                 # K1PH padded to 256 (1792)
+nil = np.zeros((1024, 1024), np.float32)
+nil[:512, 512:] = 1.0
+eng.power((nil + np.float32(1e-6)).astype(np.float32), 6)                # K1PH flag -> gated 3xTF32 chain runs
+print("k1ph fallback", eng.last_f32_fallback())
+eng.set_f32_datapath("3xtf32")
+eng.power(oracle.scaled_input(1024, np.float32, 42), 5)                 # K1P CTA pairs (3xTF32 datapath)
+eng.set_f32_datapath("auto")
 eng.power(oracle.scaled_input(256, np.float64, 42), 9)                  # FP64 DMMA
 eng.power_mod(np.arange(100 * 100, dtype=np.uint32).reshape(100, 100), 11, 65521)  # K5I (INT8)
 eng.power_mod(np.arange(300 * 300, dtype=np.uint32).reshape(300, 300) * 7919, 6, 2**31 - 1)
