@@ -48,6 +48,11 @@ struct K1HCfg {
     static constexpr uint32_t kStageBytes = 2 * kABytes + 2 * kBBytes;  // 64 KB per CTA
     static constexpr size_t kSmem = kStages * kStageBytes + 1024 + 256;
     static constexpr int kThreads = 384;
+#ifndef MXP_K1PH_CHUNK_STAGES
+#define MXP_K1PH_CHUNK_STAGES 1
+#endif
+    // stages accumulated in one TMEM chunk before the drain (bias control)
+    static constexpr int kChunkStages = MXP_K1PH_CHUNK_STAGES;
 };
 
 // kind::f16, fp16 A/B (formats 0), fp32 D, A K-major, B MN-major, M = N = 256 (pair)
@@ -189,8 +194,11 @@ __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
             for (int kb = 0; kb < num_kb; ++kb, ++g) {
                 const uint32_t stg = g % S;
                 const uint32_t ph = (g / S) & 1;
-                const uint32_t c = g & 1;
-                mbar_wait(&cempty[c], ((g >> 1) & 1) ^ 1);
+                constexpr uint32_t CS = Cfg::kChunkStages;
+                const uint32_t hc = g / CS;  // chunk counter
+                const uint32_t c = hc & 1;
+                const bool first = (g % CS) == 0, lastc = (g % CS) == CS - 1;
+                if (first) mbar_wait(&cempty[c], ((hc >> 1) & 1) ^ 1);
                 mbar_wait(&full[stg], ph);
                 tc_fence_after();
                 const uint64_t so = static_cast<uint64_t>((stg * Cfg::kStageBytes) >> 4);
@@ -199,7 +207,7 @@ __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const uint64_t ao = so + ((32 * k) >> 4), bo = so + ((2048 * k) >> 4);
-                    mma_f16_pair(d, da1 + ao, db0 + bo, kIdescPair, k > 0 ? 1u : 0u);
+                    mma_f16_pair(d, da1 + ao, db0 + bo, kIdescPair, (k > 0 || !first) ? 1u : 0u);
                     mma_f16_pair(d, da0 + ao, db1 + bo, kIdescPair, 1u);
                 }
 #pragma unroll
@@ -208,7 +216,7 @@ __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
                     mma_f16_pair(d, da0 + ao, db0 + bo, kIdescPair, 1u);
                 }
                 mma_commit_pair(&empty[stg], 0x3);
-                mma_commit_pair(&cfull[c], 0x3);
+                if (lastc) mma_commit_pair(&cfull[c], 0x3);
             }
         }
     } else if (warp >= 4) {
@@ -225,8 +233,8 @@ __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
             float sum[128];
 #pragma unroll
             for (int i = 0; i < 128; ++i) sum[i] = 0.f;
-            for (int kb = 0; kb < num_kb; ++kb, ++g) {
-                const uint32_t c = g & 1;
+            for (int kb = 0; kb < num_kb; kb += Cfg::kChunkStages, ++g) {
+                const uint32_t c = g & 1;  // (g counts chunks here)
                 mbar_wait(&cfull[c], (g >> 1) & 1);
                 tc_fence_after();
 #pragma unroll
