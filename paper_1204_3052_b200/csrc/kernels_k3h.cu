@@ -256,9 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // let the K3B fixup pass (a programmatic dependent) launch now: it only
     // waits for this grid's completion (griddepcontrol.wait), so its launch
     // latency hides under this kernel instead of adding to a short chain
-#ifndef K3H_PROBE_NO_PDL
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
     if (stamps != nullptr && blockIdx.x == 0 && tid == 0) {
         stamps[0] = clock64();
         stamps[1] = globaltimer_ns();
@@ -594,10 +592,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     {  // the last step's maxima: did the product feeding this one cancel?
                         const uint32_t mlast = slots_max(C, st);
                         const bool lost = (st.mph & kLost) || range_lost(ilogb_bits(mlast) + st.t_prev, mlast);
-#ifndef K3H_PROBE_NO_FLAG
                         if (lost && fix_idx != nullptr && warp == 0 && lane == 0)
                             fix_idx[atomicAdd(fix_count, 1)] = static_cast<int>(st.m);
-#endif
                     }
                     const uint64_t g1 = splat2(exp2i(pe / 2)), g2 = splat2(exp2i(pe - pe / 2));
                     const uint32_t old_region = s0 + st.home * kChainSmem;
