@@ -99,10 +99,11 @@ struct F16Chain {
 // sums; oi >= 0: max |out| -> maxw[oi] (atomicMax of the bit patterns), which
 // the split of the next planes turns into their exact scale.
 //
-// (Measured and rejected: writing the next planes straight from the epilogue
-// at the bound scale n max|X| max|Y|, K3H's scheme — 6% faster on C5, but the
-// bound sits lg n bits above a sparse product's max, and a signed permutation
-// power with 2^13 of dynamic range lost its exactness at n = 1024.)
+// (Measured and rejected, DESIGN.md §3 K1PH: writing the next planes straight
+// from the epilogue at a bound scale instead of this split pass — at the
+// bound n max|X| max|Y| a signed permutation power with 2^13 of dynamic range
+// lost its exactness at n = 1024; at the tighter row-norm bound it stayed
+// exact but ran no faster than the split under the board's power cap.)
 __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
     k1ph_gemm_f16x2(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUtensorMap ma1,
                     const __grid_constant__ CUtensorMap mb0, const __grid_constant__ CUtensorMap mb1,
