@@ -189,8 +189,8 @@ MXP_API int mxp_power_batched(mxp_handle h, int mode, int64_t n, int64_t batch, 
  *   batch == 1, MXP_F32, n > 128, k >= 2: row-sharded chain, each step's
  *     new rows stored by the CTA-pair GEMM epilogue straight into every
  *     device's next planes over NVLink (peer access), CUDA events between
- *     steps; bitwise equal to mxp_power where that also runs the CTA-pair
- *     kernel (n % 256 == 0, n >= 1024);
+ *     steps (3xTF32); bitwise equal to mxp_power on MXP_DATAPATH_3XTF32
+ *     where that also runs the CTA-pair kernel (n % 256 == 0, n >= 1024);
  *   batch == 1, MXP_F64, n >= 256, k >= 2: row-sharded with the DMMA
  *     row-block GEMM and peer copies of each device's rows, bitwise equal to
  *     mxp_power;

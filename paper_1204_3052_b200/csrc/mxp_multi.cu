@@ -16,8 +16,9 @@
 //     waits for every device's previous step before it overwrites their
 //     planes).  Every element's dot product is computed on one device with
 //     the single-GPU kernel and k-order, so the result is bitwise equal to
-//     mxp_power when the single-GPU chain runs the same CTA-pair kernel
-//     (n % 256 == 0, n >= 1024);
+//     mxp_power on the 3xTF32 datapath (MXP_DATAPATH_3XTF32: the same
+//     CTA-pair kernel, n % 256 == 0, n >= 1024; the default single-GPU chain
+//     at these sizes is K1PH, equal within the tolerance);
 //   * batch == 1, FP64, n >= 256, k >= 2: row-sharded with the DMMA row-block
 //     GEMM and peer copies of each device's rows (power_multi_rows_f64);
 //   * anything else (n <= 128 FP32, small FP64, k <= 1) is too small to
