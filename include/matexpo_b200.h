@@ -186,7 +186,13 @@ MXP_API int mxp_power_batched(mxp_handle h, int mode, int64_t n, int64_t batch, 
  * occurrence gets its own internal handle and stream), 1 <= ngpus <= 8.
  *   batch >= 2: contiguous batch shards, one host thread per device running
  *     mxp_power_batched — no communication, bitwise equal to one device;
- *   batch == 1, MXP_F32, n > 128, k >= 2: row-sharded chain, each step's
+ *   batch == 1, MXP_F32 at the K1PH sizes (see mxp_set_f32_datapath), k >= 2:
+ *     row-sharded K1PH chain: each device's fp32 rows, the maxima met in every
+ *     device's state (peer atomics), each device's rows split at the global
+ *     scale into every device's planes (peer stores); bitwise the
+ *     single-device K1PH chain (recomputed on the 3xTF32 row shards below if
+ *     a product loses dynamic range);
+ *   batch == 1, MXP_F32, other n > 128, k >= 2: row-sharded chain, each step's
  *     new rows stored by the CTA-pair GEMM epilogue straight into every
  *     device's next planes over NVLink (peer access), CUDA events between
  *     steps (3xTF32); bitwise equal to mxp_power on MXP_DATAPATH_3XTF32

@@ -95,8 +95,8 @@ struct F16Chain {
 //   warp 0 : TMA producer (both CTAs; bytes complete on the leader's barrier)
 //   warp 1 : MMA issuer (leader only)     warp 2 : TMEM allocator (both)
 //   warps 4-11 : epilogue (both CTAs; lane quarter = warp % 4, 128-column half)
-// out (fp32, n_out x n_out, leading dim ld_out) = 2^-(texp[xi] + texp[yi]) *
-// sums; oi >= 0: max |out| -> maxw[oi] (atomicMax of the bit patterns), which
+// out (fp32, leading dim ld_out; entries of global row >= n_out or column >=
+// n_out are not written) = 2^-(texp[xi] + texp[yi]) * sums; oi >= 0: max |out| -> maxw[oi] (atomicMax of the bit patterns), which
 // the split of the next planes turns into their exact scale.
 //
 // (Measured and rejected, DESIGN.md §3 K1PH: writing the next planes straight
@@ -107,8 +107,8 @@ struct F16Chain {
 __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
     k1ph_gemm_f16x2(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUtensorMap ma1,
                     const __grid_constant__ CUtensorMap mb0, const __grid_constant__ CUtensorMap mb1,
-                    int n_pad, float* __restrict__ out, int n_out, int ld_out,
-                    F16Chain* __restrict__ st, int xi, int yi, int oi) {
+                    int n_pad, int m_rows, int row0, float* __restrict__ out, int n_out,
+                    int ld_out, F16Chain* __restrict__ st, int xi, int yi, int oi) {
     using Cfg = K1HCfg;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -126,7 +126,9 @@ __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
 
     // grouped tile raster (as K1P); pair p takes tiles p, p + P, p + 2P, ...
     constexpr int kGroupM = 8;
-    const int num_m = n_pad / 256, num_n = n_pad / 256;
+    // row block [row0, row0 + m_rows) of the product (the whole matrix:
+    // m_rows = n_pad, row0 = 0); out row r holds global row row0 + r
+    const int num_m = m_rows / 256, num_n = n_pad / 256;
     const int num_tiles = num_m * num_n;
     const int per_group = kGroupM * num_n;
     const int num_kb = n_pad / Cfg::kBK;
@@ -173,8 +175,8 @@ __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
                 uint8_t* base = smem + stg * Cfg::kStageBytes;
                 if (leader) mbar_expect_tx(&full[stg], 2 * Cfg::kStageBytes);
                 const int kk = kb * Cfg::kBK;
-                tma_load_2d_pair(base, &ma0, &full[stg], kk, m0);
-                tma_load_2d_pair(base + Cfg::kABytes, &ma1, &full[stg], kk, m0);
+                tma_load_2d_pair(base, &ma0, &full[stg], kk, row0 + m0);
+                tma_load_2d_pair(base + Cfg::kABytes, &ma1, &full[stg], kk, row0 + m0);
                 uint8_t* b0 = base + 2 * Cfg::kABytes;
                 uint8_t* b1 = b0 + Cfg::kBBytes;
 #pragma unroll
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster_relaxed(cempty_leader0 + 8 * c);
             }
-            const int row = m0 + q * 32 + lane;
+            const int row = m0 + q * 32 + lane;  // local row of out
             uint32_t mbits = 0;
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(K1HCfg::kThreads, 1)
                     v[i] = __fmul_rn(__fmul_rn(v[i], g1), g2);
                     mbits = max(mbits, __float_as_uint(v[i]) & 0x7FFFFFFFu);
                 }
-                if (row < n_out && col < n_out) {
+                if (row0 + row < n_out && col < n_out) {
                     float* d = out + static_cast<size_t>(row) * ld_out + col;
                     if ((ld_out & 3) == 0 && col + 32 <= n_out) {
 #pragma unroll
@@ -369,6 +371,65 @@ __global__ void split16_kernel(const float* __restrict__ in, int n, int ld,
     }
 }
 
+// Row-sharded chains (mxp_power_multi): max |P_i| of this device's rows ->
+// every device's maxw[i] (system-scope atomics over peer access), so each
+// device then holds the global max.
+struct PeerStates {
+    F16Chain* st[kF16MaxPeers];
+    int n;
+};
+__global__ void max_to_peers_kernel(const F16Chain* __restrict__ mine, int i, PeerStates ps) {
+    const uint32_t v = mine->maxw[i];
+    for (int p = 0; p < ps.n; ++p) atomicMax_system(&ps.st[p]->maxw[i], v);
+}
+
+// This device's fp32 rows of P_i (m_rows x n_pad, global rows row0 ..) ->
+// the h0 / h1 rows of P_i in EVERY device's planes (peer stores), at the
+// exact scale of the global max st->maxw[i]; texp[i] and the dynamic-range
+// test as split16_kernel (every device derives the same values).
+struct PeerPlanes {
+    __half* h0[kF16MaxPeers];
+    __half* h1[kF16MaxPeers];
+    int n;
+};
+__global__ void split16_rows_peers_kernel(const float* __restrict__ in, int m_rows, int row0,
+                                          int n_pad, F16Chain* __restrict__ st, int i, int xi,
+                                          int yi, int lg_n, PeerPlanes pp) {
+    const uint32_t mb = st->maxw[i];
+    const int t = max(-126, min(126, scale_exp(mb)));
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->texp[i] = t;
+        const uint32_t xb = st->maxw[xi], yb = st->maxw[yi];
+        bool lost = mb == 0u || mb >= 0x7F800000u || xb >= 0x7F800000u || yb >= 0x7F800000u;
+        if (!lost && xb != 0u && yb != 0u) {
+            const int bound_e = (ilogb_bits(xb) + 1) + (ilogb_bits(yb) + 1) + lg_n;
+            lost = ilogb_bits(mb) < bound_e - 12;
+        }
+        if (lost) st->flag = 1;
+    }
+    const float sc = exp2i(t);
+    const size_t groups = static_cast<size_t>(m_rows) * n_pad / 8;
+    const size_t off = static_cast<size_t>(row0) * n_pad / 8;  // in 16-byte units
+    for (size_t g = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; g < groups;
+         g += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(in) + 2 * g);
+        const float4 b = __ldg(reinterpret_cast<const float4*>(in) + 2 * g + 1);
+        const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        __align__(16) __half a0[8], a1[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float x = __fmul_rn(v[k], sc);
+            a0[k] = __float2half_rn(x);
+            a1[k] = __float2half_rn(__fsub_rn(x, __half2float(a0[k])));
+        }
+        const uint4 w0 = *reinterpret_cast<const uint4*>(a0), w1 = *reinterpret_cast<const uint4*>(a1);
+        for (int p = 0; p < pp.n; ++p) {
+            reinterpret_cast<uint4*>(pp.h0[p])[off + g] = w0;
+            reinterpret_cast<uint4*>(pp.h1[p])[off + g] = w1;
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t prepare_f16x2_kernels() {
@@ -409,11 +470,12 @@ int* f16_chain_flag(void* state) { return &static_cast<F16Chain*>(state)->flag; 
 
 cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, float* out, int n_out,
                              int ld_out, void* state, int xi, int yi, int oi, int num_sms,
-                             cudaStream_t s) {
+                             cudaStream_t s, int m_rows, int row0) {
+    if (m_rows <= 0) m_rows = n_pad;
     if (!k1ph_eligible(n_pad) || xi < 0 || yi < 0 || xi > kF16MaxSteps || yi > kF16MaxSteps ||
-        oi > kF16MaxSteps)
+        oi > kF16MaxSteps || m_rows % 256 != 0 || row0 < 0 || row0 + m_rows > n_pad)
         return cudaErrorInvalidValue;
-    const int tiles = (n_pad / 256) * (n_pad / 256);
+    const int tiles = (m_rows / 256) * (n_pad / 256);
     const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * pairs);
@@ -427,8 +489,8 @@ cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, floa
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k1ph_gemm_f16x2, x.a0, x.a1, y.b0, y.b1, n_pad, out, n_out, ld_out,
-                              static_cast<F16Chain*>(state), xi, yi, oi);
+    return cudaLaunchKernelEx(&cfg, k1ph_gemm_f16x2, x.a0, x.a1, y.b0, y.b1, n_pad, m_rows, row0, out,
+                              n_out, ld_out, static_cast<F16Chain*>(state), xi, yi, oi);
 }
 
 cudaError_t launch_split16(const float* in, int n, int ld, void* h0, void* h1, int n_pad,
@@ -449,6 +511,36 @@ cudaError_t launch_split16(const float* in, int n, int ld, void* h0, void* h1, i
     if (blocks > 148 * 8) blocks = 148 * 8;
     split16_kernel<<<blocks, 256, 0, s>>>(in, n, ld, static_cast<__half*>(h0), static_cast<__half*>(h1),
                                           n_pad, st, i, xi, yi, lg_n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_max_to_peers(const void* state, int i, void* const* peer_states, int npeers,
+                                cudaStream_t s) {
+    if (npeers < 1 || npeers > kF16MaxPeers || i < 0 || i > kF16MaxSteps) return cudaErrorInvalidValue;
+    PeerStates ps{};
+    for (int p = 0; p < npeers; ++p) ps.st[p] = static_cast<F16Chain*>(peer_states[p]);
+    ps.n = npeers;
+    max_to_peers_kernel<<<1, 1, 0, s>>>(static_cast<const F16Chain*>(state), i, ps);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_split16_rows_peers(const float* in, int m_rows, int row0, int n_pad, int n,
+                                      void* state, int i, int xi, int yi, void* const* h0,
+                                      void* const* h1, int npeers, cudaStream_t s) {
+    if (npeers < 1 || npeers > kF16MaxPeers || n_pad % 8 != 0) return cudaErrorInvalidValue;
+    PeerPlanes pp{};
+    for (int p = 0; p < npeers; ++p) {
+        pp.h0[p] = static_cast<__half*>(h0[p]);
+        pp.h1[p] = static_cast<__half*>(h1[p]);
+    }
+    pp.n = npeers;
+    int lg_n = 0;
+    while ((1ll << lg_n) < n) ++lg_n;
+    const size_t groups = static_cast<size_t>(m_rows) * n_pad / 8;
+    int blocks = static_cast<int>((groups + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    split16_rows_peers_kernel<<<blocks, 256, 0, s>>>(in, m_rows, row0, n_pad,
+                                                     static_cast<F16Chain*>(state), i, xi, yi, lg_n, pp);
     return cudaGetLastError();
 }
 

@@ -148,9 +148,21 @@ cudaError_t launch_split16(const float* in, int n, int ld, void* h0, void* h1, i
                            void* state, int i, int xi, int yi, cudaStream_t s);
 // P_oi = P_xi P_yi (fp32 out: n_out x n_out, leading dim ld_out) from the
 // planes of P_xi (left) and P_yi (right); oi >= 0: max |P_oi| -> maxw[oi]
+// m_rows > 0: only rows [row0, row0 + m_rows) of the product (multiples of
+// 256), out row r = global row row0 + r (row-sharded chains)
 cudaError_t launch_k1ph_gemm(const F16Maps& x, const F16Maps& y, int n_pad, float* out, int n_out,
                              int ld_out, void* state, int xi, int yi, int oi, int num_sms,
-                             cudaStream_t s);
+                             cudaStream_t s, int m_rows = 0, int row0 = 0);
+// Row-sharded K1PH chains (mxp_multi.cu): this device's max |P_i| into every
+// device's state (system-scope atomicMax over peer access), then this
+// device's fp32 rows of P_i split at the global exact scale into every
+// device's h0 / h1 planes (peer stores), with the dynamic-range test.
+constexpr int kF16MaxPeers = 8;
+cudaError_t launch_max_to_peers(const void* state, int i, void* const* peer_states, int npeers,
+                                cudaStream_t s);
+cudaError_t launch_split16_rows_peers(const float* in, int m_rows, int row0, int n_pad, int n,
+                                      void* state, int i, int xi, int yi, void* const* h0,
+                                      void* const* h1, int npeers, cudaStream_t s);
 
 // ---- generation (kernels_gen.cu) -------------------------------------------
 // Reference random_matrix (linalg.py:127-148) on device; scale != 0 selects

@@ -19,6 +19,14 @@
 //     mxp_power on the 3xTF32 datapath (MXP_DATAPATH_3XTF32: the same
 //     CTA-pair kernel, n % 256 == 0, n >= 1024; the default single-GPU chain
 //     at these sizes is K1PH, equal within the tolerance);
+//   * batch == 1, FP32 at the K1PH sizes (n > 1408, or roundup(n, 128) a
+//     multiple of 256 >= 1024): the same row shards on scaled fp16x2 planes
+//     (power_multi_rows_f16): each device computes its fp32 rows with the
+//     K1PH row-block GEMM, the row maxima meet in every device's chain state
+//     (system-scope atomicMax over peer access), and each device splits its
+//     rows at the global exact scale straight into every device's next
+//     planes (peer stores) — bitwise the single-device K1PH chain; a chain
+//     that loses dynamic range is recomputed on the 3xTF32 row shards;
 //   * batch == 1, FP64, n >= 256, k >= 2: row-sharded with the DMMA row-block
 //     GEMM and peer copies of each device's rows (power_multi_rows_f64);
 //   * anything else (n <= 128 FP32, small FP64, k <= 1) is too small to
@@ -38,6 +46,7 @@
 #include <cuda_runtime.h>
 
 #include "matexpo_b200.h"
+#include "mxp_internal.h"
 
 // defined in mxp_api.cu: the library's (thread-local) error slot
 int mxp_internal_fail(int code, const char* fmt, ...);
@@ -474,6 +483,236 @@ int power_multi_rows(const std::vector<mxp_handle>& hs, const int* devices, int6
     return MXP_OK;
 }
 
+// ---- one FP32 matrix, row shards on scaled fp16x2 planes (K1PH) ---------
+// Returns MXP_OK with *raised = 1 when the chain lost dynamic range (the
+// caller then recomputes on the 3xTF32 row shards).
+bool k1ph_multi_eligible(int64_t n) {
+    const int64_t p128 = (n + 127) / 128 * 128;
+    return (p128 >= 1024 && p128 % 256 == 0) || n > 1408;
+}
+
+int power_multi_rows_f16(const std::vector<mxp_handle>& hs, const int* devices, int64_t n,
+                         int64_t k, const void* hA, void* hOut, mxp_stats* st, int* raised) {
+    using namespace mxp;
+    const int G = static_cast<int>(hs.size());
+    *raised = 0;
+    // the single-device chain's padded order when it is a multiple of 256 G
+    // (results are bitwise the single-device chain's for any padding: zero
+    // rows and columns only add exact zeros in the same k-blocks)
+    int64_t n_p = (n + 256 * G - 1) / (256 * G) * (256 * G);
+    if (n_p < 1024) n_p = (1024 + 256 * G - 1) / (256 * G) * (256 * G);
+    const int64_t rows = n_p / G;
+    const size_t n2 = static_cast<size_t>(n_p) * n_p;
+    std::vector<int> dev(G);
+    for (int g = 0; g < G; ++g) dev[g] = devices ? devices[g] : g;
+    int rc = enable_peers(dev);
+    if (rc) return rc;
+    struct Bufs {
+        void* plane[6] = {};  // h0/h1 of base, p0, p1 (fp16, n_p x n_p)
+        void* rowsf = nullptr;  // this device's fp32 rows of the running product
+        void* state = nullptr;
+        void* out = nullptr;    // the final fp32 rows of every device (devices[0])
+        cudaEvent_t ev = nullptr;
+        F16Maps maps[3];
+    };
+    struct Guard {
+        const std::vector<mxp_handle>& hs;
+        std::vector<Bufs> b;
+        explicit Guard(const std::vector<mxp_handle>& h) : hs(h), b(h.size()) {}
+        ~Guard() {
+            for (size_t g = 0; g < b.size(); ++g) {
+                mxp_synchronize(hs[g]);
+                for (void* p : b[g].plane)
+                    if (p) mxp_free(hs[g], p);
+                for (void* p : {b[g].rowsf, b[g].state, b[g].out})
+                    if (p) mxp_free(hs[g], p);
+                if (b[g].ev) cudaEventDestroy(b[g].ev);
+            }
+        }
+    } guard(hs);
+    auto& B = guard.b;
+    std::vector<cudaStream_t> stream(G);
+    std::vector<int> sms(G);
+    for (int g = 0; g < G && rc == MXP_OK; ++g) {
+        void* s = nullptr;
+        rc = mxp_get_stream(hs[g], &s);
+        stream[g] = static_cast<cudaStream_t>(s);
+        if (rc == MXP_OK) rc = mxp_num_sms(hs[g], &sms[g]);
+        for (int i = 0; i < 6 && rc == MXP_OK; ++i) rc = mxp_alloc(hs[g], n2 * 2, &B[g].plane[i]);
+        if (rc == MXP_OK) rc = mxp_alloc(hs[g], static_cast<size_t>(rows) * n_p * 4, &B[g].rowsf);
+        if (rc == MXP_OK) rc = mxp_alloc(hs[g], f16_chain_state_bytes(), &B[g].state);
+        if (rc == MXP_OK && g == 0) rc = mxp_alloc(hs[g], static_cast<size_t>(n) * n * 4, &B[g].out);
+        if (rc == MXP_OK) {
+            cudaSetDevice(dev[g]);
+            if (cudaEventCreateWithFlags(&B[g].ev, cudaEventDisableTiming) != cudaSuccess)
+                rc = mxp_internal_fail(MXP_E_CUDA, "event creation on device %d", dev[g]);
+            for (int i = 0; i < 3 && rc == MXP_OK; ++i) {
+                F16Maps& m = B[g].maps[i];
+                if (!encode_plane16_map(&m.a0, B[g].plane[2 * i], (int)n_p, 128) ||
+                    !encode_plane16_map(&m.a1, B[g].plane[2 * i + 1], (int)n_p, 128) ||
+                    !encode_plane16_map(&m.b0, B[g].plane[2 * i], (int)n_p, 64) ||
+                    !encode_plane16_map(&m.b1, B[g].plane[2 * i + 1], (int)n_p, 64))
+                    rc = mxp_internal_fail(MXP_E_CUDA, "cuTensorMapEncodeTiled (fp16) failed");
+            }
+        }
+    }
+    if (rc) return rc;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    cudaSetDevice(dev[0]);
+    if (cudaEventCreate(&t0) != cudaSuccess || cudaEventCreate(&t1) != cudaSuccess)
+        return mxp_internal_fail(MXP_E_CUDA, "event creation");
+    struct EvGuard {
+        cudaEvent_t a, b;
+        ~EvGuard() {
+            if (a) cudaEventDestroy(a);
+            if (b) cudaEventDestroy(b);
+        }
+    } evg{t0, t1};
+    auto fence = [&]() -> int {
+        for (int g = 0; g < G; ++g) {
+            cudaSetDevice(dev[g]);
+            if (cudaEventRecord(B[g].ev, stream[g]) != cudaSuccess)
+                return mxp_internal_fail(MXP_E_CUDA, "event record on device %d", dev[g]);
+        }
+        for (int g = 0; g < G; ++g) {
+            cudaSetDevice(dev[g]);
+            for (int q = 0; q < G; ++q)
+                if (q != g && cudaStreamWaitEvent(stream[g], B[q].ev, 0) != cudaSuccess)
+                    return mxp_internal_fail(MXP_E_CUDA, "stream wait on device %d", dev[g]);
+        }
+        return MXP_OK;
+    };
+    cudaEventRecord(t0, stream[0]);
+    // every device: A uploaded into a temporary, its state reset, the base
+    // planes and max computed locally (identical on every device)
+    std::vector<void*> a_dev(G, nullptr);
+    for (int g = 0; g < G && rc == MXP_OK; ++g) {
+        rc = mxp_alloc(hs[g], static_cast<size_t>(n) * n * 4, &a_dev[g]);
+        if (rc) break;
+        cudaSetDevice(dev[g]);
+        cudaError_t e = cudaMemsetAsync(B[g].state, 0, f16_chain_state_bytes(), stream[g]);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(a_dev[g], hA, static_cast<size_t>(n) * n * 4, cudaMemcpyHostToDevice,
+                                stream[g]);
+        // the base planes and max, identical on every device
+        if (e == cudaSuccess)
+            e = launch_split16(static_cast<const float*>(a_dev[g]), (int)n, (int)n, B[g].plane[0],
+                               B[g].plane[1], (int)n_p, B[g].state, 0, -1, -1, stream[g]);
+        if (e != cudaSuccess)
+            rc = mxp_internal_fail(MXP_E_CUDA, "upload / split on device %d: %s", dev[g],
+                                   cudaGetErrorString(e));
+    }
+    auto free_a = [&]() {
+        for (int g = 0; g < G; ++g)
+            if (a_dev[g]) {
+                mxp_synchronize(hs[g]);
+                mxp_free(hs[g], a_dev[g]);
+                a_dev[g] = nullptr;
+            }
+    };
+    // every state is reset before any device's maxima reach it
+    if (rc == MXP_OK) rc = fence();
+    if (rc) {
+        free_a();
+        return rc;
+    }
+    int64_t sq = 0;
+    const int64_t m = plan_len(k, &sq);
+    int cur = 0, cur_i = 0, launches = 0;  // plane pair of the running power, its state index
+    int64_t bit = 62;
+    while (!((k >> bit) & 1)) --bit;
+    int64_t step = 0;
+    std::vector<void*> states(G), dh0(G), dh1(G);
+    for (int g = 0; g < G; ++g) states[g] = B[g].state;
+    for (int64_t s = bit - 1; s >= 0 && rc == MXP_OK; --s) {
+        for (int mult = 0; mult < 2 && rc == MXP_OK; ++mult) {
+            if (mult && !((k >> s) & 1)) break;
+            const bool last = step == m - 1;
+            const int nxt = cur == 1 ? 2 : 1;
+            const int rhs = mult ? 0 : cur, rhs_i = mult ? 0 : cur_i;
+            const int oi = static_cast<int>(step) + 1;
+            for (int g = 0; g < G && rc == MXP_OK; ++g) {
+                cudaSetDevice(dev[g]);
+                const int64_t row0 = g * rows;
+                // last step: this device's rows of the result straight into
+                // devices[0]'s n x n output (peer stores, rows < n only)
+                float* out = last ? static_cast<float*>(B[0].out) + row0 * n
+                                  : static_cast<float*>(B[g].rowsf);
+                cudaError_t e = cudaSuccess;
+                if (!last || row0 < n)
+                    e = launch_k1ph_gemm(B[g].maps[cur], B[g].maps[rhs], (int)n_p, out,
+                                         last ? (int)n : (int)n_p, last ? (int)n : (int)n_p,
+                                         B[g].state, cur_i, rhs_i, last ? -1 : oi, sms[g], stream[g],
+                                         (int)rows, (int)row0);
+                if (e == cudaSuccess && !last) e = launch_max_to_peers(B[g].state, oi, states.data(), G, stream[g]);
+                if (e != cudaSuccess) {
+                    if (st) st->failed_step = step;
+                    rc = mxp_internal_fail(MXP_E_CUDA, "k1ph row block on device %d: %s", dev[g],
+                                           cudaGetErrorString(e));
+                }
+                launches += last ? 1 : 2;
+            }
+            if (rc == MXP_OK && !last) {
+                // every device's max is global: split the rows into everyone's planes
+                if ((rc = fence())) break;
+                for (int q = 0; q < G; ++q) {
+                    dh0[q] = B[q].plane[2 * nxt];
+                    dh1[q] = B[q].plane[2 * nxt + 1];
+                }
+                for (int g = 0; g < G && rc == MXP_OK; ++g) {
+                    cudaSetDevice(dev[g]);
+                    cudaError_t e = launch_split16_rows_peers(
+                        static_cast<const float*>(B[g].rowsf), (int)rows, (int)(g * rows), (int)n_p,
+                        (int)n, B[g].state, oi, cur_i, rhs_i, dh0.data(), dh1.data(), G, stream[g]);
+                    if (e != cudaSuccess) {
+                        if (st) st->failed_step = step;
+                        rc = mxp_internal_fail(MXP_E_CUDA, "row split on device %d: %s", dev[g],
+                                               cudaGetErrorString(e));
+                    }
+                    ++launches;
+                }
+            }
+            if (rc == MXP_OK) rc = fence();
+            cur = nxt;
+            cur_i = oi;
+            ++step;
+        }
+    }
+    if (rc) {
+        free_a();
+        return rc;
+    }
+    cudaSetDevice(dev[0]);
+    cudaEventRecord(t1, stream[0]);
+    cudaError_t e = cudaMemcpyAsync(hOut, B[0].out, static_cast<size_t>(n) * n * 4,
+                                    cudaMemcpyDeviceToHost, stream[0]);
+    for (int g = 0; g < G && e == cudaSuccess; ++g) {
+        cudaSetDevice(dev[g]);
+        e = cudaStreamSynchronize(stream[g]);
+    }
+    free_a();
+    if (e != cudaSuccess)
+        return mxp_internal_fail(MXP_E_CUDA, "row-sharded K1PH chain: %s", cudaGetErrorString(e));
+    int flag = 0;
+    cudaSetDevice(dev[0]);
+    if (cudaMemcpy(&flag, f16_chain_flag(B[0].state), sizeof flag, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return mxp_internal_fail(MXP_E_CUDA, "flag readback");
+    *raised = flag != 0;
+    if (st) {
+        st->multiply_count = m;
+        st->square_count = sq;
+        st->launches = launches + 3 * G;  // + each device's base max / split / state reset
+        st->h2d = G;
+        st->d2h = 1;
+        st->h2d_bytes = static_cast<int64_t>(G) * n * n * 4;
+        st->d2h_bytes = n * n * 4;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t0, t1);
+        st->device_ms = ms;
+    }
+    return MXP_OK;
+}
+
 }  // namespace
 
 extern "C" int mxp_power_multi(int ngpus, const int* devices, int mode, int64_t n, int64_t batch,
@@ -498,8 +737,20 @@ extern "C" int mxp_power_multi(int ngpus, const int* devices, int mode, int64_t 
         if (batch < ngpus) hs.resize(static_cast<size_t>(batch));
         return power_multi_batched(hs, mode, n, batch, k, hA, hOut, st);
     }
-    if (ngpus >= 2 && mode == MXP_F32 && n > 128 && k >= 2)
+    if (ngpus >= 2 && mode == MXP_F32 && n > 128 && k >= 2) {
+        if (k1ph_multi_eligible(n)) {
+            int raised = 0;
+            rc = power_multi_rows_f16(hs, devices, n, k, hA, hOut, st, &raised);
+            // a product lost dynamic range: the 3xTF32 row shards recompute it
+            // (bitwise the single-device chain's 3xTF32 recomputation)
+            if (rc != MXP_OK || !raised) return rc;
+            if (st) {
+                std::memset(st, 0, sizeof *st);
+                st->failed_step = -1;
+            }
+        }
         return power_multi_rows(hs, devices, n, k, hA, hOut, st);
+    }
     if (ngpus >= 2 && mode == MXP_F64 && n >= 256 && k >= 2)
         return power_multi_rows_f64(hs, devices, n, k, hA, hOut, st);
     return mxp_power(hs[0], mode, n, k, hA, hOut, st);  // replicas only

@@ -55,21 +55,51 @@ def test_batch_shards_f64(eng):
     assert got.tobytes() == eng.power_batched(a, 9).tobytes()
 
 
+@pytest.fixture(scope="module")
+def eng_auto():
+    """The default datapath: K1PH at the CTA-pair sizes (what the row shards
+    run there)."""
+    return mx.Engine(0)
+
+
 @pytest.mark.parametrize("devices,n,k", [
-    ([0, 0], 1024, 13),        # n_p = 1024 = the single chain's K1P order: bitwise
+    ([0, 0], 1024, 13),        # n_p = 1024 = the single chain's K1PH order: bitwise
     ([0, 0, 0, 0], 2048, 16),  # four row blocks of 512
-    ([0, 0, 0], 1500, 13),     # ragged: 1500 -> 3 x 512 rows (single chain: n_pad 1536, K1P)
+    ([0, 0, 0], 1500, 13),     # ragged: 1500 -> 3 x 512 rows (single chain: n_pad 1536)
+    ([0, 0], 1600, 9),         # 1600 -> 2 x 1024 rows (single chain: 1792; padding adds exact zeros)
 ])
-def test_row_shards_bitwise_single_device(eng, devices, n, k):
+def test_row_shards_bitwise_single_device(eng_auto, devices, n, k):
+    """K1PH row shards: each device's rows from the K1PH row-block GEMM, the
+    maxima met in every device's state, every device's rows split at the
+    global exact scale into every device's planes — bitwise the single-device
+    K1PH chain."""
     a = oracle.scaled_input(n, np.float32, 42)
     got = mx.exponentiate_multi(a, k, devices)
-    ref = eng.power(a, k)
+    ref = eng_auto.power(a, k)
+    assert not eng_auto.last_f32_fallback()
     assert got.tobytes() == ref.tobytes()
     st = E.power_multi.last_stats
     assert st.multiply_count == mx.multiply_count(k)
     assert st.h2d == len(devices) and st.d2h == 1
     err = oracle.compare(got, oracle.exponentiate(a, k, oracle.max_threads()))[2]
     assert err <= mx.fro_tol(n, k, "f32"), err
+
+
+@pytest.mark.parametrize("devices,n", [([0, 0], 1024), ([0, 0, 0], 1536)])
+def test_row_shards_cancellation_recomputed_on_3xtf32(eng, eng_auto, devices, n):
+    """A product that loses dynamic range (A = N + 1e-6 R, N^2 = 0) makes the
+    K1PH row shards recompute on the 3xTF32 row shards: bitwise the 3xTF32
+    single-device chain, and the default single-device chain (which falls
+    back the same way)."""
+    rng = np.random.default_rng(5)
+    nil = np.zeros((n, n))
+    nil[: n // 2, n // 2:] = rng.uniform(-1, 1, (n // 2, n // 2))
+    a = (nil + 1e-6 * rng.uniform(-1, 1, (n, n))).astype(np.float32)
+    got = mx.exponentiate_multi(a, 6, devices)
+    assert got.tobytes() == eng.power(a, 6).tobytes()   # eng: MXP_DATAPATH_3XTF32
+    auto = eng_auto.power(a, 6)
+    assert eng_auto.last_f32_fallback()
+    assert got.tobytes() == auto.tobytes()
 
 
 def test_row_shards_small_order_vs_oracle(eng):
