@@ -120,3 +120,42 @@ def test_datapath_switch_validation(eng):
         eng.set_f32_datapath("fp8")
     eng.set_f32_datapath("3xtf32")
     eng.set_f32_datapath("auto")
+
+
+@pytest.mark.parametrize("n,k", [(1024, 2), (1024, 3), (1100 + 700, 2), (8200, 2)])
+def test_k1ph_short_chains_and_large_ragged(eng, n, k):
+    """One- and two-step plans (the last GEMM writes the result straight from
+    K1PH's epilogue; no split is tested for range) and ragged orders padded to
+    256 (8200 -> 8448): vs the oracle."""
+    a = oracle.scaled_input(n, np.float32, 7)
+    eng.set_f32_datapath("auto")
+    got = eng.power(a, k)
+    assert not eng.last_f32_fallback()
+    ref = oracle.exponentiate(a, k, oracle.max_threads())
+    assert oracle.compare(got, ref)[2] <= mx.fro_tol(n, k, "f32")
+
+
+def test_k1ph_graph_cache_across_datapath_switches(eng):
+    """Cached chain graphs are dropped when the datapath changes: alternating
+    switches reproduce each datapath's own result bitwise."""
+    a = oracle.scaled_input(1024, np.float32, 9)
+    eng.set_f32_datapath("auto")
+    want16 = eng.power(a, 13)
+    eng.set_f32_datapath("3xtf32")
+    want32 = eng.power(a, 13)
+    assert want16.tobytes() != want32.tobytes()
+    for _ in range(2):
+        eng.set_f32_datapath("auto")
+        assert eng.power(a, 13).tobytes() == want16.tobytes()
+        eng.set_f32_datapath("3xtf32")
+        assert eng.power(a, 13).tobytes() == want32.tobytes()
+    eng.set_f32_datapath("auto")
+
+
+def test_k1ph_batched_chains(eng):
+    """mxp_power_batched with n > 128 runs one chain per matrix (K1PH at these
+    sizes): each matrix as its own single chain, bitwise."""
+    stack = np.stack([oracle.scaled_input(1024, np.float32, 20 + i) for i in range(3)])
+    out = eng.power_batched(stack, 9)
+    for i in range(3):
+        assert out[i].tobytes() == eng.power(stack[i], 9).tobytes()
