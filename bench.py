@@ -48,8 +48,8 @@ WORKLOADS = {
     "c3": dict(name="batched 65536 x 128x128 FP32 (split-fp32 tensor cores) A^64", n=128, batch=65536, k=64,
                dtype="f32"),
     "c2": dict(name="512x512 FP32 (3xTF32) A^1000", n=512, batch=1, k=1000, dtype="f32"),
-    # one GPU: K1PH (scaled fp16x2 planes, 3xTF32 recomputation on range
-    # loss); row-sharded over N GPUs: 3xTF32 CTA pairs with the fused exchange
+    # K1PH (scaled fp16x2 planes, 3xTF32 recomputation on range loss), on one
+    # GPU or row-sharded over N GPUs (RowShardedK1PH)
     "c5": dict(name="8192x8192 FP32 (split-fp32 tensor cores) A^1024", n=8192, batch=1, k=1024,
                dtype="f32"),
     "c4": dict(name="4096x4096 FP64 (DMMA) A^257", n=4096, batch=1, k=257, dtype="f64"),
@@ -354,7 +354,10 @@ def run_row_sharded(eng, w: dict, steps: int, warmup: int, dist, sample=True):
     a = torch.empty((n, n), dtype=torch.float32, device="cuda")
     eng.random_device(a.data_ptr(), n, 1, 42, -0.5, 0.5, math.sqrt(12.0 / n))
     eng.synchronize()
-    chain = D.RowShardedFused(n, a.device, engine=eng)  # buffers + peer mappings, once
+    # buffers + peer mappings, once: K1PH row shards at the K1PH sizes (C5),
+    # else the 3xTF32 fused exchange
+    chain = (D.RowShardedK1PH(n, a.device, engine=eng) if k1ph_runs(w)
+             else D.RowShardedFused(n, a.device, engine=eng))
     for _ in range(warmup):
         chain.power(a, k)
     dist.barrier()
@@ -542,9 +545,9 @@ def plan_only(args, w, world, rank) -> None:
 
 def k1ph_runs(w: dict, world: int = 1) -> bool:
     """Whether a single-matrix f32 chain runs K1PH (kernels_f16x2.cu): the
-    CTA-pair sizes on one GPU (the row-sharded multi-GPU chain runs 3xTF32)."""
+    CTA-pair sizes and n > 1408, on one GPU or row-sharded (RowShardedK1PH)."""
     n_pad = -(-w["n"] // 128) * 128
-    return (w["dtype"] == "f32" and w["batch"] == 1 and world == 1
+    return (w["dtype"] == "f32" and w["batch"] == 1
             and ((n_pad >= 1024 and n_pad % 256 == 0) or w["n"] > 1408))
 
 

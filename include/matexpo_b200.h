@@ -168,6 +168,35 @@ MXP_API int mxp_gemm_rows_planes_mc(mxp_handle h, int64_t n, int64_t rows, int64
 MXP_API int mxp_multiply(mxp_handle h, int mode, int64_t n, const void* hA, const void* hB, void* hC,
                  mxp_stats* stats);
 
+/* K1PH row shards across processes (distributed.RowShardedK1PH; one process
+ * per GPU, peer buffers mapped with mxp_ipc_*).  A chain state (size from
+ * mxp_k1ph_state_bytes, zeroed by the caller before a chain) holds the
+ * maxima, plane exponents and the dynamic-range flag.  fp16 planes are
+ * n x n (n % 256 == 0, n >= 1024), row-major.
+ *   mxp_k1ph_split_base: dA (n_true x n_true fp32, dense) -> base planes at
+ *     its exact scale (state index 0);
+ *   mxp_k1ph_gemm_rows: rows [row0, row0 + rows) of P_xi * P_yi (fp32, out
+ *     leading dim ld_out, entries of global row or column >= n_out skipped);
+ *     oi >= 0: their max -> maxw[oi];
+ *   mxp_k1ph_max_to_peers: this rank's maxw[i] into every peer state;
+ *   mxp_k1ph_split_rows_peers: this rank's fp32 rows of P_i -> h0 / h1 rows in
+ *     every peer's planes at the (global) exact scale, with the range test;
+ *   mxp_k1ph_read_flag: the state's flag (synchronizes the handle stream). */
+MXP_API int mxp_k1ph_state_bytes(size_t* bytes);
+MXP_API int mxp_k1ph_split_base(mxp_handle h, int64_t n_true, int64_t n, const void* dA, void* h0,
+                                void* h1, void* state);
+MXP_API int mxp_k1ph_gemm_rows(mxp_handle h, int64_t n, int64_t rows, int64_t row0,
+                               const void* x_h0, const void* x_h1, const void* y_h0,
+                               const void* y_h1, void* out, int64_t ld_out, int64_t n_out,
+                               void* state, int xi, int yi, int oi);
+MXP_API int mxp_k1ph_max_to_peers(mxp_handle h, const void* state, int i, int npeers,
+                                  void* const* peer_states);
+MXP_API int mxp_k1ph_split_rows_peers(mxp_handle h, int64_t n_true, int64_t n, int64_t rows,
+                                      int64_t row0, const void* rows_f32, void* state, int i,
+                                      int xi, int yi, int npeers, void* const* peer_h0,
+                                      void* const* peer_h1);
+MXP_API int mxp_k1ph_read_flag(mxp_handle h, const void* state, int* raised);
+
 /* A^k, whole chain on device */
 MXP_API int mxp_power_device(mxp_handle h, int mode, int64_t n, int64_t k, const void* dA, void* dOut,
                      mxp_stats* stats);

@@ -45,6 +45,8 @@ EXPORTS = (
     "mxp_mc_size", "mxp_mc_bind", "mxp_mc_destroy", "mxp_gemm_rows_planes_mc",
     "mxp_copy2d_device", "mxp_last_small_fixups", "mxp_power_multi", "mxp_multi_release",
     "mxp_set_f32_datapath", "mxp_last_f32_fallback",
+    "mxp_k1ph_state_bytes", "mxp_k1ph_split_base", "mxp_k1ph_gemm_rows", "mxp_k1ph_max_to_peers",
+    "mxp_k1ph_split_rows_peers", "mxp_k1ph_read_flag",
 )
 MXP_IPC_HANDLE_BYTES = 72
 MXP_MC_HANDLE_BYTES = 64
@@ -140,6 +142,14 @@ def load() -> ctypes.CDLL:
             "mxp_copy2d_device": [vp, vp, sz, vp, sz, sz, sz],
             "mxp_last_small_fixups": [vp, P(i64)],
             "mxp_set_f32_datapath": [vp, c_int],
+            "mxp_k1ph_state_bytes": [P(sz)],
+            "mxp_k1ph_split_base": [vp, i64, i64, vp, vp, vp, vp],
+            "mxp_k1ph_gemm_rows": [vp, i64, i64, i64, vp, vp, vp, vp, vp, i64, i64, vp, c_int, c_int,
+                                   c_int],
+            "mxp_k1ph_max_to_peers": [vp, vp, c_int, c_int, P(vp)],
+            "mxp_k1ph_split_rows_peers": [vp, i64, i64, i64, i64, vp, vp, c_int, c_int, c_int, c_int,
+                                          P(vp), P(vp)],
+            "mxp_k1ph_read_flag": [vp, vp, P(c_int)],
             "mxp_last_f32_fallback": [vp, P(c_int)],
             "mxp_power_multi": [c_int, P(c_int), c_int, i64, i64, i64, vp, vp, P(Stats)],
             "mxp_multi_release": [],

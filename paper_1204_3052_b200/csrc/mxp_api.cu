@@ -1132,6 +1132,94 @@ int mxp_gemm_rows_planes_peers(mxp_handle h, int64_t n, int64_t rows, int64_t ro
     return MXP_OK;
 }
 
+int mxp_k1ph_state_bytes(size_t* bytes) {
+    if (!bytes) return fail(MXP_E_VALIDATION, "null argument");
+    *bytes = f16_chain_state_bytes();
+    return MXP_OK;
+}
+
+namespace {
+int k1ph_rows_check(int64_t n, int64_t rows, int64_t row0) {
+    if (!k1ph_eligible(n))
+        return fail(MXP_E_UNSUPPORTED, "K1PH row shards need n %% 256 == 0 and n >= 1024, got %lld",
+                    (long long)n);
+    if (rows < 256 || rows % 256 != 0 || row0 < 0 || row0 % 256 != 0 || row0 + rows > n)
+        return fail(MXP_E_VALIDATION, "row block [%lld, +%lld) must be 256-aligned inside n",
+                    (long long)row0, (long long)rows);
+    return MXP_OK;
+}
+}  // namespace
+
+int mxp_k1ph_split_base(mxp_handle h, int64_t n_true, int64_t n, const void* dA, void* h0, void* h1,
+                        void* state) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (!k1ph_eligible(n) || n_true < 1 || n_true > n)
+        return fail(MXP_E_VALIDATION, "need n %% 256 == 0, n >= 1024 and 1 <= n_true <= n");
+    if (!dA || !h0 || !h1 || !state) return fail(MXP_E_VALIDATION, "null device pointer");
+    cudaError_t e = launch_split16(static_cast<const float*>(dA), (int)n_true, (int)n_true, h0, h1,
+                                   (int)n, state, 0, -1, -1, h->stream);
+    return e == cudaSuccess ? MXP_OK : cuda_fail(e, "k1ph base split");
+}
+
+int mxp_k1ph_gemm_rows(mxp_handle h, int64_t n, int64_t rows, int64_t row0, const void* x_h0,
+                       const void* x_h1, const void* y_h0, const void* y_h1, void* out,
+                       int64_t ld_out, int64_t n_out, void* state, int xi, int yi, int oi) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if ((rc = k1ph_rows_check(n, rows, row0))) return rc;
+    if (!x_h0 || !x_h1 || !y_h0 || !y_h1 || !out || !state)
+        return fail(MXP_E_VALIDATION, "null device pointer");
+    if (xi < 0 || yi < 0 || xi > kF16MaxSteps || yi > kF16MaxSteps || oi > kF16MaxSteps || ld_out < 1)
+        return fail(MXP_E_VALIDATION, "state index out of range");
+    F16Maps x, y;
+    if (!encode_plane16_map(&x.a0, x_h0, (int)n, 128) || !encode_plane16_map(&x.a1, x_h1, (int)n, 128) ||
+        !encode_plane16_map(&y.b0, y_h0, (int)n, 64) || !encode_plane16_map(&y.b1, y_h1, (int)n, 64))
+        return fail(MXP_E_CUDA, "cuTensorMapEncodeTiled (fp16) failed");
+    cudaError_t e = launch_k1ph_gemm(x, y, (int)n, static_cast<float*>(out), (int)n_out, (int)ld_out,
+                                     state, xi, yi, oi, h->num_sms, h->stream, (int)rows, (int)row0);
+    return e == cudaSuccess ? MXP_OK : cuda_fail(e, "k1ph_gemm_f16x2 (row block)");
+}
+
+int mxp_k1ph_max_to_peers(mxp_handle h, const void* state, int i, int npeers,
+                          void* const* peer_states) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (!state || !peer_states || npeers < 1 || npeers > kF16MaxPeers || i < 0 || i > kF16MaxSteps)
+        return fail(MXP_E_VALIDATION, "bad peer-state arguments");
+    cudaError_t e = launch_max_to_peers(state, i, peer_states, npeers, h->stream);
+    return e == cudaSuccess ? MXP_OK : cuda_fail(e, "k1ph max to peers");
+}
+
+int mxp_k1ph_split_rows_peers(mxp_handle h, int64_t n_true, int64_t n, int64_t rows, int64_t row0,
+                              const void* rows_f32, void* state, int i, int xi, int yi, int npeers,
+                              void* const* peer_h0, void* const* peer_h1) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if ((rc = k1ph_rows_check(n, rows, row0))) return rc;
+    if (!rows_f32 || !state || !peer_h0 || !peer_h1 || npeers < 1 || npeers > kF16MaxPeers ||
+        i < 1 || i > kF16MaxSteps || xi < 0 || yi < 0 || xi > kF16MaxSteps || yi > kF16MaxSteps ||
+        n_true < 1 || n_true > n)
+        return fail(MXP_E_VALIDATION, "bad split arguments");
+    cudaError_t e = launch_split16_rows_peers(static_cast<const float*>(rows_f32), (int)rows, (int)row0,
+                                              (int)n, (int)n_true, state, i, xi, yi, peer_h0, peer_h1,
+                                              npeers, h->stream);
+    return e == cudaSuccess ? MXP_OK : cuda_fail(e, "k1ph row split to peers");
+}
+
+int mxp_k1ph_read_flag(mxp_handle h, const void* state, int* raised) {
+    int rc = check_handle(h);
+    if (rc) return rc;
+    if (!state || !raised) return fail(MXP_E_VALIDATION, "null argument");
+    MXP_CUDA(cudaSetDevice(h->device));
+    MXP_CUDA(cudaStreamSynchronize(h->stream));
+    int flag = 0;
+    MXP_CUDA(cudaMemcpy(&flag, f16_chain_flag(const_cast<void*>(state)), sizeof flag,
+                        cudaMemcpyDeviceToHost));
+    *raised = flag != 0;
+    return MXP_OK;
+}
+
 int mxp_gemm_rows_planes_mc(mxp_handle h, int64_t n, int64_t rows, int64_t row0, const void* a_hi,
                             const void* a_lo, const void* b_hi, const void* b_lo, void* mc_hi,
                             void* mc_lo, void* mc_f32) {

@@ -323,6 +323,151 @@ class RowShardedFused:
             self.mc = None
 
 
+class RowShardedK1PH:
+    """The row-sharded chain on the K1PH datapath (scaled fp16x2 planes, one
+    exponent per matrix, DESIGN.md §3 K1PH) for one n x n FP32 shape on a
+    group, one process per GPU.  Per plan step every rank computes its
+    256-row blocks of the product in fp32 with the K1PH row-block GEMM, folds
+    their max into every rank's chain state (system-scope atomicMax through
+    CUDA IPC mappings), and after a flag barrier splits its rows at the now
+    global exact scale straight into every rank's next planes (peer stores:
+    the split is the all-gather); a second barrier closes the step.  Every
+    element is computed on one rank with the single-GPU kernel, k-order and
+    scale, so the result is bitwise the single-GPU K1PH chain.  A chain whose
+    product loses dynamic range (every rank sees the same flag) is recomputed
+    collectively on the 3xTF32 fused exchange (RowShardedFused), bitwise the
+    single-GPU chain's own recomputation.  Set up once (collective), reused
+    by ``power``; ``close`` is collective too."""
+
+    _SHARED = ("p0_h0", "p0_h1", "p1_h0", "p1_h1", "out", "state", "flags")
+
+    def __init__(self, n: int, device, group=None, engine=None):
+        import torch
+        import torch.distributed as dist
+
+        self.dist, self.group, self.device = dist, group, device
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.n = n
+        self.n_p, self.rows = fused_layout(n, self.world)
+        if engine is None:
+            from .engine import default_engine
+
+            engine = default_engine(torch.device(device).index or 0)
+        self.eng = engine
+        n_p = self.n_p
+        b = {k: torch.empty((n_p, n_p), dtype=torch.int16, device=device)
+             for k in ("base_h0", "base_h1", "p0_h0", "p0_h1", "p1_h0", "p1_h1")}
+        b["out"] = torch.empty((n_p, n_p), dtype=torch.float32, device=device)
+        b["rows"] = torch.empty((self.rows, n_p), dtype=torch.float32, device=device)
+        b["state"] = torch.zeros(engine.k1ph_state_bytes(), dtype=torch.uint8, device=device)
+        b["flags"] = torch.zeros(self.world, dtype=torch.int32, device=device)
+        self.buf = b
+        self.local = {k: b[k].data_ptr() for k in b}
+        torch.cuda.synchronize(device)
+        mine = {k: engine.ipc_get_handle(self.local[k]) for k in self._SHARED}
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=group)
+        self.opened = []
+        self.peer = {k: [] for k in self._SHARED}
+        for r in range(self.world):
+            for k in self._SHARED:
+                if r == self.rank:
+                    self.peer[k].append(self.local[k])
+                else:
+                    ptr = engine.ipc_open_handle(everyone[r][k])
+                    self.opened.append(ptr)
+                    self.peer[k].append(ptr)
+        self.epoch = 0
+        self.last_fallback = False
+        dist.barrier(group=group)
+
+    def _barrier(self):
+        self.epoch += 1
+        self.eng.peer_barrier(self.rank, self.peer["flags"], self.epoch)
+
+    def power(self, a, power: int):
+        """A^power (a: n x n float32 on this rank's device, replicated); the full
+        result on every rank.  Collective: every rank calls it with the same power."""
+        import torch
+
+        n, n_p, rows, eng, loc = self.n, self.n_p, self.rows, self.eng, self.local
+        if power == 0:
+            return torch.eye(n, dtype=a.dtype, device=a.device)
+        if power == 1:
+            return a.clone()
+        a = a.contiguous()
+        plan = plan_exponentiation(power)
+        ext = torch.cuda.ExternalStream(eng.stream)
+        ext.wait_stream(torch.cuda.current_stream(a.device))  # `a` is ready
+        self._barrier()  # peers are done with the previous call's buffers
+        with torch.cuda.stream(ext):
+            self.buf["state"].zero_()
+        eng.k1ph_split_base(n, n_p, a.data_ptr(), loc["base_h0"], loc["base_h1"], loc["state"])
+        self._barrier()  # every state is reset before peers' maxima arrive
+        r0 = self.rank * rows
+        cur, cur_i, nxt = "base", 0, "p0"
+        for s, step in enumerate(plan.steps):
+            last = s == len(plan.steps) - 1
+            rhs, rhs_i = (cur, cur_i) if step is Step.SQUARE else ("base", 0)
+            oi = s + 1
+            eng.k1ph_gemm_rows(n_p, rows, r0, loc[cur + "_h0"], loc[cur + "_h1"], loc[rhs + "_h0"],
+                               loc[rhs + "_h1"], loc["rows"], n_p, n if last else n_p, loc["state"],
+                               cur_i, rhs_i, -1 if last else oi)
+            if last:
+                # this rank's rows of the result into every rank's `out`
+                h = min(rows, n - r0)
+                if h > 0:
+                    for dst in self.peer["out"]:
+                        eng.copy2d_device(dst + r0 * n_p * 4, n_p * 4, loc["rows"], n_p * 4, n * 4, h)
+                self._barrier()
+                break
+            eng.k1ph_max_to_peers(loc["state"], oi, self.peer["state"])
+            self._barrier()  # the max is global on every rank
+            eng.k1ph_split_rows_peers(n, n_p, rows, r0, loc["rows"], loc["state"], oi, cur_i, rhs_i,
+                                      self.peer[nxt + "_h0"], self.peer[nxt + "_h1"])
+            self._barrier()  # every rank's rows of the next planes have landed
+            cur, cur_i = nxt, oi
+            nxt = "p1" if nxt == "p0" else "p0"
+        self.last_fallback = eng.k1ph_read_flag(loc["state"])  # (the same on every rank)
+        if self.last_fallback:
+            ctx = RowShardedFused(n, a.device, group=self.group, engine=eng, multicast=False)
+            try:
+                return ctx.power(a, power)
+            finally:
+                ctx.close()
+        with torch.cuda.stream(ext):
+            out = torch.empty((n, n), dtype=a.dtype, device=a.device)
+        eng.copy2d_device(out.data_ptr(), n * 4, loc["out"], n_p * 4, n * 4, n)
+        caller = torch.cuda.current_stream(a.device)
+        caller.wait_stream(ext)
+        out.record_stream(caller)
+        return out
+
+    def close(self):
+        self.eng.synchronize()
+        self.dist.barrier(group=self.group)  # nobody unmaps what a peer still writes through
+        for ptr in self.opened:
+            self.eng.ipc_close_handle(ptr)
+        self.opened = []
+
+
+def exponentiate_row_sharded_k1ph(a, power: int, group=None, engine=None):
+    """A^power for one n x n FP32 matrix with its rows sharded over the group
+    on the K1PH datapath (see RowShardedK1PH); the full result on every rank."""
+    import torch
+
+    if a.dtype != torch.float32:
+        raise ValueError("the K1PH row shards run the FP32 chain")
+    if power in (0, 1):
+        return torch.eye(a.shape[0], dtype=a.dtype, device=a.device) if power == 0 else a.clone()
+    ctx = RowShardedK1PH(a.shape[0], a.device, group=group, engine=engine)
+    try:
+        return ctx.power(a, power)
+    finally:
+        ctx.close()
+
+
 def exponentiate_row_sharded_fused(a, power: int, group=None, engine=None):
     """A^power for one n x n FP32 matrix with its rows sharded over the group and
     the exchange fused into the GEMM epilogue (see RowShardedFused).  `a` is

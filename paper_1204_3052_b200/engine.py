@@ -262,6 +262,43 @@ class Engine:
             ctypes.c_void_p(b_hi), ctypes.c_void_p(b_lo), npeers, self._ptr_array(peer_hi),
             self._ptr_array(peer_lo), self._ptr_array(peer_f32)), "mxp_gemm_rows_planes_peers")
 
+    # ------------------------------------------------------------ K1PH row shards (multi-process)
+    @staticmethod
+    def k1ph_state_bytes() -> int:
+        b = ctypes.c_size_t()
+        _lib.check(_lib.load().mxp_k1ph_state_bytes(ctypes.byref(b)), "mxp_k1ph_state_bytes")
+        return b.value
+
+    def k1ph_split_base(self, n_true: int, n: int, d_a: int, h0: int, h1: int, state: int) -> None:
+        _lib.check(self._L.mxp_k1ph_split_base(self._h, n_true, n, ctypes.c_void_p(d_a),
+                                               ctypes.c_void_p(h0), ctypes.c_void_p(h1),
+                                               ctypes.c_void_p(state)), "mxp_k1ph_split_base")
+
+    def k1ph_gemm_rows(self, n: int, rows: int, row0: int, x_h0: int, x_h1: int, y_h0: int,
+                       y_h1: int, out: int, ld_out: int, n_out: int, state: int, xi: int, yi: int,
+                       oi: int) -> None:
+        _lib.check(self._L.mxp_k1ph_gemm_rows(
+            self._h, n, rows, row0, ctypes.c_void_p(x_h0), ctypes.c_void_p(x_h1),
+            ctypes.c_void_p(y_h0), ctypes.c_void_p(y_h1), ctypes.c_void_p(out), ld_out, n_out,
+            ctypes.c_void_p(state), xi, yi, oi), "mxp_k1ph_gemm_rows")
+
+    def k1ph_max_to_peers(self, state: int, i: int, peer_states) -> None:
+        _lib.check(self._L.mxp_k1ph_max_to_peers(self._h, ctypes.c_void_p(state), i, len(peer_states),
+                                                 self._ptr_array(peer_states)), "mxp_k1ph_max_to_peers")
+
+    def k1ph_split_rows_peers(self, n_true: int, n: int, rows: int, row0: int, rows_f32: int,
+                              state: int, i: int, xi: int, yi: int, peer_h0, peer_h1) -> None:
+        _lib.check(self._L.mxp_k1ph_split_rows_peers(
+            self._h, n_true, n, rows, row0, ctypes.c_void_p(rows_f32), ctypes.c_void_p(state), i,
+            xi, yi, len(peer_h0), self._ptr_array(peer_h0), self._ptr_array(peer_h1)),
+            "mxp_k1ph_split_rows_peers")
+
+    def k1ph_read_flag(self, state: int) -> bool:
+        c = ctypes.c_int()
+        _lib.check(self._L.mxp_k1ph_read_flag(self._h, ctypes.c_void_p(state), ctypes.byref(c)),
+                   "mxp_k1ph_read_flag")
+        return bool(c.value)
+
     def copy2d_device(self, dst: int, dpitch: int, src: int, spitch: int, width: int,
                       rows: int) -> None:
         """rows x width bytes, device to device, on the engine's stream."""

@@ -74,8 +74,13 @@ def test_roofline_counts_the_k3h_launch_over_the_step():
     assert r["kernel"] == "k3h_batched_power"
     w5 = bench.WORKLOADS["c5"]
     f5 = bench.flops(w5)
-    # one GPU: K1PH (fp16 datapath / 3); row-sharded over 2 GPUs: 3xTF32 K1P
+    # K1PH (fp16 datapath / 3) on one GPU and row-sharded over 2
     r5 = bench.roofline_of(w5, False, f5, 24.0, 23, f5 / 24e-3 / 1e12, 1, peaks, 759.0)
     assert r5["kernel"] == "k1ph_gemm_f16x2" and 0.5 < r5["frac"] < 1.0
-    r5s = bench.roofline_of(w5, False, f5, 23.0, 21, f5 / 23e-3 / 1e12, 2, peaks, 759.0)
-    assert r5s["kernel"] == "k1p_gemm_3xtf32" and 0.5 < r5s["frac"] < 1.05
+    r5s = bench.roofline_of(w5, False, f5, 13.0, 21, f5 / 13e-3 / 1e12, 2, peaks, 759.0)
+    assert r5s["kernel"] == "k1ph_gemm_f16x2" and 0.5 < r5s["frac"] < 1.0
+    # a 3xTF32 size (n_pad 1152, inside K1C's range): cuBLAS TF32 / 3
+    w2 = bench.WORKLOADS["c2"]
+    r2 = bench.roofline_of(w2, False, bench.flops(w2), 0.1, 2, bench.flops(w2) / 0.1e-3 / 1e12, 1,
+                           peaks, 759.0)
+    assert r2["kernel"] == "k1c_chain_3xtf32"

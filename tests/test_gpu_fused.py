@@ -75,6 +75,71 @@ def test_fused_exchange_ranks_one_gpu_bitwise(world, n):
         assert oracle.compare(got, ref)[2] <= 16 * 5 * np.sqrt(n) * 2.0 ** -24
 
 
+def _worker_k1ph(rank, world, port, n, ks, cancel, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    import paper_1204_3052_b200 as mx
+    from paper_1204_3052_b200 import distributed as D
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        eng = mx.Engine(0)  # default datapath: K1PH at these sizes
+        if cancel:
+            rng = np.random.default_rng(5)
+            nil = np.zeros((n, n))
+            nil[: n // 2, n // 2:] = rng.uniform(-1, 1, (n // 2, n // 2))
+            a_np = (nil + 1e-6 * rng.uniform(-1, 1, (n, n))).astype(np.float32)
+        else:
+            a_np = oracle.scaled_input(n, np.float32, 42)
+        a = torch.from_numpy(a_np).cuda()
+        ctx = D.RowShardedK1PH(n, a.device, engine=eng)
+        res = {}
+        try:
+            for k in ks:
+                got = ctx.power(a, k).cpu().numpy()
+                res[k] = (got.tobytes(), eng.power(a_np, k).tobytes() if rank == 0 else None,
+                          ctx.last_fallback)
+        finally:
+            ctx.close()
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,n,cancel", [(2, 1024, False), (4, 2048, False), (3, 1500, False),
+                                            (2, 1024, True)])
+def test_k1ph_row_shards_ranks_one_gpu_bitwise(world, n, cancel):
+    """RowShardedK1PH (one process per rank sharing the B200): K1PH row-block
+    GEMMs, maxima into every rank's state over CUDA IPC, rows split into every
+    rank's planes, flag barriers — BITWISE the single-GPU K1PH chain; a
+    cancelling input falls back to the 3xTF32 fused exchange on every rank,
+    bitwise the single-GPU chain's own recomputation."""
+    import torch.multiprocessing as mp
+
+    ks = (6,) if cancel else (16, 13)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_k1ph, args=(r, world, port, n, ks, cancel, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for k in ks:
+        single = results[0][k][1]
+        for r in range(world):
+            assert results[r][k][0] == single, (k, r)
+            assert results[r][k][2] == cancel, (k, r)
+
+
 def test_fused_layout():
     from paper_1204_3052_b200 import distributed as D
 
