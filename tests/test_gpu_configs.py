@@ -137,3 +137,5 @@ def test_single_chain_bench_launch_vs_oracle(eng, golden, key):
     else:
         pinned = _configs()[key]  # KeyError: run tests/golden/make_golden_configs.py
         assert _sha(ref) == pinned["sha256"], f"{key}: oracle differs from the reference"
+        if key + "_single" in _configs():  # the unmodified one-core reference call
+            assert _configs()[key + "_single"]["sha256"] == pinned["sha256"]
