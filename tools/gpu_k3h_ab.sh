@@ -1,5 +1,7 @@
 #!/bin/bash
 # C3 launch time (tools/c3_time.py, synchronised launches): the round-1 build
+# (tools/_variants/r1tree: `git worktree add --detach tools/_variants/r1tree af08815`, then
+#  build it in place with paper_1204_3052_b200.build; variants: tools/build_variant.py)
 # (tools/_variants/r1tree), the product, and every tools/_variants/*.so, interleaved
 cd "$GRAFT_REPO_ROOT"
 O=gpurun_out/$1; mkdir -p $O

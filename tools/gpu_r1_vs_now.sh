@@ -1,5 +1,7 @@
 #!/bin/bash
 # C3 device time of the round-1 final build (tools/_variants/r1tree, af08815) and the current build, interleaved on one box
+# (tools/_variants/r1tree: `git worktree add --detach tools/_variants/r1tree af08815`, then
+#  build it in place with paper_1204_3052_b200.build; variants: tools/build_variant.py)
 cd "$GRAFT_REPO_ROOT"
 O=gpurun_out/$1; mkdir -p $O
 for rep in 1 2 3 4; do
