@@ -121,7 +121,7 @@ def test_k1ph_row_shards_ranks_one_gpu_bitwise(world, n, cancel):
     bitwise the single-GPU chain's own recomputation."""
     import torch.multiprocessing as mp
 
-    ks = (6,) if cancel else (16, 13)
+    ks = (6,) if cancel else (16, 13, 2)  # 2: a one-step plan (the first step is the last)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

@@ -67,6 +67,7 @@ def eng_auto():
     ([0, 0, 0, 0], 2048, 16),  # four row blocks of 512
     ([0, 0, 0], 1500, 13),     # ragged: 1500 -> 3 x 512 rows (single chain: n_pad 1536)
     ([0, 0], 1600, 9),         # 1600 -> 2 x 1024 rows (single chain: 1792; padding adds exact zeros)
+    ([0, 0, 0], 1024, 2),      # a one-step plan; 1024 -> 3 x 512 rows (1536, padding rows only on the last)
 ])
 def test_row_shards_bitwise_single_device(eng_auto, devices, n, k):
     """K1PH row shards: each device's rows from the K1PH row-block GEMM, the

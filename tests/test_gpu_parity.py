@@ -881,12 +881,13 @@ def _structured(kind, n, rng):
     return a
 
 
-@pytest.mark.parametrize("n,dt", [(64, "f32"), (128, "f32"), (300, "f32"), (1024, "f32"), (256, "f64")])
+@pytest.mark.parametrize("n,dt", [(64, "f32"), (128, "f32"), (300, "f32"), (1024, "f32"), (1600, "f32"),
+                                  (256, "f64")])
 @pytest.mark.parametrize("kind", ["upper_triangular", "two_scales", "rank_one", "integer",
                                   "signed_permutation"])
 def test_structured_inputs_every_kernel(eng, n, dt, kind):
-    """K3H/K3B (64, 128), K1C (300), K1PH (1024, with its 3xTF32 recomputation)
-    and K2 (f64): structured
+    """K3H/K3B (64, 128), K1C (300), K1PH (1024, and 1600 padded to 1792 whose
+    3xTF32 recomputation runs on K1 at 1664) and K2 (f64): structured
     matrices with cancellation, wide dynamic range, low rank, exact integer
     products and permutations.  Criterion: no further from the exact result
     than the reference's own CPU chain by more than the reference's 64x
