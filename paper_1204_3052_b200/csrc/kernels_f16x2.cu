@@ -334,6 +334,10 @@ __global__ void split16_kernel(const float* __restrict__ in, int n, int ld,
                 lost = ilogb_bits(mb) < bound_e - 12;
             }
             if (lost) st->flag = 1;
+        } else if (mb >= 0x7F800000u) {
+            // a non-finite base: the 3xTF32 recomputation gives the reference's
+            // inf / NaN pattern (an inf split into fp16 halves becomes inf + NaN)
+            st->flag = 1;
         }
     }
     const float sc = exp2i(t);

@@ -88,6 +88,12 @@ def test_k1ph_nan_zero_and_exact_inputs(eng):
     a[7, 9] = np.nan
     g16, fb, g32 = _both(eng, a, 3)
     assert fb and np.array_equal(np.isnan(g16), np.isnan(g32))
+    # an inf in the base, one-step plan (no product is split): the base split
+    # raises the flag, so the result carries the 3xTF32 chain's inf / NaN pattern
+    b = oracle.scaled_input(n, np.float32, 4)
+    b[3, 5] = np.inf
+    g16, fb, g32 = _both(eng, b, 2)
+    assert fb and g16.tobytes() == g32.tobytes()
     # zero matrix: zero product, exact zeros
     z = np.zeros((n, n), np.float32)
     g16, fb, _ = _both(eng, z, 13)
